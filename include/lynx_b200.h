@@ -1,0 +1,110 @@
+/* lynx_b200.h — C-ABI of the B200 operator library (sm_100a kernels).
+ *
+ * These are the GPT-block operators the executor (include/lynx_rt.h) launches
+ * for every forward op, backward op and recomputation of a Lynx plan. The
+ * reference has no operator library at all: its operators are names, times and
+ * byte counts in the profile JSON (reference proj/tests/fixtures/gpt-tiny.json:8-15,
+ * schema proj/include/lynx/profile.hpp:27-34). These entry points are what a
+ * GPU "model deployer" (Fig. 5, out of the reference's scope per
+ * SPEC.md:9,14) binds to.
+ *
+ * Conventions: device pointers; bf16 tensors are row-major; `stream` is a
+ * cudaStream_t (NULL = legacy default stream). Every function returns
+ * LYNX_OK (0) or an error code, with the message in lynx_last_error()
+ * (thread-local). No function allocates device memory; callers pass the
+ * workspace sizes reported by the *_workspace queries.
+ */
+#ifndef LYNX_B200_H_
+#define LYNX_B200_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LYNX_ABI_VERSION 1
+
+/* Status codes: 0-5 follow the reference CLI exit codes
+ * (proj/tools/lynx_main.cpp:30-35); 6-7 are added for the device side. */
+#define LYNX_OK 0
+#define LYNX_E_VALIDATION 1
+#define LYNX_E_PARSE 2
+#define LYNX_E_TIMED_OUT 3
+#define LYNX_E_INFEASIBLE 4
+#define LYNX_E_NO_PARTITION 5
+#define LYNX_E_CUDA 6
+#define LYNX_E_OOM 7
+
+/* GEMM epilogues */
+#define LYNX_EPI_BF16 0    /* C(bf16) = A*B^T (+ bias[n]) */
+#define LYNX_EPI_ACC_F32 1 /* C(f32) += A*B^T  (weight-gradient accumulation) */
+#define LYNX_EPI_F32 2     /* C(f32)  = A*B^T */
+
+const char* lynx_last_error(void);
+int lynx_abi_version(void);
+
+/* C[M,N] = A[M,K] * B[N,K]^T on tcgen05 tensor cores (fp32 accumulation in TMEM).
+ * a_mn_major=0: A stored [M][K] (row pitch lda); 1: A stored [K][M] (pitch lda).
+ * b_mn_major=0: B stored [N][K] (row pitch ldb); 1: B stored [K][N] (pitch ldb).
+ * Requires M % 128 == 0, N % 128 == 0, K % 64 == 0, 16-byte aligned rows. */
+int lynx_op_gemm(const void* a, long long lda, int a_mn_major, const void* b, long long ldb, int b_mn_major, void* c,
+                 long long ldc, int m, int n, int k, const void* bias, int epilogue, void* stream);
+
+/* y = (x - mean) * rstd * gamma + beta over rows of `width`; mean/rstd fp32 [rows]. */
+int lynx_op_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
+                          int rows, int width, float eps, void* stream);
+size_t lynx_op_layernorm_bwd_workspace(int rows, int width);
+/* dx = LN'(dy) (+ dres if non-NULL); dgamma_acc/dbeta_acc (fp32) += column sums. Deterministic. */
+int lynx_op_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
+                          const void* dres, void* dx, float* dgamma_acc, float* dbeta_acc, float* workspace,
+                          int rows, int width, void* stream);
+
+/* out = res + dropout_p(y + bias[col]); mask = Philox(seed, stream_id, element). bias may be NULL. */
+int lynx_op_bias_dropout_residual(const void* y, const void* bias, const void* res, void* out, long long rows,
+                                  int width, float p, unsigned long long seed, unsigned long long stream_id,
+                                  void* stream);
+/* dy = dout * mask / (1 - p) with the same mask as the forward call. */
+int lynx_op_dropout_bwd(const void* dout, void* dy, long long rows, int width, float p, unsigned long long seed,
+                        unsigned long long stream_id, void* stream);
+size_t lynx_op_column_sum_workspace(long long rows, int width);
+/* acc[col] += sum_rows x[row][col] (bias gradients), deterministic. */
+int lynx_op_column_sum_acc(const void* x, float* acc, float* workspace, long long rows, int width, void* stream);
+
+/* GPT-2 tanh GeLU on n bf16 elements (n % 8 == 0). */
+int lynx_op_gelu_fwd(const void* x, void* y, long long n, void* stream);
+int lynx_op_gelu_bwd(const void* dy, const void* x, void* dx, long long n, void* stream);
+
+/* Causal attention. qkv [batch*seq, 3*heads*head_dim] ([Q|K|V], head-major inside each),
+ * out [batch*seq, heads*head_dim], lse [batch, heads, seq] (natural log). head_dim in {64,96,112,128},
+ * seq % 64 == 0. Backward writes dQ|dK|dV into dqkv with the qkv layout; deterministic. */
+int lynx_op_attention_fwd(const void* qkv, void* out, float* lse, int batch, int seq, int heads, int head_dim,
+                          void* stream);
+size_t lynx_op_attention_bwd_workspace(int batch, int seq, int heads);
+int lynx_op_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
+                          float* workspace, int batch, int seq, int heads, int head_dim, void* stream);
+
+/* out[b,s] = dropout(wte[tokens[b,s]] + wpe[s]); backward accumulates fp32 dwte/dwpe. */
+int lynx_op_embedding_fwd(const int* tokens, const void* wte, const void* wpe, void* out, int batch, int seq,
+                          int width, float p, unsigned long long seed, unsigned long long stream_id, void* stream);
+size_t lynx_op_embedding_bwd_workspace(int batch, int seq, int width);
+int lynx_op_embedding_bwd(const int* tokens, const void* dout, float* dwte, float* dwpe, float* workspace, int batch,
+                          int seq, int width, int vocab, float p, unsigned long long seed,
+                          unsigned long long stream_id, void* stream);
+
+/* In place: logits[rows, vocab] -> (softmax - onehot(labels)) * grad_scale; loss_rows = lse - logit[label]. */
+int lynx_op_xent_fwd_bwd(void* logits, const int* labels, float* loss_rows, long long rows, int vocab,
+                         float grad_scale, void* stream);
+
+/* AdamW over flat fp32 master / m / v, writes the bf16 working copy. grad is scaled by grad_scale. */
+int lynx_op_adam(float* master, void* param, const float* grad, float* m, float* v, long long n, float lr,
+                 float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale, void* stream);
+/* param (bf16) ~ N(0, std) from Philox(seed, stream_id, index); master (may be NULL) = float(param). */
+int lynx_op_init_normal(void* param, float* master, long long n, float std, unsigned long long seed,
+                        unsigned long long stream_id, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LYNX_B200_H_ */

@@ -1,0 +1,89 @@
+// Internal (C++) interface of the operator library shared by the kernel
+// translation units, the C-ABI wrappers (capi_ops.cu) and the runtime.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace lynx {
+
+// Status codes shared with the C-ABI (include/lynx_b200.h).
+enum Status {
+  kOk = 0,
+  kValidation = 1,
+  kParse = 2,
+  kTimedOut = 3,
+  kInfeasible = 4,
+  kNoValidPartition = 5,
+  kCudaError = 6,
+  kOutOfMemory = 7,
+};
+
+int set_error(const std::string& msg, int code = kCudaError);
+int check_launch(const char* what);
+const char* last_error();
+
+enum EpiMode { EPI_BF16 = 0, EPI_ACC_F32 = 1, EPI_STORE_F32 = 2 };
+
+struct GemmDesc {
+  const void* a;  // bf16
+  long long lda;  // elements between consecutive rows of the stored matrix
+  bool a_mn;      // A stored MN-major ([K][M]) instead of K-major ([M][K])
+  const void* b;
+  long long ldb;
+  bool b_mn;  // B stored MN-major ([K][N]) instead of K-major ([N][K])
+  void* c;
+  long long ldc;
+  int M, N, K;
+  const __nv_bfloat16* bias;  // EPI_BF16 only, may be null
+  int epi;
+};
+
+int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas = 0);
+
+// ---- norm / elementwise / attention / loss (see the .cu files for contracts)
+int layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* gamma, const __nv_bfloat16* beta, __nv_bfloat16* y,
+                  float* mean, float* rstd, int rows, int width, float eps, cudaStream_t s);
+int layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* gamma, const float* mean,
+                  const float* rstd, const __nv_bfloat16* dres, __nv_bfloat16* dx, float* dgamma_acc,
+                  float* dbeta_acc, float* workspace, int rows, int width, cudaStream_t s);
+size_t layernorm_bwd_workspace(int rows, int width);
+
+int bias_dropout_residual_fwd(const __nv_bfloat16* y, const __nv_bfloat16* bias, const __nv_bfloat16* res,
+                              __nv_bfloat16* out, long long rows, int width, float p, uint64_t seed,
+                              uint64_t stream_id, cudaStream_t s);
+int dropout_bwd(const __nv_bfloat16* dout, __nv_bfloat16* dy, long long rows, int width, float p, uint64_t seed,
+                uint64_t stream_id, cudaStream_t s);
+int column_sum_acc(const __nv_bfloat16* x, float* acc, float* workspace, long long rows, int width, cudaStream_t s);
+size_t column_sum_workspace(long long rows, int width);
+int gelu_fwd(const __nv_bfloat16* x, __nv_bfloat16* y, long long n, cudaStream_t s);
+int gelu_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, __nv_bfloat16* dx, long long n, cudaStream_t s);
+int add_bf16(const __nv_bfloat16* a, const __nv_bfloat16* b, __nv_bfloat16* out, long long n, cudaStream_t s);
+
+int embedding_fwd(const int32_t* tokens, const __nv_bfloat16* wte, const __nv_bfloat16* wpe, __nv_bfloat16* out,
+                  int batch, int seq, int width, float p, uint64_t seed, uint64_t stream_id, cudaStream_t s);
+int embedding_bwd(const int32_t* tokens, const __nv_bfloat16* dout, float* dwte, float* dwpe, float* workspace,
+                  int batch, int seq, int width, int vocab, float p, uint64_t seed, uint64_t stream_id,
+                  cudaStream_t s);
+size_t embedding_bwd_workspace(int batch, int seq, int width);
+
+int xent_fwd_bwd(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows, long long rows, int vocab,
+                 float grad_scale, cudaStream_t s);
+
+int attention_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int batch, int seq, int heads,
+                  int head_dim, cudaStream_t s);
+int attention_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse,
+                  __nv_bfloat16* dqkv, float* workspace, int batch, int seq, int heads, int head_dim,
+                  cudaStream_t s);
+size_t attention_bwd_workspace(int batch, int seq, int heads);
+
+int adam_step(float* master, __nv_bfloat16* param, const float* grad, float* m, float* v, long long n, float lr,
+              float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale, cudaStream_t s);
+int fill_f32(float* p, float v, long long n, cudaStream_t s);
+int init_normal_bf16(__nv_bfloat16* p, float* master, long long n, float std, uint64_t seed, uint64_t stream_id,
+                     cudaStream_t s);
+
+}  // namespace lynx

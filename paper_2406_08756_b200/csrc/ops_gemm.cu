@@ -1,0 +1,330 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a — the dense contractions of the GPT
+// block (QKV, attention-output, FC1, FC2, LM head) in forward, dX and dW form.
+//
+//   C[M,N] (op)= A[M,K] * B[N,K]^T         bf16 inputs, fp32 accumulation in TMEM
+//
+// Each operand is either K-major (K contiguous) or MN-major (M resp. N
+// contiguous), so the three training GEMMs need no transposes:
+//   forward  Y  = X  W^T : A = X  [T,in]  K-major,  B = W [out,in] K-major
+//   dX       dX = dY W   : A = dY [T,out] K-major,  B = W          MN-major
+//   dW       dW = dY^T X : A = dY         MN-major, B = X [T,in]   MN-major
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0      TMA producer (one elected lane), 4-stage smem ring
+//   warp 1      MMA issuer (one elected lane), tcgen05.mma.cta_group::1, 128xBNx16
+//   warp 2      TMEM allocator (512 columns = 2 accumulator buffers)
+//   warps 4..7  epilogue: tcgen05.ld -> registers -> bias / convert -> global
+// The double-buffered accumulator lets tile i's epilogue overlap tile i+1's
+// main loop. No split-K and no atomics: every output element is produced by
+// exactly one CTA in a fixed K order, so results are bit-reproducible (the
+// recompute bit-identity requirement of the north star).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "lynx_ops_internal.h"
+
+namespace lynx {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle row of bf16
+constexpr int kStages = 4;
+constexpr int kThreads = 256;
+constexpr int kGroupM = 16;  // L2-friendly tile rasterisation
+
+struct Args {
+  void* c;          // bf16 or f32 output
+  const __nv_bfloat16* bias;  // optional, per output column (EPI_BF16 only)
+  long long ldc;    // elements
+  int M, N, K;
+  int epi;          // EpiMode
+};
+
+template <int BN>
+struct Smem {
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
+  const int per_group = kGroupM * n_tiles;
+  const int group = tile / per_group;
+  const int first_m = group * kGroupM;
+  const int gm = min(kGroupM, m_tiles - first_m);
+  const int in_group = tile % per_group;
+  mt = first_m + in_group % gm;
+  nt = in_group / gm;
+}
+
+template <bool kAMN, bool kBMN, int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, Args args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  using S = Smem<BN>;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int m_tiles = args.M / BM;
+  const int n_tiles = args.N / BN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int k_blocks = args.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_a);
+    tma_prefetch_desc(&tm_b);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 4);  // one elected lane per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_base_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int mt, nt;
+        tile_coords(tile, m_tiles, n_tiles, mt, nt);
+        const int m0 = mt * BM, n0 = nt * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStageBytes;
+          uint8_t* sb = sa + S::kABytes;
+          mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+          const int k0 = kb * BK;
+          if constexpr (!kAMN) {
+            tma_load_2d(&tm_a, &full[stage], sa, k0, m0, kEvictNormal);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(&tm_a, &full[stage], sa + j * (64 * BK * 2), m0 + 64 * j, k0, kEvictNormal);
+          }
+          if constexpr (!kBMN) {
+            tma_load_2d(&tm_b, &full[stage], sb, k0, n0, kEvictNormal);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d(&tm_b, &full[stage], sb + j * (64 * BK * 2), n0 + 64 * j, k0, kEvictNormal);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, kAMN, kBMN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
+          const uint32_t sb = sa + S::kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: advance 16 elements (32 B) inside the swizzled 128-B row.
+            // MN-major: advance 16 K-rows (16 x 128 B) -> two 1024-B swizzle atoms.
+            const uint64_t da = kAMN ? umma_desc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
+                                     : umma_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t db = kBMN ? umma_desc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
+                                     : umma_desc_sw128(sb + k * 32, 16, 1024);
+            umma_f16(d_tmem, da, db, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (kb == k_blocks - 1) umma_commit(&tmem_full[acc]);
+        }
+        __syncwarp();
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;  // == warp % 4: TMEM lane quadrant
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int mt, nt;
+      tile_coords(tile, m_tiles, n_tiles, mt, nt);
+      const int row = mt * BM + ew * 32 + lane;
+      const int n0 = nt * BN;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(t_row + c, r);
+        tmem_ld_wait();
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+        if (args.epi == EPI_ACC_F32) {
+          float* out = reinterpret_cast<float*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            float4 o = *reinterpret_cast<float4*>(out + i);
+            o.x += v[i];
+            o.y += v[i + 1];
+            o.z += v[i + 2];
+            o.w += v[i + 3];
+            *reinterpret_cast<float4*>(out + i) = o;
+          }
+        } else if (args.epi == EPI_STORE_F32) {
+          float* out = reinterpret_cast<float*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(out + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+          if (args.bias) {
+            const BF8* bp = reinterpret_cast<const BF8*>(args.bias + n0 + c);
+            float b[16];
+            bf8_to_f(bp[0], b);
+            bf8_to_f(bp[1], b + 8);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += b[i];
+          }
+          __nv_bfloat16* out =
+              reinterpret_cast<__nv_bfloat16*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
+          BF8* o = reinterpret_cast<BF8*>(out);
+          o[0] = f_to_bf8(v);
+          o[1] = f_to_bf8(v + 8);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem_base);
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows,
+// row pitch `ld` elements, box {box_inner, box_outer}, 128-B swizzle.
+bool make_map(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld, int box_inner,
+              int box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <bool kAMN, bool kBMN, int BN>
+int launch(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
+  CUtensorMap ma, mb;
+  // A: K-major -> rows = M, row = K contiguous.  MN-major -> rows = K, row = M contiguous.
+  bool ok = kAMN ? make_map(&ma, g.a, g.M, g.K, g.lda, 64, BK) : make_map(&ma, g.a, g.K, g.M, g.lda, BK, BM);
+  ok = ok && (kBMN ? make_map(&mb, g.b, g.N, g.K, g.ldb, 64, BK) : make_map(&mb, g.b, g.K, g.N, g.ldb, BK, BN));
+  if (!ok) return set_error("cuTensorMapEncodeTiled failed (alignment or driver entry point)");
+  auto kern = gemm_kernel<kAMN, kBMN, BN>;
+  const int smem = Smem<BN>::kBytes;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_set = true;
+  }
+  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi};
+  const int tiles = (g.M / BM) * (g.N / BN);
+  int grid = tiles < num_sms() ? tiles : num_sms();
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  kern<<<grid, kThreads, smem, stream>>>(ma, mb, args);
+  return check_launch("gemm_tcgen05");
+}
+
+}  // namespace gemm
+
+int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
+  using namespace gemm;
+  if (g.M % BM || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
+    return set_error("gemm: M must be a multiple of 128 and K of 64");
+  if (g.N % 128) return set_error("gemm: N must be a multiple of 128");
+  if ((g.epi == EPI_BF16 && g.ldc % 8) || (g.epi != EPI_BF16 && g.ldc % 4))
+    return set_error("gemm: ldc must keep 16-byte row alignment");
+  const bool wide = g.N % 256 == 0;
+#define LYNX_GEMM_CASE(AMN, BMN)                                                             \
+  if (g.a_mn == AMN && g.b_mn == BMN)                                                         \
+    return wide ? launch<AMN, BMN, 256>(g, stream, max_ctas) : launch<AMN, BMN, 128>(g, stream, max_ctas);
+  LYNX_GEMM_CASE(false, false)
+  LYNX_GEMM_CASE(false, true)
+  LYNX_GEMM_CASE(true, false)
+  LYNX_GEMM_CASE(true, true)
+#undef LYNX_GEMM_CASE
+  return set_error("gemm: bad operand majors");
+}
+
+}  // namespace lynx

@@ -1,0 +1,212 @@
+"""Numerics of the sm_100a operator library against plain PyTorch fp32 references.
+
+Tolerances (bf16 storage, fp32 accumulation): GEMM relative Frobenius error
+<= 1e-2; elementwise / norm ops max |diff| <= 2 bf16 ulps of the output scale;
+attention relative error <= 2e-2 (fwd) and <= 5e-2 (bwd). Determinism checks
+(bit-identical reruns) back the recompute bit-identity requirement.
+"""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).norm() / (b.norm() + 1e-12)).item()
+
+
+@pytest.fixture(scope="module")
+def ops(cuda):
+    from paper_2406_08756_b200 import ops as _ops
+    return _ops
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 384, 192), (512, 1536, 512), (1024, 2048, 1024)])
+def test_gemm_majors(ops, cuda, a_mn, b_mn, M, N, K):
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    B = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    a = A.t().contiguous() if a_mn else A
+    b = B.t().contiguous() if b_mn else B
+    ref = A.float() @ B.float().t()
+    out = ops.gemm(a, b, a_mn=a_mn, b_mn=b_mn)
+    torch.cuda.synchronize()
+    assert rel(out, ref) < 1e-2
+
+
+def test_gemm_bias_and_f32_epilogues(ops, cuda):
+    g = torch.Generator(device=cuda).manual_seed(7)
+    A = torch.randn(256, 512, device=cuda, generator=g).bfloat16()
+    B = torch.randn(768, 512, device=cuda, generator=g).bfloat16()
+    bias = torch.randn(768, device=cuda, generator=g).bfloat16()
+    ref = A.float() @ B.float().t()
+    out = ops.gemm(A, B, bias=bias)
+    assert rel(out, ref + bias.float()) < 1e-2
+    acc = torch.ones(256, 768, device=cuda)
+    ops.gemm(A, B, out=acc, epi=ops.EPI_ACC_F32)
+    assert rel(acc, ref + 1) < 1e-5
+    f = ops.gemm(A, B, epi=ops.EPI_F32)
+    assert rel(f, ref) < 1e-5
+
+
+def test_gemm_deterministic(ops, cuda):
+    A = torch.randn(1024, 1024, device=cuda).bfloat16()
+    B = torch.randn(1024, 1024, device=cuda).bfloat16()
+    o1 = ops.gemm(A, B)
+    o2 = ops.gemm(A, B)
+    assert torch.equal(o1, o2)
+
+
+def test_gemm_rejects_bad_shapes(ops, cuda):
+    from paper_2406_08756_b200._native import LynxError
+    A = torch.randn(100, 64, device=cuda).bfloat16()
+    with pytest.raises(LynxError):
+        ops.gemm(A, A)
+
+
+@pytest.mark.parametrize("rows,width", [(64, 512), (300, 1792), (128, 4096), (17, 6144)])
+def test_layernorm(ops, cuda, rows, width):
+    x = torch.randn(rows, width, device=cuda).bfloat16()
+    gam = (1 + 0.1 * torch.randn(width, device=cuda)).bfloat16()
+    bet = (0.1 * torch.randn(width, device=cuda)).bfloat16()
+    y, mean, rstd = ops.layernorm_fwd(x, gam, bet)
+    xr = x.float().requires_grad_()
+    gr = gam.float().requires_grad_()
+    br = bet.float().requires_grad_()
+    yr = torch.nn.functional.layer_norm(xr, (width,), gr, br, eps=1e-5)
+    assert (y.float() - yr).abs().max().item() < 3e-2
+    assert torch.allclose(mean, x.float().mean(1), atol=1e-4)
+    dy = torch.randn(rows, width, device=cuda).bfloat16()
+    dres = torch.randn(rows, width, device=cuda).bfloat16()
+    yr.backward(dy.float())
+    dg = torch.zeros(width, device=cuda)
+    db = torch.zeros(width, device=cuda)
+    dx = ops.layernorm_bwd(dy, x, gam, mean, rstd, dg, db, dres=dres)
+    assert rel(dx, xr.grad + dres.float()) < 1e-2
+    assert rel(dg, gr.grad) < 1e-3
+    assert rel(db, br.grad) < 1e-3
+    dg2 = torch.zeros(width, device=cuda)
+    db2 = torch.zeros(width, device=cuda)
+    dx2 = ops.layernorm_bwd(dy, x, gam, mean, rstd, dg2, db2, dres=dres)
+    assert torch.equal(dx, dx2) and torch.equal(dg, dg2) and torch.equal(db, db2)
+
+
+def test_dropout_residual_replays_mask(ops, cuda):
+    rows, width = 512, 1024
+    y = torch.randn(rows, width, device=cuda).bfloat16()
+    b = torch.randn(width, device=cuda).bfloat16()
+    r = torch.randn(rows, width, device=cuda).bfloat16()
+    o1 = ops.bias_dropout_residual(y, b, r, 0.1, seed=42, stream_id=1234)
+    o2 = ops.bias_dropout_residual(y, b, r, 0.1, seed=42, stream_id=1234)
+    o3 = ops.bias_dropout_residual(y, b, r, 0.1, seed=42, stream_id=1235)
+    assert torch.equal(o1, o2)
+    assert not torch.equal(o1, o3)
+    ones = torch.ones_like(y)
+    keep = ops.bias_dropout_residual(ones, None, torch.zeros_like(y), 0.1, seed=42, stream_id=1234).float() != 0
+    frac = keep.float().mean().item()
+    assert abs(frac - 0.9) < 0.01
+    ref = r.float() + keep.float() * (y.float() + b.float()) / 0.9
+    assert (o1.float() - ref).abs().max().item() < 0.05
+    o0 = ops.bias_dropout_residual(y, b, r, 0.0, seed=42, stream_id=1)
+    assert (o0.float() - (r.float() + y.float() + b.float())).abs().max().item() < 0.05
+    dout = torch.randn(rows, width, device=cuda).bfloat16()
+    dy = ops.dropout_bwd(dout, 0.1, seed=42, stream_id=1234)
+    assert (dy.float() - keep.float() * dout.float() / 0.9).abs().max().item() < 0.02
+
+
+def test_column_sum(ops, cuda):
+    x = torch.randn(5000, 768, device=cuda).bfloat16()
+    acc = torch.full((768,), 2.0, device=cuda)
+    ops.column_sum_acc(x, acc)
+    assert torch.allclose(acc, x.float().sum(0) + 2, atol=1e-2)
+
+
+def test_gelu(ops, cuda):
+    x = (3 * torch.randn(4096, 256, device=cuda)).bfloat16()
+    y = ops.gelu_fwd(x)
+    xr = x.float().requires_grad_()
+    yr = torch.nn.functional.gelu(xr, approximate="tanh")
+    assert (y.float() - yr).abs().max().item() < 3e-2
+    dy = torch.randn_like(x)
+    yr.backward(dy.float())
+    dx = ops.gelu_bwd(dy, x)
+    assert rel(dx, xr.grad) < 1e-2
+
+
+def _ref_attention(qkv, B, S, H, D):
+    q, k, v = qkv.float().view(B, S, 3, H, D).permute(2, 0, 3, 1, 4)
+    att = (q @ k.transpose(-1, -2)) / math.sqrt(D)
+    mask = torch.ones(S, S, device=qkv.device, dtype=torch.bool).triu(1)
+    att = att.masked_fill(mask, float("-inf"))
+    lse = torch.logsumexp(att, -1)
+    o = torch.softmax(att, -1) @ v
+    return o.permute(0, 2, 1, 3).reshape(B * S, H * D), lse
+
+
+@pytest.mark.parametrize("B,S,H,D", [(2, 128, 2, 64), (1, 256, 3, 128), (2, 192, 2, 96), (1, 128, 2, 112)])
+def test_attention(ops, cuda, B, S, H, D):
+    g = torch.Generator(device=cuda).manual_seed(B * S * H * D)
+    qkv = torch.randn(B * S, 3 * H * D, device=cuda, generator=g).bfloat16()
+    out, lse = ops.attention_fwd(qkv, B, S, H, D)
+    x = qkv.float().requires_grad_()
+    ref, ref_lse = _ref_attention(x, B, S, H, D)
+    assert rel(out, ref) < 2e-2
+    assert torch.allclose(lse, ref_lse, atol=2e-3)
+    dout = torch.randn(B * S, H * D, device=cuda, generator=g).bfloat16()
+    ref.backward(dout.float())
+    dqkv = ops.attention_bwd(qkv, out, dout, lse, B, S, H, D)
+    assert rel(dqkv, x.grad) < 5e-2
+    dqkv2 = ops.attention_bwd(qkv, out, dout, lse, B, S, H, D)
+    assert torch.equal(dqkv, dqkv2)
+
+
+def test_xent(ops, cuda):
+    rows, V = 256, 1024
+    logits = torch.randn(rows, V, device=cuda).bfloat16()
+    labels = torch.randint(0, V, (rows,), device=cuda, dtype=torch.int32)
+    x = logits.float().requires_grad_()
+    ref = torch.nn.functional.cross_entropy(x, labels.long(), reduction="none")
+    ref.sum().backward()
+    work = logits.clone()
+    loss = ops.xent_fwd_bwd(work, labels, 1.0)
+    assert torch.allclose(loss, ref, atol=2e-3)
+    assert (work.float() - x.grad).abs().max().item() < 1e-2
+
+
+def test_embedding(ops, cuda):
+    B, S, W, V = 2, 64, 256, 512
+    tok = torch.randint(0, V, (B * S,), device=cuda, dtype=torch.int32)
+    wte = torch.randn(V, W, device=cuda).bfloat16()
+    wpe = torch.randn(S, W, device=cuda).bfloat16()
+    out = ops.embedding_fwd(tok, wte, wpe, B, S, 0.0, 1, 2)
+    ref = wte.float()[tok.long()] + wpe.float().repeat(B, 1)
+    assert (out.float() - ref).abs().max().item() < 3e-2
+    dout = torch.randn(B * S, W, device=cuda).bfloat16()
+    dwte = torch.zeros(V, W, device=cuda)
+    dwpe = torch.zeros(S, W, device=cuda)
+    ops.embedding_bwd(tok, dout, dwte, dwpe, B, S, 0.0, 1, 2)
+    ref_wte = torch.zeros(V, W, device=cuda).index_add_(0, tok.long(), dout.float())
+    assert torch.allclose(dwte, ref_wte, atol=1e-3)
+    assert torch.allclose(dwpe, dout.float().view(B, S, W).sum(0), atol=1e-3)
+
+
+def test_adam_and_init(ops, cuda):
+    n = 10000
+    p = torch.empty(n, device=cuda, dtype=torch.bfloat16)
+    master = torch.empty(n, device=cuda)
+    ops.init_normal(p, master, 0.02, seed=42, stream_id=3)
+    assert abs(master.std().item() - 0.02) < 2e-3
+    assert torch.equal(master, p.float())
+    g = torch.randn(n, device=cuda)
+    m = torch.zeros(n, device=cuda)
+    v = torch.zeros(n, device=cuda)
+    ref = master.clone().requires_grad_()
+    opt = torch.optim.AdamW([ref], lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+    ref.grad = g.clone()
+    opt.step()
+    ops.adam(master, p, g, m, v, lr=1e-3, beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1, step=1)
+    assert torch.allclose(master, ref.detach(), atol=1e-6)
