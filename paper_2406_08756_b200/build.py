@@ -26,6 +26,7 @@ CSRC = PKG / "csrc"
 OBJ = ROOT / "build" / "obj"
 LIB = PKG / "_lib" / "liblynx_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -63,8 +64,10 @@ def _compile(src: Path, newest_header: float) -> tuple[Path, str]:
         return obj, ""
     obj.parent.mkdir(parents=True, exist_ok=True)
     cmd = [NVCC, *_flags(), "-c", str(src), "-o", str(obj)]
-    if src.suffix == ".cpp":
-        cmd = [NVCC, "-x", "cu", *_flags(), "-c", str(src), "-o", str(obj)]
+    if src.suffix == ".cpp":  # host-only C++ (planner, runtime glue): plain g++
+        cmd = [CXX, "-O2", "-std=c++17", "-fPIC", "-g", "-Wall", "-Wextra", "-Wno-unused-parameter",
+               f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{_nlohmann_include()}", "-I/usr/local/cuda/include",
+               "-c", str(src), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stdout}\n{r.stderr}")

@@ -1,0 +1,222 @@
+"""Bit-exact parity of the native host planner against the reference oracle.
+
+The oracle is the reference's own lynx_core (oracle/_ref, pinned by the
+reference's unit/acceptance/Python suites). Every document the reference
+produces — canonical profile, plan JSON, OPT schedule JSON, partition JSON,
+simreport JSON, CSV / Chrome traces, LP text, RecomputeItem timelines, stage
+periods, memory traces — must be byte-identical.
+"""
+import json
+import random
+from fractions import Fraction
+from pathlib import Path
+
+import pytest
+
+from oracle import ref as oref
+from paper_2406_08756_b200 import gpt_profile as gp
+from paper_2406_08756_b200 import planner as pl
+
+FIX = Path("/root/reference/proj/tests/fixtures")
+GOOD = ["gpt-tiny.json", "heu-five.json", "single-stage.json", "uniform-4stage.json", "memskew.json",
+        "nvlink-like.json", "pcie-like.json"]
+
+pytestmark = pytest.mark.skipif(not oref.available(), reason="oracle/_ref not built")
+
+
+@pytest.fixture(scope="module")
+def R():
+    return oref.RefLib()
+
+
+@pytest.fixture(scope="module")
+def M():
+    return oref.ref_module()
+
+
+def need_fixtures():
+    if not FIX.exists():
+        pytest.skip("reference fixtures not present (GPU box)")
+
+
+@pytest.mark.parametrize("name", GOOD)
+def test_fixture_documents_match_reference_module(M, name):
+    need_fixtures()
+    path = str(FIX / name)
+    assert pl.serialize_profile(path) == M.serialize_profile(path)
+    assert pl.validate(path) == M.validate(path)
+    prof = json.loads((FIX / name).read_text())
+    for s in range(prof["pipeline"]["n_stages"]):
+        assert pl.schedule(path, "heu", s) == M.schedule(path, "heu", s)
+    assert pl.partition(path, "heu") == M.partition(path, "heu")
+    assert pl.simulate(path, "heu") == M.simulate(path, "heu")
+    assert pl.simulate(path, "heu", [], "1") == M.simulate(path, "heu", [], "1")
+
+
+def test_opt_schedule_matches_reference_module(M):
+    need_fixtures()
+    path = str(FIX / "single-stage.json")  # 27 phases: bounded node budget, timed_out status
+    assert pl.schedule(path, "opt", 0, 20) == M.schedule(path, "opt", 0, 20)
+
+
+SMALL_OPT = {"model": {"name": "opt-small", "n_layers": 2, "static_bytes": 4, "layer": {"ops": [
+    {"id": 0, "name": "a", "kind": "compute", "time_us": 2, "out_bytes": 4, "deps": []},
+    {"id": 1, "name": "g", "kind": "comm", "time_us": 3, "out_bytes": 2, "deps": [0]},
+    {"id": 2, "name": "ck", "kind": "compute", "time_us": "3/2", "out_bytes": 2, "deps": [1]},
+    {"id": 3, "name": "d", "kind": "compute", "time_us": 2, "out_bytes": 1, "deps": [0, 2]}],
+    "fwd_comm_ids": [], "bwd_comm_ids": [], "checkpoint_id": 2}},
+    "hardware": {"mem_budget_bytes": 14, "comm_scale": 1},
+    "pipeline": {"n_stages": 2, "n_microbatches": 2}}
+
+
+def test_opt_small_documents(M, R, tmp_path):
+    path = tmp_path / "opt-small.json"
+    path.write_text(json.dumps(SMALL_OPT))
+    for s in range(2):
+        assert pl.schedule(str(path), "opt", s, 2000) == M.schedule(str(path), "opt", s, 2000)
+    assert pl.simulate(str(path), "opt", [], "0", 2000) == M.simulate(str(path), "opt", [], "0", 2000)
+    code, out = oref.run_cli("simulate", str(path), "--mode", "opt", "--format", "csv")
+    assert code == 0 and out == pl.simulate_text(path.read_text(), "opt", None, "0", "csv", time_limit_ms=10000)
+    code, out = oref.run_cli("schedule", str(path), "--mode", "opt", "--emit-lp")
+    assert out == pl.schedule_text(path.read_text(), "opt", 0, None, emit_lp=True)[0]
+
+
+@pytest.mark.parametrize("name", GOOD)
+@pytest.mark.parametrize("fmt,fmt_id", [("csv", 1), ("chrome-trace", 2), ("report", 3)])
+def test_cli_trace_formats(R, name, fmt, fmt_id):
+    need_fixtures()
+    text = (FIX / name).read_text()
+    assert pl.simulate_text(text, "heu", None, "0", fmt) == R.simulate(text, None, "0", fmt_id)
+
+
+@pytest.mark.parametrize("name", GOOD)
+def test_cli_exit_codes_and_lp(name):
+    need_fixtures()
+    text = (FIX / name).read_text()
+    code, out = oref.run_cli("schedule", str(FIX / name), "--mode", "heu", "--emit-lp")
+    mine, st = pl.schedule_text(text, "heu", 0, None, emit_lp=True)
+    assert (code, out) == (st, mine)
+    code, out = oref.run_cli("schedule", str(FIX / name), "--mode", "heu", "--stage", "0")
+    mine, st = pl.schedule_text(text, "heu", 0)
+    assert (code, out) == (st, mine)
+
+
+def test_bad_fixtures_error_codes():
+    need_fixtures()
+    from paper_2406_08756_b200._native import LynxError
+    with pytest.raises(LynxError) as e:
+        pl.validate(str(FIX / "bad-truncated.json"))
+    assert e.value.code == 2
+    with pytest.raises(LynxError) as e:
+        pl.validate(str(FIX / "bad-cycle.json"))
+    assert e.value.code == 1
+    code, _ = oref.run_cli("validate", str(FIX / "bad-cycle.json"))
+    assert code == 1
+
+
+def gpt_profiles():
+    out = []
+    for key in ["tiny", "1.3b", "7b", "13b", "20b"]:
+        c = gp.CONFIGS[key]
+        out.append((key, gp.profile_text(c)))
+    # single-GPU 7B under the B200 budget: needs recompute
+    c = gp.GPTConfig("gpt-7b-1gpu", 32, 4096, 32, 2048, 32, 50304, 1, 1, 2, mem_budget_bytes=170_000_000_000)
+    out.append(("7b-1gpu", gp.profile_text(c)))
+    # reduced budgets (BASELINE configs 2, 4): force recompute at TP>1
+    for key, budget in [("1.3b", 24_000_000_000), ("13b", 40_000_000_000), ("7b", 60_000_000_000)]:
+        c = gp.CONFIGS[key]
+        c2 = gp.GPTConfig(**{**c.__dict__, "name": c.name + "-tight", "mem_budget_bytes": budget})
+        out.append((key + "-tight", gp.profile_text(c2)))
+    return out
+
+
+@pytest.mark.parametrize("key,text", gpt_profiles(), ids=lambda x: x if isinstance(x, str) and len(x) < 20 else "")
+def test_gpt_stage_plans_match(R, key, text):
+    prof = json.loads(text)
+    S = prof["pipeline"]["n_stages"]
+    for s in range(S):
+        try:
+            ref = R.stage_plan(text, s)
+        except RuntimeError as e:
+            with pytest.raises(Exception):
+                pl.stage_plan_text(text, s)
+            continue
+        mine = pl.stage_plan_text(text, s)
+        assert mine["plan_json"] == ref["plan_json"]
+        assert mine["timeline"] == ref["timeline"]
+        assert mine["period_us"] == ref["period_us"]
+        for base, retain in [("full", False), ("retain_all", True)]:
+            r2 = R.fixed_plan(text, s, None, retain)
+            m2 = pl.stage_plan_text(text, s, None, base)
+            assert m2["plan_json"] == r2["plan_json"]
+            assert m2["timeline"] == r2["timeline"]
+            assert m2["period_us"] == r2["period_us"]
+
+
+@pytest.mark.parametrize("key,text", gpt_profiles()[:6], ids=lambda x: x if isinstance(x, str) and len(x) < 20 else "")
+def test_gpt_simulated_ledger_matches(R, key, text):
+    """Ledger peaks, memory traces and the event timeline of the executor's plan."""
+    prof = json.loads(text)
+    S = prof["pipeline"]["n_stages"]
+    try:
+        plans = [R.stage_plan(text, s) for s in range(S)]
+    except RuntimeError:
+        pytest.skip("profile infeasible under its budget")
+    layers = plans[0]["layers_per_stage"]
+    tls = [p["timeline"] for p in plans]
+    ref = R.simulate_timelines(text, layers, tls, "0")
+    mine = pl.simulate_timelines_text(text, layers, tls, "0")
+    assert mine == ref
+
+
+def _random_profile(rng: random.Random) -> str:
+    n_fwd = rng.randint(2, 6)
+    n_bwd = rng.randint(1, 4)
+    ops = []
+    comm_fwd, comm_bwd = [], []
+    for i in range(n_fwd):
+        deps = [i - 1] if i > 0 else []
+        if i > 1 and rng.random() < 0.3:
+            deps = sorted(set(deps + [rng.randrange(0, i - 1)]))
+        kind = "comm" if 0 < i < n_fwd and len(comm_fwd) < 2 and rng.random() < 0.4 else "compute"
+        if kind == "comm":
+            comm_fwd.append(i)
+        t = Fraction(rng.randint(1, 40), rng.choice([1, 2, 3, 4, 10]))
+        ops.append({"id": i, "name": f"f{i}", "kind": kind, "time_us": f"{t.numerator}/{t.denominator}",
+                    "out_bytes": rng.choice([0, 2, 4, 8, 16]), "deps": deps})
+    if len(comm_fwd) == 1:
+        ops[comm_fwd[0]]["kind"] = "compute"
+        comm_fwd = []
+    for j in range(n_bwd):
+        i = n_fwd + j
+        deps = [i - 1] if j > 0 else []
+        deps += rng.sample(range(n_fwd), k=min(2, n_fwd))
+        kind = "comm" if j > 0 and len(comm_bwd) < 2 and rng.random() < 0.5 else "compute"
+        if kind == "comm":
+            comm_bwd.append(i)
+        ops.append({"id": i, "name": f"b{j}", "kind": kind, "time_us": rng.randint(1, 30),
+                    "out_bytes": rng.choice([0, 4, 8]), "deps": sorted(set(deps))})
+    if len(comm_bwd) == 1:
+        ops[comm_bwd[0]]["kind"] = "compute"
+        comm_bwd = []
+    stages = rng.randint(1, 4)
+    layers = rng.randint(stages, stages + 4)
+    prof = {"model": {"name": "rand", "n_layers": layers, "static_bytes": rng.randint(0, 64), "layer": {
+        "ops": ops, "fwd_comm_ids": comm_fwd, "bwd_comm_ids": comm_bwd, "checkpoint_id": n_fwd - 1}},
+        "hardware": {"mem_budget_bytes": rng.randint(40, 400), "comm_scale": rng.choice([1, "1/2", 2, "3/4"])},
+        "pipeline": {"n_stages": stages, "n_microbatches": rng.randint(stages, stages + 4)}}
+    return json.dumps(prof)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_profiles_match(R, seed):
+    rng = random.Random(seed)
+    text = _random_profile(rng)
+    try:
+        ref = R.simulate(text, None, "0", 0, 2000)
+    except RuntimeError as e:
+        with pytest.raises(Exception):
+            pl.simulate_text(text, "heu", None, "0", "json", time_limit_ms=2000)
+        return
+    assert pl.simulate_text(text, "heu", None, "0", "json", time_limit_ms=2000) == ref
+    assert pl.partition_text(text, "heu", 2000) == R.partition(text, 2000)
