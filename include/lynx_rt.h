@@ -76,6 +76,44 @@ char* lynx_plan_simulate_timelines(const char* profile_json, const int* layers, 
 char* lynx_plan_solve_heu(const char* profile_json, int stage, int stage_layers, int policy,
                           const char* delta_bytes, long long time_limit_ms, int* status);
 
+/* ---------------------------------------------------------------- 2. execute */
+
+/* One executor per (pipeline stage, TP rank) process; replaces simulate().
+ * profile_json: the profile the plan was made for (GPT block template, see
+ *   gpt_profile.py; the op names bind to kernels).
+ * timeline_json: this stage's StageRecomputeTimeline as produced by
+ *   lynx_plan_stage()["timeline"] (heusched.hpp:115-135 / report_io.hpp:46-49).
+ * config_json: {"model": {hidden, heads, seq, micro_batch, vocab},
+ *   "layers_per_stage": [...], "parallel": {tp, tp_rank, world_rank, world_size,
+ *   nccl_id (hex, from lynx_rt_nccl_unique_id on rank 0)}, "train": {dropout,
+ *   seed, lr, beta1, beta2, eps, weight_decay, init_std}, "exec": {trace,
+ *   check_recompute, elide_recompute, dry_run, head_chunk}}.
+ * Weights are initialised on the device from Philox streams keyed by seed. */
+typedef struct lynx_rt lynx_rt;
+int lynx_rt_create(const char* profile_json, const char* timeline_json, const char* config_json, lynx_rt** out);
+
+/* One training iteration: H2D of this step's tokens / labels (int32
+ * [n_microbatches * micro_batch * seq], host memory; NULL where the stage does
+ * not need them), the stage's 1F1B passes with the plan's recomputation, AdamW.
+ * Blocks until the iteration's final event; *loss = mean token loss (last stage). */
+int lynx_rt_step(lynx_rt* h, const int* tokens, const int* labels, float* loss);
+
+/* Measured report of the last step (CUDA events): iteration / busy / comm /
+ * recompute on-demand and overlapped / wait-on-recompute / exposed recompute ms,
+ * recompute launches, bit-identity check counters, pool high-water bytes. */
+char* lynx_rt_report_json(lynx_rt* h, int* status);
+/* Measured timeline of the last step (exec.trace): 0 Chrome trace JSON, 1 CSV. */
+char* lynx_rt_trace(lynx_rt* h, int format, int* status);
+/* Communication program of the last step (collectives / send / recv in issue order). */
+char* lynx_rt_program_json(lynx_rt* h, int* status);
+/* Parameter ("l0.w_qkv", "wte", ...) as bf16, or its fp32 gradient ("grad:l0.w_qkv"). */
+int lynx_rt_get_tensor(lynx_rt* h, const char* name, void* host, size_t bytes);
+/* Overwrite a parameter from fp32 host values (master and bf16 copy). */
+int lynx_rt_set_tensor(lynx_rt* h, const char* name, const void* host, size_t bytes);
+/* Hex-encoded ncclUniqueId for parallel.nccl_id (call on world rank 0). */
+int lynx_rt_nccl_unique_id(char* hex_out, size_t len);
+void lynx_rt_destroy(lynx_rt* h);
+
 #ifdef __cplusplus
 }
 #endif

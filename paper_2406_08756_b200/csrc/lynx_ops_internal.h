@@ -83,6 +83,9 @@ size_t attention_bwd_workspace(int batch, int seq, int heads);
 int adam_step(float* master, __nv_bfloat16* param, const float* grad, float* m, float* v, long long n, float lr,
               float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale, cudaStream_t s);
 int fill_f32(float* p, float v, long long n, cudaStream_t s);
+int fill_param(__nv_bfloat16* p, float* master, float v, long long n, cudaStream_t s);
+// Number of 32-bit words that differ between two device buffers (bit-identity checks).
+int count_mismatch(const void* a, const void* b, size_t bytes, unsigned long long* d_count, cudaStream_t s);
 int init_normal_bf16(__nv_bfloat16* p, float* master, long long n, float std, uint64_t seed, uint64_t stream_id,
                      cudaStream_t s);
 

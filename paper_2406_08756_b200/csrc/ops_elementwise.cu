@@ -263,6 +263,23 @@ __global__ void fill_kernel(float* p, float v, long long n) {
     p[i] = v;
 }
 
+__global__ void fill_param_kernel(__nv_bfloat16* p, float* m, float v, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    p[i] = f2bf(v);
+    if (m) m[i] = v;
+  }
+}
+
+__global__ void mismatch_kernel(const uint32_t* a, const uint32_t* b, long long n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    c += a[i] != b[i];
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 // Box-Muller on Philox draws: deterministic in (seed, stream, index).
 __global__ void init_normal_kernel(__nv_bfloat16* __restrict__ p, float* __restrict__ master, long long n, float std,
                                    uint64_t seed, uint64_t stream) {
@@ -383,6 +400,20 @@ int fill_f32(float* p, float v, long long n, cudaStream_t s) {
   if (!n) return kOk;
   fill_kernel<<<grid_for(n), kBlock, 0, s>>>(p, v, n);
   return check_launch("fill_f32");
+}
+
+int fill_param(__nv_bfloat16* p, float* master, float v, long long n, cudaStream_t s) {
+  if (!n) return kOk;
+  fill_param_kernel<<<grid_for(n), kBlock, 0, s>>>(p, master, v, n);
+  return check_launch("fill_param");
+}
+
+int count_mismatch(const void* a, const void* b, size_t bytes, unsigned long long* d_count, cudaStream_t s) {
+  const long long n = static_cast<long long>(bytes / 4);
+  if (!n) return kOk;
+  mismatch_kernel<<<grid_for(n), kBlock, 0, s>>>(static_cast<const uint32_t*>(a), static_cast<const uint32_t*>(b), n,
+                                                 d_count);
+  return check_launch("count_mismatch");
 }
 
 int init_normal_bf16(__nv_bfloat16* p, float* master, long long n, float std, uint64_t seed, uint64_t stream_id,

@@ -1,0 +1,1113 @@
+#include "runtime/executor.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <stdexcept>
+
+#include <nlohmann/json.hpp>
+
+#include "host/report.hpp"
+#include "lynx_ops_internal.h"
+
+namespace lynx::rt {
+
+using Json = nlohmann::ordered_json;
+using host::Recompute;
+
+struct RtError : std::runtime_error {
+  RtError(const std::string& w, int c) : std::runtime_error(w), code(c) {}
+  int code;
+};
+
+namespace {
+int hex_val(char c) {
+  if (c >= '0' && c <= '9') return c - '0';
+  if (c >= 'a' && c <= 'f') return c - 'a' + 10;
+  if (c >= 'A' && c <= 'F') return c - 'A' + 10;
+  return 0;
+}
+constexpr uint64_t kEmbedStream = 0xFFFFull << 32;
+}  // namespace
+
+// ============================================================ setup
+void Executor::ck(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation) throw RtError(std::string(what) + ": out of device memory", kOutOfMemory);
+  if (e != cudaSuccess) throw RtError(std::string(what) + ": " + cudaGetErrorString(e), kCudaError);
+}
+void Executor::ck_op(int status, const char* what) {
+  if (status != kOk) throw RtError(std::string(what) + ": " + last_error(), status);
+}
+void Executor::nccl(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw RtError(std::string(what) + ": " + ncclGetErrorString(r), kCudaError);
+}
+
+Executor::Executor(const std::string& profile_json, const std::string& timeline_json, const std::string& config_json) {
+  prof_ = host::parse_profile(profile_json);
+  tl_ = host::parse_timeline(timeline_json);
+  parse_config(config_json);
+  bind_template();
+  if (opt_.dry_run) return;
+  for (cudaStream_t* s : {&main_, &side_, &tp_s_, &pa_s_, &pg_s_})
+    ck(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "stream");
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "device");
+  ck(cudaDeviceGetDefaultMemPool(&pool_, dev), "mempool");
+  uint64_t thr = UINT64_MAX;
+  ck(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
+  ps_.allocate_and_init(cfg_, main_);
+  alloc_persistent();
+  ck(cudaEventCreate(&t0_), "event");
+  ck(cudaEventCreate(&t1_), "event");
+  for (int i = 0; i < cfg_.n_micro; ++i) {
+    cudaEvent_t a, b;
+    ck(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
+    act_sent_.push_back(a);
+    grad_sent_.push_back(b);
+  }
+  ck(cudaStreamSynchronize(main_), "init");
+}
+
+void Executor::parse_config(const std::string& text) {
+  Json j = Json::parse(text);
+  const Json& m = j.at("model");
+  cfg_.n_layers_total = prof_.model.n_layers;
+  cfg_.hidden = m.at("hidden");
+  cfg_.heads = m.at("heads");
+  cfg_.seq = m.at("seq");
+  cfg_.micro_batch = m.at("micro_batch");
+  cfg_.vocab = m.value("vocab", 50304);
+  cfg_.head_dim = cfg_.hidden / cfg_.heads;
+  const Json par = j.value("parallel", Json::object());
+  cfg_.tp = par.value("tp", 1);
+  cfg_.tp_rank = par.value("tp_rank", 0);
+  cfg_.pp = prof_.pipeline.n_stages;
+  cfg_.pp_rank = tl_.stage;
+  cfg_.n_micro = prof_.pipeline.n_microbatches;
+  const std::vector<int> lps = j.at("layers_per_stage").get<std::vector<int>>();
+  if (static_cast<int>(lps.size()) != cfg_.pp) throw RtError("layers_per_stage does not match n_stages", kValidation);
+  int total = 0;
+  for (int x : lps) total += x;
+  if (total != prof_.model.n_layers) throw RtError("layers_per_stage does not sum to n_layers", kValidation);
+  cfg_.layers = lps[cfg_.pp_rank];
+  cfg_.layer0 = 0;
+  for (int s = 0; s < cfg_.pp_rank; ++s) cfg_.layer0 += lps[s];
+  const Json tr = j.value("train", Json::object());
+  cfg_.dropout = tr.value("dropout", 0.1f);
+  cfg_.seed = tr.value("seed", 42ull);
+  cfg_.lr = tr.value("lr", 1e-4f);
+  cfg_.beta1 = tr.value("beta1", 0.9f);
+  cfg_.beta2 = tr.value("beta2", 0.95f);
+  cfg_.adam_eps = tr.value("eps", 1e-8f);
+  cfg_.weight_decay = tr.value("weight_decay", 0.1f);
+  cfg_.init_std = tr.value("init_std", 0.02f);
+  cfg_.ln_eps = tr.value("ln_eps", 1e-5f);
+  const Json ex = j.value("exec", Json::object());
+  opt_.trace = ex.value("trace", false);
+  opt_.check_recompute = ex.value("check_recompute", false);
+  opt_.elide_recompute = ex.value("elide_recompute", false);
+  opt_.dry_run = ex.value("dry_run", false);
+  cfg_.head_chunk = static_cast<int>(std::min<long long>(ex.value("head_chunk", 4096), cfg_.tokens()));
+  if (cfg_.hidden % cfg_.heads || cfg_.heads % cfg_.tp || (cfg_.hidden / cfg_.tp) % 128)
+    throw RtError("hidden must split into heads and TP ranks in 128-column tiles", kValidation);
+  if (cfg_.tokens() % 128 || cfg_.seq % 64 || cfg_.tokens() % cfg_.head_chunk || cfg_.head_chunk % 128)
+    throw RtError("tokens per microbatch must be a multiple of 128 and of the head chunk", kValidation);
+  if (cfg_.vocab % 128) throw RtError("vocab must be padded to a multiple of 128", kValidation);
+  ps_.layout(cfg_);
+  if (!opt_.dry_run && (cfg_.tp > 1 || cfg_.pp > 1))
+    init_comms(par.value("nccl_id", std::string()), par.value("world_rank", 0), par.value("world_size", 1));
+}
+
+void Executor::init_comms(const std::string& id_hex, int world_rank, int world_size) {
+  if (id_hex.size() != 2 * sizeof(ncclUniqueId)) throw RtError("parallel.nccl_id must be a hex ncclUniqueId", kValidation);
+  ncclUniqueId id;
+  for (size_t i = 0; i < sizeof(id); ++i)
+    id.internal[i] = static_cast<char>(hex_val(id_hex[2 * i]) * 16 + hex_val(id_hex[2 * i + 1]));
+  nccl(ncclCommInitRank(&world_, world_size, id, world_rank), "ncclCommInitRank");
+  // TP groups: ranks sharing a pipeline stage; PP groups: ranks sharing a TP rank.
+  // Activations (s -> s+1) and gradients (s+1 -> s) use separate communicators
+  // and streams, so the two directions of 1F1B never wait on each other.
+  nccl(ncclCommSplit(world_, cfg_.pp_rank, cfg_.tp_rank, &tp_comm_, nullptr), "split tp");
+  nccl(ncclCommSplit(world_, cfg_.tp_rank, cfg_.pp_rank, &pa_comm_, nullptr), "split pp act");
+  nccl(ncclCommSplit(world_, cfg_.tp_rank, cfg_.pp_rank, &pg_comm_, nullptr), "split pp grad");
+}
+
+void Executor::bind_template() {
+  const host::LayerTemplate& L = prof_.model.layer;
+  nf_ = L.n_fwd();
+  n_ = static_cast<int>(L.ops.size());
+  for (const auto& o : L.ops) {
+    const Op op = op_from_name(o.name);
+    if (op == Op::UNKNOWN)
+      throw RtError("profile op '" + o.name + "' has no B200 operator (see gpt_profile.py templates)", kValidation);
+    op_of_.push_back(op);
+    std::vector<int> d;
+    for (int id : o.deps) d.push_back(L.index_of(id));
+    deps_.push_back(d);
+  }
+  const bool tp_tmpl = !L.fwd_comm_ids.empty();
+  if (tp_tmpl != (cfg_.tp > 1)) throw RtError("profile template does not match the TP degree", kValidation);
+  static const std::vector<Op> t1 = {Op::LN1, Op::QKV, Op::ATTN, Op::PROJ_RES, Op::LN2, Op::FC1,
+                                     Op::GELU, Op::FC2_RES, Op::MLP_BWD, Op::ATTN_BWD, Op::LN1_BWD};
+  static const std::vector<Op> t2 = {Op::LN1, Op::QKV, Op::ATTN, Op::PROJ, Op::AR1, Op::LN2, Op::FC1, Op::GELU,
+                                     Op::FC2, Op::AR2, Op::MLP_BWD, Op::AR_B1, Op::ATTN_BWD, Op::AR_B2, Op::LN1_BWD};
+  if (op_of_ != (tp_tmpl ? t2 : t1)) throw RtError("profile layer template is not the GPT block template", kValidation);
+  fel_ = host::layer_elements(L, prof_.hardware, false);
+  bel_ = host::layer_elements(L, prof_.hardware, true);
+  auto elem_of = [](const std::vector<host::Element>& els, int pos) {
+    for (size_t e = 0; e < els.size(); ++e)
+      if (els[e].comm ? els[e].op == pos : std::count(els[e].ops.begin(), els[e].ops.end(), pos) > 0)
+        return static_cast<int>(e);
+    return -1;
+  };
+  made_in_.assign(nf_, -1);
+  last_fwd_use_.assign(nf_, -1);
+  last_bwd_user_.assign(nf_, -1);
+  for (int i = 0; i < nf_; ++i) made_in_[i] = elem_of(fel_, i);
+  for (int i = 0; i < n_; ++i)
+    for (int d : deps_[i]) {
+      if (i < nf_) {
+        last_fwd_use_[d] = std::max(last_fwd_use_[d], made_in_[i]);
+      } else if (d < nf_) {
+        last_bwd_user_[d] = std::max(last_bwd_user_[d], elem_of(bel_, i));
+      }
+    }
+  if (static_cast<int>(tl_.plan.retained.size()) != nf_) {
+    if (!tl_.plan.retained.empty()) throw RtError("plan retention vector does not match the layer template", kValidation);
+    tl_.plan.retained.assign(nf_, true);
+  }
+  for (const Recompute& it : tl_.items) {
+    if (it.owner_mb < 0 || it.owner_mb >= cfg_.n_micro || it.owner_layer < 0 || it.owner_layer >= cfg_.layers ||
+        it.op < 0 || it.op >= nf_)
+      throw RtError("recompute item out of range for this stage", kValidation);
+    switch (it.host) {
+      case Recompute::Host::Window: win_[{it.host_mb, it.host_bwd, it.host_layer, it.host_window}].push_back(it); break;
+      case Recompute::Host::Critical: crit_[{it.host_mb, it.host_bwd, it.host_layer, it.host_elem}].push_back(it); break;
+      case Recompute::Host::Stall: stall_[it.host_mb].push_back(it); break;
+    }
+  }
+  for (auto& kv : crit_)
+    std::stable_sort(kv.second.begin(), kv.second.end(), [](const Recompute& a, const Recompute& b) {
+      return std::tie(a.owner_mb, a.owner_layer, a.op) < std::tie(b.owner_mb, b.owner_layer, b.op);
+    });
+  slots_.assign(static_cast<size_t>(cfg_.n_micro) * cfg_.layers * nf_, Slot{});
+  stage_in_.assign(cfg_.n_micro, nullptr);
+  head_dy_.assign(cfg_.n_micro, nullptr);
+  ln_f_.assign(cfg_.n_micro, nullptr);
+  grad_.assign(cfg_.n_micro, Grad{});
+}
+
+void Executor::alloc_persistent() {
+  const long long T = cfg_.tokens(), h = cfg_.hidden, hp = cfg_.hp();
+  auto m = [&](size_t b) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, b), "scratch");
+    return p;
+  };
+  const long long wide = 4 * hp;
+  sc_main_.t_h = static_cast<__nv_bfloat16*>(m(T * h * 2));
+  sc_main_.t_h2 = static_cast<__nv_bfloat16*>(m(T * h * 2));
+  sc_main_.t_wide = static_cast<__nv_bfloat16*>(m(T * wide * 2));
+  const size_t ws = std::max({layernorm_bwd_workspace(static_cast<int>(T), static_cast<int>(h)),
+                              column_sum_workspace(T, static_cast<int>(wide)),
+                              attention_bwd_workspace(cfg_.micro_batch, cfg_.seq, cfg_.heads_rank())});
+  sc_main_.ws = static_cast<float*>(m(ws));
+  sc_main_.ws_bytes = ws;
+  if (cfg_.last()) sc_main_.logits = static_cast<__nv_bfloat16*>(m(static_cast<size_t>(cfg_.head_chunk) * cfg_.vocab * 2));
+  sc_side_.t_h = static_cast<__nv_bfloat16*>(m(T * h * 2));
+  const size_t ntok = static_cast<size_t>(cfg_.n_micro) * T;
+  d_tokens_ = static_cast<int*>(m(ntok * 4));
+  d_labels_ = static_cast<int*>(m(ntok * 4));
+  d_loss_ = static_cast<float*>(m(ntok * 4));
+  d_mismatch_ = static_cast<unsigned long long*>(m(8));
+  ck(cudaMallocHost(&h_tokens_, ntok * 4), "pinned");
+  ck(cudaMallocHost(&h_labels_, ntok * 4), "pinned");
+  ck(cudaMallocHost(&h_loss_, ntok * 4), "pinned");
+}
+
+Executor::~Executor() {
+  if (opt_.dry_run) return;
+  cudaDeviceSynchronize();
+  for (auto& s : slots_) {
+    if (s.p) cudaFree(s.p);
+    if (s.shadow) cudaFree(s.shadow);
+  }
+  ps_.release();
+  for (void* p : {static_cast<void*>(sc_main_.t_h), static_cast<void*>(sc_main_.t_h2),
+                  static_cast<void*>(sc_main_.t_wide), static_cast<void*>(sc_main_.ws),
+                  static_cast<void*>(sc_main_.logits), static_cast<void*>(sc_side_.t_h), static_cast<void*>(d_tokens_),
+                  static_cast<void*>(d_labels_), static_cast<void*>(d_loss_), static_cast<void*>(d_mismatch_)})
+    if (p) cudaFree(p);
+  cudaFreeHost(h_tokens_);
+  cudaFreeHost(h_labels_);
+  cudaFreeHost(h_loss_);
+  for (auto e : ev_pool_) cudaEventDestroy(e);
+  for (auto e : act_sent_) cudaEventDestroy(e);
+  for (auto e : grad_sent_) cudaEventDestroy(e);
+  if (t0_) cudaEventDestroy(t0_);
+  if (t1_) cudaEventDestroy(t1_);
+  for (ncclComm_t c : {tp_comm_, pa_comm_, pg_comm_, world_})
+    if (c) ncclCommDestroy(c);
+  for (cudaStream_t s : {main_, side_, tp_s_, pa_s_, pg_s_})
+    if (s) cudaStreamDestroy(s);
+  cudaMemPoolTrimTo(pool_, 0);
+}
+
+// ============================================================ tensors
+void* Executor::alloc(size_t bytes, cudaStream_t s) {
+  if (opt_.dry_run) return reinterpret_cast<void*>(0x1000);
+  void* p = nullptr;
+  ck(cudaMallocFromPoolAsync(&p, bytes, pool_, s), "activation allocation");
+  return p;
+}
+
+void Executor::release(void* p, cudaStream_t s) {
+  if (!p || opt_.dry_run) return;
+  ck(cudaFreeAsync(p, s), "activation free");
+}
+
+void Executor::mark_ready(Slot& sl, cudaStream_t s) {
+  sl.stream = s;
+  sl.ready = nullptr;
+  if (s == main_ || opt_.dry_run) return;
+  sl.ready = ev();
+  ck(cudaEventRecord(sl.ready, s), "event");
+}
+
+void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
+  if (!sl.p) return;
+  if (keep_shadow && opt_.check_recompute && !sl.shadow) {
+    sl.shadow = sl.p;  // forward-produced copy, compared against the regeneration
+  } else {
+    release(sl.p, s);
+  }
+  sl.p = nullptr;
+  sl.ready = nullptr;
+  sl.regenerated = false;
+}
+
+void* Executor::need(int mb, int l, int pos, cudaStream_t s) {
+  Slot& sl = slot(mb, l, pos);
+  if (!sl.p)
+    throw RtError("tensor " + std::string(op_name(op_of_[pos])) + " (mb " + std::to_string(mb) + ", layer " +
+                      std::to_string(l) + ") is not resident: the timeline does not regenerate it before its consumer",
+                  kParse);
+  if (sl.ready && sl.stream != s) {
+    if (s == main_) span_begin(main_, 4, mb, pos);
+    ck(cudaStreamWaitEvent(s, sl.ready, 0), "wait");
+    if (s == main_) span_end(main_);
+  }
+  return sl.p;
+}
+
+void* Executor::layer_input(int mb, int l, cudaStream_t s) {
+  if (l == 0) return stage_in_[mb];
+  const int ck_pos = nf_ - 1;  // the checkpoint is the forward sink
+  return need(mb, l - 1, ck_pos, s);
+}
+
+uint64_t Executor::drop_stream(int l, int mb, Op op) const {
+  return (static_cast<uint64_t>(cfg_.layer0 + l + 1) << 32) | (static_cast<uint64_t>(mb) << 8) |
+         static_cast<uint64_t>(op);
+}
+
+// ============================================================ timing
+cudaEvent_t Executor::ev() {
+  if (ev_next_ == ev_pool_.size()) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "event");
+    ev_pool_.push_back(e);
+  }
+  return ev_pool_[ev_next_++];
+}
+
+void Executor::span_begin(cudaStream_t s, int kind, int mb, int op) {
+  if (opt_.dry_run) return;
+  TimedSpan sp{ev(), ev(), kind, mb, op, s == side_};
+  ck(cudaEventRecord(sp.a, s), "event");
+  spans_.push_back(sp);
+  open_.emplace_back(s, spans_.size() - 1);
+}
+
+void Executor::span_end(cudaStream_t s) {
+  if (opt_.dry_run) return;
+  for (size_t i = open_.size(); i-- > 0;)
+    if (open_[i].first == s) {
+      ck(cudaEventRecord(spans_[open_[i].second].b, s), "event");
+      open_.erase(open_.begin() + static_cast<long>(i));
+      return;
+    }
+}
+
+void Executor::collect_spans() {
+  rep_.busy_ms = rep_.comm_ms = rep_.recompute_on_demand_ms = rep_.recompute_overlapped_ms = 0;
+  rep_.wait_on_recompute_ms = rep_.recv_wait_ms = 0;
+  trace_.clear();
+  for (const TimedSpan& sp : spans_) {
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, sp.a, sp.b), "elapsed");
+    switch (sp.kind) {
+      case 0: rep_.busy_ms += ms; break;
+      case 1: rep_.comm_ms += ms; break;
+      case 2: rep_.recompute_on_demand_ms += ms; break;
+      case 3: rep_.recompute_overlapped_ms += ms; break;
+      case 4: rep_.wait_on_recompute_ms += ms; break;
+      case 5: rep_.recv_wait_ms += ms; break;
+      default: break;
+    }
+    if (opt_.trace) {
+      float s0 = 0.f, s1 = 0.f;
+      cudaEventElapsedTime(&s0, t0_, sp.a);
+      cudaEventElapsedTime(&s1, t0_, sp.b);
+      trace_.emplace_back(cfg_.pp_rank, sp.mb, sp.kind, sp.op, 1e3 * s0, 1e3 * s1);
+    }
+  }
+}
+
+// ============================================================ forward operators
+void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
+  const Op op = op_of_[pos];
+  Slot& out = slot(mb, l, pos);
+  if (out.p) {
+    if (recompute) return;  // already resident (duplicate placement)
+    throw RtError("forward tensor produced twice", kParse);
+  }
+  const long long T = cfg_.tokens();
+  const int h = cfg_.hidden, hp = cfg_.hp();
+  const LayerParams P = opt_.dry_run ? LayerParams{} : ps_.layer(l);
+  Scratch& sc = s == side_ ? sc_side_ : sc_main_;
+  const float p = cfg_.dropout;
+  const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
+  auto gemm = [&](const void* a, long long lda, const void* b, long long ldb, void* c, long long ldc, long long M,
+                  long long N, long long K, const __nv_bfloat16* bias) {
+    if (opt_.dry_run) return;
+    GemmDesc g{a, lda, false, b, ldb, false, c, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
+               bias, EPI_BF16};
+    ck_op(gemm_run(g, s), "gemm");
+  };
+  auto pos_of = [&](Op o) {
+    for (int i = 0; i < nf_; ++i)
+      if (op_of_[i] == o) return i;
+    return -1;
+  };
+  size_t bytes = 2 * T * h;
+  void *in = nullptr, *x = nullptr;
+  switch (op) {
+    case Op::LN1:
+      bytes = 2 * T * h + 8 * T;
+      x = layer_input(mb, l, s);
+      break;
+    case Op::QKV:
+      bytes = 2 * T * 3 * hp;
+      in = need(mb, l, pos_of(Op::LN1), s);
+      break;
+    case Op::ATTN:
+      bytes = 2 * T * hp + 4LL * cfg_.micro_batch * cfg_.heads_rank() * cfg_.seq;
+      in = need(mb, l, pos_of(Op::QKV), s);
+      break;
+    case Op::PROJ: in = need(mb, l, pos_of(Op::ATTN), s); break;
+    case Op::PROJ_RES:
+      in = need(mb, l, pos_of(Op::ATTN), s);
+      x = layer_input(mb, l, s);
+      break;
+    case Op::LN2:
+      bytes = 2 * T * h + 8 * T;
+      in = need(mb, l, pos_of(cfg_.tp > 1 ? Op::AR1 : Op::PROJ_RES), s);
+      break;
+    case Op::FC1:
+      bytes = 2 * T * 4 * hp;
+      in = need(mb, l, pos_of(Op::LN2), s);
+      break;
+    case Op::GELU:
+      bytes = 2 * T * 4 * hp;
+      in = need(mb, l, pos_of(Op::FC1), s);
+      break;
+    case Op::FC2: in = need(mb, l, pos_of(Op::GELU), s); break;
+    case Op::FC2_RES:
+      in = need(mb, l, pos_of(Op::GELU), s);
+      x = need(mb, l, pos_of(Op::PROJ_RES), s);
+      break;
+    default: throw RtError(std::string("operator ") + op_name(op) + " is not a compute forward op", kParse);
+  }
+  out.p = alloc(bytes, s);
+  out.bytes = bytes;
+  if (recompute) ++rep_.recompute_launches;
+  if (!opt_.dry_run) {
+    auto* o = static_cast<__nv_bfloat16*>(out.p);
+    switch (op) {
+      case Op::LN1:
+      case Op::LN2: {
+        auto* mean = reinterpret_cast<float*>(static_cast<char*>(out.p) + 2 * T * h);
+        const auto* src = static_cast<const __nv_bfloat16*>(op == Op::LN1 ? x : in);
+        ck_op(layernorm_fwd(src, op == Op::LN1 ? P.ln1_g : P.ln2_g, op == Op::LN1 ? P.ln1_b : P.ln2_b, o, mean,
+                            mean + T, static_cast<int>(T), h, cfg_.ln_eps, s),
+              "layernorm");
+        break;
+      }
+      case Op::QKV: gemm(in, h, P.w_qkv, h, o, 3 * hp, T, 3 * hp, h, P.b_qkv); break;
+      case Op::ATTN: {
+        auto* lse = reinterpret_cast<float*>(static_cast<char*>(out.p) + 2 * T * hp);
+        ck_op(attention_fwd(static_cast<const __nv_bfloat16*>(in), o, lse, cfg_.micro_batch, cfg_.seq,
+                            cfg_.heads_rank(), cfg_.head_dim, s),
+              "attention");
+        break;
+      }
+      case Op::PROJ: gemm(in, hp, P.w_proj, hp, o, h, T, h, hp, nullptr); break;
+      case Op::PROJ_RES:
+        gemm(in, hp, P.w_proj, hp, sc.t_h, h, T, h, hp, P.b_proj);
+        ck_op(bias_dropout_residual_fwd(sc.t_h, nullptr, static_cast<const __nv_bfloat16*>(x), o, T, h, p, seed,
+                                        drop_stream(l, mb, Op::PROJ_RES), s),
+              "residual");
+        break;
+      case Op::FC1: gemm(in, h, P.w_fc1, h, o, 4 * hp, T, 4 * hp, h, P.b_fc1); break;
+      case Op::GELU: ck_op(gelu_fwd(static_cast<const __nv_bfloat16*>(in), o, T * 4 * hp, s), "gelu"); break;
+      case Op::FC2: gemm(in, 4 * hp, P.w_fc2, 4 * hp, o, h, T, h, 4 * hp, nullptr); break;
+      case Op::FC2_RES:
+        gemm(in, 4 * hp, P.w_fc2, 4 * hp, sc.t_h, h, T, h, 4 * hp, P.b_fc2);
+        ck_op(bias_dropout_residual_fwd(sc.t_h, nullptr, static_cast<const __nv_bfloat16*>(x), o, T, h, p, seed,
+                                        drop_stream(l, mb, Op::FC2_RES), s),
+              "residual");
+        break;
+      default: break;
+    }
+  }
+  mark_ready(out, s);
+  if (recompute) {
+    out.regenerated = true;
+    if (opt_.check_recompute && out.shadow && !opt_.dry_run) {
+      ck(cudaMemsetAsync(d_mismatch_, 0, 8, s), "memset");
+      ck_op(count_mismatch(out.p, out.shadow, bytes, d_mismatch_, s), "compare");
+      unsigned long long mism = 0;
+      ck(cudaMemcpyAsync(&mism, d_mismatch_, 8, cudaMemcpyDeviceToHost, s), "copy");
+      ck(cudaStreamSynchronize(s), "sync");
+      rep_.recompute_mismatch_words += static_cast<long long>(mism);
+      ++rep_.recompute_checked;
+      release(out.shadow, s);
+      out.shadow = nullptr;
+    }
+  }
+}
+
+void Executor::run_items(const std::vector<Recompute>& items, cudaStream_t s, int span_kind) {
+  if (items.empty() || opt_.elide_recompute) return;
+  span_begin(s, span_kind, items.front().owner_mb, items.front().op);
+  for (const Recompute& it : items) {
+    const Op op = op_of_[it.op];
+    if (op == Op::AR1 || op == Op::AR2) {
+      // A discarded all-reduce output is only ever regenerated on the critical
+      // path (heusched.cpp:125): re-issue its producer, then the collective.
+      if (slot(it.owner_mb, it.owner_layer, it.op).p) continue;
+      const int prod = it.op - 1;  // PROJ / FC2 precede their all-reduce
+      fwd_op(it.owner_mb, it.owner_layer, prod, main_, true);
+      host::Element e;
+      e.comm = true;
+      e.op = it.op;
+      comm_element(it.owner_mb, false, it.owner_layer, e);
+      slot(it.owner_mb, it.owner_layer, it.op).regenerated = true;
+      continue;
+    }
+    fwd_op(it.owner_mb, it.owner_layer, it.op, s, true);
+  }
+  span_end(s);
+}
+
+void Executor::run_critical(const Key4& key) {
+  auto f = crit_.find(key);
+  if (f != crit_.end()) run_items(f->second, main_, 2);
+}
+
+// TP all-reduce element. Window items of (mb, bwd, l, window) are released on
+// the side stream at the same instant, so their kernels overlap the NCCL transfer.
+void Executor::comm_element(int mb, bool bwd, int l, const host::Element& e) {
+  const Op op = op_of_[e.op];
+  const long long T = cfg_.tokens();
+  const int h = cfg_.hidden;
+  void* buf = nullptr;
+  auto pos_of = [&](Op o) {
+    for (int i = 0; i < n_; ++i)
+      if (op_of_[i] == o) return i;
+    return -1;
+  };
+  if (op == Op::AR1) buf = need(mb, l, pos_of(Op::PROJ), main_);
+  if (op == Op::AR2) buf = need(mb, l, pos_of(Op::FC2), main_);
+  if (op == Op::AR_B1) buf = grad_[mb].dln2;
+  if (op == Op::AR_B2) buf = grad_[mb].dln1;
+  program_.push_back({"allreduce", "tp", -1, static_cast<size_t>(T * h * 2),
+                      std::string(op_name(op)) + " mb" + std::to_string(mb) + " l" + std::to_string(l)});
+  cudaEvent_t go = nullptr;
+  if (!opt_.dry_run) {
+    go = ev();
+    ck(cudaEventRecord(go, main_), "event");
+    ck(cudaStreamWaitEvent(tp_s_, go, 0), "wait");
+  }
+  // window items (the reference packs them from the comm start, pipesim.cpp:398-424)
+  if (e.window >= 0) {
+    auto w = win_.find({mb, bwd, l, e.window});
+    if (w != win_.end() && !opt_.elide_recompute) {
+      if (!opt_.dry_run) ck(cudaStreamWaitEvent(side_, go, 0), "wait");
+      run_items(w->second, side_, 3);
+    }
+  }
+  if (!opt_.dry_run) {
+    span_begin(tp_s_, 1, mb, e.op);
+    nccl(ncclAllReduce(buf, buf, static_cast<size_t>(T * h), ncclBfloat16, ncclSum, tp_comm_, tp_s_), "allreduce");
+    span_end(tp_s_);
+    cudaEvent_t done = ev();
+    ck(cudaEventRecord(done, tp_s_), "event");
+    ck(cudaStreamWaitEvent(main_, done, 0), "wait");
+  }
+  if (bwd) return;  // backward partials are reduced in place
+  // forward: bias + dropout + residual epilogue produces the op's tensor
+  Slot& out = slot(mb, l, e.op);
+  out.p = alloc(2 * T * h, main_);
+  out.bytes = 2 * T * h;
+  const void* resid = op == Op::AR1 ? layer_input(mb, l, main_) : need(mb, l, pos_of(Op::AR1), main_);
+  if (!opt_.dry_run) {
+    const LayerParams P = ps_.layer(l);
+    const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
+    ck_op(bias_dropout_residual_fwd(static_cast<const __nv_bfloat16*>(buf), op == Op::AR1 ? P.b_proj : P.b_fc2,
+                                    static_cast<const __nv_bfloat16*>(resid), static_cast<__nv_bfloat16*>(out.p), T, h,
+                                    cfg_.dropout, seed, drop_stream(l, mb, op), main_),
+          "residual");
+  }
+  mark_ready(out, main_);
+  // the partial (PROJ / FC2, 0 bytes in the profile) is consumed
+  Slot& part = slot(mb, l, pos_of(op == Op::AR1 ? Op::PROJ : Op::FC2));
+  release(part.p, main_);
+  part.p = nullptr;
+}
+
+// ============================================================ backward operators
+void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
+  const Op op = op_of_[pos];
+  const long long T = cfg_.tokens();
+  const int h = cfg_.hidden, hp = cfg_.hp();
+  const LayerParams P = opt_.dry_run ? LayerParams{} : ps_.layer(l);
+  Scratch& sc = sc_main_;
+  const float p = cfg_.dropout;
+  const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
+  Grad& G = grad_[mb];
+  auto gemm = [&](const void* a, long long lda, bool amn, const void* b, long long ldb, bool bmn, void* c, long long ldc,
+                  long long M, long long N, long long K, int epi) {
+    if (opt_.dry_run) return;
+    GemmDesc g{a, lda, amn, b, ldb, bmn, c, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), nullptr,
+               epi};
+    ck_op(gemm_run(g, s), "gemm");
+  };
+  auto pos_of = [&](Op o) {
+    for (int i = 0; i < nf_; ++i)
+      if (op_of_[i] == o) return i;
+    return -1;
+  };
+  auto colsum = [&](const void* x, float* acc, long long width) {
+    if (!opt_.dry_run)
+      ck_op(column_sum_acc(static_cast<const __nv_bfloat16*>(x), acc, sc.ws, T, static_cast<int>(width), s), "colsum");
+  };
+  const bool tp = cfg_.tp > 1;
+  switch (op) {
+    case Op::MLP_BWD: {
+      void* gelu = need(mb, l, pos_of(Op::GELU), s);
+      void* fc1 = need(mb, l, pos_of(Op::FC1), s);
+      void* y2 = need(mb, l, pos_of(Op::LN2), s);
+      if (!opt_.dry_run)
+        ck_op(dropout_bwd(static_cast<const __nv_bfloat16*>(G.dy), sc.t_h, T, h, p, seed,
+                          drop_stream(l, mb, tp ? Op::AR2 : Op::FC2_RES), s),
+              "dropout_bwd");
+      colsum(sc.t_h, P.g_b_fc2, h);
+      gemm(sc.t_h, h, true, gelu, 4 * hp, true, P.g_w_fc2, 4 * hp, h, 4 * hp, T, EPI_ACC_F32);   // dW_fc2 += d^T gelu
+      gemm(sc.t_h, h, false, P.w_fc2, 4 * hp, true, sc.t_wide, 4 * hp, T, 4 * hp, h, EPI_BF16);  // dgelu = d W_fc2
+      if (!opt_.dry_run)
+        ck_op(gelu_bwd(sc.t_wide, static_cast<const __nv_bfloat16*>(fc1), sc.t_wide, T * 4 * hp, s), "gelu_bwd");
+      colsum(sc.t_wide, P.g_b_fc1, 4 * hp);
+      gemm(sc.t_wide, 4 * hp, true, y2, h, true, P.g_w_fc1, h, 4 * hp, h, T, EPI_ACC_F32);     // dW_fc1 += dfc1^T y2
+      G.dln2 = alloc(T * h * 2, s);
+      gemm(sc.t_wide, 4 * hp, false, P.w_fc1, h, true, G.dln2, h, T, h, 4 * hp, EPI_BF16);     // dln2 = dfc1 W_fc1
+      break;
+    }
+    case Op::ATTN_BWD: {
+      void* res1 = need(mb, l, pos_of(tp ? Op::AR1 : Op::PROJ_RES), s);
+      void* ln2 = need(mb, l, pos_of(Op::LN2), s);
+      void* attn = need(mb, l, pos_of(Op::ATTN), s);
+      void* qkv = need(mb, l, pos_of(Op::QKV), s);
+      void* ln1 = need(mb, l, pos_of(Op::LN1), s);
+      const auto* mean2 = reinterpret_cast<const float*>(static_cast<char*>(ln2) + 2 * T * h);
+      const auto* lse = reinterpret_cast<const float*>(static_cast<char*>(attn) + 2 * T * hp);
+      G.dres = alloc(T * h * 2, s);
+      if (!opt_.dry_run) {
+        ck_op(layernorm_bwd(static_cast<const __nv_bfloat16*>(G.dln2), static_cast<const __nv_bfloat16*>(res1),
+                            P.ln2_g, mean2, mean2 + T, static_cast<const __nv_bfloat16*>(G.dy),
+                            static_cast<__nv_bfloat16*>(G.dres), P.g_ln2_g, P.g_ln2_b, sc.ws, static_cast<int>(T), h, s),
+              "ln2_bwd");
+        ck_op(dropout_bwd(static_cast<const __nv_bfloat16*>(G.dres), sc.t_h, T, h, p, seed,
+                          drop_stream(l, mb, tp ? Op::AR1 : Op::PROJ_RES), s),
+              "dropout_bwd");
+      }
+      release(G.dln2, s);
+      G.dln2 = nullptr;
+      colsum(sc.t_h, P.g_b_proj, h);
+      gemm(sc.t_h, h, true, attn, hp, true, P.g_w_proj, hp, h, hp, T, EPI_ACC_F32);        // dW_proj += d^T O
+      gemm(sc.t_h, h, false, P.w_proj, hp, true, sc.t_h2, hp, T, hp, h, EPI_BF16);         // dO = d W_proj
+      if (!opt_.dry_run)
+        ck_op(attention_bwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(attn), sc.t_h2,
+                            lse, sc.t_wide, sc.ws, cfg_.micro_batch, cfg_.seq, cfg_.heads_rank(), cfg_.head_dim, s),
+              "attention_bwd");
+      colsum(sc.t_wide, P.g_b_qkv, 3 * hp);
+      gemm(sc.t_wide, 3 * hp, true, ln1, h, true, P.g_w_qkv, h, 3 * hp, h, T, EPI_ACC_F32);  // dW_qkv += dqkv^T y1
+      G.dln1 = alloc(T * h * 2, s);
+      gemm(sc.t_wide, 3 * hp, false, P.w_qkv, h, true, G.dln1, h, T, h, 3 * hp, EPI_BF16);   // dln1 = dqkv W_qkv
+      break;
+    }
+    case Op::LN1_BWD: {
+      void* ln1 = need(mb, l, pos_of(Op::LN1), s);
+      const auto* mean1 = reinterpret_cast<const float*>(static_cast<char*>(ln1) + 2 * T * h);
+      void* x = layer_input(mb, l, s);
+      void* dx = alloc(T * h * 2, s);
+      if (!opt_.dry_run)
+        ck_op(layernorm_bwd(static_cast<const __nv_bfloat16*>(G.dln1), static_cast<const __nv_bfloat16*>(x), P.ln1_g,
+                            mean1, mean1 + T, static_cast<const __nv_bfloat16*>(G.dres), static_cast<__nv_bfloat16*>(dx),
+                            P.g_ln1_g, P.g_ln1_b, sc.ws, static_cast<int>(T), h, s),
+              "ln1_bwd");
+      release(G.dln1, s);
+      release(G.dres, s);
+      release(G.dy, s);  // the layer-output gradient is fully consumed
+      G.dln1 = G.dres = nullptr;
+      G.dy = dx;  // gradient sink -> the next (lower) layer's output gradient
+      break;
+    }
+    default: throw RtError(std::string("operator ") + op_name(op) + " is not a compute backward op", kParse);
+  }
+}
+
+// ============================================================ head / embedding
+void Executor::head_forward(int mb) {
+  const long long T = cfg_.tokens();
+  const int h = cfg_.hidden, V = cfg_.vocab, C = cfg_.head_chunk;
+  void* x = need(mb, cfg_.layers - 1, nf_ - 1, main_);
+  ln_f_[mb] = alloc(2 * T * h + 8 * T, main_);
+  head_dy_[mb] = alloc(2 * T * h, main_);
+  if (opt_.dry_run) return;
+  auto* y = static_cast<__nv_bfloat16*>(ln_f_[mb]);
+  auto* mean = reinterpret_cast<float*>(static_cast<char*>(ln_f_[mb]) + 2 * T * h);
+  ck_op(layernorm_fwd(static_cast<const __nv_bfloat16*>(x), ps_.p("lnf_g"), ps_.p("lnf_b"), y, mean, mean + T,
+                      static_cast<int>(T), h, cfg_.ln_eps, main_),
+        "final_ln");
+  const __nv_bfloat16* w = ps_.p("w_head");
+  float* gw = ps_.g("w_head");
+  const float scale = 1.0f / static_cast<float>(T * cfg_.n_micro);
+  for (long long c0 = 0; c0 < T; c0 += C) {
+    const __nv_bfloat16* yc = y + c0 * h;
+    GemmDesc lg{yc, h, false, w, h, false, sc_main_.logits, V, C, V, h, nullptr, EPI_BF16};
+    ck_op(gemm_run(lg, main_), "lm_head");
+    ck_op(xent_fwd_bwd(sc_main_.logits, d_labels_ + mb * T + c0, d_loss_ + mb * T + c0, C, V, scale, main_), "xent");
+    GemmDesc dw{sc_main_.logits, V, true, yc, h, true, gw, h, V, h, C, nullptr, EPI_ACC_F32};
+    ck_op(gemm_run(dw, main_), "lm_head dW");
+    GemmDesc dx{sc_main_.logits, V, false, w, h, true, static_cast<__nv_bfloat16*>(head_dy_[mb]) + c0 * h, h, C, h, V,
+                nullptr, EPI_BF16};
+    ck_op(gemm_run(dx, main_), "lm_head dX");
+  }
+}
+
+void Executor::head_backward(int mb) {
+  const long long T = cfg_.tokens();
+  const int h = cfg_.hidden;
+  void* x = need(mb, cfg_.layers - 1, nf_ - 1, main_);
+  grad_[mb].dy = alloc(2 * T * h, main_);
+  if (!opt_.dry_run) {
+    const auto* mean = reinterpret_cast<const float*>(static_cast<char*>(ln_f_[mb]) + 2 * T * h);
+    ck_op(layernorm_bwd(static_cast<const __nv_bfloat16*>(head_dy_[mb]), static_cast<const __nv_bfloat16*>(x),
+                        ps_.p("lnf_g"), mean, mean + T, nullptr, static_cast<__nv_bfloat16*>(grad_[mb].dy),
+                        ps_.g("lnf_g"), ps_.g("lnf_b"), sc_main_.ws, static_cast<int>(T), h, main_),
+          "final_ln_bwd");
+  }
+  release(head_dy_[mb], main_);
+  release(ln_f_[mb], main_);
+  head_dy_[mb] = ln_f_[mb] = nullptr;
+}
+
+// ============================================================ passes
+void Executor::forward_pass(int mb) {
+  const long long T = cfg_.tokens();
+  const int h = cfg_.hidden;
+  const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
+  stage_in_[mb] = alloc(2 * T * h, main_);
+  if (cfg_.first()) {
+    if (!opt_.dry_run)
+      ck_op(embedding_fwd(d_tokens_ + mb * T, ps_.p("wte"), ps_.p("wpe"), static_cast<__nv_bfloat16*>(stage_in_[mb]),
+                          cfg_.micro_batch, cfg_.seq, h, cfg_.dropout, seed, kEmbedStream | mb, main_),
+            "embedding");
+  } else {
+    program_.push_back({"recv", "pp_act", cfg_.pp_rank - 1, static_cast<size_t>(2 * T * h), "F mb" + std::to_string(mb)});
+    if (!opt_.dry_run) {
+      cudaEvent_t a = ev();
+      ck(cudaEventRecord(a, main_), "event");  // buffer allocated on main
+      ck(cudaStreamWaitEvent(pa_s_, a, 0), "wait");
+      nccl(ncclRecv(stage_in_[mb], static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank - 1, pa_comm_, pa_s_), "recv");
+      cudaEvent_t b = ev();
+      ck(cudaEventRecord(b, pa_s_), "event");
+      span_begin(main_, 5, mb);
+      ck(cudaStreamWaitEvent(main_, b, 0), "wait");
+      span_end(main_);
+    }
+  }
+  span_begin(main_, 0, mb);
+  for (int l = 0; l < cfg_.layers; ++l) {
+    for (size_t ei = 0; ei < fel_.size(); ++ei) {
+      const host::Element& e = fel_[ei];
+      run_critical({mb, false, l, static_cast<int>(ei)});
+      if (e.comm) {
+        comm_element(mb, false, l, e);
+      } else {
+        for (int pos : e.ops) fwd_op(mb, l, pos, main_, false);
+      }
+      // discarded tensors drop after their last forward consumer (pipesim.cpp:496-504)
+      for (int i = 0; i < nf_; ++i)
+        if (!tl_.plan.retained[i] && std::max(made_in_[i], last_fwd_use_[i]) == static_cast<int>(ei))
+          drop(slot(mb, l, i), main_, true);
+    }
+  }
+  if (cfg_.last()) {
+    head_forward(mb);
+  } else {
+    void* out = need(mb, cfg_.layers - 1, nf_ - 1, main_);
+    program_.push_back({"send", "pp_act", cfg_.pp_rank + 1, static_cast<size_t>(2 * T * h), "F mb" + std::to_string(mb)});
+    if (!opt_.dry_run) {
+      cudaEvent_t a = ev();
+      ck(cudaEventRecord(a, main_), "event");
+      ck(cudaStreamWaitEvent(pa_s_, a, 0), "wait");
+      nccl(ncclSend(out, static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank + 1, pa_comm_, pa_s_), "send");
+      ck(cudaEventRecord(act_sent_[mb], pa_s_), "event");
+    }
+  }
+  span_end(main_);
+}
+
+void Executor::backward_pass(int mb) {
+  const long long T = cfg_.tokens();
+  const int h = cfg_.hidden;
+  // cool-down stall fill: released before the gradient arrives (pipesim.cpp:620-646)
+  auto st = stall_.find(mb);
+  if (st != stall_.end() && !opt_.elide_recompute) {
+    if (!opt_.dry_run) {
+      cudaEvent_t a = ev();
+      ck(cudaEventRecord(a, main_), "event");
+      ck(cudaStreamWaitEvent(side_, a, 0), "wait");
+    }
+    run_items(st->second, side_, 3);
+  }
+  if (cfg_.last()) {
+    head_backward(mb);
+  } else {
+    grad_[mb].dy = alloc(2 * T * h, main_);
+    program_.push_back({"recv", "pp_grad", cfg_.pp_rank + 1, static_cast<size_t>(2 * T * h), "B mb" + std::to_string(mb)});
+    if (!opt_.dry_run) {
+      cudaEvent_t a = ev();
+      ck(cudaEventRecord(a, main_), "event");
+      ck(cudaStreamWaitEvent(pg_s_, a, 0), "wait");
+      nccl(ncclRecv(grad_[mb].dy, static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank + 1, pg_comm_, pg_s_), "recv");
+      cudaEvent_t b = ev();
+      ck(cudaEventRecord(b, pg_s_), "event");
+      span_begin(main_, 5, mb);
+      ck(cudaStreamWaitEvent(main_, b, 0), "wait");
+      span_end(main_);
+    }
+  }
+  span_begin(main_, 0, mb);
+  for (int l = cfg_.layers - 1; l >= 0; --l) {
+    for (size_t ei = 0; ei < bel_.size(); ++ei) {
+      const host::Element& e = bel_[ei];
+      run_critical({mb, true, l, static_cast<int>(ei)});
+      if (e.comm) {
+        comm_element(mb, true, l, e);
+      } else {
+        for (int pos : e.ops) bwd_op(mb, l, pos, main_);
+      }
+      // retained / regenerated tensors drop after their last backward consumer
+      for (int i = 0; i < nf_; ++i)
+        if (last_bwd_user_[i] == static_cast<int>(ei)) drop(slot(mb, l, i), main_, false);
+    }
+    // end-of-layer sweep (pipesim.cpp:546-569): everything else of (mb, l)
+    if (l == cfg_.layers - 1 && !cfg_.last() && !opt_.dry_run)
+      ck(cudaStreamWaitEvent(main_, act_sent_[mb], 0), "wait");  // the activation send read it
+    for (int i = 0; i < nf_; ++i) {
+      Slot& sl = slot(mb, l, i);
+      drop(sl, main_, false);
+      if (sl.shadow) {
+        release(sl.shadow, main_);
+        sl.shadow = nullptr;
+      }
+    }
+  }
+  void* dx = grad_[mb].dy;
+  if (cfg_.first()) {
+    if (!opt_.dry_run) {
+      void* ws = alloc(static_cast<size_t>(T) * h * 4, main_);
+      const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
+      ck_op(embedding_bwd(d_tokens_ + mb * T, static_cast<const __nv_bfloat16*>(dx), ps_.g("wte"), ps_.g("wpe"),
+                          static_cast<float*>(ws), cfg_.micro_batch, cfg_.seq, h, cfg_.vocab, cfg_.dropout, seed,
+                          kEmbedStream | mb, main_),
+            "embedding_bwd");
+      release(ws, main_);
+    }
+    release(dx, main_);
+  } else {
+    program_.push_back({"send", "pp_grad", cfg_.pp_rank - 1, static_cast<size_t>(2 * T * h), "B mb" + std::to_string(mb)});
+    if (!opt_.dry_run) {
+      cudaEvent_t a = ev();
+      ck(cudaEventRecord(a, main_), "event");
+      ck(cudaStreamWaitEvent(pg_s_, a, 0), "wait");
+      nccl(ncclSend(dx, static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank - 1, pg_comm_, pg_s_), "send");
+      ck(cudaEventRecord(grad_sent_[mb], pg_s_), "event");
+    }
+    release(dx, pg_s_);  // stream-ordered after the send; main never waits on the peer
+  }
+  grad_[mb].dy = nullptr;
+  release(stage_in_[mb], main_);
+  stage_in_[mb] = nullptr;
+  span_end(main_);
+}
+
+// ============================================================ step
+void Executor::step(const int* tokens, const int* labels, float* loss_out) {
+  ++step_;
+  ev_next_ = 0;
+  spans_.clear();
+  open_.clear();
+  program_.clear();
+  rep_ = StepReport{};
+  const long long T = cfg_.tokens();
+  const size_t ntok = static_cast<size_t>(cfg_.n_micro) * T;
+  const auto passes = host::stage_passes(cfg_.pp, cfg_.pp_rank, cfg_.n_micro);
+  if (opt_.dry_run) {
+    for (auto [bwd, mb] : passes) bwd ? backward_pass(mb) : forward_pass(mb);
+    return;
+  }
+  ck(cudaEventRecord(t0_, main_), "event");
+  if (cfg_.first() && tokens) {
+    std::memcpy(h_tokens_, tokens, ntok * 4);
+    ck(cudaMemcpyAsync(d_tokens_, h_tokens_, ntok * 4, cudaMemcpyHostToDevice, main_), "h2d tokens");
+  }
+  if (cfg_.last() && labels) {
+    std::memcpy(h_labels_, labels, ntok * 4);
+    ck(cudaMemcpyAsync(d_labels_, h_labels_, ntok * 4, cudaMemcpyHostToDevice, main_), "h2d labels");
+  }
+  ck(cudaMemsetAsync(ps_.grad, 0, static_cast<size_t>(ps_.count()) * 4, main_), "zero grads");
+  for (auto [bwd, mb] : passes) bwd ? backward_pass(mb) : forward_pass(mb);
+  ck(cudaStreamWaitEvent(main_, [&] {
+       cudaEvent_t e = ev();
+       ck(cudaEventRecord(e, side_), "event");
+       return e;
+     }(), 0),
+     "join side");
+  ck_op(adam_step(ps_.master, ps_.param, ps_.grad, ps_.m, ps_.v, ps_.count(), cfg_.lr, cfg_.beta1, cfg_.beta2,
+                  cfg_.adam_eps, cfg_.weight_decay, step_, 1.0f, main_),
+        "adam");
+  if (cfg_.last()) ck(cudaMemcpyAsync(h_loss_, d_loss_, ntok * 4, cudaMemcpyDeviceToHost, main_), "d2h loss");
+  ck(cudaEventRecord(t1_, main_), "event");
+  ck(cudaEventSynchronize(t1_), "step");
+  float ms = 0.f;
+  ck(cudaEventElapsedTime(&ms, t0_, t1_), "elapsed");
+  rep_.step_ms = ms;
+  collect_spans();
+  if (cfg_.last()) {
+    double s = 0;
+    for (size_t i = 0; i < ntok; ++i) s += h_loss_[i];
+    rep_.loss = s / static_cast<double>(ntok);
+  }
+  if (loss_out) *loss_out = static_cast<float>(rep_.loss);
+  size_t hw = 0;
+  cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &hw);
+  rep_.pool_high_water = hw;
+}
+
+// ============================================================ reports
+std::string Executor::report_json() const {
+  Json j;
+  j["stage"] = cfg_.pp_rank;
+  j["tp_rank"] = cfg_.tp_rank;
+  j["step"] = step_;
+  j["iteration_ms"] = rep_.step_ms;
+  j["busy_ms"] = rep_.busy_ms;
+  j["comm_ms"] = rep_.comm_ms;
+  j["recv_wait_ms"] = rep_.recv_wait_ms;
+  j["recompute_on_demand_ms"] = rep_.recompute_on_demand_ms;
+  j["recompute_overlapped_ms"] = rep_.recompute_overlapped_ms;
+  j["wait_on_recompute_ms"] = rep_.wait_on_recompute_ms;
+  j["exposed_recompute_ms"] = rep_.recompute_on_demand_ms + rep_.wait_on_recompute_ms;
+  j["recompute_launches"] = rep_.recompute_launches;
+  j["recompute_checked"] = rep_.recompute_checked;
+  j["recompute_mismatch_words"] = rep_.recompute_mismatch_words;
+  j["loss"] = rep_.loss;
+  j["pool_high_water_bytes"] = rep_.pool_high_water;
+  j["static_bytes_allocated"] = static_cast<long long>(ps_.count()) * 18;
+  j["params"] = ps_.count();
+  j["layers"] = cfg_.layers;
+  j["microbatches"] = cfg_.n_micro;
+  j["tokens_per_microbatch"] = cfg_.tokens();
+  return j.dump();
+}
+
+std::string Executor::trace(int format) const {
+  static const char* kinds[] = {"pass", "comm", "recompute", "recompute_overlapped", "wait_recompute", "recv_wait"};
+  std::ostringstream os;
+  if (format == 1) {
+    os << "stage,microbatch,kind,op_id,start_us,end_us\n";
+    for (const auto& [st, mb, k, op, a, b] : trace_)
+      os << st << "," << mb << "," << kinds[k] << "," << (op < 0 ? "" : std::to_string(op)) << "," << a << "," << b
+         << "\n";
+    return os.str();
+  }
+  os << "[";
+  bool first = true;
+  for (const auto& [st, mb, k, op, a, b] : trace_) {
+    if (!first) os << ",";
+    first = false;
+    os << "\n  {\"name\": \"" << kinds[k];
+    if (mb >= 0) os << " mb" << mb;
+    if (op >= 0) os << " op" << op;
+    os << "\", \"ph\": \"X\", \"pid\": " << st << ", \"tid\": \"" << (k == 1 ? "comm" : (k == 3 ? "side" : "compute"))
+       << "\", \"ts\": " << a << ", \"dur\": " << (b - a) << "}";
+  }
+  os << "\n]\n";
+  return os.str();
+}
+
+std::string Executor::program_json() const {
+  Json a = Json::array();
+  for (const CommOp& c : program_) {
+    Json o;
+    o["kind"] = c.kind;
+    o["comm"] = c.comm;
+    o["peer"] = c.peer;
+    o["bytes"] = c.bytes;
+    o["what"] = c.what;
+    a.push_back(o);
+  }
+  return a.dump();
+}
+
+void Executor::get_tensor(const std::string& name, void* host, size_t bytes) {
+  if (opt_.dry_run) throw RtError("dry run has no tensors", kValidation);
+  const bool grad = name.rfind("grad:", 0) == 0;
+  const std::string base = grad ? name.substr(5) : name;
+  for (const auto& r : ps_.refs())
+    if (r.name == base) {
+      const size_t want = static_cast<size_t>(r.n) * (grad ? 4 : 2);
+      if (bytes != want) throw RtError("tensor " + name + " has " + std::to_string(want) + " bytes", kValidation);
+      ck(cudaStreamSynchronize(main_), "sync");
+      ck(cudaMemcpy(host, grad ? static_cast<void*>(ps_.grad + r.off) : static_cast<void*>(ps_.param + r.off), bytes,
+                    cudaMemcpyDeviceToHost),
+         "d2h");
+      return;
+    }
+  throw RtError("unknown tensor " + name, kValidation);
+}
+
+void Executor::set_tensor(const std::string& name, const void* host, size_t bytes) {
+  // fp32 master values; the bf16 working copy is derived
+  for (const auto& r : ps_.refs())
+    if (r.name == name) {
+      if (bytes != static_cast<size_t>(r.n) * 4) throw RtError("set_tensor expects fp32 values", kValidation);
+      ck(cudaMemcpy(ps_.master + r.off, host, bytes, cudaMemcpyHostToDevice), "h2d");
+      ck_op(adam_step(ps_.master + r.off, ps_.param + r.off, ps_.grad + r.off, ps_.m + r.off, ps_.v + r.off, r.n, 0.f,
+                      cfg_.beta1, cfg_.beta2, 1.f, 0.f, 1, 0.f, main_),
+            "copy");  // lr = 0: writes bf16(master) without changing it
+      ck(cudaStreamSynchronize(main_), "sync");
+      return;
+    }
+  throw RtError("unknown tensor " + name, kValidation);
+}
+
+}  // namespace lynx::rt
+
+// ============================================================ C-ABI
+#include "../../../include/lynx_rt.h"
+
+namespace {
+char* dupstr(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const lynx::rt::RtError& e) {
+    return lynx::set_error(e.what(), e.code);
+  } catch (const lynx::host::PlanError& e) {
+    return lynx::set_error(e.what(), e.status);
+  } catch (const std::exception& e) {
+    return lynx::set_error(e.what(), lynx::kParse);
+  }
+}
+}  // namespace
+
+struct lynx_rt {
+  std::unique_ptr<lynx::rt::Executor> ex;
+};
+
+extern "C" {
+
+int lynx_rt_create(const char* profile_json, const char* timeline_json, const char* config_json, lynx_rt** out) {
+  *out = nullptr;
+  return guard([&] {
+    auto h = std::make_unique<lynx_rt>();
+    h->ex = std::make_unique<lynx::rt::Executor>(profile_json, timeline_json, config_json);
+    *out = h.release();
+  });
+}
+
+int lynx_rt_step(lynx_rt* h, const int* tokens, const int* labels, float* loss) {
+  return guard([&] { h->ex->step(tokens, labels, loss); });
+}
+
+char* lynx_rt_report_json(lynx_rt* h, int* status) {
+  std::string s;
+  const int st = guard([&] { s = h->ex->report_json(); });
+  if (status) *status = st;
+  return st ? nullptr : dupstr(s);
+}
+
+char* lynx_rt_trace(lynx_rt* h, int format, int* status) {
+  std::string s;
+  const int st = guard([&] { s = h->ex->trace(format); });
+  if (status) *status = st;
+  return st ? nullptr : dupstr(s);
+}
+
+char* lynx_rt_program_json(lynx_rt* h, int* status) {
+  std::string s;
+  const int st = guard([&] { s = h->ex->program_json(); });
+  if (status) *status = st;
+  return st ? nullptr : dupstr(s);
+}
+
+int lynx_rt_get_tensor(lynx_rt* h, const char* name, void* host, size_t bytes) {
+  return guard([&] { h->ex->get_tensor(name, host, bytes); });
+}
+
+int lynx_rt_set_tensor(lynx_rt* h, const char* name, const void* host, size_t bytes) {
+  return guard([&] { h->ex->set_tensor(name, host, bytes); });
+}
+
+int lynx_rt_nccl_unique_id(char* hex_out, size_t len) {
+  return guard([&] {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) throw lynx::rt::RtError("ncclGetUniqueId failed", lynx::kCudaError);
+    if (len < 2 * sizeof(id) + 1) throw lynx::rt::RtError("buffer too small", lynx::kValidation);
+    static const char* hx = "0123456789abcdef";
+    for (size_t i = 0; i < sizeof(id); ++i) {
+      const unsigned char c = static_cast<unsigned char>(id.internal[i]);
+      hex_out[2 * i] = hx[c >> 4];
+      hex_out[2 * i + 1] = hx[c & 15];
+    }
+    hex_out[2 * sizeof(id)] = 0;
+  });
+}
+
+void lynx_rt_destroy(lynx_rt* h) { delete h; }
+
+}  // extern "C"

@@ -1,0 +1,169 @@
+// The B200 executor: replays a Lynx recompute timeline for one pipeline stage
+// on one TP rank — the GPU replacement for the reference's CPU executor
+// simulate() (proj/src/pipesim.cpp:206-761).
+//
+// Same inputs (profile, layers per stage, the stage's StageRecomputeTimeline)
+// and the same execution semantics:
+//   * pass order: warm-up forwards, 1F1B pairs, cool-down backwards (pipesim.cpp:315-323);
+//   * per layer, the template's elements: maximal compute runs and single comm
+//     ops (pipesim.cpp:50-71);
+//   * CriticalPath items run on the main stream before their element, sorted
+//     by (owner_mb, owner_layer, op) (pipesim.cpp:426-440);
+//   * Window items run on the recompute side stream, released when their
+//     host all-reduce is issued, so they overlap the NCCL transfer
+//     (pipesim.cpp:398-424); consumers wait on per-tensor events;
+//   * StallFill items run on the side stream at the start of their backward
+//     pass, filling the pipeline bubble while the gradient recv is pending
+//     (pipesim.cpp:620-646);
+//   * tensor liveness follows the ledger rules (discarded tensors dropped after
+//     their last forward consumer, retained / regenerated ones after their last
+//     backward consumer) on a stream-ordered device memory pool.
+// TP all-reduces and PP send/recv go through NCCL on dedicated streams
+// (tensor-parallel on one communicator; activations and gradients on two
+// pipeline communicators so 1F1B cannot deadlock).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "host/pipeline.hpp"
+#include "runtime/gpt_stage.hpp"
+
+namespace lynx::rt {
+
+struct ExecOptions {
+  bool trace = false;           // per-element CUDA-event timeline
+  bool check_recompute = false; // keep forward copies, compare regenerated tensors bit-for-bit
+  bool elide_recompute = false; // timing-only: skip recompute launches (exposed-recompute cross-check)
+  bool dry_run = false;         // build the launch program only (no device)
+};
+
+struct Slot {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaEvent_t ready = nullptr;  // set when produced off the main stream
+  cudaStream_t stream = nullptr;
+  bool regenerated = false;
+  void* shadow = nullptr;  // check_recompute: forward-produced copy
+};
+
+struct StepReport {
+  double step_ms = 0, busy_ms = 0, comm_ms = 0, recompute_on_demand_ms = 0, recompute_overlapped_ms = 0,
+         wait_on_recompute_ms = 0, recv_wait_ms = 0;
+  double loss = 0;
+  long long recompute_launches = 0, recompute_mismatch_words = 0, recompute_checked = 0;
+  size_t pool_high_water = 0;
+};
+
+struct CommOp {  // launch-program record (dry runs and tests)
+  std::string kind;  // "allreduce" | "send" | "recv"
+  std::string comm;  // "tp" | "pp_act" | "pp_grad"
+  int peer = -1;
+  size_t bytes = 0;
+  std::string what;
+};
+
+class Executor {
+ public:
+  Executor(const std::string& profile_json, const std::string& timeline_json, const std::string& config_json);
+  ~Executor();
+  void step(const int* tokens_host, const int* labels_host, float* loss_out);
+  std::string report_json() const;
+  std::string trace(int format) const;
+  std::string program_json() const;
+  void get_tensor(const std::string& name, void* host, size_t bytes);
+  void set_tensor(const std::string& name, const void* host, size_t bytes);
+  const StepReport& last() const { return rep_; }
+
+ private:
+  using Key4 = std::tuple<int, bool, int, int>;
+  struct TimedSpan {
+    cudaEvent_t a, b;
+    int kind;  // 0 busy(pass), 1 comm, 2 on-demand recompute, 3 overlapped recompute, 4 wait-on-recompute, 5 recv wait
+    int mb = -1, op = -1;
+    bool on_side = false;
+  };
+
+  // setup
+  void parse_config(const std::string& cfg);
+  void bind_template();
+  void init_comms(const std::string& nccl_id_hex, int world_rank, int world_size);
+  void alloc_persistent();
+
+  // passes
+  void forward_pass(int mb);
+  void backward_pass(int mb);
+  void run_items(const std::vector<host::Recompute>& items, cudaStream_t s, int span_kind);
+  void run_critical(const Key4& key);
+  void comm_element(int mb, bool bwd, int l, const host::Element& e);
+  void fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute);
+  void bwd_op(int mb, int l, int pos, cudaStream_t s);
+  void head_forward(int mb);
+  void head_backward(int mb);
+
+  // tensors
+  Slot& slot(int mb, int l, int pos) { return slots_[(static_cast<size_t>(mb) * cfg_.layers + l) * nf_ + pos]; }
+  void* need(int mb, int l, int pos, cudaStream_t s);
+  void* layer_input(int mb, int l, cudaStream_t s);
+  void* alloc(size_t bytes, cudaStream_t s);
+  void release(void* p, cudaStream_t s);
+  void drop(Slot& sl, cudaStream_t s, bool keep_shadow);
+  void mark_ready(Slot& sl, cudaStream_t s);
+  uint64_t drop_stream(int l, int mb, Op op) const;
+
+  // timing
+  cudaEvent_t ev();
+  void span_begin(cudaStream_t s, int kind, int mb = -1, int op = -1);
+  void span_end(cudaStream_t s);
+  void collect_spans();
+
+  void ck(cudaError_t e, const char* what);
+  void ck_op(int status, const char* what);
+  void nccl(ncclResult_t r, const char* what);
+
+  host::Profile prof_;
+  host::StageTimeline tl_;
+  ModelCfg cfg_;
+  ExecOptions opt_;
+  int nf_ = 0, n_ = 0;
+  std::vector<Op> op_of_;
+  std::vector<host::Element> fel_, bel_;
+  std::vector<int> made_in_, last_fwd_use_, last_bwd_user_, ckpt_pos_;
+  std::vector<std::vector<int>> deps_;
+  std::map<Key4, std::vector<host::Recompute>> win_, crit_;
+  std::map<int, std::vector<host::Recompute>> stall_;
+
+  cudaStream_t main_ = nullptr, side_ = nullptr, tp_s_ = nullptr, pa_s_ = nullptr, pg_s_ = nullptr;
+  ncclComm_t tp_comm_ = nullptr, pa_comm_ = nullptr, pg_comm_ = nullptr, world_ = nullptr;
+  cudaMemPool_t pool_ = nullptr;
+  ParamStore ps_;
+  Scratch sc_main_, sc_side_;
+  int *d_tokens_ = nullptr, *d_labels_ = nullptr;
+  int *h_tokens_ = nullptr, *h_labels_ = nullptr;  // pinned staging
+  float *d_loss_ = nullptr, *h_loss_ = nullptr;
+  unsigned long long* d_mismatch_ = nullptr;
+  std::vector<Slot> slots_;
+  struct Grad {  // backward state of one microbatch (one layer in flight)
+    void *dy = nullptr, *dln2 = nullptr, *dres = nullptr, *dln1 = nullptr;
+  };
+  std::vector<void*> stage_in_, head_dy_, ln_f_;  // per microbatch
+  std::vector<Grad> grad_;
+  std::vector<cudaEvent_t> act_sent_, grad_sent_;
+  std::vector<cudaEvent_t> ev_pool_;
+  size_t ev_next_ = 0;
+  std::vector<TimedSpan> spans_;
+  std::vector<std::pair<cudaStream_t, size_t>> open_;
+  std::vector<CommOp> program_;
+  StepReport rep_;
+  int step_ = 0;
+  cudaEvent_t t0_ = nullptr, t1_ = nullptr;
+  std::vector<std::tuple<int, int, int, int, double, double>> trace_;  // stage, mb, kind, op, start, end
+};
+
+}  // namespace lynx::rt

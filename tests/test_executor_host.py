@@ -1,0 +1,82 @@
+"""Executor host logic without a GPU: dry-run launch programs for TP/PP configurations.
+
+The multi-GPU path cannot run in this round (one B200 per call), so these CPU
+tests build every rank's launch program in dry-run mode and check that the
+collectives are consistent: both TP ranks of a stage issue the same all-reduce
+sequence (same sizes, same order — recomputed all-reduces included), and every
+pipeline send has a matching receive of the same size, in the same order, on
+the same communicator. Activations and gradients travel on separate
+communicators whose per-direction sequences are monotone in the microbatch, so
+1F1B cannot deadlock.
+"""
+import json
+
+import pytest
+
+from paper_2406_08756_b200 import executor as ex
+from paper_2406_08756_b200 import gpt_profile as gp
+
+
+def dry_programs(c: gp.GPTConfig, budget: int | None = None):
+    if budget:
+        c = gp.GPTConfig(**{**c.__dict__, "mem_budget_bytes": budget})
+    text = gp.profile_text(c)
+    progs = {}
+    plans = [ex.plan_for(text, s) for s in range(c.pp)]
+    layers = plans[0]["layers_per_stage"]
+    for s in range(c.pp):
+        for r in range(c.tp):
+            cfg = ex.make_config(c, layers, tp_rank=r, exec_opts={"dry_run": True})
+            e = ex.Executor(text, plans[s]["timeline"], cfg)
+            e.step(None, None)
+            progs[(s, r)] = e.program()
+            e.close()
+    return progs, plans
+
+
+@pytest.mark.parametrize("key,budget", [("1.3b", None), ("1.3b", 24_000_000_000), ("7b", None), ("13b", 40_000_000_000)])
+def test_tp_allreduce_sequences_match(key, budget):
+    c = gp.CONFIGS[key]
+    progs, plans = dry_programs(c, budget)
+    for s in range(c.pp):
+        seqs = [[(o["kind"], o["bytes"], o["what"]) for o in progs[(s, r)] if o["comm"] == "tp"] for r in range(c.tp)]
+        assert all(q == seqs[0] for q in seqs)
+        # two forward and two backward all-reduces per layer per microbatch (+ phase-5 recomputes)
+        n_layers = plans[0]["layers_per_stage"][s]
+        assert len(seqs[0]) >= 4 * n_layers * c.n_microbatches
+
+
+@pytest.mark.parametrize("key", ["1.3b", "7b", "13b"])
+def test_pipeline_sends_match_receives(key):
+    c = gp.CONFIGS[key]
+    progs, _ = dry_programs(c)
+    for comm, direction in [("pp_act", +1), ("pp_grad", -1)]:
+        for r in range(c.tp):
+            for s in range(c.pp):
+                peer = s + direction
+                if not 0 <= peer < c.pp:
+                    continue
+                sends = [(o["bytes"], o["what"]) for o in progs[(s, r)] if o["comm"] == comm and o["kind"] == "send"]
+                recvs = [(o["bytes"], o["what"]) for o in progs[(peer, r)]
+                         if o["comm"] == comm and o["kind"] == "recv" and o["peer"] == s]
+                assert sends == recvs and len(sends) == c.n_microbatches
+                mbs = [int(w.split("mb")[1]) for _, w in sends]
+                assert mbs == sorted(mbs)  # monotone per direction: no 1F1B cycle
+
+
+def test_single_gpu_program_has_no_collectives():
+    c = gp.CONFIGS["tiny"]
+    progs, _ = dry_programs(c)
+    assert progs[(0, 0)] == []
+
+
+def test_executor_rejects_foreign_templates():
+    from paper_2406_08756_b200._native import LynxError
+    prof = json.loads(open("/dev/null").read() or "{}") if False else None
+    c = gp.CONFIGS["tiny"]
+    text = json.loads(gp.profile_text(c))
+    text["model"]["layer"]["ops"][1]["name"] = "mystery"
+    t = json.dumps(text)
+    plan = ex.plan_for(t, 0)
+    with pytest.raises(LynxError):
+        ex.Executor(t, plan["timeline"], ex.make_config(c, plan["layers_per_stage"], exec_opts={"dry_run": True}))
