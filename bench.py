@@ -1,0 +1,387 @@
+"""Benchmark: GPT training tokens/s with a Lynx HEU recompute plan on B200; exposed recompute ms/iter.
+
+Metric (BASELINE.json): "GPT-7B train tokens/s, 8xB200 TP2·PP4; exposed recompute ms/iter".
+One step = one full training iteration (all microbatches' 1F1B passes, the
+plan's recomputation, AdamW) executed by the native executor through the C-ABI.
+
+  python bench.py                                  # N=1: GPT-7B, TP1 PP1, mb 32, seq 2048, HEU plan
+  python -m torch.distributed.run --nproc-per-node N bench.py --gpus N   # N in {2,4,8}: TP2 x PP(N/2)
+  python bench.py --impl reference                 # CPU reference arm (host cores)
+
+At N=1 the metric's own model (GPT-7B, mb 32, s 2048) is run whole on one
+B200: 6.7 B parameters (120 GB of weights + fp32 master/grad/Adam state) leave
+~55 GB for activations, so retain-all OOMs and the HEU plan decides what to
+recompute. With TP = 1 there are no all-reduce windows, so all recomputation is
+exposed on the critical path; the baselines (retain-all, full recompute) are
+reported beside it (--baselines).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GPT-7B train tokens/s, 8×B200 TP2·PP4; exposed recompute ms/iter"
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int = 0):
+        self.gpu = gpu
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def config_for(n_gpus: int, args):
+    from paper_2406_08756_b200 import gpt_profile as gp
+    base = gp.CONFIGS[args.model]
+    if n_gpus == 1:
+        tp, pp, m = 1, 1, args.microbatches or 1
+    else:
+        tp = 2
+        pp = n_gpus // 2
+        m = args.microbatches or max(2 * pp, 2)
+    c = gp.GPTConfig(**{**base.__dict__, "tp": tp, "pp": pp, "n_microbatches": m, "dropout": 0.1})
+    if args.micro_batch:
+        c.micro_batch = args.micro_batch
+    return c
+
+
+def device_budget(c, device_bytes: int) -> int:
+    """Ledger budget = HBM minus what the ledger does not model (runtime scratch, transients, context)."""
+    T, h = c.tokens, c.hidden
+    hp = h // c.tp
+    scratch = 2 * T * h * 3 + 2 * T * 4 * hp + 4096 * c.vocab * 2 + 64 * 2**20
+    transients = 2 * T * h * 6 + 4 * T * h + (2 * T * h + 8 * T)  # grads in flight, embed ws, head dy/ln_f
+    # HEU's peak (heusched.cpp:260-277) counts retained tensors only; one layer's
+    # discarded tensors are physically alive while that layer runs.
+    one_layer = (2 * T * h + 8 * T) * 2 + 2 * T * 3 * hp + 2 * T * hp + 2 * T * h * 2 + 2 * T * 4 * hp * 2
+    context = 4 * 2**30  # CUDA context, NCCL buffers, pool fragmentation margin
+    return int(device_bytes - scratch - transients - one_layer - context)
+
+
+def plan_all(c, profile_text: str, baseline: str):
+    from paper_2406_08756_b200 import executor as ex
+    t0 = time.perf_counter()
+    plans = [ex.plan_for(profile_text, s, baseline) for s in range(c.pp)]
+    return plans, time.perf_counter() - t0
+
+
+def cpu_baseline(c, budget_s: float = 20.0) -> dict:
+    """The CPU numerical port (oracle/gpt_oracle.py) on host cores, on a bounded sample of the
+    workload (one GPT block of the same width and sequence length + LM head, micro-batch 1),
+    scaled to the whole model by model FLOPs per token."""
+    import numpy as np
+    import torch
+
+    from oracle import gpt_oracle
+    from paper_2406_08756_b200 import executor as ex
+    from paper_2406_08756_b200 import gpt_profile as gp
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    s = gp.GPTConfig("sample", 1, c.hidden, c.heads, c.seq, 1, c.vocab, 1, 1, 1, dropout=0.0)
+    shapes = ex.param_shapes(s, 1, True, True)
+    rng = np.random.default_rng(0)
+    params = {k: (rng.standard_normal(int(np.prod(v))) * 0.02).astype(np.float32) for k, v in shapes.items()}
+    for k in shapes:
+        if k.endswith("_g"):
+            params[k][:] = 1.0
+    tok, lab = ex.synthetic_batch(s)
+    n, t_total = 0, 0.0
+    while t_total < budget_s and n < 3:
+        t0 = time.perf_counter()
+        gpt_oracle.gpt_step(params, shapes, tok, lab, n_layers=1, hidden=s.hidden, heads=s.heads, seq=s.seq,
+                            micro_batch=1, n_micro=1)
+        t_total += time.perf_counter() - t0
+        n += 1
+    sample_tokens_s = n * s.tokens / t_total
+    scaled = sample_tokens_s * s.flops_per_token() / c.flops_per_token()
+    return {"value": scaled, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"torch-CPU fp32 fwd+bwd of 1 GPT block (h={c.hidden}, s={c.seq}, mb=1) + LM head, "
+                      f"{n} step(s) in {t_total:.1f}s = {sample_tokens_s:.1f} tok/s, scaled by model FLOPs/token "
+                      f"({s.flops_per_token():.3g} -> {c.flops_per_token():.3g})"}
+
+
+def reference_simulate(c, profile_text: str) -> dict | None:
+    """The reference's own CPU executor simulate() on the same profile (oracle/_ref), 1 core."""
+    try:
+        from oracle import ref as oref
+        if not oref.available():
+            return None
+        R = oref.RefLib()
+        t0 = time.perf_counter()
+        out = json.loads(R.simulate(profile_text, None, "0", 0, 10000))
+        wall = time.perf_counter() - t0
+        return {"wall_s": round(wall, 4), "predicted_iteration_us": out["iteration_us"],
+                "memory_peaks": out["memory_peaks"], "cores": 1}
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2406_08756_b200 import gpt_profile as gp
+    c = config_for(max(args.gpus, 1), args)
+    c.mem_budget_bytes = 170_000_000_000
+    text = gp.profile_text(c)
+    base = cpu_baseline(c, budget_s=min(20.0, 6.0 * max(args.steps, 1)))
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "tokens/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "ms_per_step": 1000.0 * c.tokens * c.n_microbatches / base["value"],
+            "config": workload_config(c, args), "dtype": "f32", "data": "synthetic",
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_simulate": reference_simulate(c, text), "vs_baseline": None}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(c, args) -> dict:
+    return {"workload": f"{c.name} full model, seq {c.seq}, micro-batch {c.micro_batch}, "
+                        f"{c.n_microbatches} microbatch(es)/iter, TP{c.tp}xPP{c.pp}, HEU recompute plan",
+            "model": c.name, "layers": c.n_layers, "hidden": c.hidden, "heads": c.heads,
+            "global_batch": c.micro_batch * c.n_microbatches, "seq_len": c.seq, "micro_batch": c.micro_batch,
+            "n_microbatches": c.n_microbatches, "parallelism": f"tp{c.tp}pp{c.pp}", "plan": args.plan,
+            "l2": "activations are GBs per op (> 126 MB L2); no flush needed"}
+
+
+def gemm_roofline(c, peaks: dict) -> dict:
+    """Dominant kernel: the FC1 forward tcgen05 GEMM at this workload's shape, timed standalone with CUDA
+    events on the launching (torch current) stream right after the timed region."""
+    import torch
+
+    from paper_2406_08756_b200 import ops
+    T, h = c.tokens, c.hidden
+    hp = h // c.tp
+    a = torch.randn(T, h, device="cuda").bfloat16()
+    b = torch.randn(4 * hp, h, device="cuda").bfloat16()
+    out = torch.empty(T, 4 * hp, device="cuda", dtype=torch.bfloat16)
+    for _ in range(3):
+        ops.gemm(a, b, out=out)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    n = 10
+    s.record()
+    for _ in range(n):
+        ops.gemm(a, b, out=out)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / n
+    flops = 2.0 * T * 4 * hp * h
+    ach = flops / ms / 1e9
+    peak = peaks.get("bf16_tflops", 1590.0)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            traffic = json.load(f).get("fc1_fwd_bytes_per_launch")
+    except Exception:
+        pass
+    del a, b, out
+    torch.cuda.empty_cache()
+    return {"bound": "tensor", "kernel": "gemm_tcgen05 fc1 fwd", "shape": [T, 4 * hp, h], "ms_per_launch": ms,
+            "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+            "peak_kind": "measured burst bf16 (MEASURED_PEAKS.json)", "traffic": traffic,
+            "flops_per_launch": flops}
+
+
+def run_gpu_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2406_08756_b200 import executor as ex
+    from paper_2406_08756_b200 import gpt_profile as gp
+    ws, rank, local = dist_env()
+    n = max(args.gpus, ws)
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("gloo", init_method="env://")
+    c = config_for(n, args)
+    free, total = torch.cuda.mem_get_info()
+    c.mem_budget_bytes = device_budget(c, total)
+    text = gp.profile_text(c)
+    plans, plan_s = plan_all(c, text, args.plan)
+    layers = plans[0]["layers_per_stage"]
+    stage, tp_rank = rank // c.tp, rank % c.tp
+    nccl_id = ""
+    if ws > 1:
+        obj = [ex.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    cfg = ex.make_config(c, layers, tp_rank=tp_rank, world_rank=rank, world_size=ws, nccl_id=nccl_id,
+                         exec_opts={"trace": False})
+    e = ex.Executor(text, plans[stage]["timeline"], cfg)
+    tok, lab = ex.synthetic_batch(c)
+    first, last = stage == 0, stage == c.pp - 1
+    for _ in range(args.warmup):
+        e.step(tok if first else None, lab if last else None)
+    # ---- timed region: K steps through the C-ABI with host buffers
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    step_ms, losses, reports = [], [], []
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            losses.append(e.step(tok if first else None, lab if last else None))
+            r = e.report()
+            reports.append(r)
+            step_ms.append(r["iteration_ms"])
+        wall = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    dev_ms = float(np.mean(step_ms))
+    wall_ms = 1000.0 * wall / args.steps
+    exposed = float(np.mean([r["exposed_recompute_ms"] for r in reports]))
+    if ws > 1:
+        t = torch.tensor([dev_ms, wall_ms, exposed], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, wall_ms, exposed = t.tolist()
+    tokens_iter = c.tokens * c.n_microbatches
+    value = tokens_iter / (dev_ms / 1000.0)
+    e2e = tokens_iter / (wall_ms / 1000.0)
+    rep = reports[-1]
+    plan0 = json.loads(plans[stage]["plan_json"])
+    extra = {}
+    if rank == 0 and args.baselines and ws == 1:
+        e.close()
+        del e
+        for base in ("full", "retain_all"):
+            try:
+                bp, _ = plan_all(c, text, base)
+                be = ex.Executor(text, bp[0]["timeline"], cfg)
+                for _ in range(2):
+                    be.step(tok, lab)
+                be.step(tok, lab)
+                br = be.report()
+                extra[base] = {"iteration_ms": br["iteration_ms"], "exposed_recompute_ms": br["exposed_recompute_ms"],
+                               "tokens_per_s": tokens_iter / (br["iteration_ms"] / 1000.0),
+                               "pool_high_water_bytes": br["pool_high_water_bytes"]}
+                be.close()
+            except Exception as err:
+                extra[base] = {"error": str(err).splitlines()[0][:200]}
+    if rank != 0:
+        return
+    peaks = measured_peaks()
+    roof = gemm_roofline(c, peaks)
+    step_tflops = c.flops_per_token() * tokens_iter / (dev_ms / 1000.0) / 1e12
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dev_ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights",
+        "config": workload_config(c, args),
+        "exposed_recompute_ms_per_iter": round(exposed, 3),
+        "recompute": {"plan": plan0, "items": len(plans[stage]["timeline"]["items"]),
+                      "launches_per_iter": rep["recompute_launches"],
+                      "on_demand_ms": rep["recompute_on_demand_ms"], "overlapped_ms": rep["recompute_overlapped_ms"],
+                      "wait_on_recompute_ms": rep["wait_on_recompute_ms"], "baselines": extra or None},
+        "memory": {"ledger_budget_bytes": c.mem_budget_bytes, "plan_peak_bytes": plan0["peak_bytes"],
+                   "pool_high_water_bytes": rep["pool_high_water_bytes"],
+                   "static_bytes": rep["static_bytes_allocated"], "device_total_bytes": total},
+        "loss": [round(x, 5) for x in losses],
+        "model_tflops_per_gpu": round(step_tflops / n, 1),
+        "mfu_vs_sustained": round(step_tflops / n / peaks.get("bf16_tflops_sustained", 1400.0), 4),
+        "roofline": roof,
+        "e2e": {"value": round(e2e, 1), "unit": "tokens/s",
+                "h2d_bytes_per_step": 2 * 4 * tokens_iter if ws == 1 else 4 * tokens_iter,
+                "d2h_bytes_per_step": 4 * tokens_iter},
+        "gpu_launches": None,
+        "clocks": clk.summary(),
+        "planner_s": round(plan_s, 3),
+    }
+    # kernels of liblynx_b200.so issued inside the timed region (counted at every launch site)
+    line["gpu_launches"] = int(sum(r["kernel_launches"] for r in reports))
+    if not args.no_cpu_baseline and ws == 1:
+        line["cpu_baseline"] = cpu_baseline(c, budget_s=20.0)
+        line["reference_simulate"] = reference_simulate(c, text)
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--model", default="7b")
+    ap.add_argument("--micro-batch", type=int, default=0)
+    ap.add_argument("--microbatches", type=int, default=0)
+    ap.add_argument("--plan", default="heu", choices=["heu", "full", "retain_all"])
+    ap.add_argument("--baselines", action="store_true", help="also time retain-all / full-recompute plans (N=1)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,6 +1,7 @@
 // extern "C" entry points of the operator library (include/lynx_b200.h).
 // Plain device pointers, sizes and a cudaStream_t passed as void*; every
 // function returns a Status code and leaves a message in lynx_last_error().
+#include <atomic>
 #include <cstdio>
 #include <string>
 
@@ -18,7 +19,14 @@ int set_error(const std::string& msg, int code) {
   return code;
 }
 
-int check_launch(const char* what) {
+namespace {
+std::atomic<long long> g_launches{0};
+}
+
+long long launch_count() { return g_launches.load(); }
+
+int check_launch(const char* what, int kernels) {
+  g_launches += kernels;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(std::string(what) + ": " + cudaGetErrorString(e), kCudaError);
   return kOk;

@@ -23,7 +23,10 @@ enum Status {
 };
 
 int set_error(const std::string& msg, int code = kCudaError);
-int check_launch(const char* what);
+// Checks the last launch and counts `kernels` launches of this library
+// (the bench's gpu_launches claim).
+int check_launch(const char* what, int kernels = 1);
+long long launch_count();
 const char* last_error();
 
 enum EpiMode { EPI_BF16 = 0, EPI_ACC_F32 = 1, EPI_STORE_F32 = 2 };

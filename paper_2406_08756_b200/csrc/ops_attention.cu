@@ -512,7 +512,7 @@ int bwd_launch(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bf
   auto k2 = attn_bwd_dq_kernel<D>;
   cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);
   k2<<<dim3(S / 64, H, B), 128, smem_q, s>>>(qkv, dout, lse, dvec, dqkv, S, H, scale, scale_log2);
-  return check_launch("attention_bwd");
+  return check_launch("attention_bwd", 3);
 }
 
 }  // namespace

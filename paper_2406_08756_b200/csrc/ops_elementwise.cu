@@ -376,7 +376,7 @@ int embedding_bwd(const int32_t* tokens, const __nv_bfloat16* dout, float* dwte,
   const long long n = static_cast<long long>(seq) * width;
   embedding_wpe_bwd_kernel<<<static_cast<int>((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(workspace, dwpe, batch,
                                                                                            seq, width);
-  return check_launch("embedding_bwd");
+  return check_launch("embedding_bwd", 2);
 }
 
 int xent_fwd_bwd(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows, long long rows, int vocab,

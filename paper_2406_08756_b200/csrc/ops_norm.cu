@@ -227,7 +227,7 @@ int layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bf
   const int nb = part_blocks(rows);
   ln_bwd_kernel<<<nb, kNT, 0, s>>>(dy, x, gamma, mean, rstd, dres, dx, workspace, rows, width);
   reduce_partials_kernel<<<(width + 255) / 256, 256, 0, s>>>(workspace, dgamma_acc, dbeta_acc, nb, width, 2);
-  return check_launch("layernorm_bwd");
+  return check_launch("layernorm_bwd", 2);
 }
 
 size_t column_sum_workspace(long long rows, int width) {
@@ -240,7 +240,7 @@ int column_sum_acc(const __nv_bfloat16* x, float* acc, float* workspace, long lo
   const int nb = part_blocks(rows);
   column_partial_kernel<<<nb, kNT, 0, s>>>(x, workspace, rows, width);
   reduce_partials_kernel<<<(width + 255) / 256, 256, 0, s>>>(workspace, acc, nullptr, nb, width, 1);
-  return check_launch("column_sum_acc");
+  return check_launch("column_sum_acc", 2);
 }
 
 }  // namespace lynx

@@ -883,6 +883,7 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
     for (auto [bwd, mb] : passes) bwd ? backward_pass(mb) : forward_pass(mb);
     return;
   }
+  const long long launches0 = launch_count();
   ck(cudaEventRecord(t0_, main_), "event");
   if (cfg_.first() && tokens) {
     std::memcpy(h_tokens_, tokens, ntok * 4);
@@ -905,6 +906,7 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
         "adam");
   if (cfg_.last()) ck(cudaMemcpyAsync(h_loss_, d_loss_, ntok * 4, cudaMemcpyDeviceToHost, main_), "d2h loss");
   ck(cudaEventRecord(t1_, main_), "event");
+  rep_.kernel_launches = launch_count() - launches0;
   ck(cudaEventSynchronize(t1_), "step");
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, t0_, t1_), "elapsed");
@@ -936,6 +938,7 @@ std::string Executor::report_json() const {
   j["wait_on_recompute_ms"] = rep_.wait_on_recompute_ms;
   j["exposed_recompute_ms"] = rep_.recompute_on_demand_ms + rep_.wait_on_recompute_ms;
   j["recompute_launches"] = rep_.recompute_launches;
+  j["kernel_launches"] = rep_.kernel_launches;
   j["recompute_checked"] = rep_.recompute_checked;
   j["recompute_mismatch_words"] = rep_.recompute_mismatch_words;
   j["loss"] = rep_.loss;

@@ -58,6 +58,7 @@ struct StepReport {
          wait_on_recompute_ms = 0, recv_wait_ms = 0;
   double loss = 0;
   long long recompute_launches = 0, recompute_mismatch_words = 0, recompute_checked = 0;
+  long long kernel_launches = 0;  // kernels of this library issued by the step
   size_t pool_high_water = 0;
 };
 
