@@ -259,6 +259,8 @@ def run_gpu_arm(args):
     if ws > 1:
         dist.init_process_group("gloo", init_method="env://")
     c = config_for(n, args)
+    peaks = measured_peaks()
+    roof = gemm_roofline(c, peaks) if rank == 0 else None  # before the executor owns the HBM
     free, total = torch.cuda.mem_get_info()
     c.mem_budget_bytes = device_budget(c, total)
     text = gp.profile_text(c)
@@ -309,7 +311,10 @@ def run_gpu_arm(args):
     if rank == 0 and args.baselines and ws == 1:
         e.close()
         del e
+        print(json.dumps({"partial": True, "value": value, "ms": dev_ms, "exposed_ms": exposed,
+                          "report": rep}), file=sys.stderr, flush=True)
         for base in ("full", "retain_all"):
+            be = None
             try:
                 bp, _ = plan_all(c, text, base)
                 be = ex.Executor(text, bp[0]["timeline"], cfg)
@@ -319,14 +324,16 @@ def run_gpu_arm(args):
                 br = be.report()
                 extra[base] = {"iteration_ms": br["iteration_ms"], "exposed_recompute_ms": br["exposed_recompute_ms"],
                                "tokens_per_s": tokens_iter / (br["iteration_ms"] / 1000.0),
-                               "pool_high_water_bytes": br["pool_high_water_bytes"]}
-                be.close()
+                               "pool_high_water_bytes": br["pool_high_water_bytes"],
+                               "plan_peak_bytes": json.loads(bp[0]["plan_json"])["peak_bytes"]}
             except Exception as err:
-                extra[base] = {"error": str(err).splitlines()[0][:200]}
+                extra[base] = {"error": str(err).splitlines()[0][:200],
+                               "plan_peak_bytes": json.loads(bp[0]["plan_json"])["peak_bytes"]}
+            finally:
+                if be is not None:
+                    be.close()
     if rank != 0:
         return
-    peaks = measured_peaks()
-    roof = gemm_roofline(c, peaks)
     step_tflops = c.flops_per_token() * tokens_iter / (dev_ms / 1000.0) / 1e12
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": "tokens/s", "n_gpus": n, "steps": args.steps,
