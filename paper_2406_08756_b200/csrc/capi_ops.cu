@@ -53,6 +53,8 @@ int lynx_op_gemm(const void* a, long long lda, int a_mn_major, const void* b, lo
   return gemm_run(g, STREAM(stream));
 }
 
+void lynx_op_gemm_mode(int mode) { gemm_set_mode(mode); }
+
 int lynx_op_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                           int rows, int width, float eps, void* stream) {
   return layernorm_fwd(CBF(x), CBF(gamma), CBF(beta), BF(y), mean, rstd, rows, width, eps, STREAM(stream));

@@ -46,6 +46,8 @@ struct GemmDesc {
 };
 
 int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas = 0);
+// -1: 2-CTA (cta_group::2) kernel wherever the shape allows (default); 0: 1-CTA kernel only.
+void gemm_set_mode(int mode);
 
 // ---- norm / elementwise / attention / loss (see the .cu files for contracts)
 int layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* gamma, const __nv_bfloat16* beta, __nv_bfloat16* y,

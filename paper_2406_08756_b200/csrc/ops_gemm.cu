@@ -244,6 +244,245 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem_base);
 }
 
+// ---------------------------------------------------------------- 2-CTA (cta_group::2)
+// A CTA pair (one cluster, two SMs of a TPC) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (UMMA M = 256): each CTA stages its 128 rows of A
+// and its 128 columns of B, the leader issues the MMA that reads both CTAs'
+// shared memory, and each CTA's TMEM holds its own 128 accumulator rows.
+// Per SM this moves (128 + 128) instead of (128 + 256) operand rows per
+// 128 x 256 outputs — 1.5x less L2->SM traffic than the 1-CTA tile.
+namespace pair {
+
+constexpr int kStages = 6;
+constexpr int kTileM = 256, kTileN = 256, kHalf = 128;
+constexpr int kABytes = kHalf * BK * 2;  // per CTA
+constexpr int kBBytes = kHalf * BK * 2;  // per CTA (half of N)
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the even (leader) CTA
+
+LYNX_DEV uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+LYNX_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+LYNX_DEV void arrive_leader(uint64_t* bar) {  // remote (or local) arrive on the leader's barrier
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
+               : "memory");
+}
+LYNX_DEV void tma_load_2sm(const void* desc, uint64_t* bar, void* smem, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "l"(kEvictNormal)
+      : "memory");
+}
+LYNX_DEV void umma_f16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+LYNX_DEV void umma_commit_pair(uint64_t* bar) {  // arrive on `bar` in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+template <bool kAMN, bool kBMN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, Args args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m_tiles = args.M / kTileM, n_tiles = args.N / kTileN;
+  const int num_tiles = m_tiles * n_tiles;
+  const int k_blocks = args.K / BK;
+  const int cluster = blockIdx.x / 2, n_clusters = gridDim.x / 2;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_a);
+    tma_prefetch_desc(&tm_b);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 2);   // leader's expect_tx arrival + the peer producer's arrival
+      mbar_init(&empty[s], 1);  // the leader's multicast commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+        int mt, nt;
+        tile_coords(tile, m_tiles, n_tiles, mt, nt);
+        const int m0 = mt * kTileM + rank * kHalf, n0 = nt * kTileN + rank * kHalf;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStageBytes;
+          uint8_t* sb = sa + kABytes;
+          if (leader) {
+            mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
+          } else {
+            arrive_leader(&full[stage]);
+          }
+          const int k0 = kb * BK;
+          if constexpr (!kAMN) {
+            tma_load_2sm(&tm_a, &full[stage], sa, k0, m0);
+          } else {
+            tma_load_2sm(&tm_a, &full[stage], sa, m0, k0);
+            tma_load_2sm(&tm_a, &full[stage], sa + 64 * BK * 2, m0 + 64, k0);
+          }
+          if constexpr (!kBMN) {
+            tma_load_2sm(&tm_b, &full[stage], sb, k0, n0);
+          } else {
+            tma_load_2sm(&tm_b, &full[stage], sb, n0, k0);
+            tma_load_2sm(&tm_b, &full[stage], sb + 64 * BK * 2, n0 + 64, k0);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(kTileM, kTileN, kAMN, kBMN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kTileN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(smem + stage * kStageBytes);
+            const uint32_t sb = sa + kABytes;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t da = kAMN ? umma_desc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
+                                       : umma_desc_sw128(sa + k * 32, 16, 1024);
+              const uint64_t db = kBMN ? umma_desc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
+                                       : umma_desc_sw128(sb + k * 32, 16, 1024);
+              umma_f16_pair(d_tmem, da, db, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            }
+            umma_commit_pair(&empty[stage]);
+            if (kb == k_blocks - 1) umma_commit_pair(&tmem_full[acc]);
+          }
+          __syncwarp();
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
+      int mt, nt;
+      tile_coords(tile, m_tiles, n_tiles, mt, nt);
+      const int row = mt * kTileM + rank * kHalf + ew * 32 + lane;
+      const int n0 = nt * kTileN;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kTileN;
+#pragma unroll 1
+      for (int c = 0; c < kTileN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(t_row + c, r);
+        tmem_ld_wait();
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+        if (args.epi == EPI_ACC_F32) {
+          float* out = reinterpret_cast<float*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            float4 o = *reinterpret_cast<float4*>(out + i);
+            o.x += v[i];
+            o.y += v[i + 1];
+            o.z += v[i + 2];
+            o.w += v[i + 3];
+            *reinterpret_cast<float4*>(out + i) = o;
+          }
+        } else if (args.epi == EPI_STORE_F32) {
+          float* out = reinterpret_cast<float*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(out + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+          if (args.bias) {
+            const BF8* bp = reinterpret_cast<const BF8*>(args.bias + n0 + c);
+            float b[16];
+            bf8_to_f(bp[0], b);
+            bf8_to_f(bp[1], b + 8);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += b[i];
+          }
+          __nv_bfloat16* out =
+              reinterpret_cast<__nv_bfloat16*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
+          BF8* o = reinterpret_cast<BF8*>(out);
+          o[0] = f_to_bf8(v);
+          o[1] = f_to_bf8(v + 8);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_leader(&tmem_empty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512));
+}
+
+}  // namespace pair
+
 // ---------------------------------------------------------------- host side
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -306,7 +545,35 @@ int launch(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   return check_launch("gemm_tcgen05");
 }
 
+template <bool kAMN, bool kBMN>
+int launch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
+  CUtensorMap ma, mb;
+  // each CTA loads a 128-row (A) / 128-column (B) half of the pair's 256 x 256 tile
+  bool ok = kAMN ? make_map(&ma, g.a, g.M, g.K, g.lda, 64, BK) : make_map(&ma, g.a, g.K, g.M, g.lda, BK, pair::kHalf);
+  ok = ok && (kBMN ? make_map(&mb, g.b, g.N, g.K, g.ldb, 64, BK) : make_map(&mb, g.b, g.K, g.N, g.ldb, BK, pair::kHalf));
+  if (!ok) return set_error("cuTensorMapEncodeTiled failed (alignment or driver entry point)");
+  auto kern = pair::gemm2_kernel<kAMN, kBMN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::kSmemBytes);
+    attr_set = true;
+  }
+  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi};
+  const int tiles = (g.M / pair::kTileM) * (g.N / pair::kTileN);
+  int clusters = num_sms() / 2;
+  if (max_ctas > 0) clusters = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
+  if (tiles < clusters) clusters = tiles;
+  kern<<<2 * clusters, kThreads, pair::kSmemBytes, stream>>>(ma, mb, args);
+  return check_launch("gemm_tcgen05_pair");
+}
+
 }  // namespace gemm
+
+namespace {
+int g_gemm_mode = -1;  // -1 auto (2-CTA where the shape allows), 0 force 1-CTA
+}
+
+void gemm_set_mode(int mode) { g_gemm_mode = mode; }
 
 int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   using namespace gemm;
@@ -315,6 +582,13 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   if (g.N % 128) return set_error("gemm: N must be a multiple of 128");
   if ((g.epi == EPI_BF16 && g.ldc % 8) || (g.epi != EPI_BF16 && g.ldc % 4))
     return set_error("gemm: ldc must keep 16-byte row alignment");
+  if (g_gemm_mode != 0 && g.M % pair::kTileM == 0 && g.N % pair::kTileN == 0 &&
+      (g.M / pair::kTileM) * (g.N / pair::kTileN) >= 32) {
+    if (!g.a_mn && !g.b_mn) return launch_pair<false, false>(g, stream, max_ctas);
+    if (!g.a_mn && g.b_mn) return launch_pair<false, true>(g, stream, max_ctas);
+    if (g.a_mn && !g.b_mn) return launch_pair<true, false>(g, stream, max_ctas);
+    return launch_pair<true, true>(g, stream, max_ctas);
+  }
   const bool wide = g.N % 256 == 0;
 #define LYNX_GEMM_CASE(AMN, BMN)                                                             \
   if (g.a_mn == AMN && g.b_mn == BMN)                                                         \

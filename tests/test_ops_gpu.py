@@ -38,6 +38,31 @@ def test_gemm_majors(ops, cuda, a_mn, b_mn, M, N, K):
     assert rel(out, ref) < 1e-2
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("mode", [-1, 0])
+def test_gemm_pair_and_single_cta(ops, cuda, a_mn, b_mn, mode):
+    """256x256 CTA-pair (cta_group::2) tiles vs the 128xBN single-CTA kernel on shapes both accept."""
+    from paper_2406_08756_b200._native import lib
+    M, N, K = 2048, 1536, 640
+    g = torch.Generator(device=cuda).manual_seed(11)
+    A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    B = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    a = A.t().contiguous() if a_mn else A
+    b = B.t().contiguous() if b_mn else B
+    bias = torch.randn(N, device=cuda, generator=g).bfloat16()
+    lib().lynx_op_gemm_mode(mode)
+    try:
+        out = ops.gemm(a, b, a_mn=a_mn, b_mn=b_mn, bias=bias)
+        acc = torch.ones(M, N, device=cuda)
+        ops.gemm(a, b, a_mn=a_mn, b_mn=b_mn, out=acc, epi=ops.EPI_ACC_F32)
+        torch.cuda.synchronize()
+    finally:
+        lib().lynx_op_gemm_mode(-1)
+    ref = A.float() @ B.float().t()
+    assert rel(out, ref + bias.float()) < 1e-2
+    assert rel(acc, ref + 1) < 1e-5
+
+
 def test_gemm_bias_and_f32_epilogues(ops, cuda):
     g = torch.Generator(device=cuda).manual_seed(7)
     A = torch.randn(256, 512, device=cuda, generator=g).bfloat16()
