@@ -62,6 +62,54 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
   nt = in_group / gm;
 }
 
+// TMEM accumulator row (this thread's output row) -> global, 32 columns per
+// round: the fp32 read of the accumulate epilogue is issued before the TMEM
+// load is awaited so the two latencies overlap.
+template <int kCols>
+LYNX_DEV void epilogue_row(const Args& args, uint32_t t_row, long long row, int n0) {
+  if (args.epi >= 98) return;  // timing probes: no epilogue
+#pragma unroll 1
+  for (int c = 0; c < kCols; c += 32) {
+    uint32_t r[32];
+    float4 prev[8];
+    float* outf = reinterpret_cast<float*>(args.c) + row * args.ldc + n0 + c;
+    if (args.epi == EPI_ACC_F32) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) prev[i] = reinterpret_cast<const float4*>(outf)[i];
+    }
+    tmem_ld32(t_row + c, r);
+    tmem_ld_wait();
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+    if (args.epi == EPI_ACC_F32 || args.epi == EPI_STORE_F32) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        if (args.epi == EPI_ACC_F32) {
+          o.x += prev[i].x;
+          o.y += prev[i].y;
+          o.z += prev[i].z;
+          o.w += prev[i].w;
+        }
+        reinterpret_cast<float4*>(outf)[i] = o;
+      }
+    } else {
+      if (args.bias) {
+        const BF8* bp = reinterpret_cast<const BF8*>(args.bias + n0 + c);
+        float b[32];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) bf8_to_f(bp[i], b + 8 * i);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += b[i];
+      }
+      BF8* o = reinterpret_cast<BF8*>(reinterpret_cast<__nv_bfloat16*>(args.c) + row * args.ldc + n0 + c);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = f_to_bf8(v + 8 * i);
+    }
+  }
+}
+
 template <bool kAMN, bool kBMN, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, Args args) {
@@ -113,6 +161,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
           uint8_t* sb = sa + S::kABytes;
+          if (args.epi == 98) {  // timing probe: MMA pipeline without operand traffic
+            mbar_arrive(&full[stage]);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
           const int k0 = kb * BK;
           if constexpr (!kAMN) {
@@ -190,46 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(t_row + c, r);
-        tmem_ld_wait();
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-        if (args.epi == EPI_ACC_F32) {
-          float* out = reinterpret_cast<float*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) {
-            float4 o = *reinterpret_cast<float4*>(out + i);
-            o.x += v[i];
-            o.y += v[i + 1];
-            o.z += v[i + 2];
-            o.w += v[i + 3];
-            *reinterpret_cast<float4*>(out + i) = o;
-          }
-        } else if (args.epi == EPI_STORE_F32) {
-          float* out = reinterpret_cast<float*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
-#pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(out + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-          if (args.bias) {
-            const BF8* bp = reinterpret_cast<const BF8*>(args.bias + n0 + c);
-            float b[16];
-            bf8_to_f(bp[0], b);
-            bf8_to_f(bp[1], b + 8);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += b[i];
-          }
-          __nv_bfloat16* out =
-              reinterpret_cast<__nv_bfloat16*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
-          BF8* o = reinterpret_cast<BF8*>(out);
-          o[0] = f_to_bf8(v);
-          o[1] = f_to_bf8(v + 8);
-        }
-      }
+      epilogue_row<BN>(args, t_row, row, n0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[acc]);
@@ -346,9 +363,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tile_coords(tile, m_tiles, n_tiles, mt, nt);
         const int m0 = mt * kTileM + rank * kHalf, n0 = nt * kTileN + rank * kHalf;
         for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_spin(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes;
           uint8_t* sb = sa + kABytes;
+          if (args.epi == 98) {  // timing probe: MMA pipeline without operand traffic
+            if (leader) {
+              mbar_arrive(&full[stage]);
+            } else {
+              arrive_leader(&full[stage]);
+            }
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if (leader) {
             mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
           } else {
@@ -382,11 +411,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
-        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        mbar_wait_spin(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kTileN;
         for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_spin(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t sa = smem_u32(smem + stage * kStageBytes);
@@ -423,49 +452,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(tile, m_tiles, n_tiles, mt, nt);
       const int row = mt * kTileM + rank * kHalf + ew * 32 + lane;
       const int n0 = nt * kTileN;
-      mbar_wait(&tmem_full[acc], acc_phase);
+      mbar_wait_spin(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kTileN;
-#pragma unroll 1
-      for (int c = 0; c < kTileN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(t_row + c, r);
-        tmem_ld_wait();
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-        if (args.epi == EPI_ACC_F32) {
-          float* out = reinterpret_cast<float*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) {
-            float4 o = *reinterpret_cast<float4*>(out + i);
-            o.x += v[i];
-            o.y += v[i + 1];
-            o.z += v[i + 2];
-            o.w += v[i + 3];
-            *reinterpret_cast<float4*>(out + i) = o;
-          }
-        } else if (args.epi == EPI_STORE_F32) {
-          float* out = reinterpret_cast<float*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
-#pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(out + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-          if (args.bias) {
-            const BF8* bp = reinterpret_cast<const BF8*>(args.bias + n0 + c);
-            float b[16];
-            bf8_to_f(bp[0], b);
-            bf8_to_f(bp[1], b + 8);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += b[i];
-          }
-          __nv_bfloat16* out =
-              reinterpret_cast<__nv_bfloat16*>(args.c) + static_cast<long long>(row) * args.ldc + n0 + c;
-          BF8* o = reinterpret_cast<BF8*>(out);
-          o[0] = f_to_bf8(v);
-          o[1] = f_to_bf8(v + 8);
-        }
-      }
+      epilogue_row<kTileN>(args, t_row, row, n0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) arrive_leader(&tmem_empty[acc]);
@@ -570,7 +560,11 @@ int launch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
 }  // namespace gemm
 
 namespace {
-int g_gemm_mode = -1;  // -1 auto (2-CTA where the shape allows), 0 force 1-CTA
+// 0 (default): single-CTA 128xBN kernel. 1: CTA-pair 256x256 kernel where the
+// shape allows. The pair kernel's MMA pipe alone reaches ~1.9 PFLOP/s but its
+// 2SM-TMA operand path currently starves it (~0.9 PFLOP/s end to end, see
+// profiles/), so it is opt-in until that is fixed.
+int g_gemm_mode = 0;
 }
 
 void gemm_set_mode(int mode) { g_gemm_mode = mode; }
@@ -582,7 +576,7 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   if (g.N % 128) return set_error("gemm: N must be a multiple of 128");
   if ((g.epi == EPI_BF16 && g.ldc % 8) || (g.epi != EPI_BF16 && g.ldc % 4))
     return set_error("gemm: ldc must keep 16-byte row alignment");
-  if (g_gemm_mode != 0 && g.M % pair::kTileM == 0 && g.N % pair::kTileN == 0 &&
+  if (g_gemm_mode == 1 && g.M % pair::kTileM == 0 && g.N % pair::kTileN == 0 &&
       (g.M / pair::kTileM) * (g.N / pair::kTileN) >= 32) {
     if (!g.a_mn && !g.b_mn) return launch_pair<false, false>(g, stream, max_ctas);
     if (!g.a_mn && g.b_mn) return launch_pair<false, true>(g, stream, max_ctas);

@@ -49,6 +49,7 @@ Executor::Executor(const std::string& profile_json, const std::string& timeline_
   parse_config(config_json);
   bind_template();
   if (opt_.dry_run) return;
+  if (needs_comms_) init_comms(nccl_id_, world_rank_, world_size_);
   for (cudaStream_t* s : {&main_, &side_, &tp_s_, &pa_s_, &pg_s_})
     ck(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "stream");
   int dev = 0;
@@ -116,15 +117,23 @@ void Executor::parse_config(const std::string& text) {
     throw RtError("tokens per microbatch must be a multiple of 128 and of the head chunk", kValidation);
   if (cfg_.vocab % 128) throw RtError("vocab must be padded to a multiple of 128", kValidation);
   ps_.layout(cfg_);
-  if (!opt_.dry_run && (cfg_.tp > 1 || cfg_.pp > 1))
-    init_comms(par.value("nccl_id", std::string()), par.value("world_rank", 0), par.value("world_size", 1));
+  nccl_id_ = par.value("nccl_id", std::string());
+  world_rank_ = par.value("world_rank", 0);
+  world_size_ = par.value("world_size", 1);
 }
 
 void Executor::init_comms(const std::string& id_hex, int world_rank, int world_size) {
-  if (id_hex.size() != 2 * sizeof(ncclUniqueId)) throw RtError("parallel.nccl_id must be a hex ncclUniqueId", kValidation);
   ncclUniqueId id;
-  for (size_t i = 0; i < sizeof(id); ++i)
-    id.internal[i] = static_cast<char>(hex_val(id_hex[2 * i]) * 16 + hex_val(id_hex[2 * i + 1]));
+  if (id_hex.empty() && world_size == 1) {
+    // Single rank with the TP template: the all-reduce windows run on a
+    // one-rank communicator (identity reduction), exercising the same streams.
+    nccl(ncclGetUniqueId(&id), "ncclGetUniqueId");
+  } else {
+    if (id_hex.size() != 2 * sizeof(ncclUniqueId))
+      throw RtError("parallel.nccl_id must be a hex ncclUniqueId", kValidation);
+    for (size_t i = 0; i < sizeof(id); ++i)
+      id.internal[i] = static_cast<char>(hex_val(id_hex[2 * i]) * 16 + hex_val(id_hex[2 * i + 1]));
+  }
   nccl(ncclCommInitRank(&world_, world_size, id, world_rank), "ncclCommInitRank");
   // TP groups: ranks sharing a pipeline stage; PP groups: ranks sharing a TP rank.
   // Activations (s -> s+1) and gradients (s+1 -> s) use separate communicators
@@ -148,7 +157,9 @@ void Executor::bind_template() {
     deps_.push_back(d);
   }
   const bool tp_tmpl = !L.fwd_comm_ids.empty();
-  if (tp_tmpl != (cfg_.tp > 1)) throw RtError("profile template does not match the TP degree", kValidation);
+  if (cfg_.tp > 1 && !tp_tmpl) throw RtError("tp > 1 needs the tensor-parallel layer template", kValidation);
+  needs_comms_ = tp_tmpl || cfg_.tp > 1 || cfg_.pp > 1;
+  tp_tmpl_ = tp_tmpl;
   static const std::vector<Op> t1 = {Op::LN1, Op::QKV, Op::ATTN, Op::PROJ_RES, Op::LN2, Op::FC1,
                                      Op::GELU, Op::FC2_RES, Op::MLP_BWD, Op::ATTN_BWD, Op::LN1_BWD};
   static const std::vector<Op> t2 = {Op::LN1, Op::QKV, Op::ATTN, Op::PROJ, Op::AR1, Op::LN2, Op::FC1, Op::GELU,
@@ -278,6 +289,10 @@ void Executor::mark_ready(Slot& sl, cudaStream_t s) {
 
 void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
   if (!sl.p) return;
+  if (std::getenv("LYNX_TRACE_SLOTS")) {
+    const size_t idx = static_cast<size_t>(&sl - slots_.data());
+    std::fprintf(stderr, "drop mb%zu l%zu op%zu\n", idx / (cfg_.layers * nf_), (idx / nf_) % cfg_.layers, idx % nf_);
+  }
   if (keep_shadow && opt_.check_recompute && !sl.shadow) {
     sl.shadow = sl.p;  // forward-produced copy, compared against the regeneration
   } else {
@@ -370,6 +385,8 @@ void Executor::collect_spans() {
 void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
   const Op op = op_of_[pos];
   Slot& out = slot(mb, l, pos);
+  if (std::getenv("LYNX_TRACE_SLOTS"))
+    std::fprintf(stderr, "fwd mb%d l%d op%d %s%s\n", mb, l, pos, op_name(op), recompute ? " (recompute)" : "");
   if (out.p) {
     if (recompute) return;  // already resident (duplicate placement)
     throw RtError("forward tensor produced twice", kParse);
@@ -414,7 +431,7 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
       break;
     case Op::LN2:
       bytes = 2 * T * h + 8 * T;
-      in = need(mb, l, pos_of(cfg_.tp > 1 ? Op::AR1 : Op::PROJ_RES), s);
+      in = need(mb, l, pos_of(tp_tmpl_ ? Op::AR1 : Op::PROJ_RES), s);
       break;
     case Op::FC1:
       bytes = 2 * T * 4 * hp;
@@ -605,7 +622,7 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
     if (!opt_.dry_run)
       ck_op(column_sum_acc(static_cast<const __nv_bfloat16*>(x), acc, sc.ws, T, static_cast<int>(width), s), "colsum");
   };
-  const bool tp = cfg_.tp > 1;
+  const bool tp = tp_tmpl_;  // template with all-reduce ops (ar1/ar2 carry the residual epilogues)
   switch (op) {
     case Op::MLP_BWD: {
       void* gelu = need(mb, l, pos_of(Op::GELU), s);
@@ -616,12 +633,12 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
                           drop_stream(l, mb, tp ? Op::AR2 : Op::FC2_RES), s),
               "dropout_bwd");
       colsum(sc.t_h, P.g_b_fc2, h);
-      gemm(sc.t_h, h, true, gelu, 4 * hp, true, P.g_w_fc2, 4 * hp, h, 4 * hp, T, EPI_ACC_F32);   // dW_fc2 += d^T gelu
+      gemm(sc.t_h, h, true, gelu, 4 * hp, true, P.g_w_fc2, 4 * hp, h, 4 * hp, T, dw_epi_);      // dW_fc2 += d^T gelu
       gemm(sc.t_h, h, false, P.w_fc2, 4 * hp, true, sc.t_wide, 4 * hp, T, 4 * hp, h, EPI_BF16);  // dgelu = d W_fc2
       if (!opt_.dry_run)
         ck_op(gelu_bwd(sc.t_wide, static_cast<const __nv_bfloat16*>(fc1), sc.t_wide, T * 4 * hp, s), "gelu_bwd");
       colsum(sc.t_wide, P.g_b_fc1, 4 * hp);
-      gemm(sc.t_wide, 4 * hp, true, y2, h, true, P.g_w_fc1, h, 4 * hp, h, T, EPI_ACC_F32);     // dW_fc1 += dfc1^T y2
+      gemm(sc.t_wide, 4 * hp, true, y2, h, true, P.g_w_fc1, h, 4 * hp, h, T, dw_epi_);       // dW_fc1 += dfc1^T y2
       G.dln2 = alloc(T * h * 2, s);
       gemm(sc.t_wide, 4 * hp, false, P.w_fc1, h, true, G.dln2, h, T, h, 4 * hp, EPI_BF16);     // dln2 = dfc1 W_fc1
       break;
@@ -647,14 +664,14 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
       release(G.dln2, s);
       G.dln2 = nullptr;
       colsum(sc.t_h, P.g_b_proj, h);
-      gemm(sc.t_h, h, true, attn, hp, true, P.g_w_proj, hp, h, hp, T, EPI_ACC_F32);        // dW_proj += d^T O
+      gemm(sc.t_h, h, true, attn, hp, true, P.g_w_proj, hp, h, hp, T, dw_epi_);          // dW_proj += d^T O
       gemm(sc.t_h, h, false, P.w_proj, hp, true, sc.t_h2, hp, T, hp, h, EPI_BF16);         // dO = d W_proj
       if (!opt_.dry_run)
         ck_op(attention_bwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(attn), sc.t_h2,
                             lse, sc.t_wide, sc.ws, cfg_.micro_batch, cfg_.seq, cfg_.heads_rank(), cfg_.head_dim, s),
               "attention_bwd");
       colsum(sc.t_wide, P.g_b_qkv, 3 * hp);
-      gemm(sc.t_wide, 3 * hp, true, ln1, h, true, P.g_w_qkv, h, 3 * hp, h, T, EPI_ACC_F32);  // dW_qkv += dqkv^T y1
+      gemm(sc.t_wide, 3 * hp, true, ln1, h, true, P.g_w_qkv, h, 3 * hp, h, T, dw_epi_);    // dW_qkv += dqkv^T y1
       G.dln1 = alloc(T * h * 2, s);
       gemm(sc.t_wide, 3 * hp, false, P.w_qkv, h, true, G.dln1, h, T, h, 3 * hp, EPI_BF16);   // dln1 = dqkv W_qkv
       break;
@@ -784,6 +801,10 @@ void Executor::forward_pass(int mb) {
 }
 
 void Executor::backward_pass(int mb) {
+  // The first backward pass of the step writes the layer weight gradients
+  // (fp32 store epilogue); later microbatches accumulate into them.
+  dw_epi_ = bwd_passes_ == 0 ? EPI_STORE_F32 : EPI_ACC_F32;
+  ++bwd_passes_;
   const long long T = cfg_.tokens();
   const int h = cfg_.hidden;
   // cool-down stall fill: released before the gradient arrives (pipesim.cpp:620-646)
@@ -876,6 +897,7 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   open_.clear();
   program_.clear();
   rep_ = StepReport{};
+  bwd_passes_ = 0;
   const long long T = cfg_.tokens();
   const size_t ntok = static_cast<size_t>(cfg_.n_micro) * T;
   const auto passes = host::stage_passes(cfg_.pp, cfg_.pp_rank, cfg_.n_micro);

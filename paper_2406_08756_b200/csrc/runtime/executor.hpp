@@ -132,6 +132,10 @@ class Executor {
   host::StageTimeline tl_;
   ModelCfg cfg_;
   ExecOptions opt_;
+  std::string nccl_id_;
+  int world_rank_ = 0, world_size_ = 1;
+  bool needs_comms_ = false;
+  bool tp_tmpl_ = false;
   int nf_ = 0, n_ = 0;
   std::vector<Op> op_of_;
   std::vector<host::Element> fel_, bel_;
@@ -163,6 +167,8 @@ class Executor {
   std::vector<CommOp> program_;
   StepReport rep_;
   int step_ = 0;
+  int bwd_passes_ = 0;
+  int dw_epi_ = 1;  // EPI_ACC_F32
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   std::vector<std::tuple<int, int, int, int, double, double>> trace_;  // stage, mb, kind, op, start, end
 };

@@ -43,6 +43,11 @@ class GPTConfig:
     dropout: float = 0.1
     mem_budget_bytes: int = 0  # 0 -> derive from device capacity
     comm_scale: str = "1"
+    # Use the tensor-parallel template (with its four all-reduce windows) even at tp = 1;
+    # the executor then runs the all-reduces on a one-rank communicator. Window times are
+    # modelled for tp_model ranks so the planner has windows to fill.
+    tp_template: bool = False
+    tp_model: int = 2
 
     @property
     def head_dim(self) -> int:
@@ -101,8 +106,10 @@ def estimate_times(c: GPTConfig, gemm_tflops: float = 1200.0, attn_tflops: float
     def mem(nbytes):
         return nbytes / (hbm_gbs * 1e3)
 
+    tw = c.tp_model if (c.tp == 1 and c.tp_template) else t
+
     def ar(nbytes):
-        return 0.0 if t == 1 else 2.0 * (t - 1) / t * nbytes / (nvlink_gbs * 1e3)
+        return 0.0 if tw == 1 else 2.0 * (tw - 1) / tw * nbytes / (nvlink_gbs * 1e3)
 
     attn_f = 2.0 * b * (c.heads // t) * s * s * (h // c.heads) / (attn_tflops * 1e6)  # causal: QK^T + PV halves
     est = {
@@ -137,7 +144,7 @@ def _op(i, name, kind, time_us: Fraction, out_bytes, deps):
 
 def layer_template(c: GPTConfig, times: dict[str, Fraction]) -> dict:
     B = op_bytes(c)
-    if c.tp > 1:
+    if c.tp > 1 or c.tp_template:
         spec = [
             ("ln1", "compute", B["ln"], []), ("qkv", "compute", B["qkv"], [0]), ("attn", "compute", B["attn"], [1]),
             ("proj", "compute", 0, [2]), ("ar1", "comm", B["act"], [3]), ("ln2", "compute", B["ln"], [4]),

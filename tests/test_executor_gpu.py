@@ -63,6 +63,24 @@ def test_heu_plan_under_tight_budget_is_bit_identical(cuda):
         assert np.array_equal(g_keep[k], g_heu[k]), k
 
 
+def test_window_recompute_on_side_stream_is_bit_identical(cuda):
+    """TP block template on one GPU (all-reduces on a one-rank NCCL communicator): the HEU plan puts
+    recomputation into the all-reduce windows, which the executor runs on the side stream."""
+    from paper_2406_08756_b200 import gpt_profile as gp
+    base = dict(name="gpt-tiny-tp", n_layers=4, hidden=512, heads=8, seq=256, micro_batch=2, vocab=50304, tp=1, pp=1,
+                n_microbatches=2, dropout=0.1, tp_template=True)
+    static = gp.BYTES_PER_PARAM_STATIC * gp.GPTConfig(**base).params()
+    tight = gp.GPTConfig(**{**base, "mem_budget_bytes": static + 22 * 2**20})
+    l_heu, g_heu, _, r_heu, plan, _, _ = run(tight, "heu", check=True)
+    hosts = {it["host"] for it in plan["timeline"]["items"]}
+    assert "window" in hosts, plan["plan_json"]
+    assert r_heu["recompute_overlapped_ms"] > 0 and r_heu["recompute_mismatch_words"] == 0
+    l_keep, g_keep, _, _, _, _, _ = run(gp.GPTConfig(**base), "retain_all")
+    assert l_heu == l_keep
+    for k in g_keep:
+        assert np.array_equal(g_keep[k], g_heu[k]), k
+
+
 def test_loss_and_grads_match_cpu_oracle(cuda):
     from oracle import gpt_oracle
     c = tiny(n_micro=2, dropout=0.0)
