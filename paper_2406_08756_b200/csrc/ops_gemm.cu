@@ -335,7 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_a);
     tma_prefetch_desc(&tm_b);
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 2);   // leader's expect_tx arrival + the peer producer's arrival
+      mbar_init(&full[s], 1);   // the leader's expect_tx arrival (the peer contributes bytes only)
       mbar_init(&empty[s], 1);  // the leader's multicast commit
     }
     for (int b = 0; b < 2; ++b) {
@@ -367,22 +367,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           uint8_t* sa = smem + stage * kStageBytes;
           uint8_t* sb = sa + kABytes;
           if (args.epi == 98) {  // timing probe: MMA pipeline without operand traffic
-            if (leader) {
-              mbar_arrive(&full[stage]);
-            } else {
-              arrive_leader(&full[stage]);
-            }
+            if (leader) mbar_arrive(&full[stage]);
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1;
             }
             continue;
           }
-          if (leader) {
-            mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
-          } else {
-            arrive_leader(&full[stage]);
+          if (args.epi == 97) {  // timing probe: per-CTA TMA to the CTA's own barrier (leader waits on its own)
+            const int k0 = kb * BK;
+            if (leader) mbar_arrive_expect_tx(&full[stage], kStageBytes);
+            tma_load_2d(&tm_a, &full[stage], sa, k0, m0, kEvictNormal);
+            tma_load_2d(&tm_b, &full[stage], sb, k0, n0, kEvictNormal);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
           }
+          // Only the leader arms the stage barrier (both CTAs' bytes). The peer's
+          // complete_tx may land before the arm — the transaction count is allowed
+          // to go negative while the leader's arrival is still pending — so the
+          // peer needs no remote arrive (and no cluster-scope fence) per stage.
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
           const int k0 = kb * BK;
           if constexpr (!kAMN) {
             tma_load_2sm(&tm_a, &full[stage], sa, k0, m0);
@@ -560,11 +567,10 @@ int launch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
 }  // namespace gemm
 
 namespace {
-// 0 (default): single-CTA 128xBN kernel. 1: CTA-pair 256x256 kernel where the
-// shape allows. The pair kernel's MMA pipe alone reaches ~1.9 PFLOP/s but its
-// 2SM-TMA operand path currently starves it (~0.9 PFLOP/s end to end, see
-// profiles/), so it is opt-in until that is fixed.
-int g_gemm_mode = 0;
+// -1 (default): CTA-pair 256x256 kernel for K-major-A GEMMs (forward, dX) where
+// the shape allows, single-CTA otherwise (the MN-major-A weight-gradient GEMMs
+// measure the same on both). 0: single-CTA only. 1: pair wherever the shape allows.
+int g_gemm_mode = -1;
 }
 
 void gemm_set_mode(int mode) { g_gemm_mode = mode; }
@@ -576,7 +582,8 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   if (g.N % 128) return set_error("gemm: N must be a multiple of 128");
   if ((g.epi == EPI_BF16 && g.ldc % 8) || (g.epi != EPI_BF16 && g.ldc % 4))
     return set_error("gemm: ldc must keep 16-byte row alignment");
-  if (g_gemm_mode == 1 && g.M % pair::kTileM == 0 && g.N % pair::kTileN == 0 &&
+  const bool want_pair = g_gemm_mode == 1 || (g_gemm_mode == -1 && !g.a_mn);
+  if (want_pair && g.M % pair::kTileM == 0 && g.N % pair::kTileN == 0 &&
       (g.M / pair::kTileM) * (g.N / pair::kTileN) >= 32) {
     if (!g.a_mn && !g.b_mn) return launch_pair<false, false>(g, stream, max_ctas);
     if (!g.a_mn && g.b_mn) return launch_pair<false, true>(g, stream, max_ctas);

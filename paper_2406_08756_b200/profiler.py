@@ -1,0 +1,152 @@
+"""GPU profiler: B200-measured operator times for the profile document.
+
+The reference's profile carries per-operator times the paper obtains from a
+CUDA-event profiler of the real model (out of the
+reference's own scope). This module measures exactly the kernel
+sequence the executor launches for each template operator (the same C-ABI
+kernels, the same shapes per TP rank) with CUDA events, so that HEU's window
+capacities and recompute costs are B200-true:
+
+    times = measure_op_times(cfg)            # {op name: Fraction(µs)}
+    profile = gpt_profile.profile(cfg, times=times)
+
+All-reduce ops cannot be timed on one GPU; their time is the measured residual
+epilogue plus the NVLink model (2(t-1)/t · bytes / 725 GB/s, the measured
+8-rank bus bandwidth in B200_PROFILING.md).
+"""
+from __future__ import annotations
+
+import math
+from fractions import Fraction
+
+import torch
+
+from . import gpt_profile as gp
+from . import ops
+
+NVLINK_BUS_GBS = 725.0
+
+
+def _time(fn, iters: int = 5, warm: int = 2) -> float:
+    for _ in range(warm):
+        fn()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return 1000.0 * s.elapsed_time(e) / iters  # µs
+
+
+def measure_op_times(c: gp.GPTConfig, iters: int = 5) -> dict[str, Fraction]:
+    dev = "cuda"
+    T, h, t = c.tokens, c.hidden, c.tp
+    hp = h // t
+    H = c.heads // t
+    D = c.head_dim
+    bf = torch.bfloat16
+    r = lambda *s: (torch.randn(*s, device=dev) * 0.02).to(bf)  # noqa: E731
+    x, y = r(T, h), r(T, h)
+    gam, bet = torch.ones(h, device=dev, dtype=bf), torch.zeros(h, device=dev, dtype=bf)
+    w_qkv, b_qkv, w_proj, b_proj = r(3 * hp, h), r(3 * hp), r(h, hp), r(h)
+    w_fc1, b_fc1, w_fc2, b_fc2 = r(4 * hp, h), r(4 * hp), r(h, 4 * hp), r(h)
+    qkv = r(T, 3 * hp)
+    fc1 = r(T, 4 * hp)
+    attn_o, lse = ops.attention_fwd(qkv, c.micro_batch, c.seq, H, D)
+    times: dict[str, float] = {}
+
+    times["ln1"] = times["ln2"] = _time(lambda: ops.layernorm_fwd(x, gam, bet), iters)
+    times["qkv"] = _time(lambda: ops.gemm(x, w_qkv, bias=b_qkv), iters)
+    times["attn"] = _time(lambda: ops.attention_fwd(qkv, c.micro_batch, c.seq, H, D), iters)
+    proj = lambda: ops.gemm(attn_o, w_proj, bias=b_proj if t == 1 else None)  # noqa: E731
+    times["proj"] = _time(proj, iters)
+    resid = _time(lambda: ops.bias_dropout_residual(y, b_proj, x, c.dropout, 1, 2), iters)
+    times["proj_res"] = times["proj"] + resid
+    times["fc1"] = _time(lambda: ops.gemm(y, w_fc1, bias=b_fc1), iters)
+    times["gelu"] = _time(lambda: ops.gelu_fwd(fc1), iters)
+    times["fc2"] = _time(lambda: ops.gemm(fc1, w_fc2, bias=b_fc2 if t == 1 else None), iters)
+    times["fc2_res"] = times["fc2"] + resid
+    tw = c.tp_model if (t == 1 and c.tp_template) else t
+    ar = 0.0 if tw == 1 else 2.0 * (tw - 1) / tw * (2 * T * h) / (NVLINK_BUS_GBS * 1e3)
+    times["ar1"] = times["ar2"] = ar + resid
+    times["ar_b1"] = times["ar_b2"] = ar
+
+    g_fc2 = torch.zeros(h, 4 * hp, device=dev)
+    g_fc1 = torch.zeros(4 * hp, h, device=dev)
+    g_b = torch.zeros(4 * hp, device=dev)
+
+    def mlp_bwd():
+        d = ops.dropout_bwd(y, c.dropout, 1, 3)
+        ops.column_sum_acc(d, g_b[:h])
+        ops.gemm(d, fc1, a_mn=True, b_mn=True, out=g_fc2, epi=ops.EPI_ACC_F32)
+        dg = ops.gemm(d, w_fc2, b_mn=True)
+        df = ops.gelu_bwd(dg, fc1)
+        ops.column_sum_acc(df, g_b)
+        ops.gemm(df, y, a_mn=True, b_mn=True, out=g_fc1, epi=ops.EPI_ACC_F32)
+        ops.gemm(df, w_fc1, b_mn=True)
+
+    times["mlp_bwd"] = _time(mlp_bwd, iters)
+    del g_fc2, g_fc1
+    g_proj = torch.zeros(h, hp, device=dev)
+    g_qkv = torch.zeros(3 * hp, h, device=dev)
+    mean = torch.zeros(T, device=dev)
+    rstd = torch.ones(T, device=dev)
+    gl = torch.zeros(h, device=dev)
+
+    def attn_bwd():
+        dres = ops.layernorm_bwd(y, x, gam, mean, rstd, gl, gl, dres=y)
+        d = ops.dropout_bwd(dres, c.dropout, 1, 4)
+        ops.column_sum_acc(d, gl)
+        ops.gemm(d, attn_o, a_mn=True, b_mn=True, out=g_proj, epi=ops.EPI_ACC_F32)
+        do = ops.gemm(d, w_proj, b_mn=True)
+        dqkv = ops.attention_bwd(qkv, attn_o, do, lse, c.micro_batch, c.seq, H, D)
+        ops.column_sum_acc(dqkv, g_b[:3 * hp])
+        ops.gemm(dqkv, y, a_mn=True, b_mn=True, out=g_qkv, epi=ops.EPI_ACC_F32)
+        ops.gemm(dqkv, w_qkv, b_mn=True)
+
+    times["attn_bwd"] = _time(attn_bwd, iters)
+    times["ln1_bwd"] = _time(lambda: ops.layernorm_bwd(y, x, gam, mean, rstd, gl, gl, dres=y), iters)
+    del g_proj, g_qkv, fc1
+    tok = torch.randint(0, 50257, (T,), device=dev, dtype=torch.int32)
+    wte, wpe = r(c.vocab, h), r(c.seq, h)
+    times["embed"] = _time(lambda: ops.embedding_fwd(tok, wte, wpe, c.micro_batch, c.seq, c.dropout, 1, 5), iters)
+    times["final_ln"] = times["ln1"]
+    chunk = min(4096, T)
+    w_head = r(c.vocab, h)
+    g_head = torch.zeros(c.vocab, h, device=dev)
+    logits = torch.empty(chunk, c.vocab, device=dev, dtype=bf)
+    lab = torch.randint(0, c.vocab, (chunk,), device=dev, dtype=torch.int32)
+
+    def head():
+        for c0 in range(0, T, chunk):
+            ops.gemm(x[c0:c0 + chunk], w_head, out=logits)
+            ops.xent_fwd_bwd(logits, lab, 1.0)
+            ops.gemm(logits, x[c0:c0 + chunk], a_mn=True, b_mn=True, out=g_head, epi=ops.EPI_ACC_F32)
+            ops.gemm(logits, w_head, b_mn=True)
+
+    times["lm_head"] = _time(head, max(2, iters // 2))
+    del g_head, logits, w_head, wte
+    torch.cuda.empty_cache()
+    return {k: Fraction(max(1, round(v * 1000)), 1000) for k, v in times.items()}
+
+
+def measured_profile(c: gp.GPTConfig, device_bytes: int | None = None, reserve_bytes: int = 0) -> tuple[dict, dict]:
+    times = measure_op_times(c)
+    return gp.profile(c, times=times, device_bytes=device_bytes, reserve_bytes=reserve_bytes), times
+
+
+def times_json(times: dict[str, Fraction]) -> dict[str, str]:
+    return {k: (str(v.numerator) if v.denominator == 1 else f"{v.numerator}/{v.denominator}") for k, v in times.items()}
+
+
+if __name__ == "__main__":  # pragma: no cover
+    import json
+    import sys
+    cfg = gp.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "tiny"]
+    if len(sys.argv) > 2:
+        cfg = gp.GPTConfig(**{**cfg.__dict__, "tp": int(sys.argv[2])})
+    t = measure_op_times(cfg)
+    print(json.dumps({k: float(v) for k, v in t.items()}, indent=1))
+    _ = math

@@ -111,3 +111,21 @@ def test_training_reduces_loss(cuda):
     losses = [e.step(tok, lab) for _ in range(8)]
     e.close()
     assert losses[-1] < losses[0] - 0.5, losses
+
+
+def test_profiler_measures_every_template_op(cuda):
+    """The B200 profiler times every operator of both templates; the measured
+    profile is a valid planner input and the executor runs its plan."""
+    from paper_2406_08756_b200 import gpt_profile as gp
+    from paper_2406_08756_b200 import planner
+    from paper_2406_08756_b200 import profiler
+    c = tiny()
+    times = profiler.measure_op_times(c, iters=2)
+    for op in ["ln1", "qkv", "attn", "proj_res", "ln2", "fc1", "gelu", "fc2_res", "mlp_bwd", "attn_bwd", "ln1_bwd",
+               "embed", "final_ln", "lm_head", "proj", "fc2", "ar1", "ar2"]:
+        assert times[op] > 0, op
+    assert times["fc1"] > times["gelu"] and times["attn_bwd"] > times["attn"]
+    text = gp.profile_text(c, times=times)
+    assert planner.validate_text(text)[1] == 0
+    losses, _, _, rep, _, _, _ = run(c, "heu")
+    assert np.isfinite(losses[0])

@@ -57,7 +57,7 @@ def test_gemm_pair_and_single_cta(ops, cuda, a_mn, b_mn, mode):
         ops.gemm(a, b, a_mn=a_mn, b_mn=b_mn, out=acc, epi=ops.EPI_ACC_F32)
         torch.cuda.synchronize()
     finally:
-        lib().lynx_op_gemm_mode(0)
+        lib().lynx_op_gemm_mode(-1)
     ref = A.float() @ B.float().t()
     assert rel(out, ref + bias.float()) < 1e-2
     assert rel(acc, ref + 1) < 1e-5

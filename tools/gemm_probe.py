@@ -1,4 +1,5 @@
-"""GEMM kernel variants on one shape: single-CTA vs CTA-pair; full / no epilogue (99) / MMA only (98).
+"""GEMM kernel variants on one shape: single-CTA vs CTA-pair; full / no epilogue (99) / MMA only (98) /
+pair with per-CTA TMA signalling only the CTA's own barrier (97, K-major only, timing only).
 
     python tools/gemm_probe.py [T]
 """
@@ -34,9 +35,10 @@ for (name, M, N, K, amn, bmn, epi) in [("fc1_fwd", T, 4 * h, h, False, False, 0)
     out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if epi else torch.bfloat16)
     for mode in (0, 1):
         lib().lynx_op_gemm_mode(mode)
-        for e in (epi, 99, 98):
+        variants = (epi, 99, 98) + ((97,) if (mode == 1 and not amn and not bmn) else ())
+        for e in variants:
             ms = timeit(lambda: ops.gemm(a, b, a_mn=amn, b_mn=bmn, out=out, epi=e))
             print(json.dumps({"gemm": name, "mode": "pair" if mode else "single",
-                              "variant": {98: "mma-only", 99: "no-epilogue"}.get(e, f"epi{e}"),
+                              "variant": {97: "own-barrier-tma", 98: "mma-only", 99: "no-epilogue"}.get(e, f"epi{e}"),
                               "ms": round(ms, 4), "tflops": round(2.0 * M * N * K / ms / 1e9, 1)}), flush=True)
-    lib().lynx_op_gemm_mode(0)
+    lib().lynx_op_gemm_mode(-1)
