@@ -87,6 +87,9 @@ int lynx_op_attention_fwd(const void* qkv, void* out, float* lse, int batch, int
 size_t lynx_op_attention_bwd_workspace(int batch, int seq, int heads);
 int lynx_op_attention_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
                           float* workspace, int batch, int seq, int heads, int head_dim, void* stream);
+/* Attention kernel selection: -1 (default) the tcgen05 kernels (TMEM accumulators, TMA tiles) when
+ * head_dim is 64 or 128 and seq % 128 == 0, else the mma.sync kernels; 0 mma.sync kernels only. */
+void lynx_op_attention_mode(int mode);
 
 /* out[b,s] = dropout(wte[tokens[b,s]] + wpe[s]); backward accumulates fp32 dwte/dwpe. */
 int lynx_op_embedding_fwd(const int* tokens, const void* wte, const void* wpe, void* out, int batch, int seq,

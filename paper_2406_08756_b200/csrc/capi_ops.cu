@@ -54,6 +54,7 @@ int lynx_op_gemm(const void* a, long long lda, int a_mn_major, const void* b, lo
 }
 
 void lynx_op_gemm_mode(int mode) { gemm_set_mode(mode); }
+void lynx_op_attention_mode(int mode) { attention_set_mode(mode); }
 
 int lynx_op_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,
                           int rows, int width, float eps, void* stream) {

@@ -84,6 +84,15 @@ int attention_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv
                   __nv_bfloat16* dqkv, float* workspace, int batch, int seq, int heads, int head_dim,
                   cudaStream_t s);
 size_t attention_bwd_workspace(int batch, int seq, int heads);
+// tcgen05 attention (ops_attention_tc.cu): head_dim 64/128, seq % 128 == 0.
+// attention_set_mode: -1 (default) tcgen05 kernels where the shape allows, 0 mma.sync kernels only.
+void attention_set_mode(int mode);
+int attention_mode();
+bool attention_tc_supported(int seq, int head_dim);
+int attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int batch, int seq, int heads,
+                     int head_dim, cudaStream_t s);
+int attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* dvec,
+                     __nv_bfloat16* dqkv, int batch, int seq, int heads, int head_dim, cudaStream_t s);
 
 int adam_step(float* master, __nv_bfloat16* param, const float* grad, float* m, float* v, long long n, float lr,
               float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale, cudaStream_t s);

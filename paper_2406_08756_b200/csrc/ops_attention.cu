@@ -502,6 +502,10 @@ int bwd_launch(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bf
   constexpr int P = D + 8;
   const long long rows = static_cast<long long>(B) * S * H;
   attn_bwd_pre_kernel<D><<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(out, dout, dvec, B, S, H);
+  if (attention_tc_supported(S, D)) {
+    if (int rc = check_launch("attention_bwd_pre")) return rc;
+    return attention_bwd_tc(qkv, dout, lse, dvec, dqkv, B, S, H, D, s);
+  }
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = scale * kLog2e;
   const int smem_kv = (2 * 64 * P + 4 * 32 * P) * 2 + 4 * 32 * 4;
@@ -520,6 +524,7 @@ int bwd_launch(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bf
 int attention_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, int H, int D,
                   cudaStream_t s) {
   if (S % 64) return set_error("attention: seq must be a multiple of 64", kValidation);
+  if (attention_tc_supported(S, D)) return attention_fwd_tc(qkv, out, lse, B, S, H, D, s);
   switch (D) {
     case 64: return fwd_launch<64>(qkv, out, lse, B, S, H, s);
     case 96: return fwd_launch<96>(qkv, out, lse, B, S, H, s);

@@ -1,0 +1,639 @@
+// Causal attention on tcgen05 tensor cores (head_dim 64 / 128, seq % 128 == 0).
+//
+// Same contract and layouts as ops_attention.cu (qkv [T, 3*H*D] = [Q|K|V],
+// out [T, H*D], lse [B, H, S] natural log; backward writes dQ|dK|dV with the
+// qkv layout, deterministically). Every CTA is warp-specialised:
+//   warp 0      TMA producer (cp.async.bulk.tensor, 128-B swizzled tiles),
+//   warp 1      single-thread tcgen05.mma issuer, completion via tcgen05.commit,
+//   warp 2      TMEM allocator (512 columns),
+//   warps 4..7  "row" warps: one thread per TMEM lane (= one tile row) doing
+//               the softmax / gradient elementwise work between the MMAs and
+//               the epilogue.
+// The row warps hand bf16 P / dS tiles to the tensor core through shared
+// memory written in the canonical SW128 K-major layout (16-byte chunk c of
+// row r stored at chunk c ^ (r & 7)), fenced with fence.proxy.async.
+//
+// Forward  (per 128-query tile, 128-key tiles double-buffered):
+//   S_j = Q K_j^T -> TMEM (2 buffers, S_{j+1} runs while softmax j works),
+//   P_j = exp2(S_j*c - m) -> smem, O += P_j V_j (TMEM accumulator).
+//   Online softmax with lazy rescaling: O / l are rescaled only when a warp's
+//   running max grows by more than 2^8 (P stays <= 256, exact in fp32 sums).
+// Backward dK/dV (per 128-key tile, 64-query tiles double-buffered):
+//   S^T = K Q^T, dP^T = V dO^T -> TMEM; P^T, dS^T = P^T o (dP^T - D) -> smem;
+//   dV += P^T dO, dK += dS^T Q (TMEM accumulators, scaled once at the end).
+// Backward dQ (per 128-query tile, 64-key tiles double-buffered):
+//   S = Q K^T, dP = dO V^T -> TMEM; dS -> smem; dQ += dS K.
+// dQ is its own kernel (7 tile MMAs per tile pair instead of 5) so that no
+// gradient is accumulated with atomics: results are bit-reproducible.
+#include <cuda.h>
+
+#include "common.cuh"
+#include "lynx_ops_internal.h"
+
+namespace lynx {
+namespace gemm {
+bool make_map(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld, int box_inner,
+              int box_outer);
+}
+namespace attn_tc {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescale = 8.f;  // log2 units
+constexpr int kAtom = 128;       // bytes per swizzled row (64 bf16)
+
+LYNX_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+LYNX_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 1-D bulk copy global -> shared, completing on an mbarrier (16-B aligned, size % 16 == 0).
+LYNX_DEV void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+LYNX_DEV uint8_t* align1k(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~static_cast<uintptr_t>(1023));
+}
+
+// K-major operand whose rows are 128-B swizzled atoms of `atom_bytes` (rows x 128 B);
+// K step kk (16 elements) lives in atom kk/4 at +32 B per step.
+LYNX_DEV uint64_t kmaj(uint32_t base, int kk, uint32_t atom_bytes) {
+  return umma_desc_sw128(base + (kk >> 2) * atom_bytes + (kk & 3) * 32, 16, 1024);
+}
+// MN-major operand stored [K rows][64-element MN atoms of atom_bytes]; K step kk = 16 rows.
+LYNX_DEV uint64_t mnmaj(uint32_t base, int kk, uint32_t atom_bytes) {
+  return umma_desc_sw128(base + kk * 2048, atom_bytes, 1024);
+}
+
+// Store 8 bf16 (16 B) as chunk `c` of row `r` of a SW128 K-major tile (128-B rows).
+LYNX_DEV void st_sw128(uint8_t* tile, int r, int c, const BF8& v) {
+  *reinterpret_cast<BF8*>(tile + r * kAtom + ((c ^ (r & 7)) << 4)) = v;
+}
+
+LYNX_DEV float u2f(uint32_t v) { return __uint_as_float(v); }
+
+// ============================================================== forward
+template <int D>
+struct FwdL {
+  static constexpr int kTile = 128 * D * 2;  // one 128-row x D tile (D/64 atoms of 16 KB)
+  static constexpr int kQ = 0, kK = kTile, kV = 3 * kTile, kP = 5 * kTile, kBar = kP + 128 * 128 * 2;
+  static constexpr int kBytes = kBar + 128 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ out,
+                       float* __restrict__ lse, int S, int H, float scale_log2) {
+  using L = FwdL<D>;
+  constexpr int kA = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *p_full = bar + 7,
+           *pv_done = bar + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = qb + 1, HD = H * D, row0 = b * S;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+      mbar_init(s_full + i, 1);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S buffers at columns 0 / 128, O at 256
+
+  if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch_desc(&map_qkv);
+      mbar_arrive_expect_tx(q_full, L::kTile);
+      for (int a = 0; a < kA; ++a)
+        tma_load_2d(&map_qkv, q_full, smem + L::kQ + a * 16384, h * D + 64 * a, row0 + qb * 128, kEvictFirst);
+      for (int j = 0; j < n; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(kv_empty + st, ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(kv_full + st, 2 * L::kTile);
+        for (int a = 0; a < kA; ++a) {
+          tma_load_2d(&map_qkv, kv_full + st, smem + L::kK + st * L::kTile + a * 16384, HD + h * D + 64 * a,
+                      row0 + j * 128, kEvictLast);
+          tma_load_2d(&map_qkv, kv_full + st, smem + L::kV + st * L::kTile + a * 16384, 2 * HD + h * D + 64 * a,
+                      row0 + j * 128, kEvictLast);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idO = umma_idesc_bf16(128, D, false, true);
+      const uint32_t sQ = smem_u32(smem + L::kQ), sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV),
+                     sP = smem_u32(smem + L::kP);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(kv_full + st, (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16(tmem + st * 128, kmaj(sQ, kk, 16384), kmaj(sK + st * L::kTile, kk, 16384), idS, kk > 0);
+        umma_commit(s_full + st);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      if (n > 1) issue_s(1);
+      for (int j = 0; j < n; ++j) {
+        const int st = j & 1;
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_f16(tmem + 256, kmaj(sP, kk, 16384), mnmaj(sV + st * L::kTile, kk, 16384), idO, (j | kk) != 0);
+        umma_commit(pv_done);
+        umma_commit(kv_empty + st);
+        if (j + 2 < n) issue_s(j + 2);
+      }
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;
+    const uint32_t lanes = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    uint8_t* sP = smem + L::kP;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n; ++j) {
+      const int st = j & 1;
+      mbar_wait(s_full + st, (j >> 1) & 1);
+      tc_fence_after();
+      float x[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lanes + st * 128 + c * 32, reinterpret_cast<uint32_t*>(x + c * 32));
+      tmem_ld_wait();
+      const bool diag = j == qb;
+      float mt = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        float v = x[i] * scale_log2;
+        if (diag && i > r) v = -INFINITY;
+        x[i] = v;
+        mt = fmaxf(mt, v);
+      }
+      const float m_new = fmaxf(m_run, mt);
+      const bool need = __any_sync(0xffffffffu, m_new > m_run + kRescale);
+      float corr = 1.f;
+      if (need) {
+        corr = exp2f(m_run - m_new);
+        m_run = m_new;
+      }
+      float rs = 0.f;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        x[i] = exp2f(x[i] - m_run);
+        rs += x[i];
+      }
+      l_run = l_run * corr + rs;
+      if (j > 0) {
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        if (need) {
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lanes + 256 + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(u2f(o[i]) * corr);
+            tmem_st32(tmem + lanes + 256 + c * 32, o);
+          }
+          tmem_st_wait();
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) st_sw128(sP + (c >> 3) * 16384, r, c & 7, f_to_bf8(x + c * 8));
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(pv_done, (n - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l_run;
+    const int q = qb * 128 + r;
+    BF8* orow = reinterpret_cast<BF8*>(out + static_cast<long long>(row0 + q) * HD + h * D);
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld32(tmem + lanes + 256 + c * 32, o);
+      tmem_ld_wait();
+      float f[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]) * inv;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) orow[c * 4 + i] = f_to_bf8(f + 8 * i);
+    }
+    lse[(static_cast<long long>(b) * H + h) * S + q] = (m_run + log2f(l_run)) / kLog2e;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================== backward dK / dV
+template <int D>
+struct DkvL {
+  static constexpr int kKV = 128 * D * 2;  // K or V tile: D/64 atoms of 16 KB (128 rows)
+  static constexpr int kQT = 64 * D * 2;   // Q or dO tile: D/64 atoms of 8 KB (64 rows)
+  static constexpr int kK = 0, kV = kKV, kQ = 2 * kKV, kDO = kQ + 2 * kQT, kPT = kDO + 2 * kQT;
+  static constexpr int kDS = kPT + 2 * 16384, kVec = kDS + 2 * 16384;  // lse[2][64], dvec[2][64]
+  static constexpr int kBar = kVec + 4 * 256;
+  static constexpr int kBytes = kBar + 128 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
+                        const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse,
+                        const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
+                        float scale_log2) {
+  using L = DkvL<D>;
+  constexpr int kA = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *s_full = bar + 5, *pd_full = bar + 7,
+           *mma_done = bar + 9, *fin = bar + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int i0 = 2 * kb, n = S / 64 - i0, HD = H * D, row0 = b * S;
+  const long long vec0 = (static_cast<long long>(b) * H + h) * S;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(q_full + i, 1);
+      mbar_init(q_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(pd_full + i, 128);
+      mbar_init(mma_done + i, 1);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // TMEM: S^T[2] at 0 / 64, dP^T[2] at 128 / 192, dV at 256, dK at 384.
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(kv_full, 2 * L::kKV);
+      for (int a = 0; a < kA; ++a) {
+        tma_load_2d(&map_kv, kv_full, smem + L::kK + a * 16384, HD + h * D + 64 * a, row0 + kb * 128, kEvictFirst);
+        tma_load_2d(&map_kv, kv_full, smem + L::kV + a * 16384, 2 * HD + h * D + 64 * a, row0 + kb * 128,
+                    kEvictFirst);
+      }
+      for (int i = 0; i < n; ++i) {
+        const int st = i & 1, q0 = (i0 + i) * 64;
+        if (i >= 2) mbar_wait(q_empty + st, ((i >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(q_full + st, 2 * L::kQT + 512);
+        for (int a = 0; a < kA; ++a) {
+          tma_load_2d(&map_q, q_full + st, smem + L::kQ + st * L::kQT + a * 8192, h * D + 64 * a, row0 + q0,
+                      kEvictLast);
+          tma_load_2d(&map_do, q_full + st, smem + L::kDO + st * L::kQT + a * 8192, h * D + 64 * a, row0 + q0,
+                      kEvictLast);
+        }
+        bulk_load(smem + L::kVec + st * 256, lse + vec0 + q0, 256, q_full + st);
+        bulk_load(smem + L::kVec + 512 + st * 256, dvec + vec0 + q0, 256, q_full + st);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t idG = umma_idesc_bf16(128, D, false, true);
+      const uint32_t sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV), sQ = smem_u32(smem + L::kQ),
+                     sDO = smem_u32(smem + L::kDO), sPT = smem_u32(smem + L::kPT), sDS = smem_u32(smem + L::kDS);
+      auto issue_s = [&](int i) {
+        const int st = i & 1;
+        mbar_wait(q_full + st, (i >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          umma_f16(tmem + st * 64, kmaj(sK, kk, 16384), kmaj(sQ + st * L::kQT, kk, 8192), idS, kk > 0);
+          umma_f16(tmem + 128 + st * 64, kmaj(sV, kk, 16384), kmaj(sDO + st * L::kQT, kk, 8192), idS, kk > 0);
+        }
+        umma_commit(s_full + st);
+      };
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      if (n > 1) issue_s(1);
+      for (int i = 0; i < n; ++i) {
+        const int st = i & 1;
+        mbar_wait(pd_full + st, (i >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          umma_f16(tmem + 256, kmaj(sPT + st * 16384, kk, 16384), mnmaj(sDO + st * L::kQT, kk, 8192), idG,
+                   (i | kk) != 0);
+          umma_f16(tmem + 384, kmaj(sDS + st * 16384, kk, 16384), mnmaj(sQ + st * L::kQT, kk, 8192), idG,
+                   (i | kk) != 0);
+        }
+        umma_commit(mma_done + st);
+        umma_commit(q_empty + st);
+        if (i + 2 < n) issue_s(i + 2);
+      }
+      umma_commit(fin);
+    }
+  } else if (warp >= 4) {
+    const int k = (warp - 4) * 32 + lane;  // key row of the tile
+    const int key = kb * 128 + k;
+    const uint32_t lanes = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    for (int i = 0; i < n; ++i) {
+      const int st = i & 1, q0 = (i0 + i) * 64;
+      mbar_wait(q_full + st, (i >> 1) & 1);
+      mbar_wait(s_full + st, (i >> 1) & 1);
+      if (i >= 2) mbar_wait(mma_done + st, ((i >> 1) - 1) & 1);
+      tc_fence_after();
+      const float* sl = reinterpret_cast<const float*>(smem + L::kVec + st * 256);
+      const float* sd = reinterpret_cast<const float*>(smem + L::kVec + 512 + st * 256);
+      uint8_t* pt = smem + L::kPT + st * 16384;
+      uint8_t* ds = smem + L::kDS + st * 16384;
+      const bool diag = i < 2;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t s[32], dp[32];
+        tmem_ld32(tmem + lanes + st * 64 + half * 32, s);
+        tmem_ld32(tmem + lanes + 128 + st * 64 + half * 32, dp);
+        tmem_ld_wait();
+        float p[32], g[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int qi = half * 32 + c;
+          float v = exp2f(u2f(s[c]) * scale_log2 - sl[qi] * kLog2e);
+          if (diag && key > q0 + qi) v = 0.f;
+          p[c] = v;
+          g[c] = v * (u2f(dp[c]) - sd[qi]);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          st_sw128(pt, k, half * 4 + c, f_to_bf8(p + 8 * c));
+          st_sw128(ds, k, half * 4 + c, f_to_bf8(g + 8 * c));
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(pd_full + st);
+    }
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    const long long grow = static_cast<long long>(row0 + key) * 3 * HD;
+    BF8* dk = reinterpret_cast<BF8*>(dqkv + grow + HD + h * D);
+    BF8* dv = reinterpret_cast<BF8*>(dqkv + grow + 2 * HD + h * D);
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      float f[32];
+      tmem_ld32(tmem + lanes + 256 + c * 32, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dv[c * 4 + i] = f_to_bf8(f + 8 * i);
+      tmem_ld32(tmem + lanes + 384 + c * 32, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]) * scale;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dk[c * 4 + i] = f_to_bf8(f + 8 * i);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================== backward dQ
+template <int D>
+struct DqL {
+  static constexpr int kQT = 128 * D * 2;  // Q or dO tile (128 rows)
+  static constexpr int kKT = 64 * D * 2;   // K or V tile (64 rows)
+  static constexpr int kQ = 0, kDO = kQT, kK = 2 * kQT, kV = kK + 2 * kKT, kDS = kV + 2 * kKT;
+  static constexpr int kBar = kDS + 2 * 16384;
+  static constexpr int kBytes = kBar + 128 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_dq_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                      const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse,
+                      const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
+                      float scale_log2) {
+  using L = DqL<D>;
+  constexpr int kA = D / 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *ds_full = bar + 7,
+           *ds_free = bar + 9, *fin = bar + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = 2 * (qb + 1), HD = H * D, row0 = b * S;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(ds_full + i, 128);
+      mbar_init(ds_free + i, 1);
+    }
+    mbar_init(fin, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // TMEM: S[2] at 0 / 64, dP[2] at 128 / 192, dQ at 256.
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(q_full, 2 * L::kQT);
+      for (int a = 0; a < kA; ++a) {
+        tma_load_2d(&map_q, q_full, smem + L::kQ + a * 16384, h * D + 64 * a, row0 + qb * 128, kEvictFirst);
+        tma_load_2d(&map_do, q_full, smem + L::kDO + a * 16384, h * D + 64 * a, row0 + qb * 128, kEvictFirst);
+      }
+      for (int j = 0; j < n; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(kv_empty + st, ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(kv_full + st, 2 * L::kKT);
+        for (int a = 0; a < kA; ++a) {
+          tma_load_2d(&map_kv, kv_full + st, smem + L::kK + st * L::kKT + a * 8192, HD + h * D + 64 * a,
+                      row0 + j * 64, kEvictLast);
+          tma_load_2d(&map_kv, kv_full + st, smem + L::kV + st * L::kKT + a * 8192, 2 * HD + h * D + 64 * a,
+                      row0 + j * 64, kEvictLast);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t idG = umma_idesc_bf16(128, D, false, true);
+      const uint32_t sQ = smem_u32(smem + L::kQ), sDO = smem_u32(smem + L::kDO), sK = smem_u32(smem + L::kK),
+                     sV = smem_u32(smem + L::kV), sDS = smem_u32(smem + L::kDS);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(kv_full + st, (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          umma_f16(tmem + st * 64, kmaj(sQ, kk, 16384), kmaj(sK + st * L::kKT, kk, 8192), idS, kk > 0);
+          umma_f16(tmem + 128 + st * 64, kmaj(sDO, kk, 16384), kmaj(sV + st * L::kKT, kk, 8192), idS, kk > 0);
+        }
+        umma_commit(s_full + st);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      issue_s(1);
+      for (int j = 0; j < n; ++j) {
+        const int st = j & 1;
+        mbar_wait(ds_full + st, (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_f16(tmem + 256, kmaj(sDS + st * 16384, kk, 16384), mnmaj(sK + st * L::kKT, kk, 8192), idG,
+                   (j | kk) != 0);
+        umma_commit(ds_free + st);
+        umma_commit(kv_empty + st);
+        if (j + 2 < n) issue_s(j + 2);
+      }
+      umma_commit(fin);
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;
+    const int q = qb * 128 + r;
+    const uint32_t lanes = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    const long long vi = (static_cast<long long>(b) * H + h) * S + q;
+    const float l2 = lse[vi] * kLog2e, dq = dvec[vi];
+    for (int j = 0; j < n; ++j) {
+      const int st = j & 1;
+      mbar_wait(s_full + st, (j >> 1) & 1);
+      if (j >= 2) mbar_wait(ds_free + st, ((j >> 1) - 1) & 1);
+      tc_fence_after();
+      uint8_t* ds = smem + L::kDS + st * 16384;
+      const bool diag = j >= 2 * qb;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t s[32], dp[32];
+        tmem_ld32(tmem + lanes + st * 64 + half * 32, s);
+        tmem_ld32(tmem + lanes + 128 + st * 64 + half * 32, dp);
+        tmem_ld_wait();
+        float g[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          float v = exp2f(u2f(s[c]) * scale_log2 - l2);
+          if (diag && j * 64 + half * 32 + c > q) v = 0.f;
+          g[c] = v * (u2f(dp[c]) - dq);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) st_sw128(ds, r, half * 4 + c, f_to_bf8(g + 8 * c));
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(ds_full + st);
+    }
+    mbar_wait(fin, 0);
+    tc_fence_after();
+    BF8* dqrow = reinterpret_cast<BF8*>(dqkv + static_cast<long long>(row0 + q) * 3 * HD + h * D);
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      float f[32];
+      tmem_ld32(tmem + lanes + 256 + c * 32, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]) * scale;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dqrow[c * 4 + i] = f_to_bf8(f + 8 * i);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================== host
+template <int D>
+int fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, int H, cudaStream_t s) {
+  CUtensorMap m;
+  const long long T = static_cast<long long>(B) * S, ld = 3LL * H * D;
+  if (!gemm::make_map(&m, qkv, ld, T, ld, 64, 128)) return set_error("attention: tensor map encode failed");
+  auto k = attn_fwd_tc_kernel<D>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<D>::kBytes);
+  k<<<dim3(S / 128, H, B), 256, FwdL<D>::kBytes, s>>>(m, out, lse, S, H, kLog2e / sqrtf(static_cast<float>(D)));
+  return check_launch("attention_fwd_tc");
+}
+
+template <int D>
+int bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* dvec,
+        __nv_bfloat16* dqkv, int B, int S, int H, cudaStream_t s) {
+  CUtensorMap m128, m64, d64, d128;
+  const long long T = static_cast<long long>(B) * S, ld = 3LL * H * D, hd = static_cast<long long>(H) * D;
+  bool ok = gemm::make_map(&m128, qkv, ld, T, ld, 64, 128) && gemm::make_map(&m64, qkv, ld, T, ld, 64, 64) &&
+            gemm::make_map(&d64, dout, hd, T, hd, 64, 64) && gemm::make_map(&d128, dout, hd, T, hd, 64, 128);
+  if (!ok) return set_error("attention: tensor map encode failed");
+  const float scale = 1.f / sqrtf(static_cast<float>(D)), scale_log2 = scale * kLog2e;
+  auto k1 = attn_dkdv_tc_kernel<D>;
+  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvL<D>::kBytes);
+  k1<<<dim3(S / 128, H, B), 256, DkvL<D>::kBytes, s>>>(m128, m64, d64, lse, dvec, dqkv, S, H, scale, scale_log2);
+  auto k2 = attn_dq_tc_kernel<D>;
+  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, DqL<D>::kBytes);
+  k2<<<dim3(S / 128, H, B), 256, DqL<D>::kBytes, s>>>(m128, m64, d128, lse, dvec, dqkv, S, H, scale, scale_log2);
+  return check_launch("attention_bwd_tc", 2);
+}
+
+int g_mode = -1;
+
+}  // namespace attn_tc
+
+void attention_set_mode(int mode) { attn_tc::g_mode = mode; }
+int attention_mode() { return attn_tc::g_mode; }
+bool attention_tc_supported(int seq, int head_dim) {
+  return attn_tc::g_mode != 0 && seq % 128 == 0 && (head_dim == 64 || head_dim == 128);
+}
+
+int attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, int H, int D,
+                     cudaStream_t s) {
+  return D == 64 ? attn_tc::fwd<64>(qkv, out, lse, B, S, H, s) : attn_tc::fwd<128>(qkv, out, lse, B, S, H, s);
+}
+
+int attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* dvec,
+                     __nv_bfloat16* dqkv, int B, int S, int H, int D, cudaStream_t s) {
+  return D == 64 ? attn_tc::bwd<64>(qkv, dout, lse, dvec, dqkv, B, S, H, s)
+                 : attn_tc::bwd<128>(qkv, dout, lse, dvec, dqkv, B, S, H, s);
+}
+
+}  // namespace lynx

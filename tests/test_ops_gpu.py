@@ -172,10 +172,22 @@ def _ref_attention(qkv, B, S, H, D):
     return o.permute(0, 2, 1, 3).reshape(B * S, H * D), lse
 
 
-@pytest.mark.parametrize("B,S,H,D", [(2, 128, 2, 64), (1, 256, 3, 128), (2, 192, 2, 96), (1, 128, 2, 112)])
-def test_attention(ops, cuda, B, S, H, D):
+@pytest.mark.parametrize("mode", [-1, 0])
+@pytest.mark.parametrize("B,S,H,D", [(2, 128, 2, 64), (1, 256, 3, 128), (2, 192, 2, 96), (1, 128, 2, 112),
+                                     (2, 640, 2, 128), (1, 1024, 1, 64)])
+def test_attention(ops, cuda, B, S, H, D, mode):
+    """mode -1: tcgen05 kernels where the shape allows (D 64/128, S % 128 == 0); 0: mma.sync kernels."""
+    from paper_2406_08756_b200._native import lib
     g = torch.Generator(device=cuda).manual_seed(B * S * H * D)
     qkv = torch.randn(B * S, 3 * H * D, device=cuda, generator=g).bfloat16()
+    lib().lynx_op_attention_mode(mode)
+    try:
+        _check_attention(ops, cuda, qkv, g, B, S, H, D)
+    finally:
+        lib().lynx_op_attention_mode(-1)
+
+
+def _check_attention(ops, cuda, qkv, g, B, S, H, D):
     out, lse = ops.attention_fwd(qkv, B, S, H, D)
     x = qkv.float().requires_grad_()
     ref, ref_lse = _ref_attention(x, B, S, H, D)
