@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const __nv_bfloat16* __re
 // Dvec[b,h,s] = sum_d dO * O
 template <int D>
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ out, const __nv_bfloat16* __restrict__ dout,
-                                    float* __restrict__ dvec, int B, int S, int H) {
+                                    float* __restrict__ dvec, const float* __restrict__ lse,
+                                    float* __restrict__ lse2, int B, int S, int H) {
   const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (idx >= static_cast<long long>(B) * S * H) return;
   const int h = static_cast<int>(idx % H);
@@ -240,7 +241,9 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ out, const
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc += a[j] * e[j];
   }
-  dvec[(static_cast<long long>(b) * H + h) * S + s] = acc;
+  const long long vi = (static_cast<long long>(b) * H + h) * S + s;
+  dvec[vi] = acc;
+  if (lse2) lse2[vi] = lse[vi] * kLog2e;  // log2-domain LSE for the tcgen05 kernels
 }
 
 template <int D>
@@ -501,10 +504,13 @@ int bwd_launch(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bf
                __nv_bfloat16* dqkv, float* dvec, int B, int S, int H, cudaStream_t s) {
   constexpr int P = D + 8;
   const long long rows = static_cast<long long>(B) * S * H;
-  attn_bwd_pre_kernel<D><<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(out, dout, dvec, B, S, H);
-  if (attention_tc_supported(S, D)) {
+  const bool tc = attention_tc_supported(S, D);
+  float* lse2 = tc ? dvec + rows : nullptr;
+  attn_bwd_pre_kernel<D><<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(out, dout, dvec, lse, lse2, B,
+                                                                                  S, H);
+  if (tc) {
     if (int rc = check_launch("attention_bwd_pre")) return rc;
-    return attention_bwd_tc(qkv, dout, lse, dvec, dqkv, B, S, H, D, s);
+    return attention_bwd_tc(qkv, dout, lse2, dvec, dqkv, B, S, H, D, s);
   }
   const float scale = 1.f / sqrtf(static_cast<float>(D));
   const float scale_log2 = scale * kLog2e;
@@ -534,7 +540,7 @@ int attention_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int 
   return set_error("attention: head_dim must be 64, 96, 112 or 128", kValidation);
 }
 
-size_t attention_bwd_workspace(int B, int S, int H) { return static_cast<size_t>(B) * S * H * sizeof(float); }
+size_t attention_bwd_workspace(int B, int S, int H) { return 2 * static_cast<size_t>(B) * S * H * sizeof(float); }
 
 int attention_bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bfloat16* dout, const float* lse,
                   __nv_bfloat16* dqkv, float* workspace, int B, int S, int H, int D, cudaStream_t s) {

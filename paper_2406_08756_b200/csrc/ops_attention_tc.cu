@@ -82,6 +82,12 @@ LYNX_DEV void st_sw128(uint8_t* tile, int r, int c, const BF8& v) {
 }
 
 LYNX_DEV float u2f(uint32_t v) { return __uint_as_float(v); }
+// MUFU.EX2 without the denormal-range fix-up exp2f carries (arguments here are <= 8; underflow -> 0).
+LYNX_DEV float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // ============================================================== forward
 template <int D>
@@ -100,9 +106,11 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *p_full = bar + 7,
-           *pv_done = bar + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 9);
+  // K and V stages have their own barriers: K_j is released once S_j is computed, so the
+  // load of K_{j+2} overlaps PV_j instead of waiting for it.
+  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5, *v_empty = bar + 7,
+           *s_full = bar + 9, *p_full = bar + 11, *pv_done = bar + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
   const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n = qb + 1, HD = H * D, row0 = b * S;
@@ -110,8 +118,10 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(kv_full + i, 1);
-      mbar_init(kv_empty + i, 1);
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
       mbar_init(s_full + i, 1);
     }
     mbar_init(p_full, 128);
@@ -132,14 +142,16 @@ __global__ void __launch_bounds__(256, 1)
         tma_load_2d(&map_qkv, q_full, smem + L::kQ + a * 16384, h * D + 64 * a, row0 + qb * 128, kEvictFirst);
       for (int j = 0; j < n; ++j) {
         const int st = j & 1;
-        if (j >= 2) mbar_wait(kv_empty + st, ((j >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(kv_full + st, 2 * L::kTile);
-        for (int a = 0; a < kA; ++a) {
-          tma_load_2d(&map_qkv, kv_full + st, smem + L::kK + st * L::kTile + a * 16384, HD + h * D + 64 * a,
+        if (j >= 2) mbar_wait(k_empty + st, ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(k_full + st, L::kTile);
+        for (int a = 0; a < kA; ++a)
+          tma_load_2d(&map_qkv, k_full + st, smem + L::kK + st * L::kTile + a * 16384, HD + h * D + 64 * a,
                       row0 + j * 128, kEvictLast);
-          tma_load_2d(&map_qkv, kv_full + st, smem + L::kV + st * L::kTile + a * 16384, 2 * HD + h * D + 64 * a,
+        if (j >= 2) mbar_wait(v_empty + st, ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(v_full + st, L::kTile);
+        for (int a = 0; a < kA; ++a)
+          tma_load_2d(&map_qkv, v_full + st, smem + L::kV + st * L::kTile + a * 16384, 2 * HD + h * D + 64 * a,
                       row0 + j * 128, kEvictLast);
-        }
       }
     }
   } else if (warp == 1) {
@@ -150,25 +162,27 @@ __global__ void __launch_bounds__(256, 1)
                      sP = smem_u32(smem + L::kP);
       auto issue_s = [&](int j) {
         const int st = j & 1;
-        mbar_wait(kv_full + st, (j >> 1) & 1);
+        mbar_wait(k_full + st, (j >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           umma_f16(tmem + st * 128, kmaj(sQ, kk, 16384), kmaj(sK + st * L::kTile, kk, 16384), idS, kk > 0);
         umma_commit(s_full + st);
+        umma_commit(k_empty + st);
       };
       mbar_wait(q_full, 0);
       issue_s(0);
       if (n > 1) issue_s(1);
       for (int j = 0; j < n; ++j) {
         const int st = j & 1;
+        mbar_wait(v_full + st, (j >> 1) & 1);
         mbar_wait(p_full, j & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
           umma_f16(tmem + 256, kmaj(sP, kk, 16384), mnmaj(sV + st * L::kTile, kk, 16384), idO, (j | kk) != 0);
         umma_commit(pv_done);
-        umma_commit(kv_empty + st);
+        umma_commit(v_empty + st);
         if (j + 2 < n) issue_s(j + 2);
       }
     }
@@ -185,16 +199,15 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld32(tmem + lanes + st * 128 + c * 32, reinterpret_cast<uint32_t*>(x + c * 32));
       tmem_ld_wait();
-      const bool diag = j == qb;
+      if (j == qb) {  // diagonal tile: causal mask (warp-uniform branch)
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i > r) x[i] = -INFINITY;
+      }
       float mt = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        float v = x[i] * scale_log2;
-        if (diag && i > r) v = -INFINITY;
-        x[i] = v;
-        mt = fmaxf(mt, v);
-      }
-      const float m_new = fmaxf(m_run, mt);
+      for (int i = 0; i < 128; ++i) mt = fmaxf(mt, x[i]);
+      const float m_new = fmaxf(m_run, mt * scale_log2);
       const bool need = __any_sync(0xffffffffu, m_new > m_run + kRescale);
       float corr = 1.f;
       if (need) {
@@ -204,7 +217,7 @@ __global__ void __launch_bounds__(256, 1)
       float rs = 0.f;
 #pragma unroll
       for (int i = 0; i < 128; ++i) {
-        x[i] = exp2f(x[i] - m_run);
+        x[i] = ex2(fmaf(x[i], scale_log2, -m_run));
         rs += x[i];
       }
       l_run = l_run * corr + rs;
@@ -257,28 +270,29 @@ __global__ void __launch_bounds__(256, 1)
 // ============================================================== backward dK / dV
 template <int D>
 struct DkvL {
+  static constexpr int kStages = 3;        // Q / dO / lse / D ring (each stage is used early and late)
   static constexpr int kKV = 128 * D * 2;  // K or V tile: D/64 atoms of 16 KB (128 rows)
   static constexpr int kQT = 64 * D * 2;   // Q or dO tile: D/64 atoms of 8 KB (64 rows)
-  static constexpr int kK = 0, kV = kKV, kQ = 2 * kKV, kDO = kQ + 2 * kQT, kPT = kDO + 2 * kQT;
-  static constexpr int kDS = kPT + 2 * 16384, kVec = kDS + 2 * 16384;  // lse[2][64], dvec[2][64]
-  static constexpr int kBar = kVec + 4 * 256;
+  static constexpr int kK = 0, kV = kKV, kQ = 2 * kKV, kDO = kQ + kStages * kQT, kPT = kDO + kStages * kQT;
+  static constexpr int kDS = kPT + 16384, kVec = kDS + 16384;  // lse2[kStages][64], dvec[kStages][64]
+  static constexpr int kBar = kVec + 2 * kStages * 256;
   static constexpr int kBytes = kBar + 128 + 1024;
 };
 
 template <int D>
 __global__ void __launch_bounds__(256, 1)
     attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
-                        const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse,
+                        const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
                         const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
                         float scale_log2) {
   using L = DkvL<D>;
-  constexpr int kA = D / 64;
+  constexpr int kA = D / 64, NS = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *s_full = bar + 5, *pd_full = bar + 7,
-           *mma_done = bar + 9, *fin = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = q_full + NS, *s_full = q_empty + NS, *pd_full = s_full + 2,
+           *mma_done = pd_full + 1, *fin = mma_done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
   const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int i0 = 2 * kb, n = S / 64 - i0, HD = H * D, row0 = b * S;
@@ -286,13 +300,13 @@ __global__ void __launch_bounds__(256, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
-      mbar_init(s_full + i, 1);
-      mbar_init(pd_full + i, 128);
-      mbar_init(mma_done + i, 1);
     }
+    for (int i = 0; i < 2; ++i) mbar_init(s_full + i, 1);
+    mbar_init(pd_full, 128);
+    mbar_init(mma_done, 1);
     mbar_init(fin, 1);
     fence_barrier_init();
   }
@@ -312,8 +326,8 @@ __global__ void __launch_bounds__(256, 1)
                     kEvictFirst);
       }
       for (int i = 0; i < n; ++i) {
-        const int st = i & 1, q0 = (i0 + i) * 64;
-        if (i >= 2) mbar_wait(q_empty + st, ((i >> 1) - 1) & 1);
+        const int st = i % NS, q0 = (i0 + i) * 64;
+        if (i >= NS) mbar_wait(q_empty + st, ((i / NS) - 1) & 1);
         mbar_arrive_expect_tx(q_full + st, 2 * L::kQT + 512);
         for (int a = 0; a < kA; ++a) {
           tma_load_2d(&map_q, q_full + st, smem + L::kQ + st * L::kQT + a * 8192, h * D + 64 * a, row0 + q0,
@@ -321,8 +335,8 @@ __global__ void __launch_bounds__(256, 1)
           tma_load_2d(&map_do, q_full + st, smem + L::kDO + st * L::kQT + a * 8192, h * D + 64 * a, row0 + q0,
                       kEvictLast);
         }
-        bulk_load(smem + L::kVec + st * 256, lse + vec0 + q0, 256, q_full + st);
-        bulk_load(smem + L::kVec + 512 + st * 256, dvec + vec0 + q0, 256, q_full + st);
+        bulk_load(smem + L::kVec + st * 256, lse2 + vec0 + q0, 256, q_full + st);
+        bulk_load(smem + L::kVec + (NS + st) * 256, dvec + vec0 + q0, 256, q_full + st);
       }
     }
   } else if (warp == 1) {
@@ -332,31 +346,29 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV), sQ = smem_u32(smem + L::kQ),
                      sDO = smem_u32(smem + L::kDO), sPT = smem_u32(smem + L::kPT), sDS = smem_u32(smem + L::kDS);
       auto issue_s = [&](int i) {
-        const int st = i & 1;
-        mbar_wait(q_full + st, (i >> 1) & 1);
+        const int st = i % NS, tb = i & 1;
+        mbar_wait(q_full + st, (i / NS) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          umma_f16(tmem + st * 64, kmaj(sK, kk, 16384), kmaj(sQ + st * L::kQT, kk, 8192), idS, kk > 0);
-          umma_f16(tmem + 128 + st * 64, kmaj(sV, kk, 16384), kmaj(sDO + st * L::kQT, kk, 8192), idS, kk > 0);
+          umma_f16(tmem + tb * 64, kmaj(sK, kk, 16384), kmaj(sQ + st * L::kQT, kk, 8192), idS, kk > 0);
+          umma_f16(tmem + 128 + tb * 64, kmaj(sV, kk, 16384), kmaj(sDO + st * L::kQT, kk, 8192), idS, kk > 0);
         }
-        umma_commit(s_full + st);
+        umma_commit(s_full + tb);
       };
       mbar_wait(kv_full, 0);
       issue_s(0);
       if (n > 1) issue_s(1);
       for (int i = 0; i < n; ++i) {
-        const int st = i & 1;
-        mbar_wait(pd_full + st, (i >> 1) & 1);
+        const int st = i % NS;
+        mbar_wait(pd_full, i & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          umma_f16(tmem + 256, kmaj(sPT + st * 16384, kk, 16384), mnmaj(sDO + st * L::kQT, kk, 8192), idG,
-                   (i | kk) != 0);
-          umma_f16(tmem + 384, kmaj(sDS + st * 16384, kk, 16384), mnmaj(sQ + st * L::kQT, kk, 8192), idG,
-                   (i | kk) != 0);
+          umma_f16(tmem + 256, kmaj(sPT, kk, 16384), mnmaj(sDO + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
+          umma_f16(tmem + 384, kmaj(sDS, kk, 16384), mnmaj(sQ + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
         }
-        umma_commit(mma_done + st);
+        umma_commit(mma_done);
         umma_commit(q_empty + st);
         if (i + 2 < n) issue_s(i + 2);
       }
@@ -366,41 +378,47 @@ __global__ void __launch_bounds__(256, 1)
     const int k = (warp - 4) * 32 + lane;  // key row of the tile
     const int key = kb * 128 + k;
     const uint32_t lanes = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    uint8_t* pt = smem + L::kPT;
+    uint8_t* ds = smem + L::kDS;
     for (int i = 0; i < n; ++i) {
-      const int st = i & 1, q0 = (i0 + i) * 64;
-      mbar_wait(q_full + st, (i >> 1) & 1);
-      mbar_wait(s_full + st, (i >> 1) & 1);
-      if (i >= 2) mbar_wait(mma_done + st, ((i >> 1) - 1) & 1);
+      const int st = i % NS, tb = i & 1, q0 = (i0 + i) * 64;
+      mbar_wait(q_full + st, (i / NS) & 1);
+      mbar_wait(s_full + tb, (i >> 1) & 1);
       tc_fence_after();
       const float* sl = reinterpret_cast<const float*>(smem + L::kVec + st * 256);
-      const float* sd = reinterpret_cast<const float*>(smem + L::kVec + 512 + st * 256);
-      uint8_t* pt = smem + L::kPT + st * 16384;
-      uint8_t* ds = smem + L::kDS + st * 16384;
-      const bool diag = i < 2;
+      const float* sd = reinterpret_cast<const float*>(smem + L::kVec + (NS + st) * 256);
+      BF8 pv[8], gv[8];
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        uint32_t s[32], dp[32];
-        tmem_ld32(tmem + lanes + st * 64 + half * 32, s);
-        tmem_ld32(tmem + lanes + 128 + st * 64 + half * 32, dp);
+        uint32_t sr[32], dp[32];
+        tmem_ld32(tmem + lanes + tb * 64 + half * 32, sr);
+        tmem_ld32(tmem + lanes + 128 + tb * 64 + half * 32, dp);
         tmem_ld_wait();
         float p[32], g[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int qi = half * 32 + c;
-          float v = exp2f(u2f(s[c]) * scale_log2 - sl[qi] * kLog2e);
-          if (diag && key > q0 + qi) v = 0.f;
-          p[c] = v;
-          g[c] = v * (u2f(dp[c]) - sd[qi]);
+        for (int c = 0; c < 32; ++c) p[c] = ex2(fmaf(u2f(sr[c]), scale_log2, -sl[half * 32 + c]));
+        if (i < 2) {  // the two 64-query tiles that meet the diagonal of this 128-key tile
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (key > q0 + half * 32 + c) p[c] = 0.f;
         }
 #pragma unroll
+        for (int c = 0; c < 32; ++c) g[c] = p[c] * (u2f(dp[c]) - sd[half * 32 + c]);
+#pragma unroll
         for (int c = 0; c < 4; ++c) {
-          st_sw128(pt, k, half * 4 + c, f_to_bf8(p + 8 * c));
-          st_sw128(ds, k, half * 4 + c, f_to_bf8(g + 8 * c));
+          pv[half * 4 + c] = f_to_bf8(p + 8 * c);
+          gv[half * 4 + c] = f_to_bf8(g + 8 * c);
         }
+      }
+      if (i >= 1) mbar_wait(mma_done, (i - 1) & 1);  // P^T / dS^T of the previous tile consumed
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        st_sw128(pt, k, c, pv[c]);
+        st_sw128(ds, k, c, gv[c]);
       }
       fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(pd_full + st);
+      mbar_arrive(pd_full);
     }
     mbar_wait(fin, 0);
     tc_fence_after();
@@ -436,7 +454,8 @@ template <int D>
 struct DqL {
   static constexpr int kQT = 128 * D * 2;  // Q or dO tile (128 rows)
   static constexpr int kKT = 64 * D * 2;   // K or V tile (64 rows)
-  static constexpr int kQ = 0, kDO = kQT, kK = 2 * kQT, kV = kK + 2 * kKT, kDS = kV + 2 * kKT;
+  static constexpr int kStages = 3;
+  static constexpr int kQ = 0, kDO = kQT, kK = 2 * kQT, kV = kK + kStages * kKT, kDS = kV + kStages * kKT;
   static constexpr int kBar = kDS + 2 * 16384;
   static constexpr int kBytes = kBar + 128 + 1024;
 };
@@ -444,26 +463,28 @@ struct DqL {
 template <int D>
 __global__ void __launch_bounds__(256, 1)
     attn_dq_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
-                      const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse,
+                      const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
                       const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
                       float scale_log2) {
   using L = DqL<D>;
-  constexpr int kA = D / 64;
+  constexpr int kA = D / 64, NS = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *s_full = bar + 5, *ds_full = bar + 7,
-           *ds_free = bar + 9, *fin = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = kv_full + NS, *s_full = kv_empty + NS,
+           *ds_full = s_full + 2, *ds_free = ds_full + 2, *fin = ds_free + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
   const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n = 2 * (qb + 1), HD = H * D, row0 = b * S;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(ds_full + i, 128);
       mbar_init(ds_free + i, 1);
@@ -486,8 +507,8 @@ __global__ void __launch_bounds__(256, 1)
         tma_load_2d(&map_do, q_full, smem + L::kDO + a * 16384, h * D + 64 * a, row0 + qb * 128, kEvictFirst);
       }
       for (int j = 0; j < n; ++j) {
-        const int st = j & 1;
-        if (j >= 2) mbar_wait(kv_empty + st, ((j >> 1) - 1) & 1);
+        const int st = j % NS;
+        if (j >= NS) mbar_wait(kv_empty + st, ((j / NS) - 1) & 1);
         mbar_arrive_expect_tx(kv_full + st, 2 * L::kKT);
         for (int a = 0; a < kA; ++a) {
           tma_load_2d(&map_kv, kv_full + st, smem + L::kK + st * L::kKT + a * 8192, HD + h * D + 64 * a,
@@ -504,28 +525,28 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t sQ = smem_u32(smem + L::kQ), sDO = smem_u32(smem + L::kDO), sK = smem_u32(smem + L::kK),
                      sV = smem_u32(smem + L::kV), sDS = smem_u32(smem + L::kDS);
       auto issue_s = [&](int j) {
-        const int st = j & 1;
-        mbar_wait(kv_full + st, (j >> 1) & 1);
+        const int st = j % NS, tb = j & 1;
+        mbar_wait(kv_full + st, (j / NS) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          umma_f16(tmem + st * 64, kmaj(sQ, kk, 16384), kmaj(sK + st * L::kKT, kk, 8192), idS, kk > 0);
-          umma_f16(tmem + 128 + st * 64, kmaj(sDO, kk, 16384), kmaj(sV + st * L::kKT, kk, 8192), idS, kk > 0);
+          umma_f16(tmem + tb * 64, kmaj(sQ, kk, 16384), kmaj(sK + st * L::kKT, kk, 8192), idS, kk > 0);
+          umma_f16(tmem + 128 + tb * 64, kmaj(sDO, kk, 16384), kmaj(sV + st * L::kKT, kk, 8192), idS, kk > 0);
         }
-        umma_commit(s_full + st);
+        umma_commit(s_full + tb);
       };
       mbar_wait(q_full, 0);
       issue_s(0);
       issue_s(1);
       for (int j = 0; j < n; ++j) {
-        const int st = j & 1;
-        mbar_wait(ds_full + st, (j >> 1) & 1);
+        const int st = j % NS, tb = j & 1;
+        mbar_wait(ds_full + tb, (j >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          umma_f16(tmem + 256, kmaj(sDS + st * 16384, kk, 16384), mnmaj(sK + st * L::kKT, kk, 8192), idG,
+          umma_f16(tmem + 256, kmaj(sDS + tb * 16384, kk, 16384), mnmaj(sK + st * L::kKT, kk, 8192), idG,
                    (j | kk) != 0);
-        umma_commit(ds_free + st);
+        umma_commit(ds_free + tb);
         umma_commit(kv_empty + st);
         if (j + 2 < n) issue_s(j + 2);
       }
@@ -536,7 +557,7 @@ __global__ void __launch_bounds__(256, 1)
     const int q = qb * 128 + r;
     const uint32_t lanes = static_cast<uint32_t>((warp - 4) * 32) << 16;
     const long long vi = (static_cast<long long>(b) * H + h) * S + q;
-    const float l2 = lse[vi] * kLog2e, dq = dvec[vi];
+    const float l2 = lse2[vi], dq = dvec[vi];
     for (int j = 0; j < n; ++j) {
       const int st = j & 1;
       mbar_wait(s_full + st, (j >> 1) & 1);
@@ -552,11 +573,14 @@ __global__ void __launch_bounds__(256, 1)
         tmem_ld_wait();
         float g[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          float v = exp2f(u2f(s[c]) * scale_log2 - l2);
-          if (diag && j * 64 + half * 32 + c > q) v = 0.f;
-          g[c] = v * (u2f(dp[c]) - dq);
+        for (int c = 0; c < 32; ++c) g[c] = ex2(fmaf(u2f(s[c]), scale_log2, -l2));
+        if (diag) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (j * 64 + half * 32 + c > q) g[c] = 0.f;
         }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) g[c] *= u2f(dp[c]) - dq;
 #pragma unroll
         for (int c = 0; c < 4; ++c) st_sw128(ds, r, half * 4 + c, f_to_bf8(g + 8 * c));
       }
