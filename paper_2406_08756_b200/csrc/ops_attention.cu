@@ -246,6 +246,40 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ out, const
   if (lse2) lse2[vi] = lse[vi] * kLog2e;  // log2-domain LSE for the tcgen05 kernels
 }
 
+// Coalesced variant for D in {64, 128}: one warp per token row, lanes stream the
+// row's 16-byte chunks; each head's D/8 chunks sit in a lane segment reduced by shuffles.
+template <int D>
+__global__ void __launch_bounds__(256) attn_bwd_pre_rows_kernel(const __nv_bfloat16* __restrict__ out,
+                                                                const __nv_bfloat16* __restrict__ dout,
+                                                                float* __restrict__ dvec,
+                                                                const float* __restrict__ lse,
+                                                                float* __restrict__ lse2, int B, int S, int H) {
+  constexpr int kSeg = D / 8;  // lanes per head (8 or 16)
+  const long long tok = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) / 32;
+  const int lane = threadIdx.x % 32;
+  if (tok >= static_cast<long long>(B) * S) return;
+  const int s = static_cast<int>(tok % S), b = static_cast<int>(tok / S);
+  const BF8* o = reinterpret_cast<const BF8*>(out + tok * H * D);
+  const BF8* d = reinterpret_cast<const BF8*>(dout + tok * H * D);
+  const int nit = H * kSeg / 32;
+  for (int it = 0; it < nit; ++it) {
+    const int c = it * 32 + lane;
+    float a[8], e[8], acc = 0.f;
+    bf8_to_f(o[c], a);
+    bf8_to_f(d[c], e);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += a[j] * e[j];
+#pragma unroll
+    for (int off = kSeg / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane % kSeg == 0) {
+      const int h = c / kSeg;
+      const long long vi = (static_cast<long long>(b) * H + h) * S + s;
+      dvec[vi] = acc;
+      if (lse2) lse2[vi] = lse[vi] * kLog2e;
+    }
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(128) attn_bwd_dkdv_kernel(const __nv_bfloat16* __restrict__ qkv,
                                                             const __nv_bfloat16* __restrict__ dout,
@@ -506,8 +540,14 @@ int bwd_launch(const __nv_bfloat16* qkv, const __nv_bfloat16* out, const __nv_bf
   const long long rows = static_cast<long long>(B) * S * H;
   const bool tc = attention_tc_supported(S, D);
   float* lse2 = tc ? dvec + rows : nullptr;
-  attn_bwd_pre_kernel<D><<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(out, dout, dvec, lse, lse2, B,
-                                                                                  S, H);
+  if ((D == 64 || D == 128) && (H * D / 8) % 32 == 0) {
+    const long long threads = static_cast<long long>(B) * S * 32;
+    attn_bwd_pre_rows_kernel<D><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(out, dout, dvec, lse,
+                                                                                          lse2, B, S, H);
+  } else {
+    attn_bwd_pre_kernel<D><<<static_cast<unsigned>((rows + 255) / 256), 256, 0, s>>>(out, dout, dvec, lse, lse2,
+                                                                                    B, S, H);
+  }
   if (tc) {
     if (int rc = check_launch("attention_bwd_pre")) return rc;
     return attention_bwd_tc(qkv, dout, lse2, dvec, dqkv, B, S, H, D, s);

@@ -168,18 +168,164 @@ __global__ void __launch_bounds__(kNT) ln_bwd_kernel(const __nv_bfloat16* __rest
   }
 }
 
-// acc[k][col] += sum_b ws[b][k][col] in block order (k = 0..nvec-1).
-__global__ void reduce_partials_kernel(const float* __restrict__ ws, float* __restrict__ acc0,
-                                       float* __restrict__ acc1, int nblocks, int width, int nvec) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= width) return;
-  float s0 = 0.f, s1 = 0.f;
-  for (int b = 0; b < nblocks; ++b) {
-    s0 += ws[(static_cast<long long>(b) * nvec) * width + col];
-    if (nvec > 1) s1 += ws[(static_cast<long long>(b) * nvec + 1) * width + col];
+// Row-batched backward: each CTA owns a contiguous row range and walks it R rows at a
+// time, so every thread has R*C*(2 or 3) 16-byte loads in flight per barrier round
+// (the one-row-at-a-time kernel above is latency-bound at ~20% of HBM bandwidth).
+// The thread owns the same C chunks of every row, so the dgamma/dbeta partials stay
+// in registers. The per-row sums s1 = sum(g*dy), s2 = sum(g*dy*xhat) of all R rows
+// are reduced in one shared-memory round (double-buffered, one barrier per batch).
+constexpr int kLnBlocks = 296;  // 2 CTAs per SM on 148 SMs
+
+// R = 4 / C rows per batch keeps the in-flight loads (3*R*C 16-B vectors) and the
+// register-resident dgamma/dbeta partials (16*C floats) within 128 registers.
+template <int C>
+__global__ void __launch_bounds__(256, C <= 2 ? 2 : 1) ln_bwd_rows_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                             const __nv_bfloat16* __restrict__ x,
+                                                             const __nv_bfloat16* __restrict__ gamma,
+                                                             const float* __restrict__ mean,
+                                                             const float* __restrict__ rstd,
+                                                             const __nv_bfloat16* __restrict__ dres,
+                                                             __nv_bfloat16* __restrict__ dx, float* __restrict__ ws,
+                                                             int rows, int width) {
+  constexpr int R = C >= 4 ? 1 : 4 / C;
+  __shared__ float red[2][2 * R][8];
+  const int nt = blockDim.x, nw = nt / 32, warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int per = (rows + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per;
+  const int r1 = min(rows, r0 + per);
+  const float inv_w = 1.f / width;
+  float g[C][8], gsum[C][8], bsum[C][8];
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    bf8_to_f(reinterpret_cast<const BF8*>(gamma)[threadIdx.x + i * nt], g[i]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) gsum[i][j] = bsum[i][j] = 0.f;
   }
-  acc0[col] += s0;
-  if (nvec > 1) acc1[col] += s1;
+  int it = 0;
+  for (int row = r0; row < r1; row += R, it ^= 1) {
+    BF8 dv[R][C], xv[R][C], rv[R][C];
+    float mu[R], rs[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const bool ok = row + rr < r1;
+      const long long base = static_cast<long long>(ok ? row + rr : row) * width;
+      mu[rr] = mean[ok ? row + rr : row];
+      rs[rr] = ok ? rstd[row + rr] : 0.f;  // rs = 0 zeroes an out-of-range row's contributions
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const int c = threadIdx.x + i * nt;
+        dv[rr][i] = reinterpret_cast<const BF8*>(dy + base)[c];
+        xv[rr][i] = reinterpret_cast<const BF8*>(x + base)[c];
+        if (dres) rv[rr][i] = reinterpret_cast<const BF8*>(dres + base)[c];
+      }
+    }
+    float s[2 * R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      float s1 = 0.f, s2 = 0.f;
+      const float keep = rs[rr] != 0.f ? 1.f : 0.f;
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        float d[8], xx[8];
+        bf8_to_f(dv[rr][i], d);
+        bf8_to_f(xv[rr][i], xx);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (xx[j] - mu[rr]) * rs[rr], gy = d[j] * g[i][j];
+          s1 += gy;
+          s2 += gy * xh;
+          gsum[i][j] += d[j] * xh;
+          bsum[i][j] += d[j] * keep;
+        }
+      }
+      s[2 * rr] = warp_sum(s1);
+      s[2 * rr + 1] = warp_sum(s2);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 2 * R; ++k) red[it][k][warp] = s[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 2 * R; ++k) {
+      float t = 0.f;
+      for (int w = 0; w < nw; ++w) t += red[it][k][w];
+      s[k] = t * inv_w;
+    }
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (row + rr >= r1) break;
+      BF8* dxr = reinterpret_cast<BF8*>(dx + static_cast<long long>(row + rr) * width);
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        float d[8], xx[8], o[8], r[8];
+        bf8_to_f(dv[rr][i], d);
+        bf8_to_f(xv[rr][i], xx);
+        if (dres) bf8_to_f(rv[rr][i], r);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float xh = (xx[j] - mu[rr]) * rs[rr], gy = d[j] * g[i][j];
+          o[j] = rs[rr] * (gy - s[2 * rr] - xh * s[2 * rr + 1]);
+          if (dres) o[j] += r[j];
+        }
+        dxr[threadIdx.x + i * nt] = f_to_bf8(o);
+      }
+    }
+  }
+  float* wg = ws + static_cast<long long>(blockIdx.x) * 2 * width;
+  float* wb = wg + width;
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    const int c = threadIdx.x + i * nt;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      wg[c * 8 + j] = gsum[i][j];
+      wb[c * 8 + j] = bsum[i][j];
+    }
+  }
+}
+
+// Chunks-per-thread for the row-batched kernel (0: unsupported width -> one-row kernel).
+int ln_rows_chunks(int width) {
+  const int nchunk = width / 8;
+  for (int c : {1, 2, 4})
+    if (nchunk % c == 0 && nchunk / c <= 256 && (nchunk / c) % 32 == 0) return c;
+  return 0;
+}
+
+// acc[k][col] += sum_b ws[b][k][col] in block order (k = 0..nvec-1).
+// 32 columns per CTA; warp w sums the contiguous block range [w*per, (w+1)*per) with
+// 4-way unrolled loads, then warp 0 adds the 8 warp sums in order: a fixed tree, so
+// the result is bit-reproducible, with 8x the loads in flight of a one-thread-per-column loop.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ ws,
+                                                              float* __restrict__ acc0, float* __restrict__ acc1,
+                                                              int nblocks, int width, int nvec) {
+  __shared__ float part[8][2][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int col = blockIdx.x * 32 + lane;
+  const int per = (nblocks + 7) / 8;
+  const int b0 = warp * per, b1 = min(nblocks, b0 + per);
+  float s0 = 0.f, s1 = 0.f;
+  if (col < width) {
+#pragma unroll 4
+    for (int b = b0; b < b1; ++b) {
+      s0 += ws[(static_cast<long long>(b) * nvec) * width + col];
+      if (nvec > 1) s1 += ws[(static_cast<long long>(b) * nvec + 1) * width + col];
+    }
+  }
+  part[warp][0][lane] = s0;
+  part[warp][1][lane] = s1;
+  __syncthreads();
+  if (warp == 0 && col < width) {
+    float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      t0 += part[w][0][lane];
+      t1 += part[w][1][lane];
+    }
+    acc0[col] += t0;
+    if (nvec > 1) acc1[col] += t1;
+  }
 }
 
 // Per-CTA partial column sums of a [rows, width] bf16 matrix.
@@ -224,9 +370,16 @@ int layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bf
                   float* dbeta_acc, float* workspace, int rows, int width, cudaStream_t s) {
   if (width % 8 || width > kNT * kMaxC * 8) return set_error("layernorm: width must be a multiple of 8, <= 8192", kValidation);
   if (rows == 0) return kOk;
-  const int nb = part_blocks(rows);
-  ln_bwd_kernel<<<nb, kNT, 0, s>>>(dy, x, gamma, mean, rstd, dres, dx, workspace, rows, width);
-  reduce_partials_kernel<<<(width + 255) / 256, 256, 0, s>>>(workspace, dgamma_acc, dbeta_acc, nb, width, 2);
+  const int cpt = ln_rows_chunks(width);
+  const int nb = cpt ? (rows < kLnBlocks ? rows : kLnBlocks) : part_blocks(rows);
+  const int nt = cpt ? width / 8 / cpt : kNT;
+  switch (cpt) {
+    case 1: ln_bwd_rows_kernel<1><<<nb, nt, 0, s>>>(dy, x, gamma, mean, rstd, dres, dx, workspace, rows, width); break;
+    case 2: ln_bwd_rows_kernel<2><<<nb, nt, 0, s>>>(dy, x, gamma, mean, rstd, dres, dx, workspace, rows, width); break;
+    case 4: ln_bwd_rows_kernel<4><<<nb, nt, 0, s>>>(dy, x, gamma, mean, rstd, dres, dx, workspace, rows, width); break;
+    default: ln_bwd_kernel<<<nb, kNT, 0, s>>>(dy, x, gamma, mean, rstd, dres, dx, workspace, rows, width);
+  }
+  reduce_partials_kernel<<<(width + 31) / 32, 256, 0, s>>>(workspace, dgamma_acc, dbeta_acc, nb, width, 2);
   return check_launch("layernorm_bwd", 2);
 }
 
@@ -239,7 +392,7 @@ int column_sum_acc(const __nv_bfloat16* x, float* acc, float* workspace, long lo
   if (rows == 0) return kOk;
   const int nb = part_blocks(rows);
   column_partial_kernel<<<nb, kNT, 0, s>>>(x, workspace, rows, width);
-  reduce_partials_kernel<<<(width + 255) / 256, 256, 0, s>>>(workspace, acc, nullptr, nb, width, 1);
+  reduce_partials_kernel<<<(width + 31) / 32, 256, 0, s>>>(workspace, acc, nullptr, nb, width, 1);
   return check_launch("column_sum_acc", 2);
 }
 

@@ -93,7 +93,8 @@ def test_gemm_rejects_bad_shapes(ops, cuda):
         ops.gemm(A, A)
 
 
-@pytest.mark.parametrize("rows,width", [(64, 512), (300, 1792), (128, 4096), (17, 6144)])
+@pytest.mark.parametrize("rows,width", [(64, 512), (300, 1792), (128, 4096), (17, 6144), (1000, 4096), (2001, 5120),
+                                        (50, 1000)])
 def test_layernorm(ops, cuda, rows, width):
     x = torch.randn(rows, width, device=cuda).bfloat16()
     gam = (1 + 0.1 * torch.randn(width, device=cuda)).bfloat16()
@@ -174,7 +175,7 @@ def _ref_attention(qkv, B, S, H, D):
 
 @pytest.mark.parametrize("mode", [-1, 0])
 @pytest.mark.parametrize("B,S,H,D", [(2, 128, 2, 64), (1, 256, 3, 128), (2, 192, 2, 96), (1, 128, 2, 112),
-                                     (2, 640, 2, 128), (1, 1024, 1, 64)])
+                                     (2, 640, 2, 128), (1, 1024, 1, 64), (1, 256, 4, 64)])
 def test_attention(ops, cuda, B, S, H, D, mode):
     """mode -1: tcgen05 kernels where the shape allows (D 64/128, S % 128 == 0); 0: mma.sync kernels."""
     from paper_2406_08756_b200._native import lib
