@@ -262,11 +262,25 @@ def run_gpu_arm(args):
     if ws > 1:
         dist.init_process_group("gloo", init_method="env://")
     c = config_for(n, args)
+    from paper_2406_08756_b200._native import lib
+    lib().lynx_op_gemm_mode(args.gemm_mode)
     peaks = measured_peaks()
     roof = gemm_roofline(c, peaks) if rank == 0 else None  # before the executor owns the HBM
+    times, prof_s = None, 0.0
+    if args.profile == "measured":
+        # B200-measured operator times drive the plan; rank 0 measures and
+        # broadcasts so that every rank plans from the same profile document.
+        from paper_2406_08756_b200 import profiler
+        t0 = time.perf_counter()
+        times = profiler.measure_op_times(c) if rank == 0 else None
+        if ws > 1:
+            obj = [times]
+            dist.broadcast_object_list(obj, src=0)
+            times = obj[0]
+        prof_s = time.perf_counter() - t0
     free, total = torch.cuda.mem_get_info()
     c.mem_budget_bytes = device_budget(c, total)
-    text = gp.profile_text(c)
+    text = gp.profile_text(c, times=times)
     plans, plan_s = plan_all(c, text, args.plan)
     layers = plans[0]["layers_per_stage"]
     stage, tp_rank = rank // c.tp, rank % c.tp
@@ -347,7 +361,9 @@ def run_gpu_arm(args):
         "recompute": {"plan": plan0, "items": len(plans[stage]["timeline"]["items"]),
                       "launches_per_iter": rep["recompute_launches"],
                       "on_demand_ms": rep["recompute_on_demand_ms"], "overlapped_ms": rep["recompute_overlapped_ms"],
-                      "wait_on_recompute_ms": rep["wait_on_recompute_ms"], "baselines": extra or None},
+                      "wait_on_recompute_ms": rep["wait_on_recompute_ms"], "baselines": extra or None,
+                      "profile": args.profile, "profiler_s": round(prof_s, 2),
+                      "op_times_us": {k: float(v) for k, v in (times or {}).items()}},
         "memory": {"ledger_budget_bytes": c.mem_budget_bytes, "plan_peak_bytes": plan0["peak_bytes"],
                    "pool_high_water_bytes": rep["pool_high_water_bytes"],
                    "static_bytes": rep["static_bytes_allocated"], "device_total_bytes": total},
@@ -383,6 +399,9 @@ def main():
     ap.add_argument("--microbatches", type=int, default=0)
     ap.add_argument("--plan", default="heu", choices=["heu", "full", "retain_all"])
     ap.add_argument("--baselines", action="store_true", help="also time retain-all / full-recompute plans (N=1)")
+    ap.add_argument("--gemm-mode", type=int, default=-1, help="lynx_op_gemm_mode (-1 default, 0 single-CTA, 1 pair)")
+    ap.add_argument("--profile", default="measured", choices=["measured", "estimated"],
+                    help="operator times for the planner: B200-measured (default) or the analytic estimate")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
