@@ -182,6 +182,37 @@ def reference_simulate(c, profile_text: str) -> dict | None:
         return {"error": str(e)}
 
 
+def reference_planner(total_bytes: int, model: str) -> dict | None:
+    """SURVEY §8d CPU item 1: the reference planner (shim-built lynx_core, oracle/_ref) on the
+    headline TP2xPP4 profile: search_partition plus the HEU stage plans, single-threaded, beside
+    this repo's native planner on the same text (outputs must be identical)."""
+    try:
+        from oracle import ref as oref
+        from paper_2406_08756_b200 import gpt_profile as gp
+        from paper_2406_08756_b200 import planner
+        if not oref.available():
+            return None
+        c = gp.GPTConfig(**{**gp.CONFIGS[model].__dict__, "tp": 2, "pp": 4, "n_microbatches": 8, "dropout": 0.1})
+        c.mem_budget_bytes = device_budget(c, total_bytes)
+        text = gp.profile_text(c)
+        R = oref.RefLib()
+        t0 = time.perf_counter()
+        ref_part = R.partition(text, 10000)
+        ref_plans = [R.stage_plan(text, s, None, 10000) for s in range(c.pp)]
+        t_ref = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        our_part = planner.partition_text(text)
+        our_plans = [planner.stage_plan_text(text, s) for s in range(c.pp)]
+        t_our = time.perf_counter() - t0
+        same = json.loads(ref_part) == json.loads(our_part) and all(
+            json.loads(a["plan_json"]) == json.loads(b["plan_json"]) for a, b in zip(ref_plans, our_plans))
+        return {"profile": f"gpt-{model} TP2xPP4 M=8", "reference_s": round(t_ref, 4), "native_s": round(t_our, 4),
+                "identical_outputs": same, "cores": 1,
+                "paper_s": "HEU 0.15 s / partition 1.27 s with Gurobi (PAPER.md:1333)"}
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e).splitlines()[0][:200]}
+
+
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -247,6 +278,59 @@ def gemm_roofline(c, peaks: dict) -> dict:
             "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
             "peak_kind": "measured burst bf16 (MEASURED_PEAKS.json)", "traffic": traffic,
             "flops_per_launch": flops}
+
+
+def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times) -> dict:
+    """Same-box comparison runs after the timed region (N=1):
+    - "elided": the same plan with every recompute launch skipped (timing only; regenerated
+      tensors are left uninitialised) -> T(plan) - T(elided) cross-checks the exposed recompute
+      (SURVEY §8d);
+    - with --baselines: Megatron full recompute and retain-all at this micro-batch (OOM at 7B mb32),
+      and retain-all / HEU at half the micro-batch, where retain-all fits."""
+    from paper_2406_08756_b200 import executor as ex
+    from paper_2406_08756_b200 import gpt_profile as gp
+    variants = [("elided", c, text, plans[0]["timeline"], {"elide_recompute": True})]
+    if args.baselines:
+        variants.append(("full", c, text, None, {}))
+        half = gp.GPTConfig(**{**c.__dict__, "micro_batch": max(1, c.micro_batch // 2)})
+        half.mem_budget_bytes = c.mem_budget_bytes
+        half_text = gp.profile_text(half)  # analytic op times (the measured ones are for micro-batch c)
+        for base in ("retain_all", "heu"):
+            variants.append((f"{base}_mb{half.micro_batch}", half, half_text, None, {"plan": base}))
+        variants.append(("retain_all", c, text, None, {}))  # expected OOM at 7B mb32: run last
+    out = {}
+    for name, cc, tt, timeline, opts in variants:
+        be, bp = None, None
+        try:
+            plan_kind = opts.pop("plan", None) or (name if name in ("full", "retain_all") else "heu")
+            if timeline is None:
+                bp, _ = plan_all(cc, tt, plan_kind)
+                timeline = bp[0]["timeline"]
+            ccfg = ex.make_config(cc, [cc.n_layers], exec_opts={"trace": False, **opts})
+            btok, blab = ex.synthetic_batch(cc)
+            be = ex.Executor(tt, timeline, ccfg)
+            for _ in range(2):
+                be.step(btok, blab)
+            be.step(btok, blab)
+            br = be.report()
+            tok_i = cc.tokens * cc.n_microbatches
+            out[name] = {"iteration_ms": round(br["iteration_ms"], 3),
+                         "exposed_recompute_ms": round(br["exposed_recompute_ms"], 3),
+                         "tokens_per_s": round(tok_i / (br["iteration_ms"] / 1000.0), 1),
+                         "micro_batch": cc.micro_batch, "recompute_launches": br["recompute_launches"],
+                         "pool_high_water_bytes": br["pool_high_water_bytes"]}
+            if bp is not None:
+                out[name]["plan_peak_bytes"] = json.loads(bp[0]["plan_json"])["peak_bytes"]
+            if name == "elided":
+                out[name]["exposed_recompute_crosscheck_ms"] = round(dev_ms - br["iteration_ms"], 3)
+        except Exception as err:
+            out[name] = {"error": str(err).splitlines()[0][:200], "micro_batch": cc.micro_batch}
+            if bp is not None:
+                out[name]["plan_peak_bytes"] = json.loads(bp[0]["plan_json"])["peak_bytes"]
+        finally:
+            if be is not None:
+                be.close()
+    return out
 
 
 def run_gpu_arm(args):
@@ -325,30 +409,12 @@ def run_gpu_arm(args):
     rep = reports[-1]
     plan0 = json.loads(plans[stage]["plan_json"])
     extra = {}
-    if rank == 0 and args.baselines and ws == 1:
+    if rank == 0 and ws == 1 and (args.baselines or not args.no_crosscheck):
         e.close()
         del e
         print(json.dumps({"partial": True, "value": value, "ms": dev_ms, "exposed_ms": exposed,
                           "report": rep}), file=sys.stderr, flush=True)
-        for base in ("full", "retain_all"):
-            be = None
-            try:
-                bp, _ = plan_all(c, text, base)
-                be = ex.Executor(text, bp[0]["timeline"], cfg)
-                for _ in range(2):
-                    be.step(tok, lab)
-                be.step(tok, lab)
-                br = be.report()
-                extra[base] = {"iteration_ms": br["iteration_ms"], "exposed_recompute_ms": br["exposed_recompute_ms"],
-                               "tokens_per_s": tokens_iter / (br["iteration_ms"] / 1000.0),
-                               "pool_high_water_bytes": br["pool_high_water_bytes"],
-                               "plan_peak_bytes": json.loads(bp[0]["plan_json"])["peak_bytes"]}
-            except Exception as err:
-                extra[base] = {"error": str(err).splitlines()[0][:200],
-                               "plan_peak_bytes": json.loads(bp[0]["plan_json"])["peak_bytes"]}
-            finally:
-                if be is not None:
-                    be.close()
+        extra = run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times)
     if rank != 0:
         return
     step_tflops = c.flops_per_token() * tokens_iter / (dev_ms / 1000.0) / 1e12
@@ -383,6 +449,7 @@ def run_gpu_arm(args):
     if not args.no_cpu_baseline and ws == 1:
         line["cpu_baseline"] = cpu_baseline(c, budget_s=20.0)
         line["reference_simulate"] = reference_simulate(c, text)
+        line["reference_planner"] = reference_planner(total, args.model)
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -403,6 +470,7 @@ def main():
     ap.add_argument("--profile", default="measured", choices=["measured", "estimated"],
                     help="operator times for the planner: B200-measured (default) or the analytic estimate")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-crosscheck", action="store_true", help="skip the recompute-elided timing run")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -33,6 +33,7 @@ constexpr uint64_t kEmbedStream = 0xFFFFull << 32;
 
 // ============================================================ setup
 void Executor::ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) cudaGetLastError();  // clear non-sticky errors so later launch checks do not see them
   if (e == cudaErrorMemoryAllocation) throw RtError(std::string(what) + ": out of device memory", kOutOfMemory);
   if (e != cudaSuccess) throw RtError(std::string(what) + ": " + cudaGetErrorString(e), kCudaError);
 }
@@ -49,6 +50,15 @@ Executor::Executor(const std::string& profile_json, const std::string& timeline_
   parse_config(config_json);
   bind_template();
   if (opt_.dry_run) return;
+  try {
+    init_device();
+  } catch (...) {
+    release_all();  // a throwing constructor runs no destructor: free what was already allocated
+    throw;
+  }
+}
+
+void Executor::init_device() {
   if (needs_comms_) init_comms(nccl_id_, world_rank_, world_size_);
   for (cudaStream_t* s : {&main_, &side_, &tp_s_, &pa_s_, &pg_s_})
     ck(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "stream");
@@ -240,9 +250,16 @@ void Executor::alloc_persistent() {
 
 Executor::~Executor() {
   if (opt_.dry_run) return;
+  release_all();
+}
+
+void Executor::release_all() {
   cudaDeviceSynchronize();
+  for (void* d : donor_)
+    if (d) cudaFree(d);
+  donor_.clear();
   for (auto& s : slots_) {
-    if (s.p) cudaFree(s.p);
+    if (s.p && !s.borrowed) cudaFree(s.p);
     if (s.shadow) cudaFree(s.shadow);
   }
   ps_.release();
@@ -263,7 +280,7 @@ Executor::~Executor() {
     if (c) ncclCommDestroy(c);
   for (cudaStream_t s : {main_, side_, tp_s_, pa_s_, pg_s_})
     if (s) cudaStreamDestroy(s);
-  cudaMemPoolTrimTo(pool_, 0);
+  if (pool_) cudaMemPoolTrimTo(pool_, 0);
 }
 
 // ============================================================ tensors
@@ -293,7 +310,9 @@ void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
     const size_t idx = static_cast<size_t>(&sl - slots_.data());
     std::fprintf(stderr, "drop mb%zu l%zu op%zu\n", idx / (cfg_.layers * nf_), (idx / nf_) % cfg_.layers, idx % nf_);
   }
-  if (keep_shadow && opt_.check_recompute && !sl.shadow) {
+  if (sl.borrowed) {
+    sl.borrowed = false;  // donor copy: not owned by the slot
+  } else if (keep_shadow && opt_.check_recompute && !sl.shadow) {
     sl.shadow = sl.p;  // forward-produced copy, compared against the regeneration
   } else {
     release(sl.p, s);
@@ -305,6 +324,16 @@ void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
 
 void* Executor::need(int mb, int l, int pos, cudaStream_t s) {
   Slot& sl = slot(mb, l, pos);
+  if (!sl.p && opt_.elide_recompute && pos < static_cast<int>(donor_.size()) && donor_[pos]) {
+    // Timing-only mode: the plan's regeneration was skipped; the consumer reads the donor
+    // copy of this op (real activations, so kernels see realistic data and power draw).
+    sl.p = donor_[pos];
+    sl.borrowed = true;
+    sl.regenerated = true;
+    sl.ready = nullptr;
+    sl.stream = s;
+    return sl.p;
+  }
   if (!sl.p)
     throw RtError("tensor " + std::string(op_name(op_of_[pos])) + " (mb " + std::to_string(mb) + ", layer " +
                       std::to_string(l) + ") is not resident: the timeline does not regenerate it before its consumer",
@@ -488,6 +517,13 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
               "residual");
         break;
       default: break;
+    }
+  }
+  if (opt_.elide_recompute && !recompute && !opt_.dry_run) {
+    if (donor_.empty()) donor_.assign(nf_, nullptr);
+    if (!donor_[pos]) {  // first forward production of this op: keep a copy to lend out
+      ck(cudaMalloc(&donor_[pos], bytes), "donor allocation");
+      ck(cudaMemcpyAsync(donor_[pos], out.p, bytes, cudaMemcpyDeviceToDevice, s), "donor copy");
     }
   }
   mark_ready(out, s);

@@ -50,6 +50,7 @@ struct Slot {
   cudaEvent_t ready = nullptr;  // set when produced off the main stream
   cudaStream_t stream = nullptr;
   bool regenerated = false;
+  bool borrowed = false;   // elide_recompute: points at a donor copy, not owned
   void* shadow = nullptr;  // check_recompute: forward-produced copy
 };
 
@@ -94,6 +95,8 @@ class Executor {
   // setup
   void parse_config(const std::string& cfg);
   void bind_template();
+  void init_device();
+  void release_all();
   void init_comms(const std::string& nccl_id_hex, int world_rank, int world_size);
   void alloc_persistent();
 
@@ -170,6 +173,7 @@ class Executor {
   int bwd_passes_ = 0;
   int dw_epi_ = 1;  // EPI_ACC_F32
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
+  std::vector<void*> donor_;  // elide_recompute: one forward-produced copy per op, lent to consumers
   std::vector<std::tuple<int, int, int, int, double, double>> trace_;  // stage, mb, kind, op, start, end
 };
 

@@ -103,7 +103,10 @@ LayerParams ParamStore::layer(int l) const {
 void ParamStore::allocate_and_init(const ModelCfg& c, cudaStream_t s) {
   const size_t n = static_cast<size_t>(total_);
   auto ck = [](cudaError_t e) {
-    if (e != cudaSuccess) throw std::runtime_error(std::string("parameter allocation: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error(std::string("parameter allocation: ") + cudaGetErrorString(e));
+    }
   };
   ck(cudaMalloc(&param, n * 2));
   ck(cudaMalloc(&master, n * 4));

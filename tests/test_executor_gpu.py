@@ -129,3 +129,22 @@ def test_profiler_measures_every_template_op(cuda):
     assert planner.validate_text(text)[1] == 0
     losses, _, _, rep, _, _, _ = run(c, "heu")
     assert np.isfinite(losses[0])
+
+
+def test_elided_recompute_timing_mode(cuda):
+    """Timing-only cross-check mode: the same plan with recompute launches skipped runs
+    to completion with zero recompute launches and zero exposed recompute."""
+    from paper_2406_08756_b200 import executor as ex
+    from paper_2406_08756_b200 import gpt_profile as gp
+    c0 = tiny()
+    c = tiny(budget=gp.BYTES_PER_PARAM_STATIC * c0.params() + 24 * 2**20)
+    text = gp.profile_text(c)
+    plan = ex.plan_for(text, 0, "heu")
+    assert plan["timeline"]["items"]
+    e = ex.Executor(text, plan["timeline"], ex.make_config(c, plan["layers_per_stage"],
+                                                          exec_opts={"elide_recompute": True}))
+    tok, lab = ex.synthetic_batch(c)
+    e.step(tok, lab)
+    rep = e.report()
+    e.close()
+    assert rep["recompute_launches"] == 0 and rep["exposed_recompute_ms"] == 0
