@@ -287,6 +287,8 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
       (SURVEY §8d);
     - with --baselines: Megatron full recompute and retain-all at this micro-batch (OOM at 7B mb32),
       and retain-all / HEU at half the micro-batch, where retain-all fits."""
+    import torch
+
     from paper_2406_08756_b200 import executor as ex
     from paper_2406_08756_b200 import gpt_profile as gp
     variants = [("elided", c, text, plans[0]["timeline"], {"elide_recompute": True})]
@@ -308,6 +310,8 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
                 timeline = bp[0]["timeline"]
             ccfg = ex.make_config(cc, [cc.n_layers], exec_opts={"trace": False, **opts})
             btok, blab = ex.synthetic_batch(cc)
+            torch.cuda.synchronize()
+            free_b = torch.cuda.mem_get_info()[0]
             be = ex.Executor(tt, timeline, ccfg)
             for _ in range(2):
                 be.step(btok, blab)
@@ -318,7 +322,7 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
                          "exposed_recompute_ms": round(br["exposed_recompute_ms"], 3),
                          "tokens_per_s": round(tok_i / (br["iteration_ms"] / 1000.0), 1),
                          "micro_batch": cc.micro_batch, "recompute_launches": br["recompute_launches"],
-                         "pool_high_water_bytes": br["pool_high_water_bytes"]}
+                         "pool_high_water_bytes": br["pool_high_water_bytes"], "free_bytes_before": free_b}
             if bp is not None:
                 out[name]["plan_peak_bytes"] = json.loads(bp[0]["plan_json"])["peak_bytes"]
             if name == "elided":

@@ -67,6 +67,8 @@ void Executor::init_device() {
   ck(cudaDeviceGetDefaultMemPool(&pool_, dev), "mempool");
   uint64_t thr = UINT64_MAX;
   ck(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
+  uint64_t zero = 0;  // high-water mark of this executor only (the default pool outlives it)
+  ck(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &zero), "mempool attr");
   ps_.allocate_and_init(cfg_, main_);
   alloc_persistent();
   ck(cudaEventCreate(&t0_), "event");
@@ -256,7 +258,7 @@ Executor::~Executor() {
 void Executor::release_all() {
   cudaDeviceSynchronize();
   for (void* d : donor_)
-    if (d) cudaFree(d);
+    if (d) cudaFree(d);  // pool allocations: cudaFree synchronises and returns them to the pool
   donor_.clear();
   for (auto& s : slots_) {
     if (s.p && !s.borrowed) cudaFree(s.p);
@@ -312,6 +314,13 @@ void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
   }
   if (sl.borrowed) {
     sl.borrowed = false;  // donor copy: not owned by the slot
+  } else if (keep_shadow && opt_.elide_recompute && !opt_.dry_run && sl.bytes && [&] {
+               const int pos = static_cast<int>(static_cast<size_t>(&sl - slots_.data()) % nf_);
+               if (donor_.empty()) donor_.assign(nf_, nullptr);
+               if (donor_[pos]) return false;
+               donor_[pos] = sl.p;  // the first discarded copy of this op becomes its donor (no copy)
+               return true;
+             }()) {
   } else if (keep_shadow && opt_.check_recompute && !sl.shadow) {
     sl.shadow = sl.p;  // forward-produced copy, compared against the regeneration
   } else {
@@ -517,13 +526,6 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
               "residual");
         break;
       default: break;
-    }
-  }
-  if (opt_.elide_recompute && !recompute && !opt_.dry_run) {
-    if (donor_.empty()) donor_.assign(nf_, nullptr);
-    if (!donor_[pos]) {  // first forward production of this op: keep a copy to lend out
-      ck(cudaMalloc(&donor_[pos], bytes), "donor allocation");
-      ck(cudaMemcpyAsync(donor_[pos], out.p, bytes, cudaMemcpyDeviceToDevice, s), "donor copy");
     }
   }
   mark_ready(out, s);
