@@ -313,7 +313,7 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
             torch.cuda.synchronize()
             free_b = torch.cuda.mem_get_info()[0]
             be = ex.Executor(tt, timeline, ccfg)
-            for _ in range(2):
+            for _ in range(3):  # the first steps grow the stream-ordered pool (elided mode: around the donors)
                 be.step(btok, blab)
             be.step(btok, blab)
             br = be.report()
