@@ -294,6 +294,7 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
     variants = [("elided", c, text, plans[0]["timeline"], {"elide_recompute": True})]
     if args.baselines:
         variants.append(("full", c, text, None, {}))
+        variants.append(("selective", c, text, None, {"plan": "selective"}))
         half = gp.GPTConfig(**{**c.__dict__, "micro_batch": max(1, c.micro_batch // 2)})
         half.mem_budget_bytes = c.mem_budget_bytes
         half_text = gp.profile_text(half)  # analytic op times (the measured ones are for micro-batch c)
@@ -304,7 +305,7 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
     for name, cc, tt, timeline, opts in variants:
         be, bp = None, None
         try:
-            plan_kind = opts.pop("plan", None) or (name if name in ("full", "retain_all") else "heu")
+            plan_kind = opts.pop("plan", None) or (name if name in ("full", "retain_all", "selective") else "heu")
             if timeline is None:
                 bp, _ = plan_all(cc, tt, plan_kind)
                 timeline = bp[0]["timeline"]
@@ -468,7 +469,7 @@ def main():
     ap.add_argument("--model", default="7b")
     ap.add_argument("--micro-batch", type=int, default=0)
     ap.add_argument("--microbatches", type=int, default=0)
-    ap.add_argument("--plan", default="heu", choices=["heu", "full", "retain_all"])
+    ap.add_argument("--plan", default="heu", choices=["heu", "full", "retain_all", "selective"])
     ap.add_argument("--baselines", action="store_true", help="also time retain-all / full-recompute plans (N=1)")
     ap.add_argument("--gemm-mode", type=int, default=-1, help="lynx_op_gemm_mode (-1 default, 0 single-CTA, 1 pair)")
     ap.add_argument("--profile", default="measured", choices=["measured", "estimated"],

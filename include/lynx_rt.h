@@ -61,7 +61,8 @@ char* lynx_plan_simulate(const char* profile_json, const char* mode, const int* 
                          int* status);
 
 /* One stage's plan + expanded RecomputeItem timeline + steady period:
- * baseline 0 = HEU (PlanCache::stage_plan), 1 = full recompute, 2 = retain all
+ * baseline 0 = HEU (PlanCache::stage_plan), 1 = full recompute, 2 = retain all,
+ * 3 = Megatron selective (only the core attention "attn" is recomputed; not a reference plan)
  * (heusched.cpp:313-341). JSON {plan_json, timeline, period_us, layers_per_stage}. */
 char* lynx_plan_stage(const char* profile_json, int stage, const int* layers, int n_layers, int baseline,
                       long long time_limit_ms, int* status);

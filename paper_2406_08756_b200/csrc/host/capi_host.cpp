@@ -155,9 +155,12 @@ char* lynx_plan_stage(const char* profile_json, int stage, const int* layers, in
       tl = plan.timeline;
       period = plan.period_us;
       pj = plan_json(tl.plan, stage);
-    } else {  // 1 = full recompute (Megatron full), 2 = retain all (no recompute)
+    } else {  // 1 = full recompute (Megatron full), 2 = retain all (no recompute), 3 = Megatron selective
+      if (baseline < 1 || baseline > 3) throw ValidationError("baseline must be 0 (heu), 1, 2 or 3");
       const HeuCtx ctx = heu_context(p, stage, ls[stage]);
-      const LayerPlan plan = baseline == 2 ? retain_all(p.model.layer, ctx) : full_recompute(p.model.layer, ctx);
+      const LayerPlan plan = baseline == 2   ? retain_all(p.model.layer, ctx)
+                             : baseline == 3 ? selective_recompute(p.model.layer, ctx)
+                                             : full_recompute(p.model.layer, ctx);
       tl = expand_to_stage(plan, ctx, p.pipeline, stage);
       period = steady_period(p, stage, ls[stage], tl);
       pj = plan_json(plan, stage);

@@ -74,6 +74,7 @@ Rat plan_peak(const LayerPlan& plan, const HeuCtx& ctx, const LayerTemplate& lay
 std::vector<std::string> plan_violations(const LayerPlan& plan, const HeuCtx& ctx, const LayerTemplate& layer);
 LayerPlan full_recompute(const LayerTemplate& layer, const HeuCtx& ctx);
 LayerPlan retain_all(const LayerTemplate& layer, const HeuCtx& ctx);
+LayerPlan selective_recompute(const LayerTemplate& layer, const HeuCtx& ctx);
 StageTimeline expand_to_stage(const LayerPlan& plan, const HeuCtx& ctx, const PipelineConfig& pipe, int stage);
 
 }  // namespace lynx::host

@@ -102,7 +102,7 @@ def simulate_text(profile: str, mode: str = "heu", layers_per_stage=None, p2p_us
 def stage_plan_text(profile: str, stage: int, layers_per_stage=None, baseline: str = "heu",
                     time_limit_ms: int = 10000) -> dict:
     lp, n = _layers(layers_per_stage)
-    b = {"heu": 0, "full": 1, "retain_all": 2}[baseline]
+    b = {"heu": 0, "full": 1, "retain_all": 2, "selective": 3}[baseline]
     return json.loads(_call("lynx_plan_stage", _b(profile), stage, lp, n, b, time_limit_ms)[0])
 
 

@@ -148,3 +148,15 @@ def test_elided_recompute_timing_mode(cuda):
     rep = e.report()
     e.close()
     assert rep["recompute_launches"] == 0 and rep["exposed_recompute_ms"] == 0
+
+
+def test_selective_plan_is_bit_identical(cuda):
+    """Megatron-selective baseline: only attention is regenerated (critical path); results equal retain-all."""
+    c = tiny(dropout=0.1)
+    l_sel, g_sel, _, r_sel, p_sel, _, _ = run(c, "selective", check=True)
+    assert r_sel["recompute_launches"] == len(p_sel["timeline"]["items"]) > 0
+    assert r_sel["recompute_mismatch_words"] == 0
+    l_keep, g_keep, _, _, _, _, _ = run(c, "retain_all")
+    assert l_sel == l_keep
+    for k in g_keep:
+        assert np.array_equal(g_keep[k], g_sel[k]), k

@@ -220,3 +220,23 @@ def test_random_profiles_match(R, seed):
         return
     assert pl.simulate_text(text, "heu", None, "0", "json", time_limit_ms=2000) == ref
     assert pl.partition_text(text, "heu", 2000) == R.partition(text, 2000)
+
+
+@pytest.mark.parametrize("key", ["tiny", "7b"])
+def test_selective_baseline_plan(key):
+    """Megatron-selective baseline (not a reference plan): every forward tensor retained except the
+    core attention's, regenerated on the critical path (phase 5) of every (microbatch, layer)."""
+    c = gp.CONFIGS[key]
+    text = gp.profile_text(c)
+    prof = json.loads(text)
+    names = [op["name"] for op in prof["model"]["layer"]["ops"]]
+    attn = names.index("attn")
+    for s in range(prof["pipeline"]["n_stages"]):
+        m = pl.stage_plan_text(text, s, None, "selective")
+        plan = json.loads(m["plan_json"])
+        assert attn not in plan["S"] and all(i in plan["S"] for i in range(len(plan["S"]) + 1) if i != attn)
+        items = m["timeline"]["items"]
+        assert items and all(it["op"] == attn and it["host"] == "critical" for it in items)
+        full = json.loads(pl.stage_plan_text(text, s, None, "full")["plan_json"])
+        keep = json.loads(pl.stage_plan_text(text, s, None, "retain_all")["plan_json"])
+        assert int(full["peak_bytes"]) <= int(plan["peak_bytes"]) <= int(keep["peak_bytes"])
