@@ -257,6 +257,35 @@ __global__ void adam_kernel(float* __restrict__ master, __nv_bfloat16* __restric
   }
 }
 
+// Same arithmetic as adam_kernel, 4 parameters per thread with 16-byte loads/stores
+// (HBM-bound: 30 B per parameter). n4 = n / 4; the tail is left to adam_kernel.
+__device__ __forceinline__ float adam_one(float g, float& mi, float& vi, float w, float lr, float b1, float b2,
+                                          float eps, float wd, float bc1, float bc2) {
+  mi = b1 * mi + (1.f - b1) * g;
+  vi = b2 * vi + (1.f - b2) * g * g;
+  return w - lr * ((mi / bc1) / (sqrtf(vi / bc2) + eps) + wd * w);
+}
+
+__global__ void __launch_bounds__(256) adam_vec4_kernel(float4* __restrict__ master, uint2* __restrict__ param,
+                                                        const float4* __restrict__ grad, float4* __restrict__ m,
+                                                        float4* __restrict__ v, long long n4, float lr, float b1,
+                                                        float b2, float eps, float wd, float bc1, float bc2,
+                                                        float gscale) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const float4 g = grad[i];
+    float4 mi = m[i], vi = v[i], w = master[i];
+    w.x = adam_one(g.x * gscale, mi.x, vi.x, w.x, lr, b1, b2, eps, wd, bc1, bc2);
+    w.y = adam_one(g.y * gscale, mi.y, vi.y, w.y, lr, b1, b2, eps, wd, bc1, bc2);
+    w.z = adam_one(g.z * gscale, mi.z, vi.z, w.z, lr, b1, b2, eps, wd, bc1, bc2);
+    w.w = adam_one(g.w * gscale, mi.w, vi.w, w.w, lr, b1, b2, eps, wd, bc1, bc2);
+    m[i] = mi;
+    v[i] = vi;
+    master[i] = w;
+    param[i] = make_uint2(pack_bf16x2(w.x, w.y), pack_bf16x2(w.z, w.w));
+  }
+}
+
 __global__ void fill_kernel(float* p, float v, long long n) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -391,8 +420,22 @@ int adam_step(float* master, __nv_bfloat16* param, const float* grad, float* m, 
               float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale, cudaStream_t s) {
   const float bc1 = 1.f - powf(beta1, static_cast<float>(step));
   const float bc2 = 1.f - powf(beta2, static_cast<float>(step));
-  adam_kernel<<<grid_for(n), kBlock, 0, s>>>(master, param, grad, m, v, n, lr, beta1, beta2, eps, weight_decay, bc1,
-                                             bc2, grad_scale);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(grad) |
+                         reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) % 16 == 0) &&
+                       reinterpret_cast<uintptr_t>(param) % 8 == 0;
+  const long long n4 = aligned ? n / 4 : 0;
+  if (n4) {
+    adam_vec4_kernel<<<grid_for(n4), 256, 0, s>>>(reinterpret_cast<float4*>(master), reinterpret_cast<uint2*>(param),
+                                                  reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(m),
+                                                  reinterpret_cast<float4*>(v), n4, lr, beta1, beta2, eps,
+                                                  weight_decay, bc1, bc2, grad_scale);
+  }
+  const long long done = 4 * n4;
+  if (n > done) {
+    adam_kernel<<<grid_for(n - done), kBlock, 0, s>>>(master + done, param + done, grad + done, m + done, v + done,
+                                                      n - done, lr, beta1, beta2, eps, weight_decay, bc1, bc2,
+                                                      grad_scale);
+  }
   return check_launch("adam_step");
 }
 

@@ -88,6 +88,62 @@ __global__ void __launch_bounds__(kNT) ln_fwd_kernel(const __nv_bfloat16* __rest
   }
 }
 
+// Warp-per-row forward for width = 256*C: each lane streams C 16-byte chunks (all loads
+// in flight at once), statistics by warp shuffles only (no shared memory, no barriers),
+// the row kept as raw bf16 in registers. 8 rows per 256-thread CTA.
+template <int C>
+__global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const __nv_bfloat16* __restrict__ x,
+                                                          const __nv_bfloat16* __restrict__ gamma,
+                                                          const __nv_bfloat16* __restrict__ beta,
+                                                          __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
+                                                          float* __restrict__ rstd, int rows, int width, float eps) {
+  const int lane = threadIdx.x % 32;
+  const long long row = blockIdx.x * 8LL + threadIdx.x / 32;
+  if (row >= rows) return;
+  const BF8* xr = reinterpret_cast<const BF8*>(x + row * width);
+  BF8 raw[C];
+#pragma unroll
+  for (int i = 0; i < C; ++i) raw[i] = xr[lane + 32 * i];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    float v[8];
+    bf8_to_f(raw[i], v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += v[j];
+  }
+  const float mu = warp_sum(s) / width;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    float v[8];
+    bf8_to_f(raw[i], v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float d = v[j] - mu;
+      q += d * d;
+    }
+  }
+  const float rs = rsqrtf(warp_sum(q) / width + eps);
+  const BF8* gr = reinterpret_cast<const BF8*>(gamma);
+  const BF8* br = reinterpret_cast<const BF8*>(beta);
+  BF8* yr = reinterpret_cast<BF8*>(y + row * width);
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    float v[8], g[8], b[8], o[8];
+    bf8_to_f(raw[i], v);
+    bf8_to_f(gr[lane + 32 * i], g);
+    bf8_to_f(br[lane + 32 * i], b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (v[j] - mu) * rs * g[j] + b[j];
+    yr[lane + 32 * i] = f_to_bf8(o);
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
 // dx for rows [r0, r1) of this CTA's range; partial dgamma/dbeta to ws.
 __global__ void __launch_bounds__(kNT) ln_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
                                                      const __nv_bfloat16* __restrict__ x,
@@ -357,7 +413,21 @@ int layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* gamma, const __nv
                   float* mean, float* rstd, int rows, int width, float eps, cudaStream_t s) {
   if (width % 8 || width > kNT * kMaxC * 8) return set_error("layernorm: width must be a multiple of 8, <= 8192", kValidation);
   if (rows == 0) return kOk;
-  ln_fwd_kernel<<<rows, kNT, 0, s>>>(x, gamma, beta, y, mean, rstd, width, eps);
+  const unsigned wgrid = static_cast<unsigned>((rows + 7) / 8);
+  switch (width % 256 ? 0 : width / 256) {
+#define LN_FWD_WARP(C) \
+  case C: ln_fwd_warp_kernel<C><<<wgrid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, width, eps); break;
+    LN_FWD_WARP(1)
+    LN_FWD_WARP(2)
+    LN_FWD_WARP(4)
+    LN_FWD_WARP(7)
+    LN_FWD_WARP(8)
+    LN_FWD_WARP(16)
+    LN_FWD_WARP(20)
+    LN_FWD_WARP(24)
+#undef LN_FWD_WARP
+    default: ln_fwd_kernel<<<rows, kNT, 0, s>>>(x, gamma, beta, y, mean, rstd, width, eps);
+  }
   return check_launch("layernorm_fwd");
 }
 
