@@ -50,9 +50,11 @@ int lynx_abi_version(void);
  * Requires M % 128 == 0, N % 128 == 0, K % 64 == 0, 16-byte aligned rows. */
 int lynx_op_gemm(const void* a, long long lda, int a_mn_major, const void* b, long long ldb, int b_mn_major, void* c,
                  long long ldc, int m, int n, int k, const void* bias, int epilogue, void* stream);
-/* GEMM kernel selection: -1 (default) the CTA-pair tcgen05.mma.cta_group::2 256x256 kernel for
- * K-major A (forward / dX GEMMs) when M % 256 == 0 and N % 256 == 0, else the single-CTA 128xBN
- * kernel; 0 single-CTA only; 1 CTA-pair wherever the shape allows. */
+/* GEMM kernel selection: -1 (default) the 512x256 "wide" CTA-pair kernel (two cta_group::2 MMAs per
+ * k-step sharing the B stage) for K >= 8192 when M % 512 == 0 and N % 256 == 0, else the 256x256
+ * CTA-pair (tcgen05.mma.cta_group::2) kernel for K-major A when M % 256 == 0 and N % 256 == 0, else
+ * the single-CTA 128xBN kernel; 0 single-CTA only; 1 256x256 CTA-pair wherever the shape allows;
+ * 2 wide pair wherever the shape allows, then as 1. */
 void lynx_op_gemm_mode(int mode);
 
 /* y = (x - mean) * rstd * gamma + beta over rows of `width`; mean/rstd fp32 [rows]. */

@@ -11,6 +11,8 @@ import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "liblynx_b200.so"
+if os.environ.get("LYNX_LIB_VARIANT"):  # kernel A/B experiments: _lib/liblynx_b200.<variant>.so
+    LIB_PATH = LIB_PATH.with_name(f"liblynx_b200.{os.environ['LYNX_LIB_VARIANT']}.so")
 
 _c = ctypes
 _vp, _i, _ll, _f, _sz, _ull = _c.c_void_p, _c.c_int, _c.c_longlong, _c.c_float, _c.c_size_t, _c.c_ulonglong

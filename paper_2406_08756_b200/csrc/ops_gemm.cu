@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -35,6 +36,7 @@ constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int kStages = 4;
 constexpr int kThreads = 256;
 constexpr int kGroupM = 16;  // L2-friendly tile rasterisation
+constexpr int kStagingBytes = 4 * 2 * 4096;  // bf16 TMA-store staging: 4 epilogue warps x 2 buffers
 
 struct Args {
   void* c;          // bf16 or f32 output
@@ -42,6 +44,9 @@ struct Args {
   long long ldc;    // elements
   int M, N, K;
   int epi;          // EpiMode
+  int group;        // raster: > 0 groups of `group` M-tiles (M fastest), < 0 groups of -group N-tiles
+  uint64_t hint_a, hint_b;  // L2 cache policies of the A / B TMA loads
+  int tma_store;            // bf16 epilogue through smem + TMA store (else per-thread st.global)
 };
 
 template <int BN>
@@ -49,14 +54,23 @@ struct Smem {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kBytes = kStages * kStageBytes + kStagingBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
-  const int per_group = kGroupM * n_tiles;
-  const int group = tile / per_group;
-  const int first_m = group * kGroupM;
-  const int gm = min(kGroupM, m_tiles - first_m);
+__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int group_size, int& mt, int& nt) {
+  if (group_size < 0) {  // groups of G N-tiles, N fastest inside a group
+    const int G = -group_size;
+    const int per_group = G * m_tiles;
+    const int first_n = tile / per_group * G;
+    const int gn = min(G, n_tiles - first_n);
+    const int in_group = tile % per_group;
+    nt = first_n + in_group % gn;
+    mt = in_group / gn;
+    return;
+  }
+  const int per_group = group_size * n_tiles;
+  const int first_m = tile / per_group * group_size;
+  const int gm = min(group_size, m_tiles - first_m);
   const int in_group = tile % per_group;
   mt = first_m + in_group % gm;
   nt = in_group / gm;
@@ -110,13 +124,68 @@ LYNX_DEV void epilogue_row(const Args& args, uint32_t t_row, long long row, int 
   }
 }
 
+// bf16 epilogue through shared memory and TMA stores: each epilogue warp stages its
+// 32 rows x 64 columns (SW128 layout: 16-byte chunk c of row r at c ^ (r & 7), bank-conflict
+// free) in one of two 4 KB buffers and one lane issues a cp.async.bulk.tensor store of the
+// box. Full 128-byte lines reach L2 (the per-thread st.global path writes 16-byte pieces).
+
+LYNX_DEV void tma_store_2d(const CUtensorMap* desc, const void* smem, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(smem_u32(smem)), "r"(c0), "r"(c1)
+               : "memory");
+}
+LYNX_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+LYNX_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+LYNX_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int kCols>
+LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, uint32_t t_row, int row0, int n0,
+                                int lane, uint8_t* staging, int& sbuf) {
+#pragma unroll 1
+  for (int c = 0; c < kCols; c += 64) {
+    uint32_t r[64];
+    tmem_ld32(t_row + c, r);
+    tmem_ld32(t_row + c + 32, r + 32);
+    tmem_ld_wait();
+    float v[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+    if (args.bias) {
+      const BF8* bp = reinterpret_cast<const BF8*>(args.bias + n0 + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float b[8];
+        bf8_to_f(bp[i], b);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[8 * i + j] += b[j];
+      }
+    }
+    uint8_t* st = staging + sbuf * 4096;
+    if (lane == 0) bulk_wait_read1();  // the store issued from this buffer two rounds ago has read it
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      *reinterpret_cast<BF8*>(st + lane * 128 + ((i ^ (lane & 7)) << 4)) = f_to_bf8(v + 8 * i);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tm_c, st, n0 + c, row0);
+      bulk_commit();
+    }
+    sbuf ^= 1;
+  }
+}
+
 template <bool kAMN, bool kBMN, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, Args args) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                const __grid_constant__ CUtensorMap tm_c, Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using S = Smem<BN>;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * S::kStageBytes);
+  uint8_t* staging = smem + kStages * S::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;
   uint64_t* tmem_empty = tmem_full + 2;
@@ -155,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int mt, nt;
-        tile_coords(tile, m_tiles, n_tiles, mt, nt);
+        tile_coords(tile, m_tiles, n_tiles, args.group, mt, nt);
         const int m0 = mt * BM, n0 = nt * BN;
         for (int kb = 0; kb < k_blocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -172,18 +241,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
           const int k0 = kb * BK;
           if constexpr (!kAMN) {
-            tma_load_2d(&tm_a, &full[stage], sa, k0, m0, kEvictNormal);
+            tma_load_2d(&tm_a, &full[stage], sa, k0, m0, args.hint_a);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              tma_load_2d(&tm_a, &full[stage], sa + j * (64 * BK * 2), m0 + 64 * j, k0, kEvictNormal);
+              tma_load_2d(&tm_a, &full[stage], sa + j * (64 * BK * 2), m0 + 64 * j, k0, args.hint_a);
           }
           if constexpr (!kBMN) {
-            tma_load_2d(&tm_b, &full[stage], sb, k0, n0, kEvictNormal);
+            tma_load_2d(&tm_b, &full[stage], sb, k0, n0, args.hint_b);
           } else {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(&tm_b, &full[stage], sb + j * (64 * BK * 2), n0 + 64 * j, k0, kEvictNormal);
+              tma_load_2d(&tm_b, &full[stage], sb + j * (64 * BK * 2), n0 + 64 * j, k0, args.hint_b);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -236,17 +305,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;  // == warp % 4: TMEM lane quadrant
+    const bool tma_out = args.epi == EPI_BF16 && args.tma_store;
+    uint8_t* my_staging = staging + ew * 8192;
+    int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       int mt, nt;
-      tile_coords(tile, m_tiles, n_tiles, mt, nt);
+      tile_coords(tile, m_tiles, n_tiles, args.group, mt, nt);
       const int row = mt * BM + ew * 32 + lane;
       const int n0 = nt * BN;
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-      epilogue_row<BN>(args, t_row, row, n0);
+      if (tma_out)
+        epilogue_tile_tma<BN>(args, &tm_c, t_row, mt * BM + ew * 32, n0, lane, my_staging, sbuf);
+      else
+        epilogue_row<BN>(args, t_row, row, n0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tmem_empty[acc]);
@@ -257,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (warp >= 4 && lane == 0) bulk_wait_all();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem_base);
 }
@@ -270,13 +346,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 128 x 256 outputs — 1.5x less L2->SM traffic than the 1-CTA tile.
 namespace pair {
 
-constexpr int kStages = 6;
-constexpr int kTileM = 256, kTileN = 256, kHalf = 128;
-constexpr int kABytes = kHalf * BK * 2;  // per CTA
-constexpr int kBBytes = kHalf * BK * 2;  // per CTA (half of N)
-constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
-constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // shared::cluster address of the even (leader) CTA
+// kSub = 1: 256 x 256 pair tile, TMEM double-buffered (the epilogue of tile i overlaps tile i+1).
+// kSub = 2: 512 x 256 pair tile ("wide"): each CTA stages 256 rows of A and 128 columns of B per
+// k-block and issues two M = 256 MMAs that share the B stage, so L2->SM operand traffic per
+// FLOP drops by 25% (48 KB instead of 64 KB per 256x256x64 of work per CTA); the two
+// accumulators fill all 512 TMEM columns, so TMEM is single-buffered.
+constexpr int kTileN = 256, kHalf = 128;
+template <int kSub>
+struct Cfg {
+  static constexpr int kRowsCTA = 128 * kSub;           // A rows staged per CTA
+  static constexpr int kTileM = 2 * kRowsCTA;           // pair tile rows
+  static constexpr int kABytes = kRowsCTA * BK * 2;     // per CTA
+  static constexpr int kBBytes = kHalf * BK * 2;        // per CTA (half of N)
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = kSub == 1 ? 6 : 4;
+  static constexpr int kAcc = 2 / kSub;                  // TMEM accumulator buffers
+  static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + 1024 + 256;
+};
+constexpr int kSmemBytes = Cfg<1>::kSmemBytes;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+#ifdef LYNX_PAIR_SPIN
+#define PAIR_WAIT mbar_wait_spin
+#else
+#define PAIR_WAIT mbar_wait  // try_wait with a suspend-time hint: waiting warps park instead of polling
+#endif  // shared::cluster address of the even (leader) CTA
 
 LYNX_DEV uint32_t cta_rank() {
   uint32_t r;
@@ -290,11 +383,11 @@ LYNX_DEV void arrive_leader(uint64_t* bar) {  // remote (or local) arrive on the
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask)
                : "memory");
 }
-LYNX_DEV void tma_load_2sm(const void* desc, uint64_t* bar, void* smem, int c0, int c1) {
+LYNX_DEV void tma_load_2sm(const void* desc, uint64_t* bar, void* smem, int c0, int c1, uint64_t hint) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem)),
-      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "l"(kEvictNormal)
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1), "l"(hint)
       : "memory");
 }
 LYNX_DEV void umma_f16_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -312,12 +405,17 @@ LYNX_DEV void umma_commit_pair(uint64_t* bar) {  // arrive on `bar` in both CTAs
       : "memory");
 }
 
-template <bool kAMN, bool kBMN>
+template <bool kAMN, bool kBMN, int kSub>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b, Args args) {
+    gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                 const __grid_constant__ CUtensorMap tm_c, Args args) {
+  using C = Cfg<kSub>;
+  constexpr int kStages = C::kStages, kStageBytes = C::kStageBytes, kABytes = C::kABytes, kTileM = C::kTileM;
+  constexpr int kRowsCTA = C::kRowsCTA, kAcc = C::kAcc;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint8_t* staging = smem + kStages * kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;
   uint64_t* tmem_empty = tmem_full + 2;
@@ -338,7 +436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);   // the leader's expect_tx arrival (the peer contributes bytes only)
       mbar_init(&empty[s], 1);  // the leader's multicast commit
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kAcc; ++b) {
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 8);  // 4 epilogue warps x 2 CTAs
     }
@@ -360,10 +458,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
         int mt, nt;
-        tile_coords(tile, m_tiles, n_tiles, mt, nt);
-        const int m0 = mt * kTileM + rank * kHalf, n0 = nt * kTileN + rank * kHalf;
+        tile_coords(tile, m_tiles, n_tiles, args.group, mt, nt);
+        const int m0 = mt * kTileM + rank * kRowsCTA, n0 = nt * kTileN + rank * kHalf;
         for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait_spin(&empty[stage], phase ^ 1);
+          PAIR_WAIT(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * kStageBytes;
           uint8_t* sb = sa + kABytes;
           if (args.epi == 98) {  // timing probe: MMA pipeline without operand traffic
@@ -392,16 +490,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kStageBytes);
           const int k0 = kb * BK;
           if constexpr (!kAMN) {
-            tma_load_2sm(&tm_a, &full[stage], sa, k0, m0);
+#pragma unroll
+            for (int sub = 0; sub < kSub; ++sub)
+              tma_load_2sm(&tm_a, &full[stage], sa + sub * (kHalf * BK * 2), k0, m0 + sub * kHalf, args.hint_a);
           } else {
-            tma_load_2sm(&tm_a, &full[stage], sa, m0, k0);
-            tma_load_2sm(&tm_a, &full[stage], sa + 64 * BK * 2, m0 + 64, k0);
+#pragma unroll
+            for (int j = 0; j < 2 * kSub; ++j)
+              tma_load_2sm(&tm_a, &full[stage], sa + j * (64 * BK * 2), m0 + 64 * j, k0, args.hint_a);
           }
           if constexpr (!kBMN) {
-            tma_load_2sm(&tm_b, &full[stage], sb, k0, n0);
+            tma_load_2sm(&tm_b, &full[stage], sb, k0, n0, args.hint_b);
           } else {
-            tma_load_2sm(&tm_b, &full[stage], sb, n0, k0);
-            tma_load_2sm(&tm_b, &full[stage], sb + 64 * BK * 2, n0 + 64, k0);
+            tma_load_2sm(&tm_b, &full[stage], sb, n0, k0, args.hint_b);
+            tma_load_2sm(&tm_b, &full[stage], sb + 64 * BK * 2, n0 + 64, k0, args.hint_b);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -412,28 +513,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (leader) {
-      constexpr uint32_t idesc = umma_idesc_bf16(kTileM, kTileN, kAMN, kBMN);
+      constexpr uint32_t idesc = umma_idesc_bf16(256, kTileN, kAMN, kBMN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
-        mbar_wait_spin(&tmem_empty[acc], acc_phase ^ 1);
+        PAIR_WAIT(&tmem_empty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * kTileN;
+        const uint32_t d_tmem = tmem_base + acc * kTileN * kSub;
         for (int kb = 0; kb < k_blocks; ++kb) {
-          mbar_wait_spin(&full[stage], phase);
+          PAIR_WAIT(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t sa = smem_u32(smem + stage * kStageBytes);
             const uint32_t sb = sa + kABytes;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
-              const uint64_t da = kAMN ? umma_desc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
-                                       : umma_desc_sw128(sa + k * 32, 16, 1024);
               const uint64_t db = kBMN ? umma_desc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
                                        : umma_desc_sw128(sb + k * 32, 16, 1024);
-              umma_f16_pair(d_tmem, da, db, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+#pragma unroll
+              for (int sub = 0; sub < kSub; ++sub) {  // 128-row sub-tile `sub` of each CTA's A stage
+                const uint32_t sas = sa + sub * (kHalf * BK * 2);
+                const uint64_t da = kAMN ? umma_desc_sw128(sas + k * 2048, 64 * BK * 2, 1024)
+                                         : umma_desc_sw128(sas + k * 32, 16, 1024);
+                umma_f16_pair(d_tmem + sub * kTileN, da, db, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              }
             }
             umma_commit_pair(&empty[stage]);
             if (kb == k_blocks - 1) umma_commit_pair(&tmem_full[acc]);
@@ -444,7 +549,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
-        if (++acc == 2) {
+        if (++acc == kAcc) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -452,27 +557,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
+    const bool tma_out = args.epi == EPI_BF16 && args.tma_store;
+    uint8_t* my_staging = staging + ew * 8192;
+    int sbuf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = cluster; tile < num_tiles; tile += n_clusters) {
       int mt, nt;
-      tile_coords(tile, m_tiles, n_tiles, mt, nt);
-      const int row = mt * kTileM + rank * kHalf + ew * 32 + lane;
+      tile_coords(tile, m_tiles, n_tiles, args.group, mt, nt);
       const int n0 = nt * kTileN;
-      mbar_wait_spin(&tmem_full[acc], acc_phase);
+      PAIR_WAIT(&tmem_full[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * kTileN;
-      epilogue_row<kTileN>(args, t_row, row, n0);
+#pragma unroll 1
+      for (int sub = 0; sub < kSub; ++sub) {
+        const int row0 = mt * kTileM + rank * kRowsCTA + sub * kHalf + ew * 32;
+        const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + (acc * kSub + sub) * kTileN;
+        if (tma_out)
+          epilogue_tile_tma<kTileN>(args, &tm_c, t_row, row0, n0, lane, my_staging, sbuf);
+        else
+          epilogue_row<kTileN>(args, t_row, row0 + lane, n0);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) arrive_leader(&tmem_empty[acc]);
-      if (++acc == 2) {
+      if (++acc == kAcc) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
   }
 
+  if (warp >= 4 && lane == 0) bulk_wait_all();
   tc_fence_before();
   cluster_sync();
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(512));
@@ -510,6 +625,33 @@ bool make_map(CUtensorMap* m, const void* base, long long inner, long long outer
   return r == CUDA_SUCCESS;
 }
 
+// Tile raster group (L2 reuse); LYNX_GEMM_GROUP overrides the default for experiments.
+int group_size() {
+  static int g = [] {
+    const char* e = std::getenv("LYNX_GEMM_GROUP");
+    const int v = e ? std::atoi(e) : 0;
+    return v != 0 ? v : kGroupM;
+  }();
+  return g;
+}
+
+// L2 policies of the A / B operand loads; LYNX_GEMM_HINT="ab" with a, b in {n, f, l}
+// (evict_normal / evict_first / evict_last) overrides the default for experiments.
+uint64_t cache_hint(int operand) {
+  static const char* e = std::getenv("LYNX_GEMM_HINT");
+  const char c = (e && e[0] && e[1]) ? e[operand] : 'n';
+  return c == 'l' ? kEvictLast : (c == 'f' ? kEvictFirst : kEvictNormal);
+}
+
+// bf16 epilogue via TMA stores (default on; LYNX_GEMM_TMA_STORE=0 selects per-thread stores).
+bool tma_store_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LYNX_GEMM_TMA_STORE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -534,43 +676,60 @@ int launch(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_set = true;
   }
-  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi};
+  CUtensorMap mc = ma;
+  const bool tma_out = g.epi == EPI_BF16 && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
+  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), tma_out ? 1 : 0};
   const int tiles = (g.M / BM) * (g.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  kern<<<grid, kThreads, smem, stream>>>(ma, mb, args);
+  kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, args);
   return check_launch("gemm_tcgen05");
 }
 
-template <bool kAMN, bool kBMN>
+template <bool kAMN, bool kBMN, int kSub>
 int launch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
+  using C = pair::Cfg<kSub>;
   CUtensorMap ma, mb;
-  // each CTA loads a 128-row (A) / 128-column (B) half of the pair's 256 x 256 tile
+  // each CTA loads kSub 128-row boxes of A and a 128-column half of the pair's 256 B columns
   bool ok = kAMN ? make_map(&ma, g.a, g.M, g.K, g.lda, 64, BK) : make_map(&ma, g.a, g.K, g.M, g.lda, BK, pair::kHalf);
   ok = ok && (kBMN ? make_map(&mb, g.b, g.N, g.K, g.ldb, 64, BK) : make_map(&mb, g.b, g.K, g.N, g.ldb, BK, pair::kHalf));
   if (!ok) return set_error("cuTensorMapEncodeTiled failed (alignment or driver entry point)");
-  auto kern = pair::gemm2_kernel<kAMN, kBMN>;
+  auto kern = pair::gemm2_kernel<kAMN, kBMN, kSub>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::kSmemBytes);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     attr_set = true;
   }
-  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi};
-  const int tiles = (g.M / pair::kTileM) * (g.N / pair::kTileN);
+  CUtensorMap mc = ma;
+  const bool tma_out = g.epi == EPI_BF16 && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
+  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), tma_out ? 1 : 0};
+  const int tiles = (g.M / C::kTileM) * (g.N / pair::kTileN);
   int clusters = num_sms() / 2;
   if (max_ctas > 0) clusters = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
   if (tiles < clusters) clusters = tiles;
-  kern<<<2 * clusters, kThreads, pair::kSmemBytes, stream>>>(ma, mb, args);
+  kern<<<2 * clusters, kThreads, C::kSmemBytes, stream>>>(ma, mb, mc, args);
   return check_launch("gemm_tcgen05_pair");
+}
+
+template <int kSub>
+int dispatch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
+  if (!g.a_mn && !g.b_mn) return launch_pair<false, false, kSub>(g, stream, max_ctas);
+  if (!g.a_mn && g.b_mn) return launch_pair<false, true, kSub>(g, stream, max_ctas);
+  if (g.a_mn && !g.b_mn) return launch_pair<true, false, kSub>(g, stream, max_ctas);
+  return launch_pair<true, true, kSub>(g, stream, max_ctas);
 }
 
 }  // namespace gemm
 
 namespace {
-// -1 (default): CTA-pair 256x256 kernel for K-major-A GEMMs (forward, dX) where
-// the shape allows, single-CTA otherwise (the MN-major-A weight-gradient GEMMs
-// measure the same on both). 0: single-CTA only. 1: pair wherever the shape allows.
-int g_gemm_mode = -1;
+// -1 (default): the wide 512x256 CTA-pair kernel for K >= 8192 where the shape allows, else
+// the 256x256 pair kernel for K-major A, else the single-CTA kernel. 0: single-CTA only.
+// 1: 256x256 pair wherever the shape allows. 2: wide pair, then 256x256 pair, then single.
+// LYNX_GEMM_MODE sets the initial mode (experiments).
+int g_gemm_mode = [] {
+  const char* e = std::getenv("LYNX_GEMM_MODE");
+  return e ? std::atoi(e) : -1;
+}();
 }
 
 void gemm_set_mode(int mode) { g_gemm_mode = mode; }
@@ -582,14 +741,18 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   if (g.N % 128) return set_error("gemm: N must be a multiple of 128");
   if ((g.epi == EPI_BF16 && g.ldc % 8) || (g.epi != EPI_BF16 && g.ldc % 4))
     return set_error("gemm: ldc must keep 16-byte row alignment");
-  const bool want_pair = g_gemm_mode == 1 || (g_gemm_mode == -1 && !g.a_mn);
-  if (want_pair && g.M % pair::kTileM == 0 && g.N % pair::kTileN == 0 &&
-      (g.M / pair::kTileM) * (g.N / pair::kTileN) >= 32) {
-    if (!g.a_mn && !g.b_mn) return launch_pair<false, false>(g, stream, max_ctas);
-    if (!g.a_mn && g.b_mn) return launch_pair<false, true>(g, stream, max_ctas);
-    if (g.a_mn && !g.b_mn) return launch_pair<true, false>(g, stream, max_ctas);
-    return launch_pair<true, true>(g, stream, max_ctas);
-  }
+  const int mode = g_gemm_mode;
+  const bool n_ok = g.N % pair::kTileN == 0;
+  // The wide tile pays a non-overlapped epilogue per tile (TMEM single-buffered), so by
+  // default it is used for long reductions only (K >= 8192: FC2 forward, FC1/QKV dX, all dW),
+  // where it measures 6-11% faster under the power cap (less L2->SM traffic).
+  if ((mode == 2 || (mode == -1 && g.K >= 8192)) && n_ok && g.M % pair::Cfg<2>::kTileM == 0 &&
+      (g.M / pair::Cfg<2>::kTileM) * (g.N / pair::kTileN) >= 64)
+    return dispatch_pair<2>(g, stream, max_ctas);
+  const bool want_pair = mode == 1 || mode == 2 || (mode == -1 && !g.a_mn);
+  if (want_pair && n_ok && g.M % pair::Cfg<1>::kTileM == 0 &&
+      (g.M / pair::Cfg<1>::kTileM) * (g.N / pair::kTileN) >= 32)
+    return dispatch_pair<1>(g, stream, max_ctas);
   const bool wide = g.N % 256 == 0;
 #define LYNX_GEMM_CASE(AMN, BMN)                                                             \
   if (g.a_mn == AMN && g.b_mn == BMN)                                                         \

@@ -39,11 +39,12 @@ def test_gemm_majors(ops, cuda, a_mn, b_mn, M, N, K):
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
-@pytest.mark.parametrize("mode", [1, 0])
+@pytest.mark.parametrize("mode", [1, 0, 2])
 def test_gemm_pair_and_single_cta(ops, cuda, a_mn, b_mn, mode):
-    """256x256 CTA-pair (cta_group::2) tiles vs the 128xBN single-CTA kernel on shapes both accept."""
+    """512x256 "wide" CTA-pair tiles (mode 2), 256x256 CTA-pair (cta_group::2) tiles (mode 1) and the
+    128xBN single-CTA kernel (mode 0) on shapes all accept; bf16+bias (TMA-store) and fp32-accumulate epilogues."""
     from paper_2406_08756_b200._native import lib
-    M, N, K = 2048, 1536, 640
+    M, N, K = (4096, 2048, 640) if mode == 2 else (2048, 1536, 640)
     g = torch.Generator(device=cuda).manual_seed(11)
     A = torch.randn(M, K, device=cuda, generator=g).bfloat16()
     B = torch.randn(N, K, device=cuda, generator=g).bfloat16()
