@@ -314,7 +314,7 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
             torch.cuda.synchronize()
             free_b = torch.cuda.mem_get_info()[0]
             be = ex.Executor(tt, timeline, ccfg)
-            for _ in range(3):  # the first steps grow the stream-ordered pool (elided mode: around the donors)
+            for _ in range(3):  # the first steps grow the stream-ordered pool
                 be.step(btok, blab)
             be.step(btok, blab)
             br = be.report()
@@ -323,7 +323,8 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
                          "exposed_recompute_ms": round(br["exposed_recompute_ms"], 3),
                          "tokens_per_s": round(tok_i / (br["iteration_ms"] / 1000.0), 1),
                          "micro_batch": cc.micro_batch, "recompute_launches": br["recompute_launches"],
-                         "pool_high_water_bytes": br["pool_high_water_bytes"], "free_bytes_before": free_b}
+                         "pool_high_water_bytes": br["pool_high_water_bytes"], "free_bytes_before": free_b,
+                         "loss": br["loss"]}
             if bp is not None:
                 out[name]["plan_peak_bytes"] = json.loads(bp[0]["plan_json"])["peak_bytes"]
             if name == "elided":

@@ -257,11 +257,8 @@ Executor::~Executor() {
 
 void Executor::release_all() {
   cudaDeviceSynchronize();
-  for (void* d : donor_)
-    if (d) cudaFree(d);  // pool allocations: cudaFree synchronises and returns them to the pool
-  donor_.clear();
   for (auto& s : slots_) {
-    if (s.p && !s.borrowed) cudaFree(s.p);
+    if (s.p) cudaFree(s.p);
     if (s.shadow) cudaFree(s.shadow);
   }
   ps_.release();
@@ -312,16 +309,7 @@ void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
     const size_t idx = static_cast<size_t>(&sl - slots_.data());
     std::fprintf(stderr, "drop mb%zu l%zu op%zu\n", idx / (cfg_.layers * nf_), (idx / nf_) % cfg_.layers, idx % nf_);
   }
-  if (sl.borrowed) {
-    sl.borrowed = false;  // donor copy: not owned by the slot
-  } else if (keep_shadow && opt_.elide_recompute && !opt_.dry_run && sl.bytes && [&] {
-               const int pos = static_cast<int>(static_cast<size_t>(&sl - slots_.data()) % nf_);
-               if (donor_.empty()) donor_.assign(nf_, nullptr);
-               if (donor_[pos]) return false;
-               donor_[pos] = sl.p;  // the first discarded copy of this op becomes its donor (no copy)
-               return true;
-             }()) {
-  } else if (keep_shadow && opt_.check_recompute && !sl.shadow) {
+  if (keep_shadow && opt_.check_recompute && !sl.shadow) {
     sl.shadow = sl.p;  // forward-produced copy, compared against the regeneration
   } else {
     release(sl.p, s);
@@ -333,11 +321,12 @@ void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
 
 void* Executor::need(int mb, int l, int pos, cudaStream_t s) {
   Slot& sl = slot(mb, l, pos);
-  if (!sl.p && opt_.elide_recompute && pos < static_cast<int>(donor_.size()) && donor_[pos]) {
-    // Timing-only mode: the plan's regeneration was skipped; the consumer reads the donor
-    // copy of this op (real activations, so kernels see realistic data and power draw).
-    sl.p = donor_[pos];
-    sl.borrowed = true;
+  if (!sl.p && opt_.elide_recompute && sl.bytes) {
+    // Timing-only mode: the plan's regeneration was skipped; the consumer gets a buffer of
+    // the same size from the pool (stale activations of earlier ops: realistic bit patterns,
+    // no extra memory), freed like a regenerated copy. Gradients of such a step are
+    // meaningless and are discarded before the optimizer (see step()).
+    sl.p = alloc(sl.bytes, s);
     sl.regenerated = true;
     sl.ready = nullptr;
     sl.stream = s;
@@ -961,8 +950,14 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
        return e;
      }(), 0),
      "join side");
-  ck_op(adam_step(ps_.master, ps_.param, ps_.grad, ps_.m, ps_.v, ps_.count(), cfg_.lr, cfg_.beta1, cfg_.beta2,
-                  cfg_.adam_eps, cfg_.weight_decay, step_, 1.0f, main_),
+  // Timing-only elided mode: the gradients are computed from stale buffers and may be
+  // non-finite; they are zeroed and the update runs with a zero learning rate (same bytes
+  // moved) so the weights, and the next steps' forward activations, stay valid.
+  if (opt_.elide_recompute)
+    ck(cudaMemsetAsync(ps_.grad, 0, static_cast<size_t>(ps_.count()) * 4, main_), "zero grads (elided)");
+  ck_op(adam_step(ps_.master, ps_.param, ps_.grad, ps_.m, ps_.v, ps_.count(), opt_.elide_recompute ? 0.f : cfg_.lr,
+                  cfg_.beta1, cfg_.beta2, cfg_.adam_eps, opt_.elide_recompute ? 0.f : cfg_.weight_decay, step_, 1.0f,
+                  main_),
         "adam");
   if (cfg_.last()) ck(cudaMemcpyAsync(h_loss_, d_loss_, ntok * 4, cudaMemcpyDeviceToHost, main_), "d2h loss");
   ck(cudaEventRecord(t1_, main_), "event");

@@ -50,7 +50,6 @@ struct Slot {
   cudaEvent_t ready = nullptr;  // set when produced off the main stream
   cudaStream_t stream = nullptr;
   bool regenerated = false;
-  bool borrowed = false;   // elide_recompute: points at a donor copy, not owned
   void* shadow = nullptr;  // check_recompute: forward-produced copy
 };
 
@@ -173,7 +172,6 @@ class Executor {
   int bwd_passes_ = 0;
   int dw_epi_ = 1;  // EPI_ACC_F32
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
-  std::vector<void*> donor_;  // elide_recompute: one forward-produced copy per op, lent to consumers
   std::vector<std::tuple<int, int, int, int, double, double>> trace_;  // stage, mb, kind, op, start, end
 };
 
