@@ -35,7 +35,10 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int kStages = 4;
 constexpr int kThreads = 256;
-constexpr int kGroupM = 16;  // L2-friendly tile rasterisation
+// Tile raster: groups of 16 N-tiles, N fastest (group < 0). Measured on the 7B shapes, this
+// halves DRAM re-reads against M-grouping (dX 21.7 -> 12.8 GB, dW 21.0 -> 13.0 GB, FC1 10.5 ->
+// 6.6 GB per GEMM), and under the board power cap the saved HBM power is SM clock: +6-8%.
+constexpr int kGroupM = -16;
 constexpr int kStagingBytes = 4 * 2 * 4096;  // bf16 TMA-store staging: 4 epilogue warps x 2 buffers
 
 struct Args {
