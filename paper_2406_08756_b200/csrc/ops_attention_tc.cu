@@ -204,9 +204,14 @@ __global__ void __launch_bounds__(256, 1)
         for (int i = 0; i < 128; ++i)
           if (i > r) x[i] = -INFINITY;
       }
-      float mt = -INFINITY;
+      // 8 independent max / sum chains: a single 128-long dependent chain costs ~4 cycles per
+      // element on the one row warp each SM sub-partition runs.
+      float mv[8];
 #pragma unroll
-      for (int i = 0; i < 128; ++i) mt = fmaxf(mt, x[i]);
+      for (int i = 0; i < 8; ++i) mv[i] = x[i];
+#pragma unroll
+      for (int i = 8; i < 128; ++i) mv[i & 7] = fmaxf(mv[i & 7], x[i]);
+      const float mt = fmaxf(fmaxf(fmaxf(mv[0], mv[1]), fmaxf(mv[2], mv[3])), fmaxf(fmaxf(mv[4], mv[5]), fmaxf(mv[6], mv[7])));
       const float m_new = fmaxf(m_run, mt * scale_log2);
       const bool need = __any_sync(0xffffffffu, m_new > m_run + kRescale);
       float corr = 1.f;
@@ -214,12 +219,13 @@ __global__ void __launch_bounds__(256, 1)
         corr = exp2f(m_run - m_new);
         m_run = m_new;
       }
-      float rs = 0.f;
+      float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < 128; ++i) {
         x[i] = ex2(fmaf(x[i], scale_log2, -m_run));
-        rs += x[i];
+        rv[i & 7] += x[i];
       }
+      const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
       l_run = l_run * corr + rs;
       if (j > 0) {
         mbar_wait(pv_done, (j - 1) & 1);
