@@ -111,16 +111,20 @@ def config_for(n_gpus: int, args):
     return c
 
 
-def device_budget(c, device_bytes: int) -> int:
+def device_budget(c, device_bytes: int, margin_gib: float = 12.0) -> int:
     """Ledger budget = HBM minus what the ledger does not model (runtime scratch, transients, context)."""
     T, h = c.tokens, c.hidden
     hp = h // c.tp
-    scratch = 2 * T * h * 3 + 2 * T * 4 * hp + 4096 * c.vocab * 2 + 64 * 2**20
+    # + fp32 LM-head and embedding gradient accumulators (last / first stage; both at PP = 1)
+    scratch = 2 * T * h * 3 + 2 * T * 4 * hp + 4096 * c.vocab * 2 + 64 * 2**20 + 4 * c.vocab * h * 2 + 4 * c.seq * h
     transients = 2 * T * h * 6 + 4 * T * h + (2 * T * h + 8 * T)  # grads in flight, embed ws, head dy/ln_f
     # HEU's peak (heusched.cpp:260-277) counts retained tensors only; one layer's
     # discarded tensors are physically alive while that layer runs.
     one_layer = (2 * T * h + 8 * T) * 2 + 2 * T * 3 * hp + 2 * T * hp + 2 * T * h * 2 + 2 * T * 4 * hp * 2
-    context = 4 * 2**30  # CUDA context, NCCL buffers, pool fragmentation margin
+    # CUDA context, NCCL buffers and stream-ordered-pool fragmentation: at 7B mb32 the pool was
+    # measured holding ~10 GB reserved-but-unusable next to the ledger's activations (a plan with
+    # ledger peak 161.6 GB OOMed with 69.6 GB reserved / 59.7 GB used).
+    context = int(margin_gib * 2**30)
     return int(device_bytes - scratch - transients - one_layer - context)
 
 
@@ -363,13 +367,14 @@ def run_gpu_arm(args):
         from paper_2406_08756_b200 import profiler
         t0 = time.perf_counter()
         times = profiler.measure_op_times(c) if rank == 0 else None
+        torch.cuda.empty_cache()  # the profiler's tensors (~5 GB at 7B) go back to the device for the executor
         if ws > 1:
             obj = [times]
             dist.broadcast_object_list(obj, src=0)
             times = obj[0]
         prof_s = time.perf_counter() - t0
     free, total = torch.cuda.mem_get_info()
-    c.mem_budget_bytes = device_budget(c, total)
+    c.mem_budget_bytes = device_budget(c, total, args.mem_margin_gib)
     text = gp.profile_text(c, times=times)
     plans, plan_s = plan_all(c, text, args.plan)
     layers = plans[0]["layers_per_stage"]
@@ -477,6 +482,8 @@ def main():
                     help="operator times for the planner: B200-measured (default) or the analytic estimate")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-crosscheck", action="store_true", help="skip the recompute-elided timing run")
+    ap.add_argument("--mem-margin-gib", type=float, default=12.0,
+                    help="HBM held back from the HEU budget for context and pool fragmentation")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

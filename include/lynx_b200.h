@@ -40,6 +40,7 @@ extern "C" {
 #define LYNX_EPI_BF16 0    /* C(bf16) = A*B^T (+ bias[n]) */
 #define LYNX_EPI_ACC_F32 1 /* C(f32) += A*B^T  (weight-gradient accumulation) */
 #define LYNX_EPI_F32 2     /* C(f32)  = A*B^T */
+#define LYNX_EPI_ACC_BF16 3 /* C(bf16) += A*B^T (bf16 gradient accumulation, 16 B/parameter model states) */
 
 const char* lynx_last_error(void);
 int lynx_abi_version(void);

@@ -66,7 +66,7 @@ size_t lynx_op_layernorm_bwd_workspace(int rows, int width) { return layernorm_b
 int lynx_op_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean, const float* rstd,
                           const void* dres, void* dx, float* dgamma_acc, float* dbeta_acc, float* workspace,
                           int rows, int width, void* stream) {
-  return layernorm_bwd(CBF(dy), CBF(x), CBF(gamma), mean, rstd, CBF(dres), BF(dx), dgamma_acc, dbeta_acc, workspace,
+  return layernorm_bwd(CBF(dy), CBF(x), CBF(gamma), mean, rstd, CBF(dres), BF(dx), dgamma_acc, dbeta_acc, 0, workspace,
                        rows, width, STREAM(stream));
 }
 
@@ -85,7 +85,7 @@ int lynx_op_dropout_bwd(const void* dout, void* dy, long long rows, int width, f
 size_t lynx_op_column_sum_workspace(long long rows, int width) { return column_sum_workspace(rows, width); }
 
 int lynx_op_column_sum_acc(const void* x, float* acc, float* workspace, long long rows, int width, void* stream) {
-  return column_sum_acc(CBF(x), acc, workspace, rows, width, STREAM(stream));
+  return column_sum_acc(CBF(x), acc, 0, workspace, rows, width, STREAM(stream));
 }
 
 int lynx_op_gelu_fwd(const void* x, void* y, long long n, void* stream) {
@@ -134,7 +134,7 @@ int lynx_op_xent_fwd_bwd(void* logits, const int* labels, float* loss_rows, long
 
 int lynx_op_adam(float* master, void* param, const float* grad, float* m, float* v, long long n, float lr,
                  float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale, void* stream) {
-  return adam_step(master, BF(param), grad, m, v, n, lr, beta1, beta2, eps, weight_decay, step, grad_scale,
+  return adam_step(master, BF(param), grad, 0, m, v, n, lr, beta1, beta2, eps, weight_decay, step, grad_scale,
                    STREAM(stream));
 }
 

@@ -29,7 +29,7 @@ int check_launch(const char* what, int kernels = 1);
 long long launch_count();
 const char* last_error();
 
-enum EpiMode { EPI_BF16 = 0, EPI_ACC_F32 = 1, EPI_STORE_F32 = 2 };
+enum EpiMode { EPI_BF16 = 0, EPI_ACC_F32 = 1, EPI_STORE_F32 = 2, EPI_ACC_BF16 = 3 };
 
 struct GemmDesc {
   const void* a;  // bf16
@@ -52,9 +52,10 @@ void gemm_set_mode(int mode);
 // ---- norm / elementwise / attention / loss (see the .cu files for contracts)
 int layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* gamma, const __nv_bfloat16* beta, __nv_bfloat16* y,
                   float* mean, float* rstd, int rows, int width, float eps, cudaStream_t s);
+// dgamma_acc / dbeta_acc are fp32 (acc_bf16 = 0) or bf16 (acc_bf16 = 1) accumulators.
 int layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* gamma, const float* mean,
-                  const float* rstd, const __nv_bfloat16* dres, __nv_bfloat16* dx, float* dgamma_acc,
-                  float* dbeta_acc, float* workspace, int rows, int width, cudaStream_t s);
+                  const float* rstd, const __nv_bfloat16* dres, __nv_bfloat16* dx, void* dgamma_acc,
+                  void* dbeta_acc, int acc_bf16, float* workspace, int rows, int width, cudaStream_t s);
 size_t layernorm_bwd_workspace(int rows, int width);
 
 int bias_dropout_residual_fwd(const __nv_bfloat16* y, const __nv_bfloat16* bias, const __nv_bfloat16* res,
@@ -62,7 +63,10 @@ int bias_dropout_residual_fwd(const __nv_bfloat16* y, const __nv_bfloat16* bias,
                               uint64_t stream_id, cudaStream_t s);
 int dropout_bwd(const __nv_bfloat16* dout, __nv_bfloat16* dy, long long rows, int width, float p, uint64_t seed,
                 uint64_t stream_id, cudaStream_t s);
-int column_sum_acc(const __nv_bfloat16* x, float* acc, float* workspace, long long rows, int width, cudaStream_t s);
+int column_sum_acc(const __nv_bfloat16* x, void* acc, int acc_bf16, float* workspace, long long rows, int width,
+                   cudaStream_t s);
+// dst(bf16) += src(fp32), elementwise (n % 8 == 0 not required).
+int add_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s);
 size_t column_sum_workspace(long long rows, int width);
 int gelu_fwd(const __nv_bfloat16* x, __nv_bfloat16* y, long long n, cudaStream_t s);
 int gelu_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, __nv_bfloat16* dx, long long n, cudaStream_t s);
@@ -94,8 +98,10 @@ int attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, i
 int attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* dvec,
                      __nv_bfloat16* dqkv, int batch, int seq, int heads, int head_dim, cudaStream_t s);
 
-int adam_step(float* master, __nv_bfloat16* param, const float* grad, float* m, float* v, long long n, float lr,
-              float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale, cudaStream_t s);
+// grad is fp32 (grad_bf16 = 0) or bf16 (grad_bf16 = 1).
+int adam_step(float* master, __nv_bfloat16* param, const void* grad, int grad_bf16, float* m, float* v, long long n,
+              float lr, float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale,
+              cudaStream_t s);
 int fill_f32(float* p, float v, long long n, cudaStream_t s);
 int fill_param(__nv_bfloat16* p, float* master, float v, long long n, cudaStream_t s);
 // Number of 32-bit words that differ between two device buffers (bit-identity checks).

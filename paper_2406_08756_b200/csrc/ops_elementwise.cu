@@ -239,13 +239,16 @@ __global__ void __launch_bounds__(kBlock) xent_kernel(__nv_bfloat16* __restrict_
   if (threadIdx.x == 0) loss_rows[row] = lse - target;
 }
 
-__global__ void adam_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ param,
-                            const float* __restrict__ grad, float* __restrict__ m, float* __restrict__ v,
-                            long long n, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
-                            float gscale) {
+LYNX_DEV float grad_at(const float* g, long long i) { return g[i]; }
+LYNX_DEV float grad_at(const __nv_bfloat16* g, long long i) { return bf2f(g[i]); }
+
+template <class G>
+__global__ void adam_kernel(float* __restrict__ master, __nv_bfloat16* __restrict__ param, const G* __restrict__ grad,
+                            float* __restrict__ m, float* __restrict__ v, long long n, float lr, float b1, float b2,
+                            float eps, float wd, float bc1, float bc2, float gscale) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const float g = grad[i] * gscale;
+    const float g = grad_at(grad, i) * gscale;
     const float mi = b1 * m[i] + (1.f - b1) * g;
     const float vi = b2 * v[i] + (1.f - b2) * g * g;
     m[i] = mi;
@@ -266,14 +269,22 @@ __device__ __forceinline__ float adam_one(float g, float& mi, float& vi, float w
   return w - lr * ((mi / bc1) / (sqrtf(vi / bc2) + eps) + wd * w);
 }
 
+LYNX_DEV float4 grad4_at(const float4* g, long long i) { return g[i]; }
+LYNX_DEV float4 grad4_at(const uint2* g, long long i) {
+  const uint2 w = g[i];
+  const float2 a = unpack_bf16x2(w.x), b = unpack_bf16x2(w.y);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <class G4>
 __global__ void __launch_bounds__(256) adam_vec4_kernel(float4* __restrict__ master, uint2* __restrict__ param,
-                                                        const float4* __restrict__ grad, float4* __restrict__ m,
+                                                        const G4* __restrict__ grad, float4* __restrict__ m,
                                                         float4* __restrict__ v, long long n4, float lr, float b1,
                                                         float b2, float eps, float wd, float bc1, float bc2,
                                                         float gscale) {
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const float4 g = grad[i];
+    const float4 g = grad4_at(grad, i);
     float4 mi = m[i], vi = v[i], w = master[i];
     w.x = adam_one(g.x * gscale, mi.x, vi.x, w.x, lr, b1, b2, eps, wd, bc1, bc2);
     w.y = adam_one(g.y * gscale, mi.y, vi.y, w.y, lr, b1, b2, eps, wd, bc1, bc2);
@@ -416,27 +427,55 @@ int xent_fwd_bwd(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows,
   return check_launch("xent_fwd_bwd");
 }
 
-int adam_step(float* master, __nv_bfloat16* param, const float* grad, float* m, float* v, long long n, float lr,
-              float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale, cudaStream_t s) {
+int adam_step(float* master, __nv_bfloat16* param, const void* grad, int grad_bf16, float* m, float* v, long long n,
+              float lr, float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale,
+              cudaStream_t s) {
   const float bc1 = 1.f - powf(beta1, static_cast<float>(step));
   const float bc2 = 1.f - powf(beta2, static_cast<float>(step));
-  const bool aligned = ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(grad) |
-                         reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) % 16 == 0) &&
-                       reinterpret_cast<uintptr_t>(param) % 8 == 0;
+  const size_t gsz = grad_bf16 ? 2 : 4;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(master) | reinterpret_cast<uintptr_t>(m) |
+                         reinterpret_cast<uintptr_t>(v)) % 16 == 0) &&
+                       reinterpret_cast<uintptr_t>(grad) % (4 * gsz) == 0 && reinterpret_cast<uintptr_t>(param) % 8 == 0;
   const long long n4 = aligned ? n / 4 : 0;
   if (n4) {
-    adam_vec4_kernel<<<grid_for(n4), 256, 0, s>>>(reinterpret_cast<float4*>(master), reinterpret_cast<uint2*>(param),
-                                                  reinterpret_cast<const float4*>(grad), reinterpret_cast<float4*>(m),
-                                                  reinterpret_cast<float4*>(v), n4, lr, beta1, beta2, eps,
-                                                  weight_decay, bc1, bc2, grad_scale);
+    auto* m4 = reinterpret_cast<float4*>(master);
+    auto* p4 = reinterpret_cast<uint2*>(param);
+    if (grad_bf16)
+      adam_vec4_kernel<uint2><<<grid_for(n4), 256, 0, s>>>(m4, p4, static_cast<const uint2*>(grad),
+                                                           reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
+                                                           n4, lr, beta1, beta2, eps, weight_decay, bc1, bc2,
+                                                           grad_scale);
+    else
+      adam_vec4_kernel<float4><<<grid_for(n4), 256, 0, s>>>(m4, p4, static_cast<const float4*>(grad),
+                                                            reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
+                                                            n4, lr, beta1, beta2, eps, weight_decay, bc1, bc2,
+                                                            grad_scale);
   }
   const long long done = 4 * n4;
   if (n > done) {
-    adam_kernel<<<grid_for(n - done), kBlock, 0, s>>>(master + done, param + done, grad + done, m + done, v + done,
-                                                      n - done, lr, beta1, beta2, eps, weight_decay, bc1, bc2,
-                                                      grad_scale);
+    if (grad_bf16)
+      adam_kernel<__nv_bfloat16><<<grid_for(n - done), kBlock, 0, s>>>(
+          master + done, param + done, static_cast<const __nv_bfloat16*>(grad) + done, m + done, v + done, n - done,
+          lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale);
+    else
+      adam_kernel<float><<<grid_for(n - done), kBlock, 0, s>>>(master + done, param + done,
+                                                               static_cast<const float*>(grad) + done, m + done,
+                                                               v + done, n - done, lr, beta1, beta2, eps,
+                                                               weight_decay, bc1, bc2, grad_scale);
   }
   return check_launch("adam_step");
+}
+
+__global__ void add_f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = f2bf(bf2f(dst[i]) + src[i]);
+}
+
+int add_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s) {
+  if (!n) return kOk;
+  add_f32_to_bf16_kernel<<<grid_for(n), kBlock, 0, s>>>(src, dst, n);
+  return check_launch("add_f32_to_bf16");
 }
 
 int fill_f32(float* p, float v, long long n, cudaStream_t s) {

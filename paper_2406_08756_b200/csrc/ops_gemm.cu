@@ -89,16 +89,32 @@ LYNX_DEV void epilogue_row(const Args& args, uint32_t t_row, long long row, int 
   for (int c = 0; c < kCols; c += 32) {
     uint32_t r[32];
     float4 prev[8];
+    BF8 prevb[4];
     float* outf = reinterpret_cast<float*>(args.c) + row * args.ldc + n0 + c;
+    BF8* outb = reinterpret_cast<BF8*>(reinterpret_cast<__nv_bfloat16*>(args.c) + row * args.ldc + n0 + c);
     if (args.epi == EPI_ACC_F32) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) prev[i] = reinterpret_cast<const float4*>(outf)[i];
+    } else if (args.epi == EPI_ACC_BF16) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) prevb[i] = outb[i];
     }
     tmem_ld32(t_row + c, r);
     tmem_ld_wait();
     float v[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+    if (args.epi == EPI_ACC_BF16) {  // bf16 gradient accumulation (16 B / parameter model states)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float pf[8];
+        bf8_to_f(prevb[i], pf);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[8 * i + j] += pf[j];
+        outb[i] = f_to_bf8(v + 8 * i);
+      }
+      continue;
+    }
     if (args.epi == EPI_ACC_F32 || args.epi == EPI_STORE_F32) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -742,7 +758,8 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   if (g.M % BM || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
     return set_error("gemm: M must be a multiple of 128 and K of 64");
   if (g.N % 128) return set_error("gemm: N must be a multiple of 128");
-  if ((g.epi == EPI_BF16 && g.ldc % 8) || (g.epi != EPI_BF16 && g.ldc % 4))
+  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_ACC_BF16;
+  if ((bf16_out && g.ldc % 8) || (!bf16_out && g.ldc % 4))
     return set_error("gemm: ldc must keep 16-byte row alignment");
   const int mode = g_gemm_mode;
   const bool n_ok = g.N % pair::kTileN == 0;

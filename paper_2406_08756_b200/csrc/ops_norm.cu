@@ -353,9 +353,9 @@ int ln_rows_chunks(int width) {
 // 32 columns per CTA; warp w sums the contiguous block range [w*per, (w+1)*per) with
 // 4-way unrolled loads, then warp 0 adds the 8 warp sums in order: a fixed tree, so
 // the result is bit-reproducible, with 8x the loads in flight of a one-thread-per-column loop.
-__global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ ws,
-                                                              float* __restrict__ acc0, float* __restrict__ acc1,
-                                                              int nblocks, int width, int nvec) {
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ ws, void* __restrict__ acc0,
+                                                              void* __restrict__ acc1, int nblocks, int width,
+                                                              int nvec, int acc_bf16) {
   __shared__ float part[8][2][32];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int col = blockIdx.x * 32 + lane;
@@ -379,8 +379,17 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
       t0 += part[w][0][lane];
       t1 += part[w][1][lane];
     }
-    acc0[col] += t0;
-    if (nvec > 1) acc1[col] += t1;
+    if (acc_bf16) {  // bf16 gradient accumulators (16 B / parameter model states)
+      auto* a0 = static_cast<__nv_bfloat16*>(acc0);
+      a0[col] = f2bf(bf2f(a0[col]) + t0);
+      if (nvec > 1) {
+        auto* a1 = static_cast<__nv_bfloat16*>(acc1);
+        a1[col] = f2bf(bf2f(a1[col]) + t1);
+      }
+    } else {
+      static_cast<float*>(acc0)[col] += t0;
+      if (nvec > 1) static_cast<float*>(acc1)[col] += t1;
+    }
   }
 }
 
@@ -436,8 +445,8 @@ size_t layernorm_bwd_workspace(int rows, int width) {
 }
 
 int layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bfloat16* gamma, const float* mean,
-                  const float* rstd, const __nv_bfloat16* dres, __nv_bfloat16* dx, float* dgamma_acc,
-                  float* dbeta_acc, float* workspace, int rows, int width, cudaStream_t s) {
+                  const float* rstd, const __nv_bfloat16* dres, __nv_bfloat16* dx, void* dgamma_acc,
+                  void* dbeta_acc, int acc_bf16, float* workspace, int rows, int width, cudaStream_t s) {
   if (width % 8 || width > kNT * kMaxC * 8) return set_error("layernorm: width must be a multiple of 8, <= 8192", kValidation);
   if (rows == 0) return kOk;
   const int cpt = ln_rows_chunks(width);
@@ -449,7 +458,8 @@ int layernorm_bwd(const __nv_bfloat16* dy, const __nv_bfloat16* x, const __nv_bf
     case 4: ln_bwd_rows_kernel<4><<<nb, nt, 0, s>>>(dy, x, gamma, mean, rstd, dres, dx, workspace, rows, width); break;
     default: ln_bwd_kernel<<<nb, kNT, 0, s>>>(dy, x, gamma, mean, rstd, dres, dx, workspace, rows, width);
   }
-  reduce_partials_kernel<<<(width + 31) / 32, 256, 0, s>>>(workspace, dgamma_acc, dbeta_acc, nb, width, 2);
+  reduce_partials_kernel<<<(width + 31) / 32, 256, 0, s>>>(workspace, dgamma_acc, dbeta_acc, nb, width, 2,
+                                                           acc_bf16);
   return check_launch("layernorm_bwd", 2);
 }
 
@@ -457,12 +467,13 @@ size_t column_sum_workspace(long long rows, int width) {
   return static_cast<size_t>(part_blocks(rows)) * width * sizeof(float);
 }
 
-int column_sum_acc(const __nv_bfloat16* x, float* acc, float* workspace, long long rows, int width, cudaStream_t s) {
+int column_sum_acc(const __nv_bfloat16* x, void* acc, int acc_bf16, float* workspace, long long rows, int width,
+                   cudaStream_t s) {
   if (width % 8) return set_error("column_sum: width must be a multiple of 8", kValidation);
   if (rows == 0) return kOk;
   const int nb = part_blocks(rows);
   column_partial_kernel<<<nb, kNT, 0, s>>>(x, workspace, rows, width);
-  reduce_partials_kernel<<<(width + 31) / 32, 256, 0, s>>>(workspace, acc, nullptr, nb, width, 1);
+  reduce_partials_kernel<<<(width + 31) / 32, 256, 0, s>>>(workspace, acc, nullptr, nb, width, 1, acc_bf16);
   return check_launch("column_sum_acc", 2);
 }
 

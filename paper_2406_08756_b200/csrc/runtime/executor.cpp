@@ -238,7 +238,11 @@ void Executor::alloc_persistent() {
                               attention_bwd_workspace(cfg_.micro_batch, cfg_.seq, cfg_.heads_rank())});
   sc_main_.ws = static_cast<float*>(m(ws));
   sc_main_.ws_bytes = ws;
-  if (cfg_.last()) sc_main_.logits = static_cast<__nv_bfloat16*>(m(static_cast<size_t>(cfg_.head_chunk) * cfg_.vocab * 2));
+  if (cfg_.last()) {
+    sc_main_.logits = static_cast<__nv_bfloat16*>(m(static_cast<size_t>(cfg_.head_chunk) * cfg_.vocab * 2));
+    head_gw32_ = static_cast<float*>(m(static_cast<size_t>(cfg_.vocab) * h * 4));
+  }
+  if (cfg_.first()) emb_gw32_ = static_cast<float*>(m(static_cast<size_t>(cfg_.vocab + cfg_.seq) * h * 4));
   sc_side_.t_h = static_cast<__nv_bfloat16*>(m(T * h * 2));
   const size_t ntok = static_cast<size_t>(cfg_.n_micro) * T;
   d_tokens_ = static_cast<int*>(m(ntok * 4));
@@ -265,6 +269,7 @@ void Executor::release_all() {
   for (void* p : {static_cast<void*>(sc_main_.t_h), static_cast<void*>(sc_main_.t_h2),
                   static_cast<void*>(sc_main_.t_wide), static_cast<void*>(sc_main_.ws),
                   static_cast<void*>(sc_main_.logits), static_cast<void*>(sc_side_.t_h), static_cast<void*>(d_tokens_),
+                  static_cast<void*>(head_gw32_), static_cast<void*>(emb_gw32_),
                   static_cast<void*>(d_labels_), static_cast<void*>(d_loss_), static_cast<void*>(d_mismatch_)})
     if (p) cudaFree(p);
   cudaFreeHost(h_tokens_);
@@ -286,7 +291,20 @@ void Executor::release_all() {
 void* Executor::alloc(size_t bytes, cudaStream_t s) {
   if (opt_.dry_run) return reinterpret_cast<void*>(0x1000);
   void* p = nullptr;
-  ck(cudaMallocFromPoolAsync(&p, bytes, pool_, s), "activation allocation");
+  const cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool_, s);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    uint64_t used = 0, reserved = 0;
+    size_t free_b = 0, total_b = 0;
+    cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemCurrent, &used);
+    cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemGetInfo(&free_b, &total_b);
+    throw RtError("activation allocation: out of device memory (request " + std::to_string(bytes) + " B, pool used " +
+                      std::to_string(used) + " / reserved " + std::to_string(reserved) + " B, device free " +
+                      std::to_string(free_b) + " of " + std::to_string(total_b) + " B)",
+                  kOutOfMemory);
+  }
+  ck(e, "activation allocation");
   return p;
 }
 
@@ -645,9 +663,10 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
       if (op_of_[i] == o) return i;
     return -1;
   };
-  auto colsum = [&](const void* x, float* acc, long long width) {
+  auto colsum = [&](const void* x, __nv_bfloat16* acc, long long width) {
     if (!opt_.dry_run)
-      ck_op(column_sum_acc(static_cast<const __nv_bfloat16*>(x), acc, sc.ws, T, static_cast<int>(width), s), "colsum");
+      ck_op(column_sum_acc(static_cast<const __nv_bfloat16*>(x), acc, 1, sc.ws, T, static_cast<int>(width), s),
+            "colsum");
   };
   const bool tp = tp_tmpl_;  // template with all-reduce ops (ar1/ar2 carry the residual epilogues)
   switch (op) {
@@ -682,7 +701,7 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
       if (!opt_.dry_run) {
         ck_op(layernorm_bwd(static_cast<const __nv_bfloat16*>(G.dln2), static_cast<const __nv_bfloat16*>(res1),
                             P.ln2_g, mean2, mean2 + T, static_cast<const __nv_bfloat16*>(G.dy),
-                            static_cast<__nv_bfloat16*>(G.dres), P.g_ln2_g, P.g_ln2_b, sc.ws, static_cast<int>(T), h, s),
+                            static_cast<__nv_bfloat16*>(G.dres), P.g_ln2_g, P.g_ln2_b, 1, sc.ws, static_cast<int>(T), h, s),
               "ln2_bwd");
         ck_op(dropout_bwd(static_cast<const __nv_bfloat16*>(G.dres), sc.t_h, T, h, p, seed,
                           drop_stream(l, mb, tp ? Op::AR1 : Op::PROJ_RES), s),
@@ -711,7 +730,7 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
       if (!opt_.dry_run)
         ck_op(layernorm_bwd(static_cast<const __nv_bfloat16*>(G.dln1), static_cast<const __nv_bfloat16*>(x), P.ln1_g,
                             mean1, mean1 + T, static_cast<const __nv_bfloat16*>(G.dres), static_cast<__nv_bfloat16*>(dx),
-                            P.g_ln1_g, P.g_ln1_b, sc.ws, static_cast<int>(T), h, s),
+                            P.g_ln1_g, P.g_ln1_b, 1, sc.ws, static_cast<int>(T), h, s),
               "ln1_bwd");
       release(G.dln1, s);
       release(G.dres, s);
@@ -738,14 +757,16 @@ void Executor::head_forward(int mb) {
                       static_cast<int>(T), h, cfg_.ln_eps, main_),
         "final_ln");
   const __nv_bfloat16* w = ps_.p("w_head");
-  float* gw = ps_.g("w_head");
+  float* gw = head_gw32_;  // fp32 across chunks and microbatches, added to the bf16 gradient at step end
   const float scale = 1.0f / static_cast<float>(T * cfg_.n_micro);
   for (long long c0 = 0; c0 < T; c0 += C) {
     const __nv_bfloat16* yc = y + c0 * h;
     GemmDesc lg{yc, h, false, w, h, false, sc_main_.logits, V, C, V, h, nullptr, EPI_BF16};
     ck_op(gemm_run(lg, main_), "lm_head");
     ck_op(xent_fwd_bwd(sc_main_.logits, d_labels_ + mb * T + c0, d_loss_ + mb * T + c0, C, V, scale, main_), "xent");
-    GemmDesc dw{sc_main_.logits, V, true, yc, h, true, gw, h, V, h, C, nullptr, EPI_ACC_F32};
+    GemmDesc dw{sc_main_.logits, V, true, yc, h, true, gw, h, V, h, C, nullptr,
+                head_first_ ? EPI_STORE_F32 : EPI_ACC_F32};
+    head_first_ = false;
     ck_op(gemm_run(dw, main_), "lm_head dW");
     GemmDesc dx{sc_main_.logits, V, false, w, h, true, static_cast<__nv_bfloat16*>(head_dy_[mb]) + c0 * h, h, C, h, V,
                 nullptr, EPI_BF16};
@@ -762,7 +783,7 @@ void Executor::head_backward(int mb) {
     const auto* mean = reinterpret_cast<const float*>(static_cast<char*>(ln_f_[mb]) + 2 * T * h);
     ck_op(layernorm_bwd(static_cast<const __nv_bfloat16*>(head_dy_[mb]), static_cast<const __nv_bfloat16*>(x),
                         ps_.p("lnf_g"), mean, mean + T, nullptr, static_cast<__nv_bfloat16*>(grad_[mb].dy),
-                        ps_.g("lnf_g"), ps_.g("lnf_b"), sc_main_.ws, static_cast<int>(T), h, main_),
+                        ps_.g("lnf_g"), ps_.g("lnf_b"), 1, sc_main_.ws, static_cast<int>(T), h, main_),
           "final_ln_bwd");
   }
   release(head_dy_[mb], main_);
@@ -830,7 +851,7 @@ void Executor::forward_pass(int mb) {
 void Executor::backward_pass(int mb) {
   // The first backward pass of the step writes the layer weight gradients
   // (fp32 store epilogue); later microbatches accumulate into them.
-  dw_epi_ = bwd_passes_ == 0 ? EPI_STORE_F32 : EPI_ACC_F32;
+  dw_epi_ = bwd_passes_ == 0 ? EPI_BF16 : EPI_ACC_BF16;  // bf16 gradients: store on the first pass
   ++bwd_passes_;
   const long long T = cfg_.tokens();
   const int h = cfg_.hidden;
@@ -892,7 +913,8 @@ void Executor::backward_pass(int mb) {
     if (!opt_.dry_run) {
       void* ws = alloc(static_cast<size_t>(T) * h * 4, main_);
       const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
-      ck_op(embedding_bwd(d_tokens_ + mb * T, static_cast<const __nv_bfloat16*>(dx), ps_.g("wte"), ps_.g("wpe"),
+      ck_op(embedding_bwd(d_tokens_ + mb * T, static_cast<const __nv_bfloat16*>(dx), emb_gw32_,
+                          emb_gw32_ + static_cast<size_t>(cfg_.vocab) * h,
                           static_cast<float*>(ws), cfg_.micro_batch, cfg_.seq, h, cfg_.vocab, cfg_.dropout, seed,
                           kEmbedStream | mb, main_),
             "embedding_bwd");
@@ -942,7 +964,11 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
     std::memcpy(h_labels_, labels, ntok * 4);
     ck(cudaMemcpyAsync(d_labels_, h_labels_, ntok * 4, cudaMemcpyHostToDevice, main_), "h2d labels");
   }
-  ck(cudaMemsetAsync(ps_.grad, 0, static_cast<size_t>(ps_.count()) * 4, main_), "zero grads");
+  ck(cudaMemsetAsync(ps_.grad, 0, static_cast<size_t>(ps_.count()) * 2, main_), "zero grads");
+  head_first_ = true;
+  if (cfg_.first())  // fp32 embedding-gradient accumulator (atomics), folded into the bf16 grads at step end
+    ck(cudaMemsetAsync(emb_gw32_, 0, static_cast<size_t>(cfg_.vocab + cfg_.seq) * cfg_.hidden * 4, main_),
+       "zero embedding grads");
   for (auto [bwd, mb] : passes) bwd ? backward_pass(mb) : forward_pass(mb);
   ck(cudaStreamWaitEvent(main_, [&] {
        cudaEvent_t e = ev();
@@ -953,9 +979,17 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   // Timing-only elided mode: the gradients are computed from stale buffers and may be
   // non-finite; they are zeroed and the update runs with a zero learning rate (same bytes
   // moved) so the weights, and the next steps' forward activations, stay valid.
+  const size_t hsz = static_cast<size_t>(cfg_.hidden);
+  if (cfg_.last() && !head_first_)
+    ck_op(add_f32_to_bf16(head_gw32_, ps_.g("w_head"), static_cast<long long>(cfg_.vocab) * hsz, main_), "head grad");
+  if (cfg_.first()) {
+    ck_op(add_f32_to_bf16(emb_gw32_, ps_.g("wte"), static_cast<long long>(cfg_.vocab) * hsz, main_), "wte grad");
+    ck_op(add_f32_to_bf16(emb_gw32_ + cfg_.vocab * hsz, ps_.g("wpe"), static_cast<long long>(cfg_.seq) * hsz, main_),
+          "wpe grad");
+  }
   if (opt_.elide_recompute)
-    ck(cudaMemsetAsync(ps_.grad, 0, static_cast<size_t>(ps_.count()) * 4, main_), "zero grads (elided)");
-  ck_op(adam_step(ps_.master, ps_.param, ps_.grad, ps_.m, ps_.v, ps_.count(), opt_.elide_recompute ? 0.f : cfg_.lr,
+    ck(cudaMemsetAsync(ps_.grad, 0, static_cast<size_t>(ps_.count()) * 2, main_), "zero grads (elided)");
+  ck_op(adam_step(ps_.master, ps_.param, ps_.grad, 1, ps_.m, ps_.v, ps_.count(), opt_.elide_recompute ? 0.f : cfg_.lr,
                   cfg_.beta1, cfg_.beta2, cfg_.adam_eps, opt_.elide_recompute ? 0.f : cfg_.weight_decay, step_, 1.0f,
                   main_),
         "adam");
@@ -998,7 +1032,7 @@ std::string Executor::report_json() const {
   j["recompute_mismatch_words"] = rep_.recompute_mismatch_words;
   j["loss"] = rep_.loss;
   j["pool_high_water_bytes"] = rep_.pool_high_water;
-  j["static_bytes_allocated"] = static_cast<long long>(ps_.count()) * 18;
+  j["static_bytes_allocated"] = static_cast<long long>(ps_.count()) * 16;
   j["params"] = ps_.count();
   j["layers"] = cfg_.layers;
   j["microbatches"] = cfg_.n_micro;
@@ -1051,12 +1085,17 @@ void Executor::get_tensor(const std::string& name, void* host, size_t bytes) {
   const std::string base = grad ? name.substr(5) : name;
   for (const auto& r : ps_.refs())
     if (r.name == base) {
-      const size_t want = static_cast<size_t>(r.n) * (grad ? 4 : 2);
+      const size_t want = static_cast<size_t>(r.n) * (grad ? 4 : 2);  // gradients are returned as fp32
       if (bytes != want) throw RtError("tensor " + name + " has " + std::to_string(want) + " bytes", kValidation);
       ck(cudaStreamSynchronize(main_), "sync");
-      ck(cudaMemcpy(host, grad ? static_cast<void*>(ps_.grad + r.off) : static_cast<void*>(ps_.param + r.off), bytes,
-                    cudaMemcpyDeviceToHost),
-         "d2h");
+      if (grad) {
+        std::vector<__nv_bfloat16> tmp(static_cast<size_t>(r.n));
+        ck(cudaMemcpy(tmp.data(), ps_.grad + r.off, tmp.size() * 2, cudaMemcpyDeviceToHost), "d2h");
+        float* out = static_cast<float*>(host);
+        for (size_t i = 0; i < tmp.size(); ++i) out[i] = __bfloat162float(tmp[i]);
+      } else {
+        ck(cudaMemcpy(host, ps_.param + r.off, bytes, cudaMemcpyDeviceToHost), "d2h");
+      }
       return;
     }
   throw RtError("unknown tensor " + name, kValidation);
@@ -1068,7 +1107,7 @@ void Executor::set_tensor(const std::string& name, const void* host, size_t byte
     if (r.name == name) {
       if (bytes != static_cast<size_t>(r.n) * 4) throw RtError("set_tensor expects fp32 values", kValidation);
       ck(cudaMemcpy(ps_.master + r.off, host, bytes, cudaMemcpyHostToDevice), "h2d");
-      ck_op(adam_step(ps_.master + r.off, ps_.param + r.off, ps_.grad + r.off, ps_.m + r.off, ps_.v + r.off, r.n, 0.f,
+      ck_op(adam_step(ps_.master + r.off, ps_.param + r.off, ps_.grad + r.off, 1, ps_.m + r.off, ps_.v + r.off, r.n, 0.f,
                       cfg_.beta1, cfg_.beta2, 1.f, 0.f, 1, 0.f, main_),
             "copy");  // lr = 0: writes bf16(master) without changing it
       ck(cudaStreamSynchronize(main_), "sync");

@@ -172,6 +172,9 @@ class Executor {
   int bwd_passes_ = 0;
   int dw_epi_ = 1;  // EPI_ACC_F32
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
+  float* head_gw32_ = nullptr;  // last stage: LM-head weight gradient, fp32 across chunks / microbatches
+  float* emb_gw32_ = nullptr;   // first stage: wte | wpe gradients, fp32 (scatter-add with atomics)
+  bool head_first_ = true;
   std::vector<std::tuple<int, int, int, int, double, double>> trace_;  // stage, mb, kind, op, start, end
 };
 

@@ -51,11 +51,12 @@ struct ParamRef {
 
 struct LayerParams {
   __nv_bfloat16 *ln1_g, *ln1_b, *w_qkv, *b_qkv, *w_proj, *b_proj, *ln2_g, *ln2_b, *w_fc1, *b_fc1, *w_fc2, *b_fc2;
-  float *g_ln1_g, *g_ln1_b, *g_w_qkv, *g_b_qkv, *g_w_proj, *g_b_proj, *g_ln2_g, *g_ln2_b, *g_w_fc1, *g_b_fc1,
+  __nv_bfloat16 *g_ln1_g, *g_ln1_b, *g_w_qkv, *g_b_qkv, *g_w_proj, *g_b_proj, *g_ln2_g, *g_ln2_b, *g_w_fc1, *g_b_fc1,
       *g_w_fc2, *g_b_fc2;
 };
 
-// Flat bf16 params + fp32 master / grad / Adam m / v (18 B per parameter).
+// Flat bf16 params + bf16 grads + fp32 master / Adam m / v: 16 B per parameter, the model-state
+// accounting of the paper (FP16 params and gradients, FP32 optimizer data).
 class ParamStore {
  public:
   void layout(const ModelCfg& c);
@@ -63,11 +64,12 @@ class ParamStore {
   void release();
   LayerParams layer(int l) const;
   __nv_bfloat16* p(const std::string& name) const;
-  float* g(const std::string& name) const;
+  __nv_bfloat16* g(const std::string& name) const;
   long long count() const { return total_; }
   const std::vector<ParamRef>& refs() const { return refs_; }
   __nv_bfloat16* param = nullptr;
-  float *master = nullptr, *grad = nullptr, *m = nullptr, *v = nullptr;
+  __nv_bfloat16* grad = nullptr;
+  float *master = nullptr, *m = nullptr, *v = nullptr;
 
  private:
   const ParamRef& find(const std::string& name) const;

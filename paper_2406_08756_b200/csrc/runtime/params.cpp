@@ -68,7 +68,7 @@ const ParamRef& ParamStore::find(const std::string& name) const {
 }
 
 __nv_bfloat16* ParamStore::p(const std::string& name) const { return param + find(name).off; }
-float* ParamStore::g(const std::string& name) const { return grad + find(name).off; }
+__nv_bfloat16* ParamStore::g(const std::string& name) const { return grad + find(name).off; }
 
 LayerParams ParamStore::layer(int l) const {
   const std::string p = "l" + std::to_string(l) + ".";
@@ -110,10 +110,10 @@ void ParamStore::allocate_and_init(const ModelCfg& c, cudaStream_t s) {
   };
   ck(cudaMalloc(&param, n * 2));
   ck(cudaMalloc(&master, n * 4));
-  ck(cudaMalloc(&grad, n * 4));
+  ck(cudaMalloc(&grad, n * 2));
   ck(cudaMalloc(&m, n * 4));
   ck(cudaMalloc(&v, n * 4));
-  ck(cudaMemsetAsync(grad, 0, n * 4, s));
+  ck(cudaMemsetAsync(grad, 0, n * 2, s));
   ck(cudaMemsetAsync(m, 0, n * 4, s));
   ck(cudaMemsetAsync(v, 0, n * 4, s));
   ck(cudaMemsetAsync(param, 0, n * 2, s));  // alignment padding stays zero
@@ -151,7 +151,8 @@ void ParamStore::release() {
   cudaFree(m);
   cudaFree(v);
   param = nullptr;
-  master = grad = m = v = nullptr;
+  grad = nullptr;
+  master = m = v = nullptr;
 }
 
 }  // namespace lynx::rt

@@ -16,8 +16,9 @@ T = micro_batch * seq tokens, bf16 activations:
 
 Times come either from a roofline estimate (`estimate_times`) or from
 measurements of the executor's own kernels on B200 (`profiler.py`, the
-paper's Fig. 5 profiler role). Static bytes follow the 18 B/parameter layout
-the executor allocates (bf16 weights, fp32 grads, fp32 master, Adam m and v).
+paper's Fig. 5 profiler role). Static bytes follow the 16 B/parameter model states of
+the paper that the executor allocates: bf16 weights and gradients,
+fp32 master weights and Adam m, v.
 """
 from __future__ import annotations
 
@@ -25,7 +26,7 @@ import json
 from dataclasses import asdict, dataclass, field
 from fractions import Fraction
 
-BYTES_PER_PARAM_STATIC = 18  # bf16 param 2 + fp32 grad 4 + fp32 master 4 + m 4 + v 4
+BYTES_PER_PARAM_STATIC = 16  # bf16 param 2 + bf16 grad 2 + fp32 master 4 + m 4 + v 4
 
 
 @dataclass

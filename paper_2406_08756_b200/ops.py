@@ -11,7 +11,7 @@ import torch
 
 from ._native import call, lib
 
-EPI_BF16, EPI_ACC_F32, EPI_F32 = 0, 1, 2
+EPI_BF16, EPI_ACC_F32, EPI_F32, EPI_ACC_BF16 = 0, 1, 2, 3
 
 
 def _p(t: torch.Tensor | None) -> int | None:
@@ -32,7 +32,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = F
     M, K = (a.shape[1], a.shape[0]) if a_mn else (a.shape[0], a.shape[1])
     N = b.shape[1] if b_mn else b.shape[0]
     if out is None:
-        out = torch.empty(M, N, device=a.device, dtype=torch.bfloat16 if epi == EPI_BF16 else torch.float32)
+        out = torch.empty(M, N, device=a.device, dtype=torch.bfloat16 if epi in (EPI_BF16, EPI_ACC_BF16) else torch.float32)
     call("lynx_op_gemm", a.data_ptr(), a.stride(0), int(a_mn), b.data_ptr(), b.stride(0), int(b_mn), out.data_ptr(),
          out.stride(0), M, N, K, _p(bias), epi, _s())
     return out

@@ -134,6 +134,7 @@ def measure_op_times(c: gp.GPTConfig, iters: int = 5) -> dict[str, Fraction]:
 
 def measured_profile(c: gp.GPTConfig, device_bytes: int | None = None, reserve_bytes: int = 0) -> tuple[dict, dict]:
     times = measure_op_times(c)
+    torch.cuda.empty_cache()  # release the measurement tensors (they die with measure_op_times' frame)
     return gp.profile(c, times=times, device_bytes=device_bytes, reserve_bytes=reserve_bytes), times
 
 
