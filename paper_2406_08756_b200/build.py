@@ -37,7 +37,7 @@ def _nlohmann_include() -> str:
 
 def _flags() -> list[str]:
     return [
-        "-O3", "-std=c++17", "-lineinfo", *ARCH,
+        "-O3", "-std=c++17", "-lineinfo", *ARCH, *(["-DLYNX_ATTN_TRACE"] if os.environ.get("LYNX_BUILD_TRACE") else []),
         "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
         "--expt-relaxed-constexpr",
         f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{_nlohmann_include()}",

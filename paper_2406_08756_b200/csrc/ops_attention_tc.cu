@@ -77,8 +77,21 @@ LYNX_DEV uint64_t mnmaj(uint32_t base, int kk, uint32_t atom_bytes) {
 }
 
 // Store 8 bf16 (16 B) as chunk `c` of row `r` of a SW128 K-major tile (128-B rows).
+// Explicit st.shared: through a generic pointer the compiler emits generic ST, which costs
+// an address-space resolution per access on the row warps' critical path.
 LYNX_DEV void st_sw128(uint8_t* tile, int r, int c, const BF8& v) {
-  *reinterpret_cast<BF8*>(tile + r * kAtom + ((c ^ (r & 7)) << 4)) = v;
+  const uint32_t a = smem_u32(tile + r * kAtom + ((c ^ (r & 7)) << 4));
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]),
+               "r"(v.w[3])
+               : "memory");
+}
+// 4 consecutive fp32 from shared memory.
+LYNX_DEV float4 lds128(const void* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
 }
 
 LYNX_DEV float u2f(uint32_t v) { return __uint_as_float(v); }
@@ -88,6 +101,31 @@ LYNX_DEV float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// Per-tile event timeline of CTA (0,0,0) for kernel tuning: build with -DLYNX_ATTN_TRACE
+// (LYNX_BUILD_TRACE=1 python -m paper_2406_08756_b200.build); compiled out otherwise.
+#ifdef LYNX_ATTN_TRACE
+__device__ long long g_atrace[8][64];
+#define ATRACE(tag, j)                                                              \
+  do {                                                                              \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64)          \
+      g_atrace[tag][j] = clock64();                                                 \
+  } while (0)
+#define ATRACE_DUMP(n)                                                              \
+  do {                                                                              \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)  \
+      for (int t_ = 0; t_ < 8; ++t_)                                                \
+        for (int j_ = 0; j_ < (n) && j_ < 64; ++j_)                                 \
+          printf("T %d %d %lld\n", t_, j_, g_atrace[t_][j_]);                       \
+  } while (0)
+#else
+#define ATRACE(tag, j) \
+  do {                 \
+  } while (0)
+#define ATRACE_DUMP(n) \
+  do {                 \
+  } while (0)
+#endif
 
 // ============================================================== forward
 template <int D>
@@ -286,7 +324,7 @@ struct DkvL {
 };
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
                         const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
                         const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
@@ -311,7 +349,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(q_empty + i, 1);
     }
     for (int i = 0; i < 2; ++i) mbar_init(s_full + i, 1);
-    mbar_init(pd_full, 128);
+    mbar_init(pd_full, 256);
     mbar_init(mma_done, 1);
     mbar_init(fin, 1);
     fence_barrier_init();
@@ -334,6 +372,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int i = 0; i < n; ++i) {
         const int st = i % NS, q0 = (i0 + i) * 64;
         if (i >= NS) mbar_wait(q_empty + st, ((i / NS) - 1) & 1);
+        ATRACE(0, i);
         mbar_arrive_expect_tx(q_full + st, 2 * L::kQT + 512);
         for (int a = 0; a < kA; ++a) {
           tma_load_2d(&map_q, q_full + st, smem + L::kQ + st * L::kQT + a * 8192, h * D + 64 * a, row0 + q0,
@@ -354,6 +393,7 @@ __global__ void __launch_bounds__(256, 1)
       auto issue_s = [&](int i) {
         const int st = i % NS, tb = i & 1;
         mbar_wait(q_full + st, (i / NS) & 1);
+        ATRACE(1, i);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -368,6 +408,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int i = 0; i < n; ++i) {
         const int st = i % NS;
         mbar_wait(pd_full, i & 1);
+        ATRACE(2, i);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
@@ -381,77 +422,87 @@ __global__ void __launch_bounds__(256, 1)
       umma_commit(fin);
     }
   } else if (warp >= 4) {
-    const int k = (warp - 4) * 32 + lane;  // key row of the tile
+    // Two row warpgroups: warps 4-7 take query columns 0-31 of each 64-query tile, warps 8-11
+    // columns 32-63 (same key rows / TMEM lanes). The work is elementwise, so the halves never
+    // exchange data; two warps per SM sub-partition hide the latencies one row warp cannot (a
+    // clock64 trace showed ~1500 cycles of row work per tile against ~1000 of MMA).
+    const int half = warp >= 8 ? 1 : 0;
+    const int k = (warp % 4) * 32 + lane;  // key row of the tile
     const int key = kb * 128 + k;
-    const uint32_t lanes = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
     uint8_t* pt = smem + L::kPT;
     uint8_t* ds = smem + L::kDS;
     for (int i = 0; i < n; ++i) {
       const int st = i % NS, tb = i & 1, q0 = (i0 + i) * 64;
       mbar_wait(q_full + st, (i / NS) & 1);
       mbar_wait(s_full + tb, (i >> 1) & 1);
+      if (threadIdx.x == 128) ATRACE(3, i);
       tc_fence_after();
-      const float* sl = reinterpret_cast<const float*>(smem + L::kVec + st * 256);
-      const float* sd = reinterpret_cast<const float*>(smem + L::kVec + (NS + st) * 256);
-      BF8 pv[8], gv[8];
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      const float* sl = reinterpret_cast<const float*>(smem + L::kVec + st * 256) + half * 32;
+      const float* sd = reinterpret_cast<const float*>(smem + L::kVec + (NS + st) * 256) + half * 32;
+      BF8 pv[4], gv[4];
+      {
         uint32_t sr[32], dp[32];
         tmem_ld32(tmem + lanes + tb * 64 + half * 32, sr);
         tmem_ld32(tmem + lanes + 128 + tb * 64 + half * 32, dp);
         tmem_ld_wait();
-        float p[32], g[32];
+        float p[32], g[32], lv[32], dv[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) p[c] = ex2(fmaf(u2f(sr[c]), scale_log2, -sl[half * 32 + c]));
+        for (int c = 0; c < 8; ++c) {
+          const float4 a = lds128(sl + 4 * c), d4 = lds128(sd + 4 * c);
+          lv[4 * c] = a.x, lv[4 * c + 1] = a.y, lv[4 * c + 2] = a.z, lv[4 * c + 3] = a.w;
+          dv[4 * c] = d4.x, dv[4 * c + 1] = d4.y, dv[4 * c + 2] = d4.z, dv[4 * c + 3] = d4.w;
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) p[c] = ex2(fmaf(u2f(sr[c]), scale_log2, -lv[c]));
         if (i < 2) {  // the two 64-query tiles that meet the diagonal of this 128-key tile
 #pragma unroll
           for (int c = 0; c < 32; ++c)
             if (key > q0 + half * 32 + c) p[c] = 0.f;
         }
 #pragma unroll
-        for (int c = 0; c < 32; ++c) g[c] = p[c] * (u2f(dp[c]) - sd[half * 32 + c]);
+        for (int c = 0; c < 32; ++c) g[c] = p[c] * (u2f(dp[c]) - dv[c]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          pv[half * 4 + c] = f_to_bf8(p + 8 * c);
-          gv[half * 4 + c] = f_to_bf8(g + 8 * c);
+          pv[c] = f_to_bf8(p + 8 * c);
+          gv[c] = f_to_bf8(g + 8 * c);
         }
       }
+      if (threadIdx.x == 128) ATRACE(4, i);
       if (i >= 1) mbar_wait(mma_done, (i - 1) & 1);  // P^T / dS^T of the previous tile consumed
+      if (threadIdx.x == 128) ATRACE(5, i);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        st_sw128(pt, k, c, pv[c]);
-        st_sw128(ds, k, c, gv[c]);
+      for (int c = 0; c < 4; ++c) {
+        st_sw128(pt, k, half * 4 + c, pv[c]);
+        st_sw128(ds, k, half * 4 + c, gv[c]);
       }
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(pd_full);
+      if (threadIdx.x == 128) ATRACE(6, i);
     }
     mbar_wait(fin, 0);
     tc_fence_after();
+    // epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled)
     const long long grow = static_cast<long long>(row0 + key) * 3 * HD;
-    BF8* dk = reinterpret_cast<BF8*>(dqkv + grow + HD + h * D);
-    BF8* dv = reinterpret_cast<BF8*>(dqkv + grow + 2 * HD + h * D);
+    BF8* dst = reinterpret_cast<BF8*>(dqkv + grow + (half ? HD : 2 * HD) + h * D);
+    const float mul = half ? scale : 1.f;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       uint32_t o[32];
       float f[32];
-      tmem_ld32(tmem + lanes + 256 + c * 32, o);
+      tmem_ld32(tmem + lanes + (half ? 384 : 256) + c * 32, o);
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]);
+      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]) * mul;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) dv[c * 4 + i] = f_to_bf8(f + 8 * i);
-      tmem_ld32(tmem + lanes + 384 + c * 32, o);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]) * scale;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dk[c * 4 + i] = f_to_bf8(f + 8 * i);
+      for (int i = 0; i < 4; ++i) dst[c * 4 + i] = f_to_bf8(f + 8 * i);
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  ATRACE_DUMP(n);
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
@@ -467,7 +518,7 @@ struct DqL {
 };
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_dq_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                       const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
                       const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
@@ -492,7 +543,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
-      mbar_init(ds_full + i, 128);
+      mbar_init(ds_full + i, 256);
       mbar_init(ds_free + i, 1);
     }
     mbar_init(fin, 1);
@@ -559,9 +610,11 @@ __global__ void __launch_bounds__(256, 1)
       umma_commit(fin);
     }
   } else if (warp >= 4) {
-    const int r = (warp - 4) * 32 + lane;
+    // Two row warpgroups split each 64-key tile's columns (0-31 / 32-63), as in dK/dV.
+    const int half = warp >= 8 ? 1 : 0;
+    const int r = (warp % 4) * 32 + lane;
     const int q = qb * 128 + r;
-    const uint32_t lanes = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const long long vi = (static_cast<long long>(b) * H + h) * S + q;
     const float l2 = lse2[vi], dq = dvec[vi];
     for (int j = 0; j < n; ++j) {
@@ -571,8 +624,7 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       uint8_t* ds = smem + L::kDS + st * 16384;
       const bool diag = j >= 2 * qb;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      {
         uint32_t s[32], dp[32];
         tmem_ld32(tmem + lanes + st * 64 + half * 32, s);
         tmem_ld32(tmem + lanes + 128 + st * 64 + half * 32, dp);
@@ -596,12 +648,12 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_wait(fin, 0);
     tc_fence_after();
-    BF8* dqrow = reinterpret_cast<BF8*>(dqkv + static_cast<long long>(row0 + q) * 3 * HD + h * D);
+    BF8* dqrow = reinterpret_cast<BF8*>(dqkv + static_cast<long long>(row0 + q) * 3 * HD + h * D + half * (D / 2));
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < D / 64; ++c) {  // each warpgroup writes half of the D columns
       uint32_t o[32];
       float f[32];
-      tmem_ld32(tmem + lanes + 256 + c * 32, o);
+      tmem_ld32(tmem + lanes + 256 + half * (D / 2) + c * 32, o);
       tmem_ld_wait();
 #pragma unroll
       for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]) * scale;
@@ -638,10 +690,10 @@ int bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, c
   const float scale = 1.f / sqrtf(static_cast<float>(D)), scale_log2 = scale * kLog2e;
   auto k1 = attn_dkdv_tc_kernel<D>;
   cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvL<D>::kBytes);
-  k1<<<dim3(S / 128, H, B), 256, DkvL<D>::kBytes, s>>>(m128, m64, d64, lse, dvec, dqkv, S, H, scale, scale_log2);
+  k1<<<dim3(S / 128, H, B), 384, DkvL<D>::kBytes, s>>>(m128, m64, d64, lse, dvec, dqkv, S, H, scale, scale_log2);
   auto k2 = attn_dq_tc_kernel<D>;
   cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, DqL<D>::kBytes);
-  k2<<<dim3(S / 128, H, B), 256, DqL<D>::kBytes, s>>>(m128, m64, d128, lse, dvec, dqkv, S, H, scale, scale_log2);
+  k2<<<dim3(S / 128, H, B), 384, DqL<D>::kBytes, s>>>(m128, m64, d128, lse, dvec, dqkv, S, H, scale, scale_log2);
   return check_launch("attention_bwd_tc", 2);
 }
 
