@@ -9,9 +9,11 @@
 //   warps 4..7  "row" warps: one thread per TMEM lane (= one tile row) doing
 //               the softmax / gradient elementwise work between the MMAs and
 //               the epilogue.
-// The row warps hand bf16 P / dS tiles to the tensor core through shared
-// memory written in the canonical SW128 K-major layout (16-byte chunk c of
-// row r stored at chunk c ^ (r & 7)), fenced with fence.proxy.async.
+// The row warps hand bf16 P / dS tiles to the tensor core through tensor
+// memory: they overwrite the fp32 S / dP columns they just read with packed
+// bf16 pairs (tcgen05.st) and the MMA reads its A operand from TMEM
+// (tcgen05.mma [d], [a_tmem], b_desc) — no shared-memory round trip and no
+// generic -> async proxy fence on the row warps' critical path.
 //
 // Forward  (per 128-query tile, 128-key tiles double-buffered):
 //   S_j = Q K_j^T -> TMEM (2 buffers, S_{j+1} runs while softmax j works),
@@ -52,6 +54,25 @@ LYNX_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
       : "memory");
 }
 LYNX_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+LYNX_DEV void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T: A (128 rows x 16 K, bf16 pairs packed per 32-bit TMEM cell,
+// one row per lane, 8 columns per K step) is read from tensor memory, so a row warp can hand
+// its P / dS tile to the tensor core with tcgen05.st — no shared-memory round trip and no
+// generic -> async proxy fence.
+LYNX_DEV void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
+}
 
 // 1-D bulk copy global -> shared, completing on an mbarrier (16-B aligned, size % 16 == 0).
 LYNX_DEV void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
@@ -76,15 +97,6 @@ LYNX_DEV uint64_t mnmaj(uint32_t base, int kk, uint32_t atom_bytes) {
   return umma_desc_sw128(base + kk * 2048, atom_bytes, 1024);
 }
 
-// Store 8 bf16 (16 B) as chunk `c` of row `r` of a SW128 K-major tile (128-B rows).
-// Explicit st.shared: through a generic pointer the compiler emits generic ST, which costs
-// an address-space resolution per access on the row warps' critical path.
-LYNX_DEV void st_sw128(uint8_t* tile, int r, int c, const BF8& v) {
-  const uint32_t a = smem_u32(tile + r * kAtom + ((c ^ (r & 7)) << 4));
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]),
-               "r"(v.w[3])
-               : "memory");
-}
 // 4 consecutive fp32 from shared memory.
 LYNX_DEV float4 lds128(const void* p) {
   float4 v;
@@ -131,7 +143,7 @@ __device__ long long g_atrace[8][64];
 template <int D>
 struct FwdL {
   static constexpr int kTile = 128 * D * 2;  // one 128-row x D tile (D/64 atoms of 16 KB)
-  static constexpr int kQ = 0, kK = kTile, kV = 3 * kTile, kP = 5 * kTile, kBar = kP + 128 * 128 * 2;
+  static constexpr int kQ = 0, kK = kTile, kV = 3 * kTile, kBar = 5 * kTile;  // P lives in TMEM
   static constexpr int kBytes = kBar + 128 + 1024;
 };
 
@@ -196,8 +208,7 @@ __global__ void __launch_bounds__(256, 1)
     if (elect_one()) {
       constexpr uint32_t idS = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idO = umma_idesc_bf16(128, D, false, true);
-      const uint32_t sQ = smem_u32(smem + L::kQ), sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV),
-                     sP = smem_u32(smem + L::kP);
+      const uint32_t sQ = smem_u32(smem + L::kQ), sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV);
       auto issue_s = [&](int j) {
         const int st = j & 1;
         mbar_wait(k_full + st, (j >> 1) & 1);
@@ -218,7 +229,8 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          umma_f16(tmem + 256, kmaj(sP, kk, 16384), mnmaj(sV + st * L::kTile, kk, 16384), idO, (j | kk) != 0);
+          umma_f16_ts(tmem + 256, tmem + st * 128 + kk * 8, mnmaj(sV + st * L::kTile, kk, 16384), idO,
+                      (j | kk) != 0);  // A = P(j), packed bf16 over S(j) in TMEM
         umma_commit(pv_done);
         umma_commit(v_empty + st);
         if (j + 2 < n) issue_s(j + 2);
@@ -227,7 +239,6 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     const int r = (warp - 4) * 32 + lane;
     const uint32_t lanes = static_cast<uint32_t>((warp - 4) * 32) << 16;
-    uint8_t* sP = smem + L::kP;
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n; ++j) {
       const int st = j & 1;
@@ -265,7 +276,10 @@ __global__ void __launch_bounds__(256, 1)
       }
       const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
       l_run = l_run * corr + rs;
-      if (j > 0) {
+      // O is rescaled (rarely) after PV(j-1) completes. P(j) needs no wait: PV(j-2), the last
+      // reader of TMEM buffer st, completed before S(j) (tensor-pipe order). pv_done can be at
+      // most at phase j here (PV(j) needs this tile's P), so skipping waits is safe.
+      if (j > 0 && need) {
         mbar_wait(pv_done, (j - 1) & 1);
         tc_fence_after();
         if (need) {
@@ -282,8 +296,13 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
 #pragma unroll
-      for (int c = 0; c < 16; ++c) st_sw128(sP + (c >> 3) * 16384, r, c & 7, f_to_bf8(x + c * 8));
-      fence_proxy_async();
+      for (int c = 0; c < 4; ++c) {
+        uint32_t packed[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(x[32 * c + 2 * i], x[32 * c + 2 * i + 1]);
+        tmem_st16(tmem + lanes + st * 128 + c * 16, packed);
+      }
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(p_full);
     }
@@ -317,8 +336,8 @@ struct DkvL {
   static constexpr int kStages = 3;        // Q / dO / lse / D ring (each stage is used early and late)
   static constexpr int kKV = 128 * D * 2;  // K or V tile: D/64 atoms of 16 KB (128 rows)
   static constexpr int kQT = 64 * D * 2;   // Q or dO tile: D/64 atoms of 8 KB (64 rows)
-  static constexpr int kK = 0, kV = kKV, kQ = 2 * kKV, kDO = kQ + kStages * kQT, kPT = kDO + kStages * kQT;
-  static constexpr int kDS = kPT + 16384, kVec = kDS + 16384;  // lse2[kStages][64], dvec[kStages][64]
+  static constexpr int kK = 0, kV = kKV, kQ = 2 * kKV, kDO = kQ + kStages * kQT;
+  static constexpr int kVec = kDO + kStages * kQT;  // lse2[kStages][64], dvec[kStages][64]; P^T / dS^T live in TMEM
   static constexpr int kBar = kVec + 2 * kStages * 256;
   static constexpr int kBytes = kBar + 128 + 1024;
 };
@@ -389,7 +408,7 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idS = umma_idesc_bf16(128, 64, false, false);
       constexpr uint32_t idG = umma_idesc_bf16(128, D, false, true);
       const uint32_t sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV), sQ = smem_u32(smem + L::kQ),
-                     sDO = smem_u32(smem + L::kDO), sPT = smem_u32(smem + L::kPT), sDS = smem_u32(smem + L::kDS);
+                     sDO = smem_u32(smem + L::kDO);
       auto issue_s = [&](int i) {
         const int st = i % NS, tb = i & 1;
         mbar_wait(q_full + st, (i / NS) & 1);
@@ -410,10 +429,12 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(pd_full, i & 1);
         ATRACE(2, i);
         tc_fence_after();
+        const uint32_t tb = static_cast<uint32_t>(i & 1);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          umma_f16(tmem + 256, kmaj(sPT, kk, 16384), mnmaj(sDO + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
-          umma_f16(tmem + 384, kmaj(sDS, kk, 16384), mnmaj(sQ + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
+        for (int kk = 0; kk < 4; ++kk) {  // A = P^T / dS^T, packed bf16 over S^T / dP^T in TMEM buffer tb
+          umma_f16_ts(tmem + 256, tmem + tb * 64 + kk * 8, mnmaj(sDO + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
+          umma_f16_ts(tmem + 384, tmem + 128 + tb * 64 + kk * 8, mnmaj(sQ + st * L::kQT, kk, 8192), idG,
+                      (i | kk) != 0);
         }
         umma_commit(mma_done);
         umma_commit(q_empty + st);
@@ -430,8 +451,6 @@ __global__ void __launch_bounds__(384, 1)
     const int k = (warp % 4) * 32 + lane;  // key row of the tile
     const int key = kb * 128 + k;
     const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
-    uint8_t* pt = smem + L::kPT;
-    uint8_t* ds = smem + L::kDS;
     for (int i = 0; i < n; ++i) {
       const int st = i % NS, tb = i & 1, q0 = (i0 + i) * 64;
       mbar_wait(q_full + st, (i / NS) & 1);
@@ -440,7 +459,6 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       const float* sl = reinterpret_cast<const float*>(smem + L::kVec + st * 256) + half * 32;
       const float* sd = reinterpret_cast<const float*>(smem + L::kVec + (NS + st) * 256) + half * 32;
-      BF8 pv[4], gv[4];
       {
         uint32_t sr[32], dp[32];
         tmem_ld32(tmem + lanes + tb * 64 + half * 32, sr);
@@ -462,21 +480,19 @@ __global__ void __launch_bounds__(384, 1)
         }
 #pragma unroll
         for (int c = 0; c < 32; ++c) g[c] = p[c] * (u2f(dp[c]) - dv[c]);
+        uint32_t pp[16], gp[16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          pv[c] = f_to_bf8(p + 8 * c);
-          gv[c] = f_to_bf8(g + 8 * c);
+        for (int c = 0; c < 16; ++c) {
+          pp[c] = pack_bf16x2(p[2 * c], p[2 * c + 1]);
+          gp[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
         }
+        if (threadIdx.x == 128) ATRACE(4, i);
+        // P^T(i) / dS^T(i) overwrite S^T(i) / dP^T(i) in place (this half's 32 queries -> 16
+        // packed columns). dV / dK(i-2), the last readers of buffer tb, completed before S^T(i).
+        tmem_st16(tmem + lanes + tb * 64 + half * 16, pp);
+        tmem_st16(tmem + lanes + 128 + tb * 64 + half * 16, gp);
+        tmem_st_wait();
       }
-      if (threadIdx.x == 128) ATRACE(4, i);
-      if (i >= 1) mbar_wait(mma_done, (i - 1) & 1);  // P^T / dS^T of the previous tile consumed
-      if (threadIdx.x == 128) ATRACE(5, i);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        st_sw128(pt, k, half * 4 + c, pv[c]);
-        st_sw128(ds, k, half * 4 + c, gv[c]);
-      }
-      fence_proxy_async();
       tc_fence_before();
       mbar_arrive(pd_full);
       if (threadIdx.x == 128) ATRACE(6, i);
@@ -512,8 +528,8 @@ struct DqL {
   static constexpr int kQT = 128 * D * 2;  // Q or dO tile (128 rows)
   static constexpr int kKT = 64 * D * 2;   // K or V tile (64 rows)
   static constexpr int kStages = 3;
-  static constexpr int kQ = 0, kDO = kQT, kK = 2 * kQT, kV = kK + kStages * kKT, kDS = kV + kStages * kKT;
-  static constexpr int kBar = kDS + 2 * 16384;
+  static constexpr int kQ = 0, kDO = kQT, kK = 2 * kQT, kV = kK + kStages * kKT;
+  static constexpr int kBar = kV + kStages * kKT;  // dS lives in TMEM
   static constexpr int kBytes = kBar + 128 + 1024;
 };
 
@@ -580,7 +596,7 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idS = umma_idesc_bf16(128, 64, false, false);
       constexpr uint32_t idG = umma_idesc_bf16(128, D, false, true);
       const uint32_t sQ = smem_u32(smem + L::kQ), sDO = smem_u32(smem + L::kDO), sK = smem_u32(smem + L::kK),
-                     sV = smem_u32(smem + L::kV), sDS = smem_u32(smem + L::kDS);
+                     sV = smem_u32(smem + L::kV);
       auto issue_s = [&](int j) {
         const int st = j % NS, tb = j & 1;
         mbar_wait(kv_full + st, (j / NS) & 1);
@@ -600,9 +616,8 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(ds_full + tb, (j >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_f16(tmem + 256, kmaj(sDS + tb * 16384, kk, 16384), mnmaj(sK + st * L::kKT, kk, 8192), idG,
-                   (j | kk) != 0);
+        for (int kk = 0; kk < 4; ++kk)  // A = dS(j), packed bf16 over the S(j) columns of TMEM buffer tb
+          umma_f16_ts(tmem + 256, tmem + tb * 64 + kk * 8, mnmaj(sK + st * L::kKT, kk, 8192), idG, (j | kk) != 0);
         umma_commit(ds_free + tb);
         umma_commit(kv_empty + st);
         if (j + 2 < n) issue_s(j + 2);
@@ -620,9 +635,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int j = 0; j < n; ++j) {
       const int st = j & 1;
       mbar_wait(s_full + st, (j >> 1) & 1);
-      if (j >= 2) mbar_wait(ds_free + st, ((j >> 1) - 1) & 1);
       tc_fence_after();
-      uint8_t* ds = smem + L::kDS + st * 16384;
       const bool diag = j >= 2 * qb;
       {
         uint32_t s[32], dp[32];
@@ -639,10 +652,14 @@ __global__ void __launch_bounds__(384, 1)
         }
 #pragma unroll
         for (int c = 0; c < 32; ++c) g[c] *= u2f(dp[c]) - dq;
+        uint32_t packed[16];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) st_sw128(ds, r, half * 4 + c, f_to_bf8(g + 8 * c));
+        for (int c = 0; c < 16; ++c) packed[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
+        // dS(j) overwrites S(j) in place (this row's 32 keys -> 16 packed columns); dQ(j-2), the
+        // last reader of this buffer, completed before S(j) (tensor-pipe order).
+        tmem_st16(tmem + lanes + st * 64 + half * 16, packed);
+        tmem_st_wait();
       }
-      fence_proxy_async();
       tc_fence_before();
       mbar_arrive(ds_full + st);
     }
