@@ -88,22 +88,26 @@ __global__ void __launch_bounds__(kNT) ln_fwd_kernel(const __nv_bfloat16* __rest
   }
 }
 
-// Warp-per-row forward for width = 256*C: each lane streams C 16-byte chunks (all loads
-// in flight at once), statistics by warp shuffles only (no shared memory, no barriers),
-// the row kept as raw bf16 in registers. 8 rows per 256-thread CTA.
-template <int C>
+// Warp-group-per-row forward for width = 256*C*W: W warps (1 or 2) share a row, each lane
+// streams C 16-byte chunks (all loads in flight at once), statistics by warp shuffles plus,
+// for W = 2, one shared-memory exchange; the row stays raw bf16 in registers. 8/W rows per
+// 256-thread CTA. W = 2 for wide rows keeps registers low enough for 2+ CTAs per SM (a
+// 16-chunk-per-lane warp needed 254 registers and ran latency-bound at one CTA per SM).
+template <int C, int W>
 __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const __nv_bfloat16* __restrict__ x,
                                                           const __nv_bfloat16* __restrict__ gamma,
                                                           const __nv_bfloat16* __restrict__ beta,
                                                           __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
                                                           float* __restrict__ rstd, int rows, int width, float eps) {
-  const int lane = threadIdx.x % 32;
-  const long long row = blockIdx.x * 8LL + threadIdx.x / 32;
-  if (row >= rows) return;
-  const BF8* xr = reinterpret_cast<const BF8*>(x + row * width);
+  __shared__ float xch[8][2];
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, part = warp % W;
+  const long long row = blockIdx.x * (8LL / W) + warp / W;
+  const bool live = row < rows;
+  const BF8* xr = reinterpret_cast<const BF8*>(x + (live ? row : 0) * width);
+  const int c0 = part * 32 * C + lane;  // this lane's chunks: c0 + 32 i
   BF8 raw[C];
 #pragma unroll
-  for (int i = 0; i < C; ++i) raw[i] = xr[lane + 32 * i];
+  for (int i = 0; i < C; ++i) raw[i] = xr[c0 + 32 * i];
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < C; ++i) {
@@ -112,7 +116,13 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const __nv_bfloat16* _
 #pragma unroll
     for (int j = 0; j < 8; ++j) s += v[j];
   }
-  const float mu = warp_sum(s) / width;
+  s = warp_sum(s);
+  if (W == 2) {
+    if (lane == 0) xch[warp][0] = s;
+    __syncthreads();
+    s = xch[warp][0] + xch[warp ^ 1][0];
+  }
+  const float mu = s / width;
   float q = 0.f;
 #pragma unroll
   for (int i = 0; i < C; ++i) {
@@ -124,7 +134,14 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const __nv_bfloat16* _
       q += d * d;
     }
   }
-  const float rs = rsqrtf(warp_sum(q) / width + eps);
+  q = warp_sum(q);
+  if (W == 2) {
+    if (lane == 0) xch[warp][1] = q;
+    __syncthreads();
+    q = xch[warp][1] + xch[warp ^ 1][1];
+  }
+  const float rs = rsqrtf(q / width + eps);
+  if (!live) return;
   const BF8* gr = reinterpret_cast<const BF8*>(gamma);
   const BF8* br = reinterpret_cast<const BF8*>(beta);
   BF8* yr = reinterpret_cast<BF8*>(y + row * width);
@@ -132,13 +149,13 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const __nv_bfloat16* _
   for (int i = 0; i < C; ++i) {
     float v[8], g[8], b[8], o[8];
     bf8_to_f(raw[i], v);
-    bf8_to_f(gr[lane + 32 * i], g);
-    bf8_to_f(br[lane + 32 * i], b);
+    bf8_to_f(gr[c0 + 32 * i], g);
+    bf8_to_f(br[c0 + 32 * i], b);
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = (v[j] - mu) * rs * g[j] + b[j];
-    yr[lane + 32 * i] = f_to_bf8(o);
+    yr[c0 + 32 * i] = f_to_bf8(o);
   }
-  if (lane == 0) {
+  if (lane == 0 && part == 0) {
     mean[row] = mu;
     rstd[row] = rs;
   }
@@ -422,19 +439,22 @@ int layernorm_fwd(const __nv_bfloat16* x, const __nv_bfloat16* gamma, const __nv
                   float* mean, float* rstd, int rows, int width, float eps, cudaStream_t s) {
   if (width % 8 || width > kNT * kMaxC * 8) return set_error("layernorm: width must be a multiple of 8, <= 8192", kValidation);
   if (rows == 0) return kOk;
-  const unsigned wgrid = static_cast<unsigned>((rows + 7) / 8);
+  const unsigned grid1 = static_cast<unsigned>((rows + 7) / 8), grid2 = static_cast<unsigned>((rows + 3) / 4);
   switch (width % 256 ? 0 : width / 256) {
-#define LN_FWD_WARP(C) \
-  case C: ln_fwd_warp_kernel<C><<<wgrid, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, width, eps); break;
-    LN_FWD_WARP(1)
-    LN_FWD_WARP(2)
-    LN_FWD_WARP(4)
-    LN_FWD_WARP(7)
-    LN_FWD_WARP(8)
-    LN_FWD_WARP(16)
-    LN_FWD_WARP(20)
-    LN_FWD_WARP(24)
-#undef LN_FWD_WARP
+#define LN_FWD_W1(C) \
+  case C: ln_fwd_warp_kernel<C, 1><<<grid1, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, width, eps); break;
+#define LN_FWD_W2(C) \
+  case C: ln_fwd_warp_kernel<C / 2, 2><<<grid2, 256, 0, s>>>(x, gamma, beta, y, mean, rstd, rows, width, eps); break;
+    LN_FWD_W1(1)
+    LN_FWD_W1(2)
+    LN_FWD_W1(4)
+    LN_FWD_W1(7)
+    LN_FWD_W1(8)
+    LN_FWD_W2(16)
+    LN_FWD_W2(20)
+    LN_FWD_W2(24)
+#undef LN_FWD_W1
+#undef LN_FWD_W2
     default: ln_fwd_kernel<<<rows, kNT, 0, s>>>(x, gamma, beta, y, mean, rstd, width, eps);
   }
   return check_launch("layernorm_fwd");
