@@ -65,6 +65,7 @@ __global__ void dropout_bwd_kernel(const BF8* __restrict__ dout, BF8* __restrict
                                    uint64_t seed, uint64_t stream) {
   const uint32_t thr = drop_threshold(p);
   const float scale = p > 0.f ? 1.f / (1.f - p) : 1.f;
+#pragma unroll 4  // several 16-byte vectors in flight per thread (HBM-bound)
   for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < nvec;
        v += static_cast<long long>(gridDim.x) * blockDim.x) {
     float d[8], o[8];
@@ -89,6 +90,7 @@ LYNX_DEV float gelu_grad(float x) {
 }
 
 __global__ void gelu_fwd_kernel(const BF8* __restrict__ x, BF8* __restrict__ y, long long nvec) {
+#pragma unroll 4  // several 16-byte vectors in flight per thread (HBM-bound)
   for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < nvec;
        v += static_cast<long long>(gridDim.x) * blockDim.x) {
     float a[8];
@@ -101,6 +103,7 @@ __global__ void gelu_fwd_kernel(const BF8* __restrict__ x, BF8* __restrict__ y, 
 
 __global__ void gelu_bwd_kernel(const BF8* __restrict__ dy, const BF8* __restrict__ x, BF8* __restrict__ dx,
                                 long long nvec) {
+#pragma unroll 4  // several 16-byte vectors in flight per thread (HBM-bound)
   for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < nvec;
        v += static_cast<long long>(gridDim.x) * blockDim.x) {
     float a[8], d[8];
@@ -113,6 +116,7 @@ __global__ void gelu_bwd_kernel(const BF8* __restrict__ dy, const BF8* __restric
 }
 
 __global__ void add_kernel(const BF8* __restrict__ a, const BF8* __restrict__ b, BF8* __restrict__ o, long long nvec) {
+#pragma unroll 4  // several 16-byte vectors in flight per thread (HBM-bound)
   for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < nvec;
        v += static_cast<long long>(gridDim.x) * blockDim.x) {
     float x[8], y[8];
