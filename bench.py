@@ -374,7 +374,12 @@ def run_gpu_arm(args):
             times = obj[0]
         prof_s = time.perf_counter() - t0
     free, total = torch.cuda.mem_get_info()
-    c.mem_budget_bytes = device_budget(c, total, args.mem_margin_gib)
+    # Memory margin ladder: a plan whose physical footprint (ledger + per-layer transients + pool
+    # fragmentation) overflows HBM fails with LYNX_E_OOM in the first warm-up step; at N = 1 the
+    # bench then re-plans with a larger margin (recorded in the JSON line as memory.oom_retries).
+    margins = [args.mem_margin_gib] + ([m for m in (12.0, 16.0) if m > args.mem_margin_gib] if ws == 1 else [])
+    oom_retries = []
+    c.mem_budget_bytes = device_budget(c, total, margins[0])
     text = gp.profile_text(c, times=times)
     plans, plan_s = plan_all(c, text, args.plan)
     layers = plans[0]["layers_per_stage"]
@@ -386,11 +391,27 @@ def run_gpu_arm(args):
         nccl_id = obj[0]
     cfg = ex.make_config(c, layers, tp_rank=tp_rank, world_rank=rank, world_size=ws, nccl_id=nccl_id,
                          exec_opts={"trace": False})
-    e = ex.Executor(text, plans[stage]["timeline"], cfg)
     tok, lab = ex.synthetic_batch(c)
     first, last = stage == 0, stage == c.pp - 1
-    for _ in range(args.warmup):
-        e.step(tok if first else None, lab if last else None)
+    for mi, margin in enumerate(margins):
+        e = None
+        try:
+            if mi > 0:
+                c.mem_budget_bytes = device_budget(c, total, margin)
+                text = gp.profile_text(c, times=times)
+                plans, plan_s = plan_all(c, text, args.plan)
+            e = ex.Executor(text, plans[stage]["timeline"], cfg)
+            for _ in range(args.warmup):
+                e.step(tok if first else None, lab if last else None)
+            break
+        except ex.LynxError as err:
+            if err.code != 7 or mi + 1 == len(margins):
+                raise
+            oom_retries.append({"margin_gib": margin, "plan_S": json.loads(plans[stage]["plan_json"])["S"],
+                                "error": str(err)[:160]})
+            if e is not None:
+                e.close()
+            torch.cuda.empty_cache()
     # ---- timed region: K steps through the C-ABI with host buffers
     torch.cuda.synchronize()
     if ws > 1:
@@ -442,6 +463,7 @@ def run_gpu_arm(args):
                       "profile": args.profile, "profiler_s": round(prof_s, 2),
                       "op_times_us": {k: float(v) for k, v in (times or {}).items()}},
         "memory": {"ledger_budget_bytes": c.mem_budget_bytes, "plan_peak_bytes": plan0["peak_bytes"],
+                   "margin_gib": margins[len(oom_retries)], "oom_retries": oom_retries,
                    "pool_high_water_bytes": rep["pool_high_water_bytes"],
                    "static_bytes": rep["static_bytes_allocated"], "device_total_bytes": total},
         "loss": [round(x, 5) for x in losses],
