@@ -32,6 +32,12 @@ constexpr uint64_t kEmbedStream = 0xFFFFull << 32;
 }  // namespace
 
 // ============================================================ setup
+// LYNX_TRACE_SLOTS=1: print every tensor production / drop (ledger debugging), read once.
+static bool trace_slots() {
+  static const bool on = std::getenv("LYNX_TRACE_SLOTS") != nullptr;
+  return on;
+}
+
 void Executor::ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) cudaGetLastError();  // clear non-sticky errors so later launch checks do not see them
   if (e == cudaErrorMemoryAllocation) throw RtError(std::string(what) + ": out of device memory", kOutOfMemory);
@@ -323,7 +329,7 @@ void Executor::mark_ready(Slot& sl, cudaStream_t s) {
 
 void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
   if (!sl.p) return;
-  if (std::getenv("LYNX_TRACE_SLOTS")) {
+  if (trace_slots()) {
     const size_t idx = static_cast<size_t>(&sl - slots_.data());
     std::fprintf(stderr, "drop mb%zu l%zu op%zu\n", idx / (cfg_.layers * nf_), (idx / nf_) % cfg_.layers, idx % nf_);
   }
@@ -430,7 +436,7 @@ void Executor::collect_spans() {
 void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
   const Op op = op_of_[pos];
   Slot& out = slot(mb, l, pos);
-  if (std::getenv("LYNX_TRACE_SLOTS"))
+  if (trace_slots())
     std::fprintf(stderr, "fwd mb%d l%d op%d %s%s\n", mb, l, pos, op_name(op), recompute ? " (recompute)" : "");
   if (out.p) {
     if (recompute) return;  // already resident (duplicate placement)
