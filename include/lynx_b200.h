@@ -51,6 +51,11 @@ int lynx_abi_version(void);
  * Requires M % 128 == 0, N % 128 == 0, K % 64 == 0, 16-byte aligned rows. */
 int lynx_op_gemm(const void* a, long long lda, int a_mn_major, const void* b, long long ldb, int b_mn_major, void* c,
                  long long ldc, int m, int n, int k, const void* bias, int epilogue, void* stream);
+/* FC1 with its GeLU fused into the epilogue: c = bf16(A*B^T + bias[n]) and
+ * c_gelu = bf16(gelu(c)) (GPT-2 tanh GeLU of the bf16-rounded c, bit-identical to lynx_op_gelu_fwd
+ * on c). Same shape / layout rules as lynx_op_gemm; c and c_gelu share ldc. */
+int lynx_op_gemm_gelu(const void* a, long long lda, int a_mn_major, const void* b, long long ldb, int b_mn_major,
+                      void* c, void* c_gelu, long long ldc, int m, int n, int k, const void* bias, void* stream);
 /* GEMM kernel selection: -1 (default) the 512x256 "wide" CTA-pair kernel (two cta_group::2 MMAs per
  * k-step sharing the B stage) for K >= 8192 when M % 512 == 0 and N % 256 == 0, else the 256x256
  * CTA-pair (tcgen05.mma.cta_group::2) kernel for K-major A when M % 256 == 0 and N % 256 == 0, else

@@ -23,6 +23,7 @@ _SIGNATURES: dict[str, tuple] = {
     "lynx_last_error": (_c.c_char_p, []),
     "lynx_abi_version": (_i, []),
     "lynx_op_gemm": (_i, [_vp, _ll, _i, _vp, _ll, _i, _vp, _ll, _i, _i, _i, _vp, _i, _vp]),
+    "lynx_op_gemm_gelu": (_i, [_vp, _ll, _i, _vp, _ll, _i, _vp, _vp, _ll, _i, _i, _i, _vp, _vp]),
     "lynx_op_gemm_mode": (None, [_i]),
     "lynx_op_attention_mode": (None, [_i]),
     "lynx_op_layernorm_fwd": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _f, _vp]),

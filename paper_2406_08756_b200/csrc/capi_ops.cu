@@ -53,6 +53,12 @@ int lynx_op_gemm(const void* a, long long lda, int a_mn_major, const void* b, lo
   return gemm_run(g, STREAM(stream));
 }
 
+int lynx_op_gemm_gelu(const void* a, long long lda, int a_mn_major, const void* b, long long ldb, int b_mn_major,
+                      void* c, void* c_gelu, long long ldc, int m, int n, int k, const void* bias, void* stream) {
+  GemmDesc g{a, lda, a_mn_major != 0, b, ldb, b_mn_major != 0, c, ldc, m, n, k, CBF(bias), EPI_BF16_GELU, c_gelu};
+  return gemm_run(g, STREAM(stream));
+}
+
 void lynx_op_gemm_mode(int mode) { gemm_set_mode(mode); }
 void lynx_op_attention_mode(int mode) { attention_set_mode(mode); }
 

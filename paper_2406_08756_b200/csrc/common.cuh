@@ -57,6 +57,16 @@ LYNX_DEV T warp_max(T v) {
   return v;
 }
 
+// GPT-2 tanh GeLU with every rounding pinned (explicit __fmul_rn / __fadd_rn, no FMA
+// contraction): the stand-alone GeLU kernel and the FC1 GEMM epilogue that fuses it must
+// produce bit-identical activations, because a recomputed GeLU may come from either.
+LYNX_DEV float gelu_exact(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float x3 = __fmul_rn(__fmul_rn(x, x), x);
+  const float u = __fmul_rn(k0, __fadd_rn(x, __fmul_rn(k1, x3)));
+  return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.f, tanhf(u)));
+}
+
 // ---------------------------------------------------------------- Philox
 // Philox-4x32-10 (Salmon et al., SC'11). Counter = (element group, stream),
 // key = seed. Deterministic in (seed, stream, element) only, so a forward op

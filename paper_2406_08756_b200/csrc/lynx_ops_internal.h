@@ -29,7 +29,8 @@ int check_launch(const char* what, int kernels = 1);
 long long launch_count();
 const char* last_error();
 
-enum EpiMode { EPI_BF16 = 0, EPI_ACC_F32 = 1, EPI_STORE_F32 = 2, EPI_ACC_BF16 = 3 };
+// EPI_BF16_GELU: c = bf16(acc + bias) and c2 = bf16(gelu(c)) (FC1 with its GeLU fused).
+enum EpiMode { EPI_BF16 = 0, EPI_ACC_F32 = 1, EPI_STORE_F32 = 2, EPI_ACC_BF16 = 3, EPI_BF16_GELU = 4 };
 
 struct GemmDesc {
   const void* a;  // bf16
@@ -41,8 +42,9 @@ struct GemmDesc {
   void* c;
   long long ldc;
   int M, N, K;
-  const __nv_bfloat16* bias;  // EPI_BF16 only, may be null
+  const __nv_bfloat16* bias;  // EPI_BF16 / EPI_BF16_GELU only, may be null
   int epi;
+  void* c2 = nullptr;  // EPI_BF16_GELU: second bf16 output (same shape and ldc as c)
 };
 
 int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas = 0);

@@ -78,10 +78,7 @@ __global__ void dropout_bwd_kernel(const BF8* __restrict__ dout, BF8* __restrict
 }
 
 // GPT-2 tanh GeLU.
-LYNX_DEV float gelu_f(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
-}
+LYNX_DEV float gelu_f(float x) { return gelu_exact(x); }
 LYNX_DEV float gelu_grad(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   const float u = k0 * (x + k1 * x * x * x);

@@ -50,6 +50,7 @@ struct Args {
   int group;        // raster: > 0 groups of `group` M-tiles (M fastest), < 0 groups of -group N-tiles
   uint64_t hint_a, hint_b;  // L2 cache policies of the A / B TMA loads
   int tma_store;            // bf16 epilogue through smem + TMA store (else per-thread st.global)
+  void* c2;                 // EPI_BF16_GELU second output
 };
 
 template <int BN>
@@ -139,6 +140,17 @@ LYNX_DEV void epilogue_row(const Args& args, uint32_t t_row, long long row, int 
       BF8* o = reinterpret_cast<BF8*>(reinterpret_cast<__nv_bfloat16*>(args.c) + row * args.ldc + n0 + c);
 #pragma unroll
       for (int i = 0; i < 4; ++i) o[i] = f_to_bf8(v + 8 * i);
+      if (args.epi == EPI_BF16_GELU) {
+        BF8* o2 = reinterpret_cast<BF8*>(reinterpret_cast<__nv_bfloat16*>(args.c2) + row * args.ldc + n0 + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float t[8];
+          bf8_to_f(f_to_bf8(v + 8 * i), t);  // GeLU of the bf16-rounded FC1 output, as the GeLU kernel
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t[j] = gelu_exact(t[j]);
+          o2[i] = f_to_bf8(t);
+        }
+      }
     }
   }
 }
@@ -157,10 +169,12 @@ LYNX_DEV void tma_store_2d(const CUtensorMap* desc, const void* smem, int c0, in
 LYNX_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 LYNX_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 LYNX_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+LYNX_DEV void bulk_wait_all_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
 template <int kCols>
-LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, uint32_t t_row, int row0, int n0,
-                                int lane, uint8_t* staging, int& sbuf) {
+LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, const CUtensorMap* tm_c2, uint32_t t_row,
+                                int row0, int n0, int lane, uint8_t* staging, int& sbuf) {
+  const bool gelu = args.epi == EPI_BF16_GELU;
 #pragma unroll 1
   for (int c = 0; c < kCols; c += 64) {
     uint32_t r[64];
@@ -179,6 +193,28 @@ LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, uint3
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[8 * i + j] += b[j];
       }
+    }
+    if (gelu) {  // both buffers per round: c in buffer 0, gelu(c) in buffer 1
+      if (lane == 0) bulk_wait_all_read();
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const BF8 cv = f_to_bf8(v + 8 * i);
+        *reinterpret_cast<BF8*>(staging + lane * 128 + ((i ^ (lane & 7)) << 4)) = cv;
+        float t[8];
+        bf8_to_f(cv, t);  // GeLU of the bf16-rounded FC1 output, exactly as the GeLU kernel computes it
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t[j] = gelu_exact(t[j]);
+        *reinterpret_cast<BF8*>(staging + 4096 + lane * 128 + ((i ^ (lane & 7)) << 4)) = f_to_bf8(t);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tm_c, staging, n0 + c, row0);
+        tma_store_2d(tm_c2, staging + 4096, n0 + c, row0);
+        bulk_commit();
+      }
+      continue;
     }
     uint8_t* st = staging + sbuf * 4096;
     if (lane == 0) bulk_wait_read1();  // the store issued from this buffer two rounds ago has read it
@@ -199,7 +235,7 @@ LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, uint3
 template <bool kAMN, bool kBMN, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                const __grid_constant__ CUtensorMap tm_c, Args args) {
+                const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_c2, Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using S = Smem<BN>;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -324,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;  // == warp % 4: TMEM lane quadrant
-    const bool tma_out = args.epi == EPI_BF16 && args.tma_store;
+    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU) && args.tma_store;
     uint8_t* my_staging = staging + ew * 8192;
     int sbuf = 0;
     int acc = 0;
@@ -338,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       if (tma_out)
-        epilogue_tile_tma<BN>(args, &tm_c, t_row, mt * BM + ew * 32, n0, lane, my_staging, sbuf);
+        epilogue_tile_tma<BN>(args, &tm_c, &tm_c2, t_row, mt * BM + ew * 32, n0, lane, my_staging, sbuf);
       else
         epilogue_row<BN>(args, t_row, row, n0);
       tc_fence_before();
@@ -427,7 +463,7 @@ LYNX_DEV void umma_commit_pair(uint64_t* bar) {  // arrive on `bar` in both CTAs
 template <bool kAMN, bool kBMN, int kSub>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
-                 const __grid_constant__ CUtensorMap tm_c, Args args) {
+                 const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tm_c2, Args args) {
   using C = Cfg<kSub>;
   constexpr int kStages = C::kStages, kStageBytes = C::kStageBytes, kABytes = C::kABytes, kTileM = C::kTileM;
   constexpr int kRowsCTA = C::kRowsCTA, kAcc = C::kAcc;
@@ -576,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    const bool tma_out = args.epi == EPI_BF16 && args.tma_store;
+    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU) && args.tma_store;
     uint8_t* my_staging = staging + ew * 8192;
     int sbuf = 0;
     int acc = 0;
@@ -592,7 +628,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int row0 = mt * kTileM + rank * kRowsCTA + sub * kHalf + ew * 32;
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + (acc * kSub + sub) * kTileN;
         if (tma_out)
-          epilogue_tile_tma<kTileN>(args, &tm_c, t_row, row0, n0, lane, my_staging, sbuf);
+          epilogue_tile_tma<kTileN>(args, &tm_c, &tm_c2, t_row, row0, n0, lane, my_staging, sbuf);
         else
           epilogue_row<kTileN>(args, t_row, row0 + lane, n0);
       }
@@ -695,13 +731,16 @@ int launch(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_set = true;
   }
-  CUtensorMap mc = ma;
-  const bool tma_out = g.epi == EPI_BF16 && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
-  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), tma_out ? 1 : 0};
+  CUtensorMap mc = ma, mc2 = ma;
+  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU;
+  bool tma_out = bf16_out && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
+  if (tma_out && g.epi == EPI_BF16_GELU) tma_out = make_map(&mc2, g.c2, g.N, g.M, g.ldc, 64, 32);
+  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), tma_out ? 1 : 0,
+            g.c2};
   const int tiles = (g.M / BM) * (g.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, args);
+  kern<<<grid, kThreads, smem, stream>>>(ma, mb, mc, mc2, args);
   return check_launch("gemm_tcgen05");
 }
 
@@ -719,14 +758,17 @@ int launch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
     attr_set = true;
   }
-  CUtensorMap mc = ma;
-  const bool tma_out = g.epi == EPI_BF16 && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
-  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), tma_out ? 1 : 0};
+  CUtensorMap mc = ma, mc2 = ma;
+  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU;
+  bool tma_out = bf16_out && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
+  if (tma_out && g.epi == EPI_BF16_GELU) tma_out = make_map(&mc2, g.c2, g.N, g.M, g.ldc, 64, 32);
+  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), tma_out ? 1 : 0,
+            g.c2};
   const int tiles = (g.M / C::kTileM) * (g.N / pair::kTileN);
   int clusters = num_sms() / 2;
   if (max_ctas > 0) clusters = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
   if (tiles < clusters) clusters = tiles;
-  kern<<<2 * clusters, kThreads, C::kSmemBytes, stream>>>(ma, mb, mc, args);
+  kern<<<2 * clusters, kThreads, C::kSmemBytes, stream>>>(ma, mb, mc, mc2, args);
   return check_launch("gemm_tcgen05_pair");
 }
 
@@ -758,7 +800,8 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   if (g.M % BM || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
     return set_error("gemm: M must be a multiple of 128 and K of 64");
   if (g.N % 128) return set_error("gemm: N must be a multiple of 128");
-  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_ACC_BF16;
+  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_ACC_BF16 || g.epi == EPI_BF16_GELU;
+  if (g.epi == EPI_BF16_GELU && !g.c2) return set_error("gemm: the GeLU epilogue needs a second output");
   if ((bf16_out && g.ldc % 8) || (!bf16_out && g.ldc % 4))
     return set_error("gemm: ldc must keep 16-byte row alignment");
   const int mode = g_gemm_mode;

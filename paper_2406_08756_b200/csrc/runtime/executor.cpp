@@ -341,6 +341,7 @@ void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
   sl.p = nullptr;
   sl.ready = nullptr;
   sl.regenerated = false;
+  sl.fused = false;
 }
 
 void* Executor::need(int mb, int l, int pos, cudaStream_t s) {
@@ -439,6 +440,10 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
   if (trace_slots())
     std::fprintf(stderr, "fwd mb%d l%d op%d %s%s\n", mb, l, pos, op_name(op), recompute ? " (recompute)" : "");
   if (out.p) {
+    if (out.fused) {  // GeLU already written by the FC1 epilogue of this pass
+      out.fused = false;
+      return;
+    }
     if (recompute) return;  // already resident (duplicate placement)
     throw RtError("forward tensor produced twice", kParse);
   }
@@ -502,6 +507,19 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
   out.p = alloc(bytes, s);
   out.bytes = bytes;
   if (recompute) ++rep_.recompute_launches;
+  // FC1 with its GeLU fused into the GEMM epilogue when the GeLU tensor is not resident (forward
+  // pass, or both discarded and regenerated): the GeLU slot is produced here, its own op call
+  // becomes a no-op. Same element, so the ledger's liveness is unchanged.
+  Slot* gelu_slot = nullptr;
+  if (op == Op::FC1) {
+    const int gpos = pos_of(Op::GELU);
+    if (gpos >= 0 && !slot(mb, l, gpos).p) {
+      gelu_slot = &slot(mb, l, gpos);
+      gelu_slot->p = alloc(2 * T * 4 * hp, s);
+      gelu_slot->bytes = 2 * T * 4 * hp;
+      if (recompute) ++rep_.recompute_launches;
+    }
+  }
   if (!opt_.dry_run) {
     auto* o = static_cast<__nv_bfloat16*>(out.p);
     switch (op) {
@@ -529,7 +547,15 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
                                         drop_stream(l, mb, Op::PROJ_RES), s),
               "residual");
         break;
-      case Op::FC1: gemm(in, h, P.w_fc1, h, o, 4 * hp, T, 4 * hp, h, P.b_fc1); break;
+      case Op::FC1:
+        if (gelu_slot) {
+          GemmDesc g{in, h, false, P.w_fc1, h, false, o, 4 * hp, static_cast<int>(T), 4 * hp, h, P.b_fc1,
+                     EPI_BF16_GELU, gelu_slot->p};
+          ck_op(gemm_run(g, s), "fc1 + gelu");
+        } else {
+          gemm(in, h, P.w_fc1, h, o, 4 * hp, T, 4 * hp, h, P.b_fc1);
+        }
+        break;
       case Op::GELU: ck_op(gelu_fwd(static_cast<const __nv_bfloat16*>(in), o, T * 4 * hp, s), "gelu"); break;
       case Op::FC2: gemm(in, 4 * hp, P.w_fc2, 4 * hp, o, h, T, h, 4 * hp, nullptr); break;
       case Op::FC2_RES:
@@ -541,6 +567,14 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
       default: break;
     }
   }
+  finish_production(out, bytes, s, recompute);
+  if (gelu_slot) {
+    finish_production(*gelu_slot, gelu_slot->bytes, s, recompute);
+    gelu_slot->fused = true;
+  }
+}
+
+void Executor::finish_production(Slot& out, size_t bytes, cudaStream_t s, bool recompute) {
   mark_ready(out, s);
   if (recompute) {
     out.regenerated = true;

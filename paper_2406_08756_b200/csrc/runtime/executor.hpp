@@ -50,6 +50,7 @@ struct Slot {
   cudaEvent_t ready = nullptr;  // set when produced off the main stream
   cudaStream_t stream = nullptr;
   bool regenerated = false;
+  bool fused = false;      // produced early by the FC1 + GeLU epilogue; its own op call is a no-op
   void* shadow = nullptr;  // check_recompute: forward-produced copy
 };
 
@@ -95,6 +96,7 @@ class Executor {
   void parse_config(const std::string& cfg);
   void bind_template();
   void init_device();
+  void finish_production(Slot& out, size_t bytes, cudaStream_t s, bool recompute);
   void release_all();
   void init_comms(const std::string& nccl_id_hex, int world_rank, int world_size);
   void alloc_persistent();

@@ -38,6 +38,17 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, a_mn: bool = False, b_mn: bool = F
     return out
 
 
+def gemm_gelu(a: torch.Tensor, b: torch.Tensor, *, bias: torch.Tensor | None = None):
+    """(C, gelu(C)) with C = bf16(a @ b^T + bias): the FC1 GEMM with its GeLU fused (K-major operands)."""
+    M, K = a.shape
+    N = b.shape[0]
+    c = torch.empty(M, N, device=a.device, dtype=torch.bfloat16)
+    g = torch.empty_like(c)
+    call("lynx_op_gemm_gelu", a.data_ptr(), a.stride(0), 0, b.data_ptr(), b.stride(0), 0, c.data_ptr(), g.data_ptr(),
+         c.stride(0), M, N, K, _p(bias), _s())
+    return c, g
+
+
 def layernorm_fwd(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float = 1e-5):
     rows, width = x.shape
     y = torch.empty_like(x)

@@ -64,6 +64,26 @@ def test_gemm_pair_and_single_cta(ops, cuda, a_mn, b_mn, mode):
     assert rel(acc, ref + 1) < 1e-5
 
 
+@pytest.mark.parametrize("mode,M,N,K", [(-1, 512, 1024, 256), (0, 256, 384, 128), (1, 512, 512, 192),
+                                        (2, 1024, 2048, 8192)])
+def test_gemm_gelu_epilogue_matches_gelu_kernel(ops, cuda, mode, M, N, K):
+    """The fused FC1+GeLU epilogue writes C and gelu(C); gelu(C) must equal the stand-alone GeLU
+    kernel on C bit for bit (a recomputed GeLU may come from either path)."""
+    from paper_2406_08756_b200._native import lib
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    a = (torch.randn(M, K, device=cuda, generator=g) * 0.3).bfloat16()
+    b = (torch.randn(N, K, device=cuda, generator=g) * 0.3).bfloat16()
+    bias = torch.randn(N, device=cuda, generator=g).bfloat16()
+    lib().lynx_op_gemm_mode(mode)
+    try:
+        c, gc = ops.gemm_gelu(a, b, bias=bias)
+        c_ref = ops.gemm(a, b, bias=bias)
+    finally:
+        lib().lynx_op_gemm_mode(-1)
+    assert torch.equal(c, c_ref)
+    assert torch.equal(gc, ops.gelu_fwd(c))
+
+
 def test_gemm_bias_and_f32_epilogues(ops, cuda):
     g = torch.Generator(device=cuda).manual_seed(7)
     A = torch.randn(256, 512, device=cuda, generator=g).bfloat16()
