@@ -56,6 +56,12 @@ int lynx_op_gemm(const void* a, long long lda, int a_mn_major, const void* b, lo
  * on c). Same shape / layout rules as lynx_op_gemm; c and c_gelu share ldc. */
 int lynx_op_gemm_gelu(const void* a, long long lda, int a_mn_major, const void* b, long long ldb, int b_mn_major,
                       void* c, void* c_gelu, long long ldc, int m, int n, int k, const void* bias, void* stream);
+/* Projection + bias + dropout + residual in one kernel: c = bf16(res + dropout_p(bf16(A*B^T + bias)))
+ * with the keep mask of lynx_op_bias_dropout_residual (Philox(seed, stream_id, row*ldc + col)); A [m,k]
+ * and B [n,k] K-major, res and c [m,n] with pitch ldc. */
+int lynx_op_gemm_residual(const void* a, long long lda, const void* b, long long ldb, void* c, long long ldc, int m,
+                          int n, int k, const void* bias, const void* res, float p, unsigned long long seed,
+                          unsigned long long stream_id, void* stream);
 /* GEMM kernel selection: -1 (default) the 512x256 "wide" CTA-pair kernel (two cta_group::2 MMAs per
  * k-step sharing the B stage) for K >= 8192 when M % 512 == 0 and N % 256 == 0, else the 256x256
  * CTA-pair (tcgen05.mma.cta_group::2) kernel for K-major A when M % 256 == 0 and N % 256 == 0, else

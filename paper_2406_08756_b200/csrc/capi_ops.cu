@@ -59,6 +59,17 @@ int lynx_op_gemm_gelu(const void* a, long long lda, int a_mn_major, const void* 
   return gemm_run(g, STREAM(stream));
 }
 
+int lynx_op_gemm_residual(const void* a, long long lda, const void* b, long long ldb, void* c, long long ldc, int m,
+                          int n, int k, const void* bias, const void* res, float p, unsigned long long seed,
+                          unsigned long long stream_id, void* stream) {
+  GemmDesc g{a, lda, false, b, ldb, false, c, ldc, m, n, k, CBF(bias), EPI_BF16_RESID};
+  g.res = CBF(res);
+  g.drop_p = p;
+  g.drop_seed = seed;
+  g.drop_stream = stream_id;
+  return gemm_run(g, STREAM(stream));
+}
+
 void lynx_op_gemm_mode(int mode) { gemm_set_mode(mode); }
 void lynx_op_attention_mode(int mode) { attention_set_mode(mode); }
 

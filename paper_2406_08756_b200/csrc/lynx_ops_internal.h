@@ -30,7 +30,9 @@ long long launch_count();
 const char* last_error();
 
 // EPI_BF16_GELU: c = bf16(acc + bias) and c2 = bf16(gelu(c)) (FC1 with its GeLU fused).
-enum EpiMode { EPI_BF16 = 0, EPI_ACC_F32 = 1, EPI_STORE_F32 = 2, EPI_ACC_BF16 = 3, EPI_BF16_GELU = 4 };
+// EPI_BF16_RESID: c = bf16(res + dropout(bf16(acc + bias))) with the Philox mask of
+// bias_dropout_residual_fwd (element index row * ldc + col), i.e. PROJ_RES / FC2_RES in one kernel.
+enum EpiMode { EPI_BF16 = 0, EPI_ACC_F32 = 1, EPI_STORE_F32 = 2, EPI_ACC_BF16 = 3, EPI_BF16_GELU = 4, EPI_BF16_RESID = 5 };
 
 struct GemmDesc {
   const void* a;  // bf16
@@ -45,6 +47,9 @@ struct GemmDesc {
   const __nv_bfloat16* bias;  // EPI_BF16 / EPI_BF16_GELU only, may be null
   int epi;
   void* c2 = nullptr;  // EPI_BF16_GELU: second bf16 output (same shape and ldc as c)
+  const __nv_bfloat16* res = nullptr;  // EPI_BF16_RESID: residual input (same shape and ldc as c)
+  float drop_p = 0.f;
+  uint64_t drop_seed = 0, drop_stream = 0;
 };
 
 int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas = 0);

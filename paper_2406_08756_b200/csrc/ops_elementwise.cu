@@ -21,22 +21,6 @@ int grid_for(long long nvec) {
   return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
-LYNX_DEV uint32_t drop_threshold(float p) {
-  const double t = static_cast<double>(p) * 4294967296.0;
-  return t >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(t);
-}
-
-// keep-mask bits for elements [8v, 8v+8)
-LYNX_DEV uint32_t keep_bits8(uint64_t seed, uint64_t stream, long long v, uint32_t thr) {
-  const uint4 a = philox_group(seed, stream, static_cast<uint64_t>(2 * v));
-  const uint4 b = philox_group(seed, stream, static_cast<uint64_t>(2 * v + 1));
-  const uint32_t r[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-  uint32_t bits = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) bits |= (r[j] >= thr ? 1u : 0u) << j;
-  return bits;
-}
-
 __global__ void bias_dropout_residual_kernel(const BF8* __restrict__ y, const BF8* __restrict__ bias,
                                              const BF8* __restrict__ res, BF8* __restrict__ out, long long nvec,
                                              int wvec, float p, uint64_t seed, uint64_t stream) {

@@ -51,7 +51,23 @@ struct Args {
   uint64_t hint_a, hint_b;  // L2 cache policies of the A / B TMA loads
   int tma_store;            // bf16 epilogue through smem + TMA store (else per-thread st.global)
   void* c2;                 // EPI_BF16_GELU second output
+  const __nv_bfloat16* res;  // EPI_BF16_RESID residual
+  float drop_p, drop_scale;
+  uint32_t drop_thr;
+  uint64_t drop_seed, drop_stream;
 };
+
+// EPI_BF16_RESID on 8 outputs (columns col..col+7 of `row`): out = res + dropout(bf16(v)).
+LYNX_DEV BF8 resid_dropout8(const Args& args, long long row, int col, const float* v) {
+  float y[8], r[8], o[8];
+  bf8_to_f(f_to_bf8(v), y);  // the projection output is rounded to bf16 first, as in the two-kernel path
+  bf8_to_f(*reinterpret_cast<const BF8*>(args.res + row * args.ldc + col), r);
+  const uint32_t keep =
+      args.drop_p > 0.f ? keep_bits8(args.drop_seed, args.drop_stream, (row * args.ldc + col) / 8, args.drop_thr) : 0xFFu;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j] = ((keep >> j) & 1u) ? __fmaf_rn(y[j], args.drop_scale, r[j]) : r[j];
+  return f_to_bf8(o);
+}
 
 template <int BN>
 struct Smem {
@@ -138,6 +154,11 @@ LYNX_DEV void epilogue_row(const Args& args, uint32_t t_row, long long row, int 
         for (int i = 0; i < 32; ++i) v[i] += b[i];
       }
       BF8* o = reinterpret_cast<BF8*>(reinterpret_cast<__nv_bfloat16*>(args.c) + row * args.ldc + n0 + c);
+      if (args.epi == EPI_BF16_RESID) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = resid_dropout8(args, row, n0 + c + 8 * i, v + 8 * i);
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) o[i] = f_to_bf8(v + 8 * i);
       if (args.epi == EPI_BF16_GELU) {
@@ -221,7 +242,9 @@ LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, const
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-      *reinterpret_cast<BF8*>(st + lane * 128 + ((i ^ (lane & 7)) << 4)) = f_to_bf8(v + 8 * i);
+      *reinterpret_cast<BF8*>(st + lane * 128 + ((i ^ (lane & 7)) << 4)) =
+          args.epi == EPI_BF16_RESID ? resid_dropout8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
+                                     : f_to_bf8(v + 8 * i);
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
@@ -360,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;  // == warp % 4: TMEM lane quadrant
-    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU) && args.tma_store;
+    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU || args.epi == EPI_BF16_RESID) && args.tma_store;
     uint8_t* my_staging = staging + ew * 8192;
     int sbuf = 0;
     int acc = 0;
@@ -612,7 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU) && args.tma_store;
+    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU || args.epi == EPI_BF16_RESID) && args.tma_store;
     uint8_t* my_staging = staging + ew * 8192;
     int sbuf = 0;
     int acc = 0;
@@ -707,6 +730,14 @@ bool tma_store_enabled() {
   return on;
 }
 
+Args make_args(const GemmDesc& g, bool tma_out) {
+  Args a{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), tma_out ? 1 : 0, g.c2,
+         g.res, g.drop_p, g.drop_p > 0.f ? 1.f / (1.f - g.drop_p) : 1.f, 0u, g.drop_seed, g.drop_stream};
+  const double t = static_cast<double>(g.drop_p) * 4294967296.0;  // == drop_threshold(p)
+  a.drop_thr = t >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(t);
+  return a;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -732,11 +763,10 @@ int launch(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
     attr_set = true;
   }
   CUtensorMap mc = ma, mc2 = ma;
-  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU;
+  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID;
   bool tma_out = bf16_out && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
   if (tma_out && g.epi == EPI_BF16_GELU) tma_out = make_map(&mc2, g.c2, g.N, g.M, g.ldc, 64, 32);
-  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), tma_out ? 1 : 0,
-            g.c2};
+  const Args args = make_args(g, tma_out);
   const int tiles = (g.M / BM) * (g.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
@@ -759,11 +789,10 @@ int launch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
     attr_set = true;
   }
   CUtensorMap mc = ma, mc2 = ma;
-  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU;
+  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID;
   bool tma_out = bf16_out && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
   if (tma_out && g.epi == EPI_BF16_GELU) tma_out = make_map(&mc2, g.c2, g.N, g.M, g.ldc, 64, 32);
-  Args args{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), tma_out ? 1 : 0,
-            g.c2};
+  const Args args = make_args(g, tma_out);
   const int tiles = (g.M / C::kTileM) * (g.N / pair::kTileN);
   int clusters = num_sms() / 2;
   if (max_ctas > 0) clusters = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
@@ -800,8 +829,9 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   if (g.M % BM || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
     return set_error("gemm: M must be a multiple of 128 and K of 64");
   if (g.N % 128) return set_error("gemm: N must be a multiple of 128");
-  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_ACC_BF16 || g.epi == EPI_BF16_GELU;
+  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_ACC_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID;
   if (g.epi == EPI_BF16_GELU && !g.c2) return set_error("gemm: the GeLU epilogue needs a second output");
+  if (g.epi == EPI_BF16_RESID && !g.res) return set_error("gemm: the residual epilogue needs the residual input");
   if ((bf16_out && g.ldc % 8) || (!bf16_out && g.ldc % 4))
     return set_error("gemm: ldc must keep 16-byte row alignment");
   const int mode = g_gemm_mode;

@@ -541,12 +541,15 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
         break;
       }
       case Op::PROJ: gemm(in, hp, P.w_proj, hp, o, h, T, h, hp, nullptr); break;
-      case Op::PROJ_RES:
-        gemm(in, hp, P.w_proj, hp, sc.t_h, h, T, h, hp, P.b_proj);
-        ck_op(bias_dropout_residual_fwd(sc.t_h, nullptr, static_cast<const __nv_bfloat16*>(x), o, T, h, p, seed,
-                                        drop_stream(l, mb, Op::PROJ_RES), s),
-              "residual");
+      case Op::PROJ_RES: {  // out = x + dropout(attn W_proj^T + b), one GEMM with the residual epilogue
+        GemmDesc g{in, hp, false, P.w_proj, hp, false, o, h, static_cast<int>(T), h, hp, P.b_proj, EPI_BF16_RESID};
+        g.res = static_cast<const __nv_bfloat16*>(x);
+        g.drop_p = p;
+        g.drop_seed = seed;
+        g.drop_stream = drop_stream(l, mb, Op::PROJ_RES);
+        ck_op(gemm_run(g, s), "proj + residual");
         break;
+      }
       case Op::FC1:
         if (gelu_slot) {
           GemmDesc g{in, h, false, P.w_fc1, h, false, o, 4 * hp, static_cast<int>(T), 4 * hp, h, P.b_fc1,
@@ -558,12 +561,16 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
         break;
       case Op::GELU: ck_op(gelu_fwd(static_cast<const __nv_bfloat16*>(in), o, T * 4 * hp, s), "gelu"); break;
       case Op::FC2: gemm(in, 4 * hp, P.w_fc2, 4 * hp, o, h, T, h, 4 * hp, nullptr); break;
-      case Op::FC2_RES:
-        gemm(in, 4 * hp, P.w_fc2, 4 * hp, sc.t_h, h, T, h, 4 * hp, P.b_fc2);
-        ck_op(bias_dropout_residual_fwd(sc.t_h, nullptr, static_cast<const __nv_bfloat16*>(x), o, T, h, p, seed,
-                                        drop_stream(l, mb, Op::FC2_RES), s),
-              "residual");
+      case Op::FC2_RES: {
+        GemmDesc g{in, 4 * hp, false, P.w_fc2, 4 * hp, false, o, h, static_cast<int>(T), h, 4 * hp, P.b_fc2,
+                   EPI_BF16_RESID};
+        g.res = static_cast<const __nv_bfloat16*>(x);
+        g.drop_p = p;
+        g.drop_seed = seed;
+        g.drop_stream = drop_stream(l, mb, Op::FC2_RES);
+        ck_op(gemm_run(g, s), "fc2 + residual");
         break;
+      }
       default: break;
     }
   }

@@ -49,6 +49,16 @@ def gemm_gelu(a: torch.Tensor, b: torch.Tensor, *, bias: torch.Tensor | None = N
     return c, g
 
 
+def gemm_residual(a, b, res, *, bias=None, p: float = 0.0, seed: int = 0, stream_id: int = 0):
+    """res + dropout_p(bf16(a @ b^T + bias)) in one GEMM (K-major operands)."""
+    M, K = a.shape
+    N = b.shape[0]
+    c = torch.empty(M, N, device=a.device, dtype=torch.bfloat16)
+    call("lynx_op_gemm_residual", a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), c.data_ptr(), c.stride(0), M,
+         N, K, _p(bias), res.data_ptr(), p, seed, stream_id, _s())
+    return c
+
+
 def layernorm_fwd(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float = 1e-5):
     rows, width = x.shape
     y = torch.empty_like(x)

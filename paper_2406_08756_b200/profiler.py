@@ -63,11 +63,14 @@ def measure_op_times(c: gp.GPTConfig, iters: int = 5) -> dict[str, Fraction]:
     proj = lambda: ops.gemm(attn_o, w_proj, bias=b_proj if t == 1 else None)  # noqa: E731
     times["proj"] = _time(proj, iters)
     resid = _time(lambda: ops.bias_dropout_residual(y, b_proj, x, c.dropout, 1, 2), iters)
-    times["proj_res"] = times["proj"] + resid
+    # TP = 1: the executor runs PROJ_RES / FC2_RES as one GEMM with the residual epilogue
+    times["proj_res"] = _time(lambda: ops.gemm_residual(attn_o, w_proj, x, bias=b_proj, p=c.dropout, seed=1,
+                                                        stream_id=2), iters)
     times["fc1"] = _time(lambda: ops.gemm(y, w_fc1, bias=b_fc1), iters)
-    times["gelu"] = _time(lambda: ops.gelu_fwd(fc1), iters)
+    times["gelu"] = _time(lambda: ops.gelu_fwd(fc1), iters)  # stand-alone (a GeLU recomputed from a kept FC1)
     times["fc2"] = _time(lambda: ops.gemm(fc1, w_fc2, bias=b_fc2 if t == 1 else None), iters)
-    times["fc2_res"] = times["fc2"] + resid
+    times["fc2_res"] = _time(lambda: ops.gemm_residual(fc1, w_fc2, x, bias=b_fc2, p=c.dropout, seed=1, stream_id=3),
+                             iters)
     tw = c.tp_model if (t == 1 and c.tp_template) else t
     ar = 0.0 if tw == 1 else 2.0 * (tw - 1) / tw * (2 * T * h) / (NVLINK_BUS_GBS * 1e3)
     times["ar1"] = times["ar2"] = ar + resid

@@ -84,6 +84,33 @@ def test_gemm_gelu_epilogue_matches_gelu_kernel(ops, cuda, mode, M, N, K):
     assert torch.equal(gc, ops.gelu_fwd(c))
 
 
+@pytest.mark.parametrize("mode,M,N,K,p", [(-1, 512, 1024, 256, 0.1), (0, 256, 384, 128, 0.1), (-1, 1024, 2048, 8192, 0.0),
+                                          (1, 512, 512, 192, 0.5)])
+def test_gemm_residual_epilogue(ops, cuda, mode, M, N, K, p):
+    """Projection + bias + dropout + residual fused in the GEMM epilogue: the same keep mask as the
+    two-kernel path (GEMM, then bias_dropout_residual), values within one bf16 rounding; reruns
+    are bit-identical (a regenerated PROJ_RES / FC2_RES must equal the forward's)."""
+    from paper_2406_08756_b200._native import lib
+    g = torch.Generator(device=cuda).manual_seed(M * 7 + N + K)
+    a = (torch.randn(M, K, device=cuda, generator=g) * 0.3).bfloat16()
+    b = (torch.randn(N, K, device=cuda, generator=g) * 0.3).bfloat16()
+    bias = torch.randn(N, device=cuda, generator=g).bfloat16()
+    res = torch.randn(M, N, device=cuda, generator=g).bfloat16()
+    lib().lynx_op_gemm_mode(mode)
+    try:
+        out = ops.gemm_residual(a, b, res, bias=bias, p=p, seed=7, stream_id=11)
+        out2 = ops.gemm_residual(a, b, res, bias=bias, p=p, seed=7, stream_id=11)
+        y = ops.gemm(a, b, bias=bias)
+    finally:
+        lib().lynx_op_gemm_mode(-1)
+    ref = ops.bias_dropout_residual(y, None, res, p, 7, 11)
+    assert torch.equal(out, out2)
+    kept_fused = out != res
+    kept_ref = ref != res
+    assert (kept_fused == kept_ref).float().mean() > 0.999  # same mask (ties where y*scale rounds to 0)
+    assert rel(out, ref) < 1e-2
+
+
 def test_gemm_bias_and_f32_epilogues(ops, cuda):
     g = torch.Generator(device=cuda).manual_seed(7)
     A = torch.randn(256, 512, device=cuda, generator=g).bfloat16()
