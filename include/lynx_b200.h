@@ -62,6 +62,10 @@ int lynx_op_gemm_gelu(const void* a, long long lda, int a_mn_major, const void* 
 int lynx_op_gemm_residual(const void* a, long long lda, const void* b, long long ldb, void* c, long long ldc, int m,
                           int n, int k, const void* bias, const void* res, float p, unsigned long long seed,
                           unsigned long long stream_id, void* stream);
+/* GeLU backward fused into a dX GEMM: c = bf16((A*B^T) * gelu'(x)), x the GeLU input [m,n] (pitch ldc).
+ * A [m,k] K-major; B [n,k] (b_mn_major = 0) or [k,n] (1). */
+int lynx_op_gemm_gelu_bwd(const void* a, long long lda, const void* b, long long ldb, int b_mn_major, void* c,
+                          long long ldc, int m, int n, int k, const void* x, void* stream);
 /* GEMM kernel selection: -1 (default) the 512x256 "wide" CTA-pair kernel (two cta_group::2 MMAs per
  * k-step sharing the B stage) for K >= 8192 when M % 512 == 0 and N % 256 == 0, else the 256x256
  * CTA-pair (tcgen05.mma.cta_group::2) kernel for K-major A when M % 256 == 0 and N % 256 == 0, else

@@ -70,6 +70,13 @@ int lynx_op_gemm_residual(const void* a, long long lda, const void* b, long long
   return gemm_run(g, STREAM(stream));
 }
 
+int lynx_op_gemm_gelu_bwd(const void* a, long long lda, const void* b, long long ldb, int b_mn_major, void* c,
+                          long long ldc, int m, int n, int k, const void* x, void* stream) {
+  GemmDesc g{a, lda, false, b, ldb, b_mn_major != 0, c, ldc, m, n, k, nullptr, EPI_BF16_GELU_BWD};
+  g.res = CBF(x);
+  return gemm_run(g, STREAM(stream));
+}
+
 void lynx_op_gemm_mode(int mode) { gemm_set_mode(mode); }
 void lynx_op_attention_mode(int mode) { attention_set_mode(mode); }
 

@@ -67,6 +67,14 @@ LYNX_DEV float gelu_exact(float x) {
   return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.f, tanhf(u)));
 }
 
+// d gelu(x) / dx for the same tanh GeLU.
+LYNX_DEV float gelu_grad_f(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float u = k0 * (x + k1 * x * x * x);
+  const float t = tanhf(u);
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
 // ---------------------------------------------------------------- Philox
 // Philox-4x32-10 (Salmon et al., SC'11). Counter = (element group, stream),
 // key = seed. Deterministic in (seed, stream, element) only, so a forward op

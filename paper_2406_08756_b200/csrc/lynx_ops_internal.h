@@ -32,7 +32,17 @@ const char* last_error();
 // EPI_BF16_GELU: c = bf16(acc + bias) and c2 = bf16(gelu(c)) (FC1 with its GeLU fused).
 // EPI_BF16_RESID: c = bf16(res + dropout(bf16(acc + bias))) with the Philox mask of
 // bias_dropout_residual_fwd (element index row * ldc + col), i.e. PROJ_RES / FC2_RES in one kernel.
-enum EpiMode { EPI_BF16 = 0, EPI_ACC_F32 = 1, EPI_STORE_F32 = 2, EPI_ACC_BF16 = 3, EPI_BF16_GELU = 4, EPI_BF16_RESID = 5 };
+// EPI_BF16_GELU_BWD: c = bf16(acc * gelu'(res)) with res the FC1 output (GeLU backward fused into the
+// dX GEMM of FC2).
+enum EpiMode {
+  EPI_BF16 = 0,
+  EPI_ACC_F32 = 1,
+  EPI_STORE_F32 = 2,
+  EPI_ACC_BF16 = 3,
+  EPI_BF16_GELU = 4,
+  EPI_BF16_RESID = 5,
+  EPI_BF16_GELU_BWD = 6
+};
 
 struct GemmDesc {
   const void* a;  // bf16
@@ -47,7 +57,7 @@ struct GemmDesc {
   const __nv_bfloat16* bias;  // EPI_BF16 / EPI_BF16_GELU only, may be null
   int epi;
   void* c2 = nullptr;  // EPI_BF16_GELU: second bf16 output (same shape and ldc as c)
-  const __nv_bfloat16* res = nullptr;  // EPI_BF16_RESID: residual input (same shape and ldc as c)
+  const __nv_bfloat16* res = nullptr;  // EPI_BF16_RESID residual / EPI_BF16_GELU_BWD GeLU input (shape, ldc of c)
   float drop_p = 0.f;
   uint64_t drop_seed = 0, drop_stream = 0;
 };

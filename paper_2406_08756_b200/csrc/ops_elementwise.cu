@@ -63,12 +63,7 @@ __global__ void dropout_bwd_kernel(const BF8* __restrict__ dout, BF8* __restrict
 
 // GPT-2 tanh GeLU.
 LYNX_DEV float gelu_f(float x) { return gelu_exact(x); }
-LYNX_DEV float gelu_grad(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float u = k0 * (x + k1 * x * x * x);
-  const float t = tanhf(u);
-  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
-}
+LYNX_DEV float gelu_grad(float x) { return gelu_grad_f(x); }
 
 __global__ void gelu_fwd_kernel(const BF8* __restrict__ x, BF8* __restrict__ y, long long nvec) {
 #pragma unroll 4  // several 16-byte vectors in flight per thread (HBM-bound)

@@ -57,6 +57,15 @@ struct Args {
   uint64_t drop_seed, drop_stream;
 };
 
+// EPI_BF16_GELU_BWD on 8 outputs: dfc1 = dgelu * gelu'(fc1), fc1 read from `res`.
+LYNX_DEV BF8 gelu_bwd8(const Args& args, long long row, int col, const float* v) {
+  float x[8], o[8];
+  bf8_to_f(*reinterpret_cast<const BF8*>(args.res + row * args.ldc + col), x);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j] = v[j] * gelu_grad_f(x[j]);
+  return f_to_bf8(o);
+}
+
 // EPI_BF16_RESID on 8 outputs (columns col..col+7 of `row`): out = res + dropout(bf16(v)).
 LYNX_DEV BF8 resid_dropout8(const Args& args, long long row, int col, const float* v) {
   float y[8], r[8], o[8];
@@ -154,9 +163,11 @@ LYNX_DEV void epilogue_row(const Args& args, uint32_t t_row, long long row, int 
         for (int i = 0; i < 32; ++i) v[i] += b[i];
       }
       BF8* o = reinterpret_cast<BF8*>(reinterpret_cast<__nv_bfloat16*>(args.c) + row * args.ldc + n0 + c);
-      if (args.epi == EPI_BF16_RESID) {
+      if (args.epi == EPI_BF16_RESID || args.epi == EPI_BF16_GELU_BWD) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] = resid_dropout8(args, row, n0 + c + 8 * i, v + 8 * i);
+        for (int i = 0; i < 4; ++i)
+          o[i] = args.epi == EPI_BF16_RESID ? resid_dropout8(args, row, n0 + c + 8 * i, v + 8 * i)
+                                            : gelu_bwd8(args, row, n0 + c + 8 * i, v + 8 * i);
         continue;
       }
 #pragma unroll
@@ -243,8 +254,9 @@ LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, const
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       *reinterpret_cast<BF8*>(st + lane * 128 + ((i ^ (lane & 7)) << 4)) =
-          args.epi == EPI_BF16_RESID ? resid_dropout8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
-                                     : f_to_bf8(v + 8 * i);
+          args.epi == EPI_BF16_RESID      ? resid_dropout8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
+          : args.epi == EPI_BF16_GELU_BWD ? gelu_bwd8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
+                                          : f_to_bf8(v + 8 * i);
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
@@ -383,7 +395,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;  // == warp % 4: TMEM lane quadrant
-    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU || args.epi == EPI_BF16_RESID) && args.tma_store;
+    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU || args.epi == EPI_BF16_RESID ||
+                          args.epi == EPI_BF16_GELU_BWD) &&
+                         args.tma_store;
     uint8_t* my_staging = staging + ew * 8192;
     int sbuf = 0;
     int acc = 0;
@@ -635,7 +649,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU || args.epi == EPI_BF16_RESID) && args.tma_store;
+    const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU || args.epi == EPI_BF16_RESID ||
+                          args.epi == EPI_BF16_GELU_BWD) &&
+                         args.tma_store;
     uint8_t* my_staging = staging + ew * 8192;
     int sbuf = 0;
     int acc = 0;
@@ -763,7 +779,8 @@ int launch(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
     attr_set = true;
   }
   CUtensorMap mc = ma, mc2 = ma;
-  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID;
+  const bool bf16_out =
+      g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID || g.epi == EPI_BF16_GELU_BWD;
   bool tma_out = bf16_out && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
   if (tma_out && g.epi == EPI_BF16_GELU) tma_out = make_map(&mc2, g.c2, g.N, g.M, g.ldc, 64, 32);
   const Args args = make_args(g, tma_out);
@@ -789,7 +806,8 @@ int launch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
     attr_set = true;
   }
   CUtensorMap mc = ma, mc2 = ma;
-  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID;
+  const bool bf16_out =
+      g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID || g.epi == EPI_BF16_GELU_BWD;
   bool tma_out = bf16_out && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
   if (tma_out && g.epi == EPI_BF16_GELU) tma_out = make_map(&mc2, g.c2, g.N, g.M, g.ldc, 64, 32);
   const Args args = make_args(g, tma_out);
@@ -829,9 +847,11 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   if (g.M % BM || g.K % BK || g.M <= 0 || g.N <= 0 || g.K <= 0)
     return set_error("gemm: M must be a multiple of 128 and K of 64");
   if (g.N % 128) return set_error("gemm: N must be a multiple of 128");
-  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_ACC_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID;
+  const bool bf16_out = g.epi == EPI_BF16 || g.epi == EPI_ACC_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID ||
+                        g.epi == EPI_BF16_GELU_BWD;
   if (g.epi == EPI_BF16_GELU && !g.c2) return set_error("gemm: the GeLU epilogue needs a second output");
-  if (g.epi == EPI_BF16_RESID && !g.res) return set_error("gemm: the residual epilogue needs the residual input");
+  if ((g.epi == EPI_BF16_RESID || g.epi == EPI_BF16_GELU_BWD) && !g.res)
+    return set_error("gemm: this epilogue needs its auxiliary input");
   if ((bf16_out && g.ldc % 8) || (!bf16_out && g.ldc % 4))
     return set_error("gemm: ldc must keep 16-byte row alignment");
   const int mode = g_gemm_mode;

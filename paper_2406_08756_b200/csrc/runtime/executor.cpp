@@ -727,9 +727,12 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
               "dropout_bwd");
       colsum(sc.t_h, P.g_b_fc2, h);
       gemm(sc.t_h, h, true, gelu, 4 * hp, true, P.g_w_fc2, 4 * hp, h, 4 * hp, T, dw_epi_);      // dW_fc2 += d^T gelu
-      gemm(sc.t_h, h, false, P.w_fc2, 4 * hp, true, sc.t_wide, 4 * hp, T, 4 * hp, h, EPI_BF16);  // dgelu = d W_fc2
-      if (!opt_.dry_run)
-        ck_op(gelu_bwd(sc.t_wide, static_cast<const __nv_bfloat16*>(fc1), sc.t_wide, T * 4 * hp, s), "gelu_bwd");
+      if (!opt_.dry_run) {  // dfc1 = (d W_fc2) * gelu'(fc1): the GeLU backward rides in the dX GEMM epilogue
+        GemmDesc g{sc.t_h, h, false, P.w_fc2, 4 * hp, true, sc.t_wide, 4 * hp, static_cast<int>(T), 4 * hp, h,
+                   nullptr, EPI_BF16_GELU_BWD};
+        g.res = static_cast<const __nv_bfloat16*>(fc1);
+        ck_op(gemm_run(g, s), "dgelu");
+      }
       colsum(sc.t_wide, P.g_b_fc1, 4 * hp);
       gemm(sc.t_wide, 4 * hp, true, y2, h, true, P.g_w_fc1, h, 4 * hp, h, T, dw_epi_);       // dW_fc1 += dfc1^T y2
       G.dln2 = alloc(T * h * 2, s);

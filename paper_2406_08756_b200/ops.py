@@ -59,6 +59,16 @@ def gemm_residual(a, b, res, *, bias=None, p: float = 0.0, seed: int = 0, stream
     return c
 
 
+def gemm_gelu_bwd(a, b, x, *, b_mn: bool = False):
+    """(a @ B^T) * gelu'(x) in one GEMM; B = b ([N,K]) or b.T (b_mn, b is [K,N])."""
+    M, K = a.shape
+    N = b.shape[1] if b_mn else b.shape[0]
+    c = torch.empty(M, N, device=a.device, dtype=torch.bfloat16)
+    call("lynx_op_gemm_gelu_bwd", a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), int(b_mn), c.data_ptr(),
+         c.stride(0), M, N, K, x.data_ptr(), _s())
+    return c
+
+
 def layernorm_fwd(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float = 1e-5):
     rows, width = x.shape
     y = torch.empty_like(x)

@@ -111,6 +111,24 @@ def test_gemm_residual_epilogue(ops, cuda, mode, M, N, K, p):
     assert rel(out, ref) < 1e-2
 
 
+@pytest.mark.parametrize("mode,M,N,K", [(-1, 512, 1024, 256), (0, 256, 384, 128), (1, 512, 2048, 512)])
+def test_gemm_gelu_bwd_epilogue(ops, cuda, mode, M, N, K):
+    """GeLU backward fused into the dX GEMM (B MN-major, as the executor calls it) vs GEMM + gelu_bwd."""
+    from paper_2406_08756_b200._native import lib
+    g = torch.Generator(device=cuda).manual_seed(M + 3 * N + K)
+    a = (torch.randn(M, K, device=cuda, generator=g) * 0.3).bfloat16()
+    bt = (torch.randn(K, N, device=cuda, generator=g) * 0.3).bfloat16()  # stored [K][N]
+    x = torch.randn(M, N, device=cuda, generator=g).bfloat16()
+    lib().lynx_op_gemm_mode(mode)
+    try:
+        fused = ops.gemm_gelu_bwd(a, bt, x, b_mn=True)
+        dg = ops.gemm(a, bt, b_mn=True)
+    finally:
+        lib().lynx_op_gemm_mode(-1)
+    ref = ops.gelu_bwd(dg, x)
+    assert rel(fused, ref) < 1e-2
+
+
 def test_gemm_bias_and_f32_epilogues(ops, cuda):
     g = torch.Generator(device=cuda).manual_seed(7)
     A = torch.randn(256, 512, device=cuda, generator=g).bfloat16()
