@@ -35,12 +35,32 @@ def _nlohmann_include() -> str:
     return str(p)
 
 
+def _nccl_dir() -> Path | None:
+    """NCCL bundled with PyTorch (nvidia-nccl wheel). Linking against the same libnccl.so.2 as torch
+    matters: the soname is shared, so whichever copy loads first serves both (the system 2.27 copy
+    lacks symbols torch's 2.28 build needs)."""
+    p = Path(sysconfig.get_paths()["purelib"]) / "nvidia" / "nccl"
+    return p if (p / "lib" / "libnccl.so.2").exists() and (p / "include" / "nccl.h").exists() else None
+
+
+def _nccl_include() -> list[str]:
+    d = _nccl_dir()
+    return [f"-I{d / 'include'}"] if d else []
+
+
+def _nccl_link() -> list[str]:
+    d = _nccl_dir()
+    if d:
+        return [f"-L{d / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{d / 'lib'}"]
+    return ["-lnccl", "-L/usr/lib/x86_64-linux-gnu", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+
+
 def _flags() -> list[str]:
     return [
         "-O3", "-std=c++17", "-lineinfo", *ARCH, *(["-DLYNX_ATTN_TRACE"] if os.environ.get("LYNX_BUILD_TRACE") else []),
         "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
         "--expt-relaxed-constexpr",
-        f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{_nlohmann_include()}",
+        f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{_nlohmann_include()}", *_nccl_include(),
         "-diag-suppress", "177,550",
     ]
 
@@ -66,7 +86,8 @@ def _compile(src: Path, newest_header: float) -> tuple[Path, str]:
     cmd = [NVCC, *_flags(), "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cpp":  # host-only C++ (planner, runtime glue): plain g++
         cmd = [CXX, "-O2", "-std=c++17", "-fPIC", "-g", "-Wall", "-Wextra", "-Wno-unused-parameter",
-               f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{_nlohmann_include()}", "-I/usr/local/cuda/include",
+               f"-I{ROOT / 'include'}", f"-I{CSRC}", f"-I{_nlohmann_include()}", *_nccl_include(),
+               "-I/usr/local/cuda/include",
                "-c", str(src), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -92,7 +113,7 @@ def build(clean: bool = False, jobs: int | None = None, verbose: bool = False) -
     LIB.parent.mkdir(parents=True, exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs),
-           "-lcudart", "-lnccl", "-L/usr/lib/x86_64-linux-gnu", "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+           "-lcudart", *_nccl_link()]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

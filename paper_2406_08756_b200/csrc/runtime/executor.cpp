@@ -128,6 +128,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.check_recompute = ex.value("check_recompute", false);
   opt_.elide_recompute = ex.value("elide_recompute", false);
   opt_.dry_run = ex.value("dry_run", false);
+  opt_.standalone = ex.value("standalone_stage", false);
   cfg_.head_chunk = static_cast<int>(std::min<long long>(ex.value("head_chunk", 4096), cfg_.tokens()));
   if (cfg_.hidden % cfg_.heads || cfg_.heads % cfg_.tp || (cfg_.hidden / cfg_.tp) % 128)
     throw RtError("hidden must split into heads and TP ranks in 128-column tiles", kValidation);
@@ -138,6 +139,8 @@ void Executor::parse_config(const std::string& text) {
   nccl_id_ = par.value("nccl_id", std::string());
   world_rank_ = par.value("world_rank", 0);
   world_size_ = par.value("world_size", 1);
+  if (opt_.standalone && (cfg_.tp != 1 || world_size_ != 1))
+    throw RtError("standalone_stage runs one stage at TP = 1 in a single process", kValidation);
 }
 
 void Executor::init_comms(const std::string& id_hex, int world_rank, int world_size) {
@@ -176,7 +179,7 @@ void Executor::bind_template() {
   }
   const bool tp_tmpl = !L.fwd_comm_ids.empty();
   if (cfg_.tp > 1 && !tp_tmpl) throw RtError("tp > 1 needs the tensor-parallel layer template", kValidation);
-  needs_comms_ = tp_tmpl || cfg_.tp > 1 || cfg_.pp > 1;
+  needs_comms_ = tp_tmpl || cfg_.tp > 1 || (cfg_.pp > 1 && !opt_.standalone);
   tp_tmpl_ = tp_tmpl;
   static const std::vector<Op> t1 = {Op::LN1, Op::QKV, Op::ATTN, Op::PROJ_RES, Op::LN2, Op::FC1,
                                      Op::GELU, Op::FC2_RES, Op::MLP_BWD, Op::ATTN_BWD, Op::LN1_BWD};
@@ -249,6 +252,12 @@ void Executor::alloc_persistent() {
     head_gw32_ = static_cast<float*>(m(static_cast<size_t>(cfg_.vocab) * h * 4));
   }
   if (cfg_.first()) emb_gw32_ = static_cast<float*>(m(static_cast<size_t>(cfg_.vocab + cfg_.seq) * h * 4));
+  if (opt_.standalone) {  // activations ~ N(0, 1), gradients ~ N(0, 1e-2): realistic operands for timing
+    syn_act_ = static_cast<__nv_bfloat16*>(m(static_cast<size_t>(T) * h * 2));
+    syn_grad_ = static_cast<__nv_bfloat16*>(m(static_cast<size_t>(T) * h * 2));
+    ck_op(init_normal_bf16(syn_act_, nullptr, T * h, 1.0f, cfg_.seed, 0xAC7ull, main_), "synthetic activations");
+    ck_op(init_normal_bf16(syn_grad_, nullptr, T * h, 0.01f, cfg_.seed, 0x6AADull, main_), "synthetic gradients");
+  }
   sc_side_.t_h = static_cast<__nv_bfloat16*>(m(T * h * 2));
   const size_t ntok = static_cast<size_t>(cfg_.n_micro) * T;
   d_tokens_ = static_cast<int*>(m(ntok * 4));
@@ -275,7 +284,8 @@ void Executor::release_all() {
   for (void* p : {static_cast<void*>(sc_main_.t_h), static_cast<void*>(sc_main_.t_h2),
                   static_cast<void*>(sc_main_.t_wide), static_cast<void*>(sc_main_.ws),
                   static_cast<void*>(sc_main_.logits), static_cast<void*>(sc_side_.t_h), static_cast<void*>(d_tokens_),
-                  static_cast<void*>(head_gw32_), static_cast<void*>(emb_gw32_),
+                  static_cast<void*>(head_gw32_), static_cast<void*>(emb_gw32_), static_cast<void*>(syn_act_),
+                  static_cast<void*>(syn_grad_),
                   static_cast<void*>(d_labels_), static_cast<void*>(d_loss_), static_cast<void*>(d_mismatch_)})
     if (p) cudaFree(p);
   cudaFreeHost(h_tokens_);
@@ -854,7 +864,10 @@ void Executor::forward_pass(int mb) {
             "embedding");
   } else {
     program_.push_back({"recv", "pp_act", cfg_.pp_rank - 1, static_cast<size_t>(2 * T * h), "F mb" + std::to_string(mb)});
-    if (!opt_.dry_run) {
+    if (opt_.standalone && !opt_.dry_run) {
+      ck(cudaMemcpyAsync(stage_in_[mb], syn_act_, static_cast<size_t>(2 * T * h), cudaMemcpyDeviceToDevice, main_),
+         "synthetic activation");
+    } else if (!opt_.dry_run) {
       cudaEvent_t a = ev();
       ck(cudaEventRecord(a, main_), "event");  // buffer allocated on main
       ck(cudaStreamWaitEvent(pa_s_, a, 0), "wait");
@@ -887,7 +900,10 @@ void Executor::forward_pass(int mb) {
   } else {
     void* out = need(mb, cfg_.layers - 1, nf_ - 1, main_);
     program_.push_back({"send", "pp_act", cfg_.pp_rank + 1, static_cast<size_t>(2 * T * h), "F mb" + std::to_string(mb)});
-    if (!opt_.dry_run) {
+    if (opt_.standalone && !opt_.dry_run) {
+      (void)out;
+      ck(cudaEventRecord(act_sent_[mb], main_), "event");
+    } else if (!opt_.dry_run) {
       cudaEvent_t a = ev();
       ck(cudaEventRecord(a, main_), "event");
       ck(cudaStreamWaitEvent(pa_s_, a, 0), "wait");
@@ -920,7 +936,10 @@ void Executor::backward_pass(int mb) {
   } else {
     grad_[mb].dy = alloc(2 * T * h, main_);
     program_.push_back({"recv", "pp_grad", cfg_.pp_rank + 1, static_cast<size_t>(2 * T * h), "B mb" + std::to_string(mb)});
-    if (!opt_.dry_run) {
+    if (opt_.standalone && !opt_.dry_run) {
+      ck(cudaMemcpyAsync(grad_[mb].dy, syn_grad_, static_cast<size_t>(2 * T * h), cudaMemcpyDeviceToDevice, main_),
+         "synthetic gradient");
+    } else if (!opt_.dry_run) {
       cudaEvent_t a = ev();
       ck(cudaEventRecord(a, main_), "event");
       ck(cudaStreamWaitEvent(pg_s_, a, 0), "wait");
@@ -973,14 +992,18 @@ void Executor::backward_pass(int mb) {
     release(dx, main_);
   } else {
     program_.push_back({"send", "pp_grad", cfg_.pp_rank - 1, static_cast<size_t>(2 * T * h), "B mb" + std::to_string(mb)});
-    if (!opt_.dry_run) {
-      cudaEvent_t a = ev();
-      ck(cudaEventRecord(a, main_), "event");
-      ck(cudaStreamWaitEvent(pg_s_, a, 0), "wait");
-      nccl(ncclSend(dx, static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank - 1, pg_comm_, pg_s_), "send");
-      ck(cudaEventRecord(grad_sent_[mb], pg_s_), "event");
+    if (opt_.standalone && !opt_.dry_run) {
+      release(dx, main_);
+    } else {
+      if (!opt_.dry_run) {
+        cudaEvent_t a = ev();
+        ck(cudaEventRecord(a, main_), "event");
+        ck(cudaStreamWaitEvent(pg_s_, a, 0), "wait");
+        nccl(ncclSend(dx, static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank - 1, pg_comm_, pg_s_), "send");
+        ck(cudaEventRecord(grad_sent_[mb], pg_s_), "event");
+      }
+      release(dx, pg_s_);  // stream-ordered after the send; main never waits on the peer
     }
-    release(dx, pg_s_);  // stream-ordered after the send; main never waits on the peer
   }
   grad_[mb].dy = nullptr;
   release(stage_in_[mb], main_);

@@ -42,6 +42,8 @@ struct ExecOptions {
   bool check_recompute = false; // keep forward copies, compare regenerated tensors bit-for-bit
   bool elide_recompute = false; // timing-only: skip recompute launches (exposed-recompute cross-check)
   bool dry_run = false;         // build the launch program only (no device)
+  bool standalone = false;      // time one pipeline stage alone on one GPU: receives read synthetic
+                                // activations / gradients, sends are skipped (measured partitioning)
 };
 
 struct Slot {
@@ -174,6 +176,7 @@ class Executor {
   int bwd_passes_ = 0;
   int dw_epi_ = 1;  // EPI_ACC_F32
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
+  __nv_bfloat16 *syn_act_ = nullptr, *syn_grad_ = nullptr;  // standalone stage: stand-ins for PP receives
   float* head_gw32_ = nullptr;  // last stage: LM-head weight gradient, fp32 across chunks / microbatches
   float* emb_gw32_ = nullptr;   // first stage: wte | wpe gradients, fp32 (scatter-add with atomics)
   bool head_first_ = true;
