@@ -237,11 +237,12 @@ def run_reference_arm(args):
 
 
 def workload_config(c, args) -> dict:
-    return {"workload": f"{c.name} full model, seq {c.seq}, micro-batch {c.micro_batch}, "
-                        f"{c.n_microbatches} microbatch(es)/iter, TP{c.tp}xPP{c.pp}, HEU recompute plan",
-            "model": c.name, "layers": c.n_layers, "hidden": c.hidden, "heads": c.heads,
-            "global_batch": c.micro_batch * c.n_microbatches, "seq_len": c.seq, "micro_batch": c.micro_batch,
-            "n_microbatches": c.n_microbatches, "parallelism": f"tp{c.tp}pp{c.pp}", "plan": args.plan,
+    return {"workload": f"{c.name} training step (BASELINE configs[2] shape), seq {c.seq}, micro-batch "
+                        f"{c.micro_batch}, {c.n_microbatches} microbatch(es)/iter, TP{c.tp}xPP{c.pp}, "
+                        f"{args.plan.upper()} recompute plan",
+            "layers": c.n_layers, "hidden": c.hidden, "heads": c.heads, "seq": c.seq, "micro_batch": c.micro_batch,
+            "n_microbatches": c.n_microbatches, "tokens_per_step": c.micro_batch * c.seq * c.n_microbatches,
+            "parallelism": f"tp{c.tp}pp{c.pp}", "plan": args.plan,
             "l2": "activations are GBs per op (> 126 MB L2); no flush needed"}
 
 
