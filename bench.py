@@ -391,7 +391,7 @@ def run_gpu_arm(args):
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     cfg = ex.make_config(c, layers, tp_rank=tp_rank, world_rank=rank, world_size=ws, nccl_id=nccl_id,
-                         exec_opts={"trace": False})
+                         exec_opts={"trace": False, "probe_fc1": True})
     tok, lab = ex.synthetic_batch(c)
     first, last = stage == 0, stage == c.pp - 1
     for mi, margin in enumerate(margins):
@@ -478,6 +478,21 @@ def run_gpu_arm(args):
         "clocks": clk.summary(),
         "planner_s": round(plan_s, 3),
     }
+    # roofline of the dominant kernel from CUDA events around every FC1 forward GEMM launch inside the
+    # timed steps (forward and recompute, on the launching stream); the isolated pre-run measurement is
+    # kept beside it
+    n_probe = sum(r.get("probe_fc1_launches", 0) for r in reports)
+    if roof is not None and n_probe:
+        ms_probe = sum(r["probe_fc1_ms"] for r in reports) / n_probe
+        iso = {k: roof[k] for k in ("ms_per_launch", "achieved", "frac")}
+        ach = roof["flops_per_launch"] / ms_probe / 1e9
+        iso["peak"], iso["peak_kind"] = roof["peak"], roof["peak_kind"]
+        peak = peaks.get("bf16_tflops_sustained", roof["peak"])  # kernel timed inside a long step
+        roof.update({"peak": peak, "peak_kind": "measured sustained bf16 (MEASURED_PEAKS.json; kernel timed inside "
+                     "the step)",
+                     "ms_per_launch": round(ms_probe, 4), "achieved": round(ach, 1), "frac": round(ach / peak, 4),
+                     "launches_timed": n_probe, "measured": "CUDA events on the launching stream around each FC1 "
+                     "forward GEMM (fused GeLU epilogue) inside the timed steps", "isolated": iso})
     # kernels of liblynx_b200.so issued inside the timed region (counted at every launch site)
     line["gpu_launches"] = int(sum(r["kernel_launches"] for r in reports))
     if not args.no_cpu_baseline and ws == 1:

@@ -129,6 +129,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.elide_recompute = ex.value("elide_recompute", false);
   opt_.dry_run = ex.value("dry_run", false);
   opt_.standalone = ex.value("standalone_stage", false);
+  opt_.probe_fc1 = ex.value("probe_fc1", false);
   cfg_.head_chunk = static_cast<int>(std::min<long long>(ex.value("head_chunk", 4096), cfg_.tokens()));
   if (cfg_.hidden % cfg_.heads || cfg_.heads % cfg_.tp || (cfg_.hidden / cfg_.tp) % 128)
     throw RtError("hidden must split into heads and TP ranks in 128-column tiles", kValidation);
@@ -560,7 +561,13 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
         ck_op(gemm_run(g, s), "proj + residual");
         break;
       }
-      case Op::FC1:
+      case Op::FC1: {
+        cudaEvent_t pa = nullptr, pb = nullptr;
+        if (opt_.probe_fc1) {  // the bench's roofline kernel, timed on its own stream inside the step
+          pa = ev();
+          pb = ev();
+          ck(cudaEventRecord(pa, s), "event");
+        }
         if (gelu_slot) {
           GemmDesc g{in, h, false, P.w_fc1, h, false, o, 4 * hp, static_cast<int>(T), 4 * hp, h, P.b_fc1,
                      EPI_BF16_GELU, gelu_slot->p};
@@ -568,7 +575,12 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
         } else {
           gemm(in, h, P.w_fc1, h, o, 4 * hp, T, 4 * hp, h, P.b_fc1);
         }
+        if (opt_.probe_fc1) {
+          ck(cudaEventRecord(pb, s), "event");
+          probes_.emplace_back(pa, pb);
+        }
         break;
+      }
       case Op::GELU: ck_op(gelu_fwd(static_cast<const __nv_bfloat16*>(in), o, T * 4 * hp, s), "gelu"); break;
       case Op::FC2: gemm(in, 4 * hp, P.w_fc2, 4 * hp, o, h, T, h, 4 * hp, nullptr); break;
       case Op::FC2_RES: {
@@ -1019,6 +1031,7 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   open_.clear();
   program_.clear();
   rep_ = StepReport{};
+  probes_.clear();
   bwd_passes_ = 0;
   const long long T = cfg_.tokens();
   const size_t ntok = static_cast<size_t>(cfg_.n_micro) * T;
@@ -1074,6 +1087,13 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   ck(cudaEventElapsedTime(&ms, t0_, t1_), "elapsed");
   rep_.step_ms = ms;
   collect_spans();
+  for (const auto& [a, b] : probes_) {
+    float pm = 0.f;
+    ck(cudaEventElapsedTime(&pm, a, b), "probe");
+    rep_.probe_ms += pm;
+    ++rep_.probe_launches;
+  }
+  probes_.clear();
   if (cfg_.last()) {
     double s = 0;
     for (size_t i = 0; i < ntok; ++i) s += h_loss_[i];
@@ -1105,6 +1125,8 @@ std::string Executor::report_json() const {
   j["recompute_mismatch_words"] = rep_.recompute_mismatch_words;
   j["loss"] = rep_.loss;
   j["pool_high_water_bytes"] = rep_.pool_high_water;
+  j["probe_fc1_launches"] = rep_.probe_launches;
+  j["probe_fc1_ms"] = rep_.probe_ms;
   j["static_bytes_allocated"] = static_cast<long long>(ps_.count()) * 16;
   j["params"] = ps_.count();
   j["layers"] = cfg_.layers;

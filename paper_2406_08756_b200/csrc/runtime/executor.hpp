@@ -42,6 +42,7 @@ struct ExecOptions {
   bool check_recompute = false; // keep forward copies, compare regenerated tensors bit-for-bit
   bool elide_recompute = false; // timing-only: skip recompute launches (exposed-recompute cross-check)
   bool dry_run = false;         // build the launch program only (no device)
+  bool probe_fc1 = false;       // CUDA events around every FC1 forward GEMM launch (roofline line)
   bool standalone = false;      // time one pipeline stage alone on one GPU: receives read synthetic
                                 // activations / gradients, sends are skipped (measured partitioning)
 };
@@ -63,6 +64,8 @@ struct StepReport {
   long long recompute_launches = 0, recompute_mismatch_words = 0, recompute_checked = 0;
   long long kernel_launches = 0;  // kernels of this library issued by the step
   size_t pool_high_water = 0;
+  long long probe_launches = 0;  // exec.probe_fc1: FC1 forward GEMM launches timed in this step
+  double probe_ms = 0;           // ... and their summed CUDA-event durations
 };
 
 struct CommOp {  // launch-program record (dry runs and tests)
@@ -177,6 +180,7 @@ class Executor {
   int dw_epi_ = 1;  // EPI_ACC_F32
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   __nv_bfloat16 *syn_act_ = nullptr, *syn_grad_ = nullptr;  // standalone stage: stand-ins for PP receives
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probes_;  // exec.probe_fc1 event pairs of this step
   float* head_gw32_ = nullptr;  // last stage: LM-head weight gradient, fp32 across chunks / microbatches
   float* emb_gw32_ = nullptr;   // first stage: wte | wpe gradients, fp32 (scatter-add with atomics)
   bool head_first_ = true;
