@@ -1,6 +1,7 @@
 """Run the bench's dominant GEMM shapes a few times (target for ncu --set full captures).
 
-    python tools/gemm_one.py [T]   -> 4x FC1 forward [T,16384,4096], then 4x FC1 dW [16384,4096,T]
+    python tools/gemm_one.py [T]   -> 4x FC1 forward with the fused GeLU epilogue [T,16384,4096] (as in the
+                                      training step), then 4x FC1 dW [16384,4096,T] (bf16 store epilogue)
 """
 import sys
 
@@ -13,11 +14,11 @@ T = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 h = 4096
 x = torch.randn(T, h, device="cuda").bfloat16()
 w = torch.randn(4 * h, h, device="cuda").bfloat16()
-y = torch.empty(T, 4 * h, device="cuda", dtype=torch.bfloat16)
+b = torch.randn(4 * h, device="cuda").bfloat16()
 for _ in range(4):
-    ops.gemm(x, w, out=y)
-g = torch.zeros(4 * h, h, device="cuda")
+    y, g = ops.gemm_gelu(x, w, bias=b)
+gw = torch.empty(4 * h, h, device="cuda", dtype=torch.bfloat16)
 for _ in range(4):
-    ops.gemm(y, x, a_mn=True, b_mn=True, out=g, epi=ops.EPI_ACC_F32)
+    ops.gemm(y, x, a_mn=True, b_mn=True, out=gw, epi=ops.EPI_BF16)
 torch.cuda.synchronize()
 print("ok")
