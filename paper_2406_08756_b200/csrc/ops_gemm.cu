@@ -118,15 +118,19 @@ LYNX_DEV void epilogue_row(const Args& args, uint32_t t_row, long long row, int 
     BF8 prevb[4];
     float* outf = reinterpret_cast<float*>(args.c) + row * args.ldc + n0 + c;
     BF8* outb = reinterpret_cast<BF8*>(reinterpret_cast<__nv_bfloat16*>(args.c) + row * args.ldc + n0 + c);
-    if (args.epi == EPI_ACC_F32) {
+    // Partial edge tiles (M or N not a tile multiple, 128-aligned): every lane still runs the
+    // warp-collective TMEM load; out-of-range rows / 32-column chunks are not read or written.
+    const bool in = row < args.M && n0 + c < args.N;
+    if (in && args.epi == EPI_ACC_F32) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) prev[i] = reinterpret_cast<const float4*>(outf)[i];
-    } else if (args.epi == EPI_ACC_BF16) {
+    } else if (in && args.epi == EPI_ACC_BF16) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) prevb[i] = outb[i];
     }
     tmem_ld32(t_row + c, r);
     tmem_ld_wait();
+    if (!in) continue;
     float v[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -252,11 +256,14 @@ LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, const
     if (lane == 0) bulk_wait_read1();  // the store issued from this buffer two rounds ago has read it
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 8; ++i) {
+      // auxiliary inputs are read only in range (the TMA store clips partial edge tiles)
+      const bool in = row0 + lane < args.M && n0 + c + 8 * i < args.N;
       *reinterpret_cast<BF8*>(st + lane * 128 + ((i ^ (lane & 7)) << 4)) =
-          args.epi == EPI_BF16_RESID      ? resid_dropout8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
-          : args.epi == EPI_BF16_GELU_BWD ? gelu_bwd8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
-                                          : f_to_bf8(v + 8 * i);
+          in && args.epi == EPI_BF16_RESID      ? resid_dropout8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
+          : in && args.epi == EPI_BF16_GELU_BWD ? gelu_bwd8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
+                                                : f_to_bf8(v + 8 * i);
+    }
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
@@ -516,7 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m_tiles = args.M / kTileM, n_tiles = args.N / kTileN;
+  const int m_tiles = (args.M + kTileM - 1) / kTileM, n_tiles = (args.N + kTileN - 1) / kTileN;
   const int num_tiles = m_tiles * n_tiles;
   const int k_blocks = args.K / BK;
   const int cluster = blockIdx.x / 2, n_clusters = gridDim.x / 2;
@@ -811,7 +818,7 @@ int launch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   bool tma_out = bf16_out && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
   if (tma_out && g.epi == EPI_BF16_GELU) tma_out = make_map(&mc2, g.c2, g.N, g.M, g.ldc, 64, 32);
   const Args args = make_args(g, tma_out);
-  const int tiles = (g.M / C::kTileM) * (g.N / pair::kTileN);
+  const int tiles = ((g.M + C::kTileM - 1) / C::kTileM) * ((g.N + pair::kTileN - 1) / pair::kTileN);
   int clusters = num_sms() / 2;
   if (max_ctas > 0) clusters = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
   if (tiles < clusters) clusters = tiles;
@@ -830,8 +837,8 @@ int dispatch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
 }  // namespace gemm
 
 namespace {
-// -1 (default): the wide 512x256 CTA-pair kernel for K >= 8192 where the shape allows, else
-// the 256x256 pair kernel for K-major A, else the single-CTA kernel. 0: single-CTA only.
+// -1 (default): the wide 512x256 CTA-pair kernel for K >= 8192, else the 256x256 pair kernel for
+// K-major A, else the single-CTA kernel (pair kernels accept 128-aligned edge tiles). 0: single-CTA only.
 // 1: 256x256 pair wherever the shape allows. 2: wide pair, then 256x256 pair, then single.
 // LYNX_GEMM_MODE sets the initial mode (experiments).
 int g_gemm_mode = [] {
@@ -855,17 +862,17 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   if ((bf16_out && g.ldc % 8) || (!bf16_out && g.ldc % 4))
     return set_error("gemm: ldc must keep 16-byte row alignment");
   const int mode = g_gemm_mode;
-  const bool n_ok = g.N % pair::kTileN == 0;
+  // CTA-pair kernels take 128-aligned M and N; partial edge tiles are zero-filled by TMA on load
+  // and clipped by the TMA store / bounds-checked in the direct epilogue (e.g. the LM head's
+  // logits, N = V = 50304 = 196.5 x 256).
+  auto tiles_of = [&](int tm) { return ((g.M + tm - 1) / tm) * ((g.N + pair::kTileN - 1) / pair::kTileN); };
   // The wide tile pays a non-overlapped epilogue per tile (TMEM single-buffered), so by
   // default it is used for long reductions only (K >= 8192: FC2 forward, FC1/QKV dX, all dW),
   // where it measures 6-11% faster under the power cap (less L2->SM traffic).
-  if ((mode == 2 || (mode == -1 && g.K >= 8192)) && n_ok && g.M % pair::Cfg<2>::kTileM == 0 &&
-      (g.M / pair::Cfg<2>::kTileM) * (g.N / pair::kTileN) >= 64)
+  if ((mode == 2 || (mode == -1 && g.K >= 8192)) && tiles_of(pair::Cfg<2>::kTileM) >= 64)
     return dispatch_pair<2>(g, stream, max_ctas);
   const bool want_pair = mode == 1 || mode == 2 || (mode == -1 && !g.a_mn);
-  if (want_pair && n_ok && g.M % pair::Cfg<1>::kTileM == 0 &&
-      (g.M / pair::Cfg<1>::kTileM) * (g.N / pair::kTileN) >= 32)
-    return dispatch_pair<1>(g, stream, max_ctas);
+  if (want_pair && tiles_of(pair::Cfg<1>::kTileM) >= 32) return dispatch_pair<1>(g, stream, max_ctas);
   const bool wide = g.N % 256 == 0;
 #define LYNX_GEMM_CASE(AMN, BMN)                                                             \
   if (g.a_mn == AMN && g.b_mn == BMN)                                                         \

@@ -129,6 +129,36 @@ def test_gemm_gelu_bwd_epilogue(ops, cuda, mode, M, N, K):
     assert rel(fused, ref) < 1e-2
 
 
+@pytest.mark.parametrize("mode", [1, 2, -1])
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (True, True), (False, True)])
+def test_gemm_pair_edge_tiles(ops, cuda, mode, a_mn, b_mn):
+    """CTA-pair kernels on 128-aligned shapes that are not tile multiples (M = 2.5 x 256 rows of the
+    pair tile, N = 4.5 x 256: the LM head's V = 50304 case): TMA zero-fills the loads, the TMA store
+    clips and the direct epilogues bounds-check."""
+    from paper_2406_08756_b200._native import lib
+    M, N, K = 5 * 128 * (2 if mode == 2 else 1), 9 * 128, 512
+    g = torch.Generator(device=cuda).manual_seed(M + N)
+    A = (torch.randn(M, K, device=cuda, generator=g) * 0.3).bfloat16()
+    B = (torch.randn(N, K, device=cuda, generator=g) * 0.3).bfloat16()
+    a = A.t().contiguous() if a_mn else A
+    b = B.t().contiguous() if b_mn else B
+    bias = torch.randn(N, device=cuda, generator=g).bfloat16()
+    ref = A.float() @ B.float().t()
+    lib().lynx_op_gemm_mode(mode)
+    try:
+        out = ops.gemm(a, b, a_mn=a_mn, b_mn=b_mn, bias=bias)
+        acc = torch.ones(M, N, device=cuda)
+        ops.gemm(a, b, a_mn=a_mn, b_mn=b_mn, out=acc, epi=ops.EPI_ACC_F32)
+        accb = torch.ones(M, N, device=cuda, dtype=torch.bfloat16)
+        ops.gemm(a, b, a_mn=a_mn, b_mn=b_mn, out=accb, epi=ops.EPI_ACC_BF16)
+        torch.cuda.synchronize()
+    finally:
+        lib().lynx_op_gemm_mode(-1)
+    assert rel(out, ref + bias.float()) < 1e-2
+    assert rel(acc, ref + 1) < 1e-5
+    assert rel(accb, ref + 1) < 1e-2
+
+
 def test_gemm_bias_and_f32_epilogues(ops, cuda):
     g = torch.Generator(device=cuda).manual_seed(7)
     A = torch.randn(256, 512, device=cuda, generator=g).bfloat16()
