@@ -468,6 +468,7 @@ def run_gpu_arm(args):
                    "pool_high_water_bytes": rep["pool_high_water_bytes"],
                    "static_bytes": rep["static_bytes_allocated"], "device_total_bytes": total},
         "loss": [round(x, 5) for x in losses],
+        "step_ms_each": [round(x, 1) for x in step_ms],
         "model_tflops_per_gpu": round(step_tflops / n, 1),
         "mfu_vs_sustained": round(step_tflops / n / peaks.get("bf16_tflops_sustained", 1400.0), 4),
         "roofline": roof,
