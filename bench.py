@@ -118,7 +118,7 @@ def config_for(n_gpus: int, args):
     return c
 
 
-def device_budget(c, device_bytes: int, margin_gib: float = 12.0) -> int:
+def device_budget(c, device_bytes: int, margin_gib: float = 8.0) -> int:
     """Ledger budget = HBM minus what the ledger does not model (runtime scratch, transients, context)."""
     T, h = c.tokens, c.hidden
     hp = h // c.tp
@@ -529,8 +529,9 @@ def main():
                     help="operator times for the planner: B200-measured (default) or the analytic estimate")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-crosscheck", action="store_true", help="skip the recompute-elided timing run")
-    ap.add_argument("--mem-margin-gib", type=float, default=12.0,
-                    help="HBM held back from the HEU budget for context and pool fragmentation")
+    ap.add_argument("--mem-margin-gib", type=float, default=8.0,
+                    help="HBM held back from the HEU budget for context and pool fragmentation "
+                         "(an OOM retries with 12 and 16 GiB)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -65,6 +65,12 @@ Executor::Executor(const std::string& profile_json, const std::string& timeline_
 }
 
 void Executor::init_device() {
+  // Reserve the per-thread local-memory (stack) the library's kernels can need before the big
+  // allocations: growing it lazily mid-step, with HBM nearly full, stalls the device (observed as
+  // sporadic 1-4 s steps under high-memory plans).
+  size_t stack = 0;
+  ck(cudaDeviceGetLimit(&stack, cudaLimitStackSize), "stack limit");
+  if (stack < 1024) ck(cudaDeviceSetLimit(cudaLimitStackSize, 1024), "stack limit");
   if (needs_comms_) init_comms(nccl_id_, world_rank_, world_size_);
   for (cudaStream_t* s : {&main_, &side_, &tp_s_, &pa_s_, &pg_s_})
     ck(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "stream");
