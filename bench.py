@@ -328,15 +328,18 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
             be = ex.Executor(tt, timeline, ccfg)
             for _ in range(3):  # the first steps grow the stream-ordered pool
                 be.step(btok, blab)
-            be.step(btok, blab)
-            br = be.report()
+            reps = []
+            for _ in range(3):  # the median of three steps (one slow step must not decide the cross-check)
+                be.step(btok, blab)
+                reps.append(be.report())
+            br = sorted(reps, key=lambda r: r["iteration_ms"])[1]
             tok_i = cc.tokens * cc.n_microbatches
             out[name] = {"iteration_ms": round(br["iteration_ms"], 3),
                          "exposed_recompute_ms": round(br["exposed_recompute_ms"], 3),
                          "tokens_per_s": round(tok_i / (br["iteration_ms"] / 1000.0), 1),
                          "micro_batch": cc.micro_batch, "recompute_launches": br["recompute_launches"],
                          "pool_high_water_bytes": br["pool_high_water_bytes"], "free_bytes_before": free_b,
-                         "loss": br["loss"]}
+                         "loss": br["loss"], "step_ms_each": [round(r["iteration_ms"], 1) for r in reps]}
             if bp is not None:
                 out[name]["plan_peak_bytes"] = json.loads(bp[0]["plan_json"])["peak_bytes"]
             if name == "elided":

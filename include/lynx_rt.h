@@ -77,6 +77,25 @@ char* lynx_plan_simulate_timelines(const char* profile_json, const int* layers, 
 char* lynx_plan_solve_heu(const char* profile_json, int stage, int stage_layers, int policy,
                           const char* delta_bytes, long long time_limit_ms, int* status);
 
+/* OPT at GPT scale through an external MILP solver (replaces the embedded
+ * B&B of optsched.cpp:216-243, which cannot solve a 7B stage). The model is the reference's
+ * OPT program (optsched.cpp:54-214) over `slice_layers` consecutive layers of the stage
+ * (0 = all), extended for replication over the stage: a variable Y bounds the slice's retained
+ * bytes at every phase entry and each ledger point carries (L/k - 1) Y for the other copies.
+ * Slice budget = static(k) + (mem_budget - static(L)) - reserve_bytes (null: 0).
+ * lynx_plan_opt_export: {n_vars, lo, hi, integer, objective [[var, c]], n_rows, row/col/val
+ *   (coordinate form), sense (-1 <=, 0 =, 1 >=), rhs, R[t][i], S[t][i] (variable indices),
+ *   budget_bytes, static_bytes, stage_activation_bytes, n_ops}; coefficients as doubles.
+ * lynx_plan_opt_timeline: schedule_json = {"keep": [[t, i]...], "recompute": [[t, i]...]} from
+ *   the solver. The schedule is checked exactly (check_schedule, optsched.cpp:245-338);
+ *   violations return status 1 with {"issues"}. Otherwise timeline_from_opt_schedule
+ *   (report_io.cpp:187-294) on the slice, replicated over the stage's layers:
+ *   {issues: "", cost_us, n_recompute, n_overlapped, timeline, slice_items}. */
+char* lynx_plan_opt_export(const char* profile_json, int stage, const int* layers, int n_layers, int slice_layers,
+                           const char* reserve_bytes, int* status);
+char* lynx_plan_opt_timeline(const char* profile_json, int stage, const int* layers, int n_layers, int slice_layers,
+                             const char* reserve_bytes, const char* schedule_json, int* status);
+
 /* ---------------------------------------------------------------- 2. execute */
 
 /* One executor per (pipeline stage, TP rank) process; replaces simulate().

@@ -4,6 +4,8 @@
 // string (free with lynx_free) and reports the CLI's exit-code semantics in
 // *status. Exceptions never cross the boundary.
 #include <cstdlib>
+#include <map>
+#include <set>
 #include <cstring>
 #include <string>
 
@@ -47,6 +49,62 @@ std::vector<int> layers_for(const Profile& p, const int* layers, int n) {
     return std::vector<int>(layers, layers + n);
   }
   return even_partition(p).layers;
+}
+
+// OPT over a slice of `slice` consecutive layers of an L-layer stage: the
+// unrolled phase grid of the full stage is Θ(n²) booleans (~10^6 at 7B), the slice's is small
+// enough for an external MILP solver. The slice is solved for replication over the stage: one
+// extra continuous variable Y bounds the slice's retained bytes at every phase entry
+// (schedulable ops only: the embedding / head tensors are not replicated), and every ledger
+// point carries the other L/k - 1 copies' Y on top: U_t_k + (L/k - 1) Y <= budget. The budget is
+// the slice's static share plus the stage's activation budget minus `reserve` bytes (null: 0).
+struct OptSlice {
+  Profile p;
+  int L = 0, k = 0;
+  UnrolledStage u;
+  OptModel m;
+};
+
+OptSlice opt_slice(const char* profile_json, int stage, const int* layers, int n_layers, int slice,
+                   const char* reserve_bytes) {
+  OptSlice o;
+  o.p = parse_profile(profile_json);
+  if (stage < 0 || stage >= o.p.pipeline.n_stages) throw ValidationError("stage out of range");
+  o.L = layers_for(o.p, layers, n_layers)[stage];
+  o.k = slice <= 0 ? o.L : slice;
+  if (o.k > o.L || o.L % o.k != 0) throw ValidationError("slice_layers must divide the stage's layer count");
+  const Rat st_L(static_share_ceil(o.p, o.L)), st_k(static_share_ceil(o.p, o.k));
+  const Rat act = Rat(o.p.hardware.mem_budget_bytes) - st_L;
+  Rat reserve(0);
+  if (reserve_bytes && *reserve_bytes) {
+    auto r = parse_rat(reserve_bytes);
+    if (!r || r->sign() < 0) throw ValidationError("reserve_bytes must be a non-negative rational");
+    reserve = *r;
+  }
+  if ((act - reserve).sign() <= 0) throw BudgetTooSmall("no activation budget left for the slice");
+  HardwareProfile hw = o.p.hardware;
+  const Rat b = st_k + act - reserve;
+  hw.mem_budget_bytes = (b.num() / b.den()).to_i64();
+  o.u = stage_phase_graph(o.p, stage, o.k);
+  o.m = opt_model(o.u.graph, hw, static_share_ceil(o.p, o.k));
+  const int copies = o.L / o.k - 1;
+  if (copies > 0) {
+    Program& P = o.m.prog;
+    const StageGraph& g = o.u.graph;
+    const int n_before = P.size();
+    const int y = P.new_cont("Y_retained", Rat(0), Rat(hw.mem_budget_bytes));
+    for (int t = 1; t < g.size(); ++t) {
+      Linear e;
+      e.add(1, y);
+      for (int i = 0; i < t; ++i)
+        if (g.schedulable[i] && g.ops[i].out_bytes > 0) e.add(Rat(-g.ops[i].out_bytes), o.m.S[t][i]);
+      P.add_row(std::move(e), Sense::Ge, 0, "retained_" + std::to_string(t));
+    }
+    for (int v = 0; v < n_before; ++v)
+      if (P.type(v) == VarType::Cont && P.name(v).rfind("U_", 0) == 0)
+        P.add_row(Linear().add(1, v).add(copies, y), Sense::Le, Rat(hw.mem_budget_bytes), "copies_" + P.name(v));
+  }
+  return o;
 }
 
 PlanMode mode_of(const char* m) {
@@ -219,6 +277,160 @@ char* lynx_plan_solve_heu(const char* profile_json, int stage, int stage_layers,
     j["lp"] = to_lp_text(hm.prog, "heu_stage_" + std::to_string(stage));
     j["check"] = plan_violations(plan, ctx, p.model.layer);
     j["timeline"] = nlohmann::ordered_json::parse(timeline_json(expand_to_stage(plan, ctx, p.pipeline, stage)));
+    return j.dump();
+  });
+}
+
+char* lynx_plan_opt_export(const char* profile_json, int stage, const int* layers, int n_layers, int slice_layers,
+                           const char* reserve_bytes, int* status) {
+  return guarded(status, [&](int&) -> std::string {
+    const OptSlice o = opt_slice(profile_json, stage, layers, n_layers, slice_layers, reserve_bytes);
+    const Program& P = o.m.prog;
+    nlohmann::ordered_json j;
+    j["stage"] = stage;
+    j["stage_layers"] = o.L;
+    j["slice_layers"] = o.k;
+    j["n_ops"] = o.u.graph.size();
+    j["budget_bytes"] = o.m.budget;
+    j["static_bytes"] = o.m.static_bytes;
+    j["stage_activation_bytes"] = to_canonical(Rat(o.p.hardware.mem_budget_bytes) - Rat(static_share_ceil(o.p, o.L)));
+    nlohmann::ordered_json lo = nlohmann::ordered_json::array(), hi = lo, integ = lo;
+    for (int v = 0; v < P.size(); ++v) {
+      lo.push_back(P.lo(v).to_double());
+      hi.push_back(P.hi(v).to_double());
+      integ.push_back(P.type(v) == VarType::Bool ? 1 : 0);
+    }
+    j["n_vars"] = P.size();
+    j["lo"] = lo;
+    j["hi"] = hi;
+    j["integer"] = integ;
+    nlohmann::ordered_json c = nlohmann::ordered_json::array();
+    for (const auto& [v, k] : P.objective().coef) c.push_back({v, k.to_double()});
+    j["objective"] = c;
+    // rows in coordinate form: row index, var, coefficient; sense -1 (<=), 0 (=), 1 (>=)
+    nlohmann::ordered_json ri = nlohmann::ordered_json::array(), vi = ri, cv = ri, sense = ri, rhs = ri;
+    int r = 0;
+    for (const Row& row : P.rows()) {
+      for (const auto& [v, k] : row.lhs.coef) {
+        ri.push_back(r);
+        vi.push_back(v);
+        cv.push_back(k.to_double());
+      }
+      sense.push_back(row.sense == Sense::Le ? -1 : (row.sense == Sense::Eq ? 0 : 1));
+      rhs.push_back((row.rhs - row.lhs.constant).to_double());
+      ++r;
+    }
+    j["n_rows"] = r;
+    j["row"] = ri;
+    j["col"] = vi;
+    j["val"] = cv;
+    j["sense"] = sense;
+    j["rhs"] = rhs;
+    nlohmann::ordered_json R = nlohmann::ordered_json::array(), S = R;
+    for (int t = 0; t < o.u.graph.size(); ++t) {
+      R.push_back(o.m.R[t]);
+      S.push_back(o.m.S[t]);
+    }
+    j["R"] = R;
+    j["S"] = S;
+    return j.dump();
+  });
+}
+
+char* lynx_plan_opt_timeline(const char* profile_json, int stage, const int* layers, int n_layers, int slice_layers,
+                             const char* reserve_bytes, const char* schedule, int* status) {
+  return guarded(status, [&](int& st) -> std::string {
+    const OptSlice o = opt_slice(profile_json, stage, layers, n_layers, slice_layers, reserve_bytes);
+    const auto in = nlohmann::json::parse(schedule);
+    PhaseSchedule s;
+    s.status = SolveStatus::Optimal;
+    if (in.contains("status") && in["status"].get<std::string>() != "optimal") s.status = SolveStatus::Feasible;
+    for (const auto& pr : in["keep"]) s.keep.emplace_back(pr[0].get<int>(), pr[1].get<int>());
+    for (const auto& pr : in["recompute"]) s.recompute.emplace_back(pr[0].get<int>(), pr[1].get<int>());
+    const int n = o.u.graph.size();
+    s.cost_us = Rat(0);
+    for (int t = 0; t < n; ++t) s.cost_us += o.m.cost[t];
+    for (auto [t, i] : s.recompute) {
+      if (t < 0 || t >= n || i < 0 || i >= t) continue;  // reported by schedule_issues
+      if (o.u.graph.is_comm(t)) s.overlapped.emplace_back(t, i);
+      else s.cost_us += o.m.cost[i];
+    }
+    const std::string issues = schedule_issues(s, o.m);
+    nlohmann::ordered_json j;
+    j["issues"] = issues;
+    j["cost_us"] = to_canonical(s.cost_us);
+    j["n_recompute"] = static_cast<int>(s.recompute.size());
+    j["n_overlapped"] = static_cast<int>(s.overlapped.size());
+    if (!issues.empty()) {
+      st = kStValidation;
+      return j.dump();
+    }
+    std::vector<bool> in_layer;
+    const StageTimeline slice_tl = timeline_from_schedule(o.p, stage, o.k, s, o.u, &in_layer);
+    StageTimeline tl = slice_tl;
+    tl.items.clear();
+    const int copies = o.L / o.k;
+    for (int r = 0; r < copies; ++r) {
+      for (size_t x = 0; x < slice_tl.items.size(); ++x) {
+        Recompute it = slice_tl.items[x];
+        it.owner_layer += r * o.k;
+        if (in_layer[x]) {
+          it.host_layer += r * o.k;
+        } else {
+          // timeline_from_opt_schedule files hosts outside the layers (embedding / head phases) as
+          // CriticalPath at layer 0, elem 0 — in the backward that is after every other layer's
+          // consumer. The executor needs the copy before its consumer: regenerate on demand at
+          // the start of the owner layer's backward instead.
+          it.host = Recompute::Host::Critical;
+          it.host_mb = it.owner_mb;
+          it.host_bwd = true;
+          it.host_layer = it.owner_layer;
+          it.host_elem = 0;
+        }
+        tl.items.push_back(it);
+      }
+    }
+    // timeline_from_opt_schedule marks an op discarded for every (microbatch, layer) once any of
+    // its instances is recomputed (aggregate retention, report_io.cpp:249-261), while OPT may have
+    // kept other instances; the reference simulator tolerates the gap (strict_deps = false), the
+    // executor frees a discarded tensor and needs its copy. An owner (microbatch, layer) missing
+    // a discarded op gets all its regenerations on demand at the start of its backward, in op
+    // order (dependencies first).
+    {
+      const int nf = o.p.model.layer.n_fwd();
+      std::vector<int> discarded;
+      for (int i = 0; i < nf; ++i)
+        if (!tl.plan.retained[i]) discarded.push_back(i);
+      std::map<std::pair<int, int>, std::set<int>> have;
+      for (const Recompute& it : tl.items) have[{it.owner_mb, it.owner_layer}].insert(it.op);
+      std::set<std::pair<int, int>> rebuild;
+      for (int mb = 0; mb < o.p.pipeline.n_microbatches; ++mb)
+        for (int l = 0; l < o.L; ++l)
+          for (int i : discarded)
+            if (!have[{mb, l}].count(i)) rebuild.insert({mb, l});
+      if (!rebuild.empty()) {
+        std::vector<Recompute> kept;
+        for (const Recompute& it : tl.items)
+          if (!rebuild.count({it.owner_mb, it.owner_layer})) kept.push_back(it);
+        for (auto [mb, l] : rebuild)
+          for (int i : discarded) {
+            Recompute it;
+            it.owner_mb = mb;
+            it.owner_layer = l;
+            it.op = i;
+            it.host = Recompute::Host::Critical;
+            it.host_mb = mb;
+            it.host_bwd = true;
+            it.host_layer = l;
+            it.host_elem = 0;
+            kept.push_back(it);
+          }
+        tl.items = std::move(kept);
+      }
+      j["completed_owners"] = static_cast<int>(rebuild.size());
+    }
+    j["timeline"] = nlohmann::ordered_json::parse(timeline_json(tl));
+    j["slice_items"] = static_cast<int>(slice_tl.items.size());
     return j.dump();
   });
 }

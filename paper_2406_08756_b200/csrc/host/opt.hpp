@@ -46,7 +46,9 @@ std::string schedule_issues(const PhaseSchedule& s, const OptModel& m);  // "" w
 UnrolledStage unroll(const StageGraph& single, int n_microbatches, int n_batch);
 UnrolledStage stage_phase_graph(const Profile& p, int stage, int stage_layers);
 int64_t static_share_ceil(const Profile& p, int stage_layers);
+// host_in_layer (optional): per emitted item, whether its host phase lies inside the stage's layers
+// (false: the embedding / head phases, emitted as CriticalPath at layer 0, elem 0).
 StageTimeline timeline_from_schedule(const Profile& p, int stage, int stage_layers, const PhaseSchedule& s,
-                                     const UnrolledStage& u);
+                                     const UnrolledStage& u, std::vector<bool>* host_in_layer = nullptr);
 
 }  // namespace lynx::host

@@ -31,6 +31,10 @@ _SIGS = {
                                                    _c.POINTER(_c.c_int)]),
     "lynx_plan_solve_heu": (_c.c_void_p, [_c.c_char_p, _c.c_int, _c.c_int, _c.c_int, _c.c_char_p, _c.c_longlong,
                                           _c.POINTER(_c.c_int)]),
+    "lynx_plan_opt_export": (_c.c_void_p, [_c.c_char_p, _c.c_int, _c.c_void_p, _c.c_int, _c.c_int, _c.c_char_p,
+                                           _c.POINTER(_c.c_int)]),
+    "lynx_plan_opt_timeline": (_c.c_void_p, [_c.c_char_p, _c.c_int, _c.c_void_p, _c.c_int, _c.c_int, _c.c_char_p,
+                                             _c.c_char_p, _c.POINTER(_c.c_int)]),
 }
 _bound = False
 
@@ -116,6 +120,22 @@ def solve_heu_text(profile: str, stage: int, stage_layers: int, policy: int = 0,
                    time_limit_ms: int = 10000) -> dict:
     return json.loads(_call("lynx_plan_solve_heu", _b(profile), stage, stage_layers, policy, _b(delta_bytes),
                             time_limit_ms)[0])
+
+
+def opt_export_text(profile: str, stage: int, layers_per_stage=None, slice_layers: int = 0,
+                    reserve_bytes: str | None = None) -> dict:
+    """The OPT program of a layer slice in matrix form (include/lynx_rt.h: lynx_plan_opt_export)."""
+    lp, n = _layers(layers_per_stage)
+    return json.loads(_call("lynx_plan_opt_export", _b(profile), stage, lp, n, slice_layers, _b(reserve_bytes))[0])
+
+
+def opt_timeline_text(profile: str, stage: int, schedule: dict, layers_per_stage=None, slice_layers: int = 0,
+                      reserve_bytes: str | None = None) -> tuple[dict, int]:
+    """Exact check of a solver's schedule + its replayable stage timeline (lynx_plan_opt_timeline)."""
+    lp, n = _layers(layers_per_stage)
+    text, st = _call("lynx_plan_opt_timeline", _b(profile), stage, lp, n, slice_layers, _b(reserve_bytes),
+                     _b(json.dumps(schedule)), ok_codes=(0, 1))
+    return json.loads(text), st
 
 
 # ------------------------------------------------ the reference's _lynx API
