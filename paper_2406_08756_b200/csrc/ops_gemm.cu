@@ -57,20 +57,32 @@ struct Args {
   uint64_t drop_seed, drop_stream;
 };
 
-// EPI_BF16_GELU_BWD on 8 outputs: dfc1 = dgelu * gelu'(fc1), fc1 read from `res`.
-LYNX_DEV BF8 gelu_bwd8(const Args& args, long long row, int col, const float* v) {
+// Auxiliary-input epilogues. The 16-byte aux chunks are loaded up front (ld_aux, read-only
+// path, all chunks of a round in flight together, overlapping the TMEM load) and combined here:
+// loaded one by one between the staging stores, the loads serialized behind the smem writes and
+// made the FC2-dX / FC2 / projection epilogues longer than their main loops.
+LYNX_DEV BF8 ld_aux(const __nv_bfloat16* p) {
+  BF8 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3])
+               : "l"(p));
+  return v;
+}
+
+// EPI_BF16_GELU_BWD on 8 outputs: dfc1 = dgelu * gelu'(fc1), fc1 = `xin` (from `res`).
+LYNX_DEV BF8 gelu_bwd8(BF8 xin, const float* v) {
   float x[8], o[8];
-  bf8_to_f(*reinterpret_cast<const BF8*>(args.res + row * args.ldc + col), x);
+  bf8_to_f(xin, x);
 #pragma unroll
   for (int j = 0; j < 8; ++j) o[j] = v[j] * gelu_grad_f(x[j]);
   return f_to_bf8(o);
 }
 
-// EPI_BF16_RESID on 8 outputs (columns col..col+7 of `row`): out = res + dropout(bf16(v)).
-LYNX_DEV BF8 resid_dropout8(const Args& args, long long row, int col, const float* v) {
+// EPI_BF16_RESID on 8 outputs (columns col..col+7 of `row`): out = res + dropout(bf16(v)), res = `rin`.
+LYNX_DEV BF8 resid_dropout8(const Args& args, long long row, int col, BF8 rin, const float* v) {
   float y[8], r[8], o[8];
   bf8_to_f(f_to_bf8(v), y);  // the projection output is rounded to bf16 first, as in the two-kernel path
-  bf8_to_f(*reinterpret_cast<const BF8*>(args.res + row * args.ldc + col), r);
+  bf8_to_f(rin, r);
   const uint32_t keep =
       args.drop_p > 0.f ? keep_bits8(args.drop_seed, args.drop_stream, (row * args.ldc + col) / 8, args.drop_thr) : 0xFFu;
 #pragma unroll
@@ -168,10 +180,13 @@ LYNX_DEV void epilogue_row(const Args& args, uint32_t t_row, long long row, int 
       }
       BF8* o = reinterpret_cast<BF8*>(reinterpret_cast<__nv_bfloat16*>(args.c) + row * args.ldc + n0 + c);
       if (args.epi == EPI_BF16_RESID || args.epi == EPI_BF16_GELU_BWD) {
+        BF8 aux[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) aux[i] = ld_aux(args.res + row * args.ldc + n0 + c + 8 * i);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          o[i] = args.epi == EPI_BF16_RESID ? resid_dropout8(args, row, n0 + c + 8 * i, v + 8 * i)
-                                            : gelu_bwd8(args, row, n0 + c + 8 * i, v + 8 * i);
+          o[i] = args.epi == EPI_BF16_RESID ? resid_dropout8(args, row, n0 + c + 8 * i, aux[i], v + 8 * i)
+                                            : gelu_bwd8(aux[i], v + 8 * i);
         continue;
       }
 #pragma unroll
@@ -207,15 +222,85 @@ LYNX_DEV void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;
 LYNX_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 LYNX_DEV void bulk_wait_all_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
+// EPI_BF16_RESID / EPI_BF16_GELU_BWD: the auxiliary tile (residual, or the FC1 output) comes in by
+// TMA into the same 4 KB staging buffer the output leaves from (tm_c2 maps `res` with C's box):
+// each lane reads its row, writes the result in place, one lane TMA-stores the box, then loads
+// the next round's aux box into the other buffer. Full-line loads: the per-thread 16-byte row
+// reads they replace made these epilogues longer than the main loop (FC2-dX with the GeLU
+// backward: 10.5 vs 6.7 ms per GPT-7B launch). abar: this warp's two buffer barriers, aphase:
+// their parities (bit b for buffer b).
 template <int kCols>
-LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, const CUtensorMap* tm_c2, uint32_t t_row,
-                                int row0, int n0, int lane, uint8_t* staging, int& sbuf) {
-  const bool gelu = args.epi == EPI_BF16_GELU;
+LYNX_DEV void epilogue_aux_tma(const Args& args, const CUtensorMap* tm_c, const CUtensorMap* tm_aux, uint32_t t_row,
+                               int row0, int n0, int lane, uint8_t* staging, int& sbuf, uint64_t* abar,
+                               uint32_t& aphase) {
+  const bool resid = args.epi == EPI_BF16_RESID;
+  if (lane == 0) {  // round 0: the store issued from this buffer two rounds ago has read it
+    bulk_wait_read1();
+    mbar_arrive_expect_tx(&abar[sbuf], 4096);
+    tma_load_2d(tm_aux, &abar[sbuf], staging + sbuf * 4096, n0, row0, kEvictFirst);
+  }
 #pragma unroll 1
   for (int c = 0; c < kCols; c += 64) {
     uint32_t r[64];
     tmem_ld32(t_row + c, r);
     tmem_ld32(t_row + c + 32, r + 32);
+    uint8_t* st = staging + sbuf * 4096;
+    mbar_wait(&abar[sbuf], (aphase >> sbuf) & 1u);
+    aphase ^= 1u << sbuf;
+    tmem_ld_wait();
+    float v[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+    if (args.bias) {
+      const BF8* bp = reinterpret_cast<const BF8*>(args.bias + n0 + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float b[8];
+        bf8_to_f(bp[i], b);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[8 * i + j] += b[j];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      BF8* q = reinterpret_cast<BF8*>(st + lane * 128 + ((i ^ (lane & 7)) << 4));
+      *q = resid ? resid_dropout8(args, row0 + lane, n0 + c + 8 * i, *q, v + 8 * i) : gelu_bwd8(*q, v + 8 * i);
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tm_c, st, n0 + c, row0);
+      bulk_commit();
+      if (c + 64 < kCols) {  // prefetch the next round's aux box into the other buffer
+        bulk_wait_read1();   // ... whose store (the previous round) has been read
+        mbar_arrive_expect_tx(&abar[sbuf ^ 1], 4096);
+        tma_load_2d(tm_aux, &abar[sbuf ^ 1], staging + (sbuf ^ 1) * 4096, n0 + c + 64, row0, kEvictFirst);
+      }
+    }
+    sbuf ^= 1;
+  }
+}
+
+template <int kCols>
+LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, const CUtensorMap* tm_c2, uint32_t t_row,
+                                int row0, int n0, int lane, uint8_t* staging, int& sbuf) {
+  const bool gelu = args.epi == EPI_BF16_GELU;
+  const bool aux_in = args.epi == EPI_BF16_RESID || args.epi == EPI_BF16_GELU_BWD;
+#pragma unroll 1
+  for (int c = 0; c < kCols; c += 64) {
+    uint32_t r[64];
+    tmem_ld32(t_row + c, r);
+    tmem_ld32(t_row + c + 32, r + 32);
+    BF8 aux[8];
+    if (aux_in) {  // all 8 chunks in flight while the TMEM load completes
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        // auxiliary inputs are read only in range (the TMA store clips partial edge tiles)
+        const bool in = row0 + lane < args.M && n0 + c + 8 * i < args.N;
+        aux[i] = in ? ld_aux(args.res + static_cast<long long>(row0 + lane) * args.ldc + n0 + c + 8 * i)
+                    : BF8{{0u, 0u, 0u, 0u}};
+      }
+    }
     tmem_ld_wait();
     float v[64];
 #pragma unroll
@@ -257,12 +342,10 @@ LYNX_DEV void epilogue_tile_tma(const Args& args, const CUtensorMap* tm_c, const
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      // auxiliary inputs are read only in range (the TMA store clips partial edge tiles)
-      const bool in = row0 + lane < args.M && n0 + c + 8 * i < args.N;
       *reinterpret_cast<BF8*>(st + lane * 128 + ((i ^ (lane & 7)) << 4)) =
-          in && args.epi == EPI_BF16_RESID      ? resid_dropout8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
-          : in && args.epi == EPI_BF16_GELU_BWD ? gelu_bwd8(args, row0 + lane, n0 + c + 8 * i, v + 8 * i)
-                                                : f_to_bf8(v + 8 * i);
+          args.epi == EPI_BF16_RESID      ? resid_dropout8(args, row0 + lane, n0 + c + 8 * i, aux[i], v + 8 * i)
+          : args.epi == EPI_BF16_GELU_BWD ? gelu_bwd8(aux[i], v + 8 * i)
+                                          : f_to_bf8(v + 8 * i);
     }
     fence_proxy_async();
     __syncwarp();
@@ -287,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tmem_full = empty + kStages;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* aux_bar = tmem_empty + 3;  // 4 epilogue warps x 2 aux-load barriers (after the TMEM slot)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -306,6 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 4);  // one elected lane per epilogue warp
     }
+    for (int b = 0; b < 8; ++b) mbar_init(&aux_bar[b], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_base_slot);
@@ -405,6 +490,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU || args.epi == EPI_BF16_RESID ||
                           args.epi == EPI_BF16_GELU_BWD) &&
                          args.tma_store;
+    const bool aux_tma = tma_out && args.tma_store == 2;  // aux input by TMA (tm_c2 maps `res`)
+    uint32_t aphase = 0;
     uint8_t* my_staging = staging + ew * 8192;
     int sbuf = 0;
     int acc = 0;
@@ -418,7 +505,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
       if (tma_out)
-        epilogue_tile_tma<BN>(args, &tm_c, &tm_c2, t_row, mt * BM + ew * 32, n0, lane, my_staging, sbuf);
+        if (aux_tma)
+          epilogue_aux_tma<BN>(args, &tm_c, &tm_c2, t_row, mt * BM + ew * 32, n0, lane, my_staging, sbuf,
+                               aux_bar + 2 * ew, aphase);
+        else
+          epilogue_tile_tma<BN>(args, &tm_c, &tm_c2, t_row, mt * BM + ew * 32, n0, lane, my_staging, sbuf);
       else
         epilogue_row<BN>(args, t_row, row, n0);
       tc_fence_before();
@@ -519,6 +610,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* tmem_full = empty + kStages;
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* aux_bar = tmem_empty + 3;  // 4 epilogue warps x 2 aux-load barriers (after the TMEM slot)
 
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
@@ -539,6 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 8);  // 4 epilogue warps x 2 CTAs
     }
+    for (int b = 0; b < 8; ++b) mbar_init(&aux_bar[b], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -659,6 +752,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const bool tma_out = (args.epi == EPI_BF16 || args.epi == EPI_BF16_GELU || args.epi == EPI_BF16_RESID ||
                           args.epi == EPI_BF16_GELU_BWD) &&
                          args.tma_store;
+    const bool aux_tma = tma_out && args.tma_store == 2;  // aux input by TMA (tm_c2 maps `res`)
+    uint32_t aphase = 0;
     uint8_t* my_staging = staging + ew * 8192;
     int sbuf = 0;
     int acc = 0;
@@ -674,7 +769,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int row0 = mt * kTileM + rank * kRowsCTA + sub * kHalf + ew * 32;
         const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + (acc * kSub + sub) * kTileN;
         if (tma_out)
-          epilogue_tile_tma<kTileN>(args, &tm_c, &tm_c2, t_row, row0, n0, lane, my_staging, sbuf);
+          if (aux_tma)
+            epilogue_aux_tma<kTileN>(args, &tm_c, &tm_c2, t_row, row0, n0, lane, my_staging, sbuf, aux_bar + 2 * ew,
+                                     aphase);
+          else
+            epilogue_tile_tma<kTileN>(args, &tm_c, &tm_c2, t_row, row0, n0, lane, my_staging, sbuf);
         else
           epilogue_row<kTileN>(args, t_row, row0 + lane, n0);
       }
@@ -745,6 +844,15 @@ uint64_t cache_hint(int operand) {
 }
 
 // bf16 epilogue via TMA stores (default on; LYNX_GEMM_TMA_STORE=0 selects per-thread stores).
+// LYNX_GEMM_AUX_TMA=0: the residual / FC1 input of the aux epilogues read per thread instead of by TMA.
+bool aux_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("LYNX_GEMM_AUX_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool tma_store_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("LYNX_GEMM_TMA_STORE");
@@ -790,7 +898,10 @@ int launch(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
       g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID || g.epi == EPI_BF16_GELU_BWD;
   bool tma_out = bf16_out && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
   if (tma_out && g.epi == EPI_BF16_GELU) tma_out = make_map(&mc2, g.c2, g.N, g.M, g.ldc, 64, 32);
-  const Args args = make_args(g, tma_out);
+  const bool aux_tma = tma_out && (g.epi == EPI_BF16_RESID || g.epi == EPI_BF16_GELU_BWD) && aux_tma_enabled() &&
+                       make_map(&mc2, g.res, g.N, g.M, g.ldc, 64, 32);
+  Args args = make_args(g, tma_out);
+  if (aux_tma) args.tma_store = 2;
   const int tiles = (g.M / BM) * (g.N / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
@@ -817,7 +928,10 @@ int launch_pair(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
       g.epi == EPI_BF16 || g.epi == EPI_BF16_GELU || g.epi == EPI_BF16_RESID || g.epi == EPI_BF16_GELU_BWD;
   bool tma_out = bf16_out && tma_store_enabled() && make_map(&mc, g.c, g.N, g.M, g.ldc, 64, 32);
   if (tma_out && g.epi == EPI_BF16_GELU) tma_out = make_map(&mc2, g.c2, g.N, g.M, g.ldc, 64, 32);
-  const Args args = make_args(g, tma_out);
+  const bool aux_tma = tma_out && (g.epi == EPI_BF16_RESID || g.epi == EPI_BF16_GELU_BWD) && aux_tma_enabled() &&
+                       make_map(&mc2, g.res, g.N, g.M, g.ldc, 64, 32);
+  Args args = make_args(g, tma_out);
+  if (aux_tma) args.tma_store = 2;
   const int tiles = ((g.M + C::kTileM - 1) / C::kTileM) * ((g.N + pair::kTileN - 1) / pair::kTileN);
   int clusters = num_sms() / 2;
   if (max_ctas > 0) clusters = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
@@ -871,7 +985,10 @@ int gemm_run(const GemmDesc& g, cudaStream_t stream, int max_ctas) {
   // where it measures 6-11% faster under the power cap (less L2->SM traffic).
   if ((mode == 2 || (mode == -1 && g.K >= 8192)) && tiles_of(pair::Cfg<2>::kTileM) >= 64)
     return dispatch_pair<2>(g, stream, max_ctas);
-  const bool want_pair = mode == 1 || mode == 2 || (mode == -1 && !g.a_mn);
+  // MN-major A with a short reduction (the LM head's weight gradient per 4096-token chunk):
+  // the pair kernel measures 10% faster than the single-CTA one under the power cap
+  // (tools/gemm_sustained.py headdw: 1.32 vs 1.46 ms).
+  const bool want_pair = mode == 1 || mode == 2 || mode == -1;
   if (want_pair && tiles_of(pair::Cfg<1>::kTileM) >= 32) return dispatch_pair<1>(g, stream, max_ctas);
   const bool wide = g.N % 256 == 0;
 #define LYNX_GEMM_CASE(AMN, BMN)                                                             \

@@ -1,6 +1,8 @@
 #include "runtime/executor.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <map>
 #include <cmath>
 #include <cstring>
 #include <sstream>
@@ -45,7 +47,22 @@ void Executor::ck(cudaError_t e, const char* what) {
 }
 void Executor::ck_op(int status, const char* what) {
   if (status != kOk) throw RtError(std::string(what) + ": " + last_error(), status);
+  if (opt_.probe_ops && probe_stream_) {
+    cudaEvent_t e = ev();
+    ck(cudaEventRecord(e, probe_stream_), "event");
+    op_events_.emplace_back(what, probe_stream_, e);
+  }
 }
+
+namespace {
+// Sets the stream exec.probe_ops attributes operator launches to, for one scope.
+struct ProbeStream {
+  cudaStream_t& slot;
+  cudaStream_t saved;
+  ProbeStream(cudaStream_t& sl, cudaStream_t s) : slot(sl), saved(sl) { slot = s; }
+  ~ProbeStream() { slot = saved; }
+};
+}  // namespace
 void Executor::nccl(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw RtError(std::string(what) + ": " + ncclGetErrorString(r), kCudaError);
 }
@@ -136,6 +153,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.dry_run = ex.value("dry_run", false);
   opt_.standalone = ex.value("standalone_stage", false);
   opt_.probe_fc1 = ex.value("probe_fc1", false);
+  opt_.probe_ops = ex.value("probe_ops", false);
   cfg_.head_chunk = static_cast<int>(std::min<long long>(ex.value("head_chunk", 4096), cfg_.tokens()));
   if (cfg_.hidden % cfg_.heads || cfg_.heads % cfg_.tp || (cfg_.hidden / cfg_.tp) % 128)
     throw RtError("hidden must split into heads and TP ranks in 128-column tiles", kValidation);
@@ -314,7 +332,11 @@ void Executor::release_all() {
 void* Executor::alloc(size_t bytes, cudaStream_t s) {
   if (opt_.dry_run) return reinterpret_cast<void*>(0x1000);
   void* p = nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
   const cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool_, s);
+  const double hms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+  rep_.alloc_host_ms += hms;
+  rep_.alloc_host_max_ms = std::max(rep_.alloc_host_max_ms, hms);
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();
     uint64_t used = 0, reserved = 0;
@@ -452,6 +474,7 @@ void Executor::collect_spans() {
 
 // ============================================================ forward operators
 void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
+  const ProbeStream probe(probe_stream_, s);
   const Op op = op_of_[pos];
   Slot& out = slot(mb, l, pos);
   if (trace_slots())
@@ -475,7 +498,7 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
     if (opt_.dry_run) return;
     GemmDesc g{a, lda, false, b, ldb, false, c, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
                bias, EPI_BF16};
-    ck_op(gemm_run(g, s), "gemm");
+    ck_op(gemm_run(g, s), op_name(op));
   };
   auto pos_of = [&](Op o) {
     for (int i = 0; i < nf_; ++i)
@@ -718,6 +741,7 @@ void Executor::comm_element(int mb, bool bwd, int l, const host::Element& e) {
 
 // ============================================================ backward operators
 void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
+  const ProbeStream probe(probe_stream_, s);
   const Op op = op_of_[pos];
   const long long T = cfg_.tokens();
   const int h = cfg_.hidden, hp = cfg_.hp();
@@ -731,7 +755,7 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
     if (opt_.dry_run) return;
     GemmDesc g{a, lda, amn, b, ldb, bmn, c, ldc, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), nullptr,
                epi};
-    ck_op(gemm_run(g, s), "gemm");
+    ck_op(gemm_run(g, s), amn && bmn ? "bwd dW gemm" : "bwd dX gemm");  // dW: both operands MN-major
   };
   auto pos_of = [&](Op o) {
     for (int i = 0; i < nf_; ++i)
@@ -1038,6 +1062,7 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   program_.clear();
   rep_ = StepReport{};
   probes_.clear();
+  op_events_.clear();
   bwd_passes_ = 0;
   const long long T = cfg_.tokens();
   const size_t ntok = static_cast<size_t>(cfg_.n_micro) * T;
@@ -1047,7 +1072,15 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
     return;
   }
   const long long launches0 = launch_count();
+  const auto host0 = std::chrono::steady_clock::now();
   ck(cudaEventRecord(t0_, main_), "event");
+  const ProbeStream probe(probe_stream_, main_);
+  if (opt_.probe_ops) {  // the side stream's first operator is timed from here too
+    cudaEvent_t e = ev();
+    ck(cudaEventRecord(e, side_), "event");
+    op_events_.emplace_back("(start)", side_, e);
+    op_events_.emplace_back("(start)", main_, t0_);
+  }
   if (cfg_.first() && tokens) {
     std::memcpy(h_tokens_, tokens, ntok * 4);
     ck(cudaMemcpyAsync(d_tokens_, h_tokens_, ntok * 4, cudaMemcpyHostToDevice, main_), "h2d tokens");
@@ -1087,6 +1120,7 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
         "adam");
   if (cfg_.last()) ck(cudaMemcpyAsync(h_loss_, d_loss_, ntok * 4, cudaMemcpyDeviceToHost, main_), "d2h loss");
   ck(cudaEventRecord(t1_, main_), "event");
+  rep_.host_issue_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host0).count();
   rep_.kernel_launches = launch_count() - launches0;
   ck(cudaEventSynchronize(t1_), "step");
   float ms = 0.f;
@@ -1100,6 +1134,26 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
     ++rep_.probe_launches;
   }
   probes_.clear();
+  if (opt_.probe_ops) {
+    std::map<std::string, std::pair<long long, double>> acc;
+    std::map<cudaStream_t, cudaEvent_t> prev;
+    op_stream_ms_[0] = op_stream_ms_[1] = 0;
+    for (const auto& [name, st, e] : op_events_) {
+      auto it = prev.find(st);
+      if (it != prev.end()) {
+        float d = 0.f;
+        ck(cudaEventElapsedTime(&d, it->second, e), "probe");
+        auto& a = acc[std::string(st == side_ ? "side: " : "") + name];
+        ++a.first;
+        a.second += d;
+        op_stream_ms_[st == side_ ? 1 : 0] += d;
+      }
+      prev[st] = e;
+    }
+    op_times_.clear();
+    for (const auto& [k, v] : acc) op_times_.emplace_back(k, v.first, v.second);
+    op_events_.clear();
+  }
   if (cfg_.last()) {
     double s = 0;
     for (size_t i = 0; i < ntok; ++i) s += h_loss_[i];
@@ -1109,6 +1163,9 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   size_t hw = 0;
   cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &hw);
   rep_.pool_high_water = hw;
+  uint64_t rsv = 0;
+  cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrReservedMemCurrent, &rsv);
+  rep_.pool_reserved = rsv;
 }
 
 // ============================================================ reports
@@ -1133,6 +1190,17 @@ std::string Executor::report_json() const {
   j["pool_high_water_bytes"] = rep_.pool_high_water;
   j["probe_fc1_launches"] = rep_.probe_launches;
   j["probe_fc1_ms"] = rep_.probe_ms;
+  j["alloc_host_ms"] = rep_.alloc_host_ms;
+  j["alloc_host_max_ms"] = rep_.alloc_host_max_ms;
+  j["host_issue_ms"] = rep_.host_issue_ms;
+  j["pool_reserved_bytes"] = rep_.pool_reserved;
+  if (opt_.probe_ops) {
+    Json po = Json::object();
+    for (const auto& [k, n, ms] : op_times_) po[k] = {n, ms};
+    j["probe_ops"] = po;
+    j["probe_ops_main_ms"] = op_stream_ms_[0];
+    j["probe_ops_side_ms"] = op_stream_ms_[1];
+  }
   j["static_bytes_allocated"] = static_cast<long long>(ps_.count()) * 16;
   j["params"] = ps_.count();
   j["layers"] = cfg_.layers;

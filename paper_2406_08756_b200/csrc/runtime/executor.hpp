@@ -43,6 +43,8 @@ struct ExecOptions {
   bool elide_recompute = false; // timing-only: skip recompute launches (exposed-recompute cross-check)
   bool dry_run = false;         // build the launch program only (no device)
   bool probe_fc1 = false;       // CUDA events around every FC1 forward GEMM launch (roofline line)
+  bool probe_ops = false;       // one CUDA event after every operator launch on its stream: in-step
+                                // time per operator name, gaps included (report "probe_ops")
   bool standalone = false;      // time one pipeline stage alone on one GPU: receives read synthetic
                                 // activations / gradients, sends are skipped (measured partitioning)
 };
@@ -66,6 +68,9 @@ struct StepReport {
   size_t pool_high_water = 0;
   long long probe_launches = 0;  // exec.probe_fc1: FC1 forward GEMM launches timed in this step
   double probe_ms = 0;           // ... and their summed CUDA-event durations
+  double alloc_host_ms = 0, alloc_host_max_ms = 0;  // host time inside pool allocations (stall diagnosis)
+  double host_issue_ms = 0;                         // host time to issue the step (before the final sync)
+  size_t pool_reserved = 0;
 };
 
 struct CommOp {  // launch-program record (dry runs and tests)
@@ -181,6 +186,10 @@ class Executor {
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   __nv_bfloat16 *syn_act_ = nullptr, *syn_grad_ = nullptr;  // standalone stage: stand-ins for PP receives
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probes_;  // exec.probe_fc1 event pairs of this step
+  cudaStream_t probe_stream_ = nullptr;  // exec.probe_ops: the stream the current operator launches on
+  std::vector<std::tuple<const char*, cudaStream_t, cudaEvent_t>> op_events_;  // exec.probe_ops, this step
+  std::vector<std::tuple<std::string, long long, double>> op_times_;           // name, launches, ms (last step)
+  double op_stream_ms_[2] = {0, 0};                                            // main, side: sum of op times
   float* head_gw32_ = nullptr;  // last stage: LM-head weight gradient, fp32 across chunks / microbatches
   float* emb_gw32_ = nullptr;   // first stage: wte | wpe gradients, fp32 (scatter-add with atomics)
   bool head_first_ = true;

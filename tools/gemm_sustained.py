@@ -22,11 +22,24 @@ def main():
         a, b, kw, fl = torch.randn(T, 4 * h), torch.randn(h, 4 * h), {}, 2.0 * T * 4 * h * h
     elif shape == "dx":
         a, b, kw, fl = torch.randn(T, 4 * h), torch.randn(4 * h, h), {"b_mn": True}, 2.0 * T * 4 * h * h
+    elif shape in ("dgelu", "dgelu_plain"):  # FC2 dX with (or without) the fused GeLU backward
+        a, b, kw, fl = torch.randn(T, h), torch.randn(h, 4 * h), {"b_mn": True}, 2.0 * T * 4 * h * h
+    elif shape in ("fc2res", "fc2_plain"):  # FC2 forward with (or without) the fused bias-dropout-residual
+        a, b, kw, fl = torch.randn(T, 4 * h), torch.randn(h, 4 * h), {}, 2.0 * T * 4 * h * h
+    elif shape == "headdw":  # LM-head weight gradient per 4096-token chunk: [V, h] += logits^T X
+        V, C = 50304, 4096
+        a, b, kw, fl = torch.randn(C, V), torch.randn(C, h), {"a_mn": True, "b_mn": True}, 2.0 * V * h * C
+    elif shape == "headfwd":  # LM-head logits per chunk: [C, V] = X W^T
+        V, C = 50304, 4096
+        a, b, kw, fl = torch.randn(C, h), torch.randn(V, h), {}, 2.0 * V * h * C
     else:
         a, b, kw, fl = torch.randn(T, 4 * h), torch.randn(T, h), {"a_mn": True, "b_mn": True}, 2.0 * T * 4 * h * h
     a, b = a.cuda().bfloat16(), b.cuda().bfloat16()
     if shape == "dw":
         out = torch.zeros(4 * h, h, device="cuda")
+        kw["epi"] = ops.EPI_F32
+    elif shape == "headdw":
+        out = torch.zeros(50304, h, device="cuda")
         kw["epi"] = ops.EPI_F32
     else:
         out = None
@@ -38,6 +51,16 @@ def main():
 
         def run():
             torch.matmul(A, B)
+    elif shape == "dgelu":
+        x = torch.randn(T, 4 * h, device="cuda").bfloat16()
+
+        def run():
+            ops.gemm_gelu_bwd(a, b, x, b_mn=True)
+    elif shape == "fc2res":
+        res = torch.randn(T, h, device="cuda").bfloat16()
+
+        def run():
+            ops.gemm_residual(a, b, res, p=0.1, seed=1, stream_id=2)
     else:
         def run():
             ops.gemm(a, b, out=out, **kw)
