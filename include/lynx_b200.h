@@ -92,6 +92,11 @@ int lynx_op_dropout_bwd(const void* dout, void* dy, long long rows, int width, f
 size_t lynx_op_column_sum_workspace(long long rows, int width);
 /* acc[col] += sum_rows x[row][col] (bias gradients), deterministic. */
 int lynx_op_column_sum_acc(const void* x, float* acc, float* workspace, long long rows, int width, void* stream);
+/* dy = dropout_bwd(dout) and acc[col] += sum_rows dy[row][col] in one pass (the residual branch's
+ * gradient and its bias gradient); bit-identical to lynx_op_dropout_bwd + lynx_op_column_sum_acc.
+ * workspace: lynx_op_column_sum_workspace(rows, width) bytes. */
+int lynx_op_dropout_bwd_colsum(const void* dout, void* dy, float* acc, float* workspace, long long rows, int width,
+                               float p, unsigned long long seed, unsigned long long stream_id, void* stream);
 
 /* GPT-2 tanh GeLU on n bf16 elements (n % 8 == 0). */
 int lynx_op_gelu_fwd(const void* x, void* y, long long n, void* stream);

@@ -35,6 +35,7 @@ _SIGNATURES: dict[str, tuple] = {
     "lynx_op_dropout_bwd": (_i, [_vp, _vp, _ll, _i, _f, _ull, _ull, _vp]),
     "lynx_op_column_sum_workspace": (_sz, [_ll, _i]),
     "lynx_op_column_sum_acc": (_i, [_vp, _vp, _vp, _ll, _i, _vp]),
+    "lynx_op_dropout_bwd_colsum": (_i, [_vp, _vp, _vp, _vp, _ll, _i, _f, _ull, _ull, _vp]),
     "lynx_op_gelu_fwd": (_i, [_vp, _vp, _ll, _vp]),
     "lynx_op_gelu_bwd": (_i, [_vp, _vp, _vp, _ll, _vp]),
     "lynx_op_attention_fwd": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp]),

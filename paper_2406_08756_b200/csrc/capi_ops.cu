@@ -112,6 +112,11 @@ int lynx_op_column_sum_acc(const void* x, float* acc, float* workspace, long lon
   return column_sum_acc(CBF(x), acc, 0, workspace, rows, width, STREAM(stream));
 }
 
+int lynx_op_dropout_bwd_colsum(const void* dout, void* dy, float* acc, float* workspace, long long rows, int width,
+                               float p, unsigned long long seed, unsigned long long stream_id, void* stream) {
+  return dropout_bwd_colsum(CBF(dout), BF(dy), acc, 0, workspace, rows, width, p, seed, stream_id, STREAM(stream));
+}
+
 int lynx_op_gelu_fwd(const void* x, void* y, long long n, void* stream) {
   return gelu_fwd(CBF(x), BF(y), n, STREAM(stream));
 }

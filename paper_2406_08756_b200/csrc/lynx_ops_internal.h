@@ -82,6 +82,10 @@ int dropout_bwd(const __nv_bfloat16* dout, __nv_bfloat16* dy, long long rows, in
                 uint64_t stream_id, cudaStream_t s);
 int column_sum_acc(const __nv_bfloat16* x, void* acc, int acc_bf16, float* workspace, long long rows, int width,
                    cudaStream_t s);
+// dy = dropout_bwd(dout) and acc += column sums of dy (bias gradient) in one pass; dy and acc are
+// bit-identical to dropout_bwd followed by column_sum_acc.
+int dropout_bwd_colsum(const __nv_bfloat16* dout, __nv_bfloat16* dy, void* acc, int acc_bf16, float* workspace,
+                       long long rows, int width, float p, uint64_t seed, uint64_t stream_id, cudaStream_t s);
 // dst(bf16) += src(fp32), elementwise (n % 8 == 0 not required).
 int add_f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s);
 size_t column_sum_workspace(long long rows, int width);

@@ -419,11 +419,48 @@ __global__ void __launch_bounds__(kNT) column_partial_kernel(const __nv_bfloat16
   const long long r1 = min(rows, r0 + per);
   for (int c = threadIdx.x; c < nchunk; c += kNT) {
     float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4  // independent row loads in flight (the sums stay in row order)
     for (long long row = r0; row < r1; ++row) {
       float v[8];
       bf8_to_f(reinterpret_cast<const BF8*>(x + row * width)[c], v);
 #pragma unroll
       for (int j = 0; j < 8; ++j) s[j] += v[j];
+    }
+    float* w = ws + static_cast<long long>(blockIdx.x) * width + c * 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w[j] = s[j];
+  }
+}
+
+// dy = dropout_bwd(dout) (the Philox mask of dropout_bwd_kernel, element vector index
+// row * width / 8 + c) and the column partial sums of the bf16 dy in one pass: the bias gradient
+// of the projection / FC2 branch. Same row partition and summation order as column_partial_kernel,
+// so the bias gradient is bit-identical to the two-kernel path.
+__global__ void __launch_bounds__(kNT) dropout_bwd_colsum_kernel(const __nv_bfloat16* __restrict__ dout,
+                                                                 __nv_bfloat16* __restrict__ dy, float* __restrict__ ws,
+                                                                 long long rows, int width, float p, uint64_t seed,
+                                                                 uint64_t stream) {
+  const uint32_t thr = drop_threshold(p);
+  const float scale = p > 0.f ? 1.f / (1.f - p) : 1.f;
+  const int nchunk = width / 8;
+  const long long per = (rows + gridDim.x - 1) / gridDim.x;
+  const long long r0 = blockIdx.x * per;
+  const long long r1 = min(rows, r0 + per);
+  for (int c = threadIdx.x; c < nchunk; c += kNT) {
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+    for (long long row = r0; row < r1; ++row) {
+      float d[8], o[8];
+      const long long vec = row * nchunk + c;
+      bf8_to_f(reinterpret_cast<const BF8*>(dout)[vec], d);
+      const uint32_t keep = p > 0.f ? keep_bits8(seed, stream, vec, thr) : 0xFFu;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = ((keep >> j) & 1u) ? d[j] * scale : 0.f;
+      const BF8 ob = f_to_bf8(o);
+      reinterpret_cast<BF8*>(dy)[vec] = ob;
+      bf8_to_f(ob, o);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s[j] += o[j];
     }
     float* w = ws + static_cast<long long>(blockIdx.x) * width + c * 8;
 #pragma unroll
@@ -495,6 +532,17 @@ int column_sum_acc(const __nv_bfloat16* x, void* acc, int acc_bf16, float* works
   column_partial_kernel<<<nb, kNT, 0, s>>>(x, workspace, rows, width);
   reduce_partials_kernel<<<(width + 31) / 32, 256, 0, s>>>(workspace, acc, nullptr, nb, width, 1, acc_bf16);
   return check_launch("column_sum_acc", 2);
+}
+
+int dropout_bwd_colsum(const __nv_bfloat16* dout, __nv_bfloat16* dy, void* acc, int acc_bf16, float* workspace,
+                       long long rows, int width, float p, uint64_t seed, uint64_t stream_id, cudaStream_t s) {
+  if (width % 8) return set_error("dropout_bwd_colsum: width must be a multiple of 8", kValidation);
+  if (p < 0.f || p >= 1.f) return set_error("dropout: p must be in [0, 1)", kValidation);
+  if (rows == 0) return kOk;
+  const int nb = part_blocks(rows);
+  dropout_bwd_colsum_kernel<<<nb, kNT, 0, s>>>(dout, dy, workspace, rows, width, p, seed, stream_id);
+  reduce_partials_kernel<<<(width + 31) / 32, 256, 0, s>>>(workspace, acc, nullptr, nb, width, 1, acc_bf16);
+  return check_launch("dropout_bwd_colsum", 2);
 }
 
 }  // namespace lynx

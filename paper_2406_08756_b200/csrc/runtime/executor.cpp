@@ -100,6 +100,7 @@ void Executor::init_device() {
   ck(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &zero), "mempool attr");
   ps_.allocate_and_init(cfg_, main_);
   alloc_persistent();
+  if (opt_.reserve_pool) reserve_pool();
   ck(cudaEventCreate(&t0_), "event");
   ck(cudaEventCreate(&t1_), "event");
   for (int i = 0; i < cfg_.n_micro; ++i) {
@@ -110,6 +111,33 @@ void Executor::init_device() {
     grad_sent_.push_back(b);
   }
   ck(cudaStreamSynchronize(main_), "init");
+}
+
+// Map the activation pool's physical memory once, up front: all free HBM but a small reserve for
+// the runtime and library workspaces, allocated from the pool and freed back into it (the release
+// threshold keeps it mapped). Growing the pool lazily inside the steps, with HBM nearly full,
+// made single cudaMallocFromPoolAsync calls block the host for up to 2.6 s while the driver
+// mapped memory (seen as 3-10 s steps with `alloc_host_ms` in the report); afterwards the pool
+// only splits and reuses what it holds.
+void Executor::reserve_pool() {
+  size_t free_b = 0, total_b = 0;
+  ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
+  const size_t keep = size_t{2} << 30, step = size_t{1} << 30;
+  if (free_b <= keep + step) return;
+  size_t want = (free_b - keep) / step * step;
+  void* p = nullptr;
+  while (want >= step) {
+    if (cudaMallocFromPoolAsync(&p, want, pool_, main_) == cudaSuccess) break;
+    cudaGetLastError();
+    p = nullptr;
+    want -= step;
+  }
+  if (!p) return;
+  ck(cudaFreeAsync(p, main_), "pool reserve");
+  ck(cudaStreamSynchronize(main_), "pool reserve");
+  pool_reserved_init_ = want;
+  uint64_t zero = 0;
+  ck(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &zero), "mempool attr");
 }
 
 void Executor::parse_config(const std::string& text) {
@@ -154,6 +182,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.standalone = ex.value("standalone_stage", false);
   opt_.probe_fc1 = ex.value("probe_fc1", false);
   opt_.probe_ops = ex.value("probe_ops", false);
+  opt_.reserve_pool = ex.value("reserve_pool", true);
   cfg_.head_chunk = static_cast<int>(std::min<long long>(ex.value("head_chunk", 4096), cfg_.tokens()));
   if (cfg_.hidden % cfg_.heads || cfg_.heads % cfg_.tp || (cfg_.hidden / cfg_.tp) % 128)
     throw RtError("hidden must split into heads and TP ranks in 128-column tiles", kValidation);
@@ -773,11 +802,10 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
       void* gelu = need(mb, l, pos_of(Op::GELU), s);
       void* fc1 = need(mb, l, pos_of(Op::FC1), s);
       void* y2 = need(mb, l, pos_of(Op::LN2), s);
-      if (!opt_.dry_run)
-        ck_op(dropout_bwd(static_cast<const __nv_bfloat16*>(G.dy), sc.t_h, T, h, p, seed,
-                          drop_stream(l, mb, tp ? Op::AR2 : Op::FC2_RES), s),
-              "dropout_bwd");
-      colsum(sc.t_h, P.g_b_fc2, h);
+      if (!opt_.dry_run)  // the FC2 branch gradient and its bias gradient in one pass
+        ck_op(dropout_bwd_colsum(static_cast<const __nv_bfloat16*>(G.dy), sc.t_h, P.g_b_fc2, 1, sc.ws, T, h, p, seed,
+                                 drop_stream(l, mb, tp ? Op::AR2 : Op::FC2_RES), s),
+              "dropout_bwd + bias grad");
       gemm(sc.t_h, h, true, gelu, 4 * hp, true, P.g_w_fc2, 4 * hp, h, 4 * hp, T, dw_epi_);      // dW_fc2 += d^T gelu
       if (!opt_.dry_run) {  // dfc1 = (d W_fc2) * gelu'(fc1): the GeLU backward rides in the dX GEMM epilogue
         GemmDesc g{sc.t_h, h, false, P.w_fc2, 4 * hp, true, sc.t_wide, 4 * hp, static_cast<int>(T), 4 * hp, h,
@@ -805,13 +833,12 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
                             P.ln2_g, mean2, mean2 + T, static_cast<const __nv_bfloat16*>(G.dy),
                             static_cast<__nv_bfloat16*>(G.dres), P.g_ln2_g, P.g_ln2_b, 1, sc.ws, static_cast<int>(T), h, s),
               "ln2_bwd");
-        ck_op(dropout_bwd(static_cast<const __nv_bfloat16*>(G.dres), sc.t_h, T, h, p, seed,
-                          drop_stream(l, mb, tp ? Op::AR1 : Op::PROJ_RES), s),
-              "dropout_bwd");
+        ck_op(dropout_bwd_colsum(static_cast<const __nv_bfloat16*>(G.dres), sc.t_h, P.g_b_proj, 1, sc.ws, T, h, p,
+                                 seed, drop_stream(l, mb, tp ? Op::AR1 : Op::PROJ_RES), s),
+              "dropout_bwd + bias grad");
       }
       release(G.dln2, s);
       G.dln2 = nullptr;
-      colsum(sc.t_h, P.g_b_proj, h);
       gemm(sc.t_h, h, true, attn, hp, true, P.g_w_proj, hp, h, hp, T, dw_epi_);          // dW_proj += d^T O
       gemm(sc.t_h, h, false, P.w_proj, hp, true, sc.t_h2, hp, T, hp, h, EPI_BF16);         // dO = d W_proj
       if (!opt_.dry_run)
@@ -1194,6 +1221,7 @@ std::string Executor::report_json() const {
   j["alloc_host_max_ms"] = rep_.alloc_host_max_ms;
   j["host_issue_ms"] = rep_.host_issue_ms;
   j["pool_reserved_bytes"] = rep_.pool_reserved;
+  j["pool_reserved_at_init_bytes"] = pool_reserved_init_;
   if (opt_.probe_ops) {
     Json po = Json::object();
     for (const auto& [k, n, ms] : op_times_) po[k] = {n, ms};

@@ -43,6 +43,7 @@ struct ExecOptions {
   bool elide_recompute = false; // timing-only: skip recompute launches (exposed-recompute cross-check)
   bool dry_run = false;         // build the launch program only (no device)
   bool probe_fc1 = false;       // CUDA events around every FC1 forward GEMM launch (roofline line)
+  bool reserve_pool = true;     // map all free HBM (but 2 GiB) into the activation pool at construction
   bool probe_ops = false;       // one CUDA event after every operator launch on its stream: in-step
                                 // time per operator name, gaps included (report "probe_ops")
   bool standalone = false;      // time one pipeline stage alone on one GPU: receives read synthetic
@@ -140,6 +141,7 @@ class Executor {
 
   void ck(cudaError_t e, const char* what);
   void ck_op(int status, const char* what);
+  void reserve_pool();
   void nccl(ncclResult_t r, const char* what);
 
   host::Profile prof_;
@@ -186,6 +188,7 @@ class Executor {
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   __nv_bfloat16 *syn_act_ = nullptr, *syn_grad_ = nullptr;  // standalone stage: stand-ins for PP receives
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probes_;  // exec.probe_fc1 event pairs of this step
+  size_t pool_reserved_init_ = 0;  // bytes mapped into the pool by reserve_pool()
   cudaStream_t probe_stream_ = nullptr;  // exec.probe_ops: the stream the current operator launches on
   std::vector<std::tuple<const char*, cudaStream_t, cudaEvent_t>> op_events_;  // exec.probe_ops, this step
   std::vector<std::tuple<std::string, long long, double>> op_times_;           // name, launches, ms (last step)

@@ -104,6 +104,16 @@ def dropout_bwd(dout, p: float, seed: int, stream_id: int):
     return dy
 
 
+def dropout_bwd_colsum(dout, acc, p: float, seed: int, stream_id: int):
+    """(dropout_bwd(dout), acc += column sums of it) in one pass."""
+    rows, width = dout.shape
+    dy = torch.empty_like(dout)
+    ws = torch.empty(lib().lynx_op_column_sum_workspace(rows, width) // 4 + 1, device=dout.device, dtype=torch.float32)
+    call("lynx_op_dropout_bwd_colsum", dout.data_ptr(), dy.data_ptr(), acc.data_ptr(), ws.data_ptr(), rows, width,
+         float(p), seed, stream_id, _s())
+    return dy, acc
+
+
 def column_sum_acc(x, acc):
     rows, width = x.shape
     ws = torch.empty(lib().lynx_op_column_sum_workspace(rows, width) // 4 + 1, device=x.device, dtype=torch.float32)

@@ -247,6 +247,19 @@ def test_column_sum(ops, cuda):
     assert torch.allclose(acc, x.float().sum(0) + 2, atol=1e-2)
 
 
+@pytest.mark.parametrize("rows,width,p", [(65536 // 8, 4096, 0.1), (5000, 768, 0.1), (777, 1024, 0.0)])
+def test_dropout_bwd_colsum_matches_two_kernels(ops, cuda, rows, width, p):
+    """The fused branch-gradient + bias-gradient pass equals dropout_bwd then column_sum_acc bit for bit."""
+    dout = torch.randn(rows, width, device=cuda).bfloat16()
+    acc1 = torch.full((width,), 0.5, device=cuda)
+    acc2 = acc1.clone()
+    dy1 = ops.dropout_bwd(dout, p, seed=7, stream_id=99)
+    ops.column_sum_acc(dy1, acc1)
+    dy2, _ = ops.dropout_bwd_colsum(dout, acc2, p, seed=7, stream_id=99)
+    assert torch.equal(dy1, dy2)
+    assert torch.equal(acc1, acc2)
+
+
 def test_gelu(ops, cuda):
     x = (3 * torch.randn(4096, 256, device=cuda)).bfloat16()
     y = ops.gelu_fwd(x)

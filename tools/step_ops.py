@@ -40,8 +40,10 @@ def main():
                                                           exec_opts={"probe_ops": True}))
     tok, lab = ex.synthetic_batch(c)
     reps, clocks = [], []
+    cs = bench.ClockSampler(0)  # NVML initialised once, before the steps (as in bench.py)
     for _ in range(args.steps):
-        cs = bench.ClockSampler(0)
+        cs.rows.clear()
+        cs._stop.clear()
         with cs:
             e.step(tok, lab)
         clocks.append(cs.summary())
