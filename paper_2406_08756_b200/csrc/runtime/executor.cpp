@@ -114,7 +114,7 @@ void Executor::init_device() {
 }
 
 // Map the activation pool's physical memory once, up front: all free HBM but a small reserve for
-// the runtime and library workspaces, allocated from the pool and freed back into it (the release
+// the runtime, library workspaces and NCCL (2 GiB, 6 GiB with communicators), allocated from the pool and freed back into it (the release
 // threshold keeps it mapped). Growing the pool lazily inside the steps, with HBM nearly full,
 // made single cudaMallocFromPoolAsync calls block the host for up to 2.6 s while the driver
 // mapped memory (seen as 3-10 s steps with `alloc_host_ms` in the report); afterwards the pool
@@ -122,7 +122,8 @@ void Executor::init_device() {
 void Executor::reserve_pool() {
   size_t free_b = 0, total_b = 0;
   ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
-  const size_t keep = size_t{2} << 30, step = size_t{1} << 30;
+  // NCCL sets up P2P / NVLS buffers lazily at a communicator's first operation: leave it room
+  const size_t keep = (needs_comms_ ? size_t{6} : size_t{2}) << 30, step = size_t{1} << 30;
   if (free_b <= keep + step) return;
   size_t want = (free_b - keep) / step * step;
   void* p = nullptr;
