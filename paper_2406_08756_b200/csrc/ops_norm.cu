@@ -19,7 +19,7 @@ namespace {
 
 constexpr int kNT = 256;    // threads per row-CTA
 constexpr int kMaxC = 4;    // chunks of 8 per thread -> width <= 8192
-constexpr int kPartBlocks = 512;
+constexpr int kPartBlocks = 1184;  // 8 x 148 SMs: row-partitioned partial sums (bias gradients)
 
 template <int NT>
 LYNX_DEV float block_sum(float v, float* red) {

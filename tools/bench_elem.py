@@ -50,6 +50,8 @@ def main():
         ("gelu_fwd [T,4h]", lambda: ops.gelu_fwd(f), 8 * e),
         ("gelu_bwd [T,4h]", lambda: ops.gelu_bwd(f, f), 12 * e),
         ("column_sum [T,4h]", lambda: ops.column_sum_acc(f, acc), 4 * e),
+        ("column_sum [T,h]", lambda: ops.column_sum_acc(y, dg), e),
+        ("dropout_bwd_colsum", lambda: ops.dropout_bwd_colsum(y, dg, 0.1, 1, 2), 2 * e),
     ]
     for name, fn, nbytes in cases:
         t = timeit(fn)
