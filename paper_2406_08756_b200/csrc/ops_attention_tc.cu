@@ -158,9 +158,12 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
   // K and V stages have their own barriers: K_j is released once S_j is computed, so the
   // load of K_{j+2} overlaps PV_j instead of waiting for it.
+  // p_full is double-buffered like S: with one barrier, a row warp that ran ahead to tile j+1 (S(j+1)
+  // is issued early) arrived again before a slower warp's tile-j arrival, completed tile j's phase
+  // early and let PV(j) read that warp's stale P rows (a rare, timing-dependent race).
   uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5, *v_empty = bar + 7,
-           *s_full = bar + 9, *p_full = bar + 11, *pv_done = bar + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+           *s_full = bar + 9, *p_full = bar + 11, *pv_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
   const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n = qb + 1, HD = H * D, row0 = b * S;
@@ -173,8 +176,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(v_full + i, 1);
       mbar_init(v_empty + i, 1);
       mbar_init(s_full + i, 1);
+      mbar_init(p_full + i, 128);
     }
-    mbar_init(p_full, 128);
     mbar_init(pv_done, 1);
     fence_barrier_init();
   }
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int j = 0; j < n; ++j) {
         const int st = j & 1;
         mbar_wait(v_full + st, (j >> 1) & 1);
-        mbar_wait(p_full, j & 1);
+        mbar_wait(p_full + st, (j >> 1) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(p_full + st);
     }
     mbar_wait(pv_done, (n - 1) & 1);
     tc_fence_after();
@@ -353,8 +356,11 @@ __global__ void __launch_bounds__(384, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  // pd_full is double-buffered by tile parity (see the forward kernel's p_full: one barrier let a
+  // row warp's arrival for tile i+1 complete tile i's phase before a slower warp had written its
+  // P^T / dS^T rows, and dV / dK of those 32 keys picked up stale values, ~3 % of runs).
   uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = q_full + NS, *s_full = q_empty + NS, *pd_full = s_full + 2,
-           *mma_done = pd_full + 1, *fin = mma_done + 1;
+           *mma_done = pd_full + 2, *fin = mma_done + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
   const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -367,8 +373,10 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
     }
-    for (int i = 0; i < 2; ++i) mbar_init(s_full + i, 1);
-    mbar_init(pd_full, 256);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(pd_full + i, 256);
+    }
     mbar_init(mma_done, 1);
     mbar_init(fin, 1);
     fence_barrier_init();
@@ -426,15 +434,15 @@ __global__ void __launch_bounds__(384, 1)
       if (n > 1) issue_s(1);
       for (int i = 0; i < n; ++i) {
         const int st = i % NS;
-        mbar_wait(pd_full, i & 1);
+        mbar_wait(pd_full + (i & 1), (i >> 1) & 1);
         ATRACE(2, i);
         tc_fence_after();
         const uint32_t tb = static_cast<uint32_t>(i & 1);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // A = P^T / dS^T, packed bf16 over S^T / dP^T in TMEM buffer tb
-          umma_f16_ts(tmem + 256, tmem + tb * 64 + kk * 8, mnmaj(sDO + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
-          umma_f16_ts(tmem + 384, tmem + 128 + tb * 64 + kk * 8, mnmaj(sQ + st * L::kQT, kk, 8192), idG,
-                      (i | kk) != 0);
+          const uint32_t ac = tb * 64 + kk * 8 + (kk >= 2 ? 32 : 0);  // queries 0-31: cols 0-15, 32-63: 48-63
+          umma_f16_ts(tmem + 256, tmem + ac, mnmaj(sDO + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
+          umma_f16_ts(tmem + 384, tmem + 128 + ac, mnmaj(sQ + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
         }
         umma_commit(mma_done);
         umma_commit(q_empty + st);
@@ -487,14 +495,17 @@ __global__ void __launch_bounds__(384, 1)
           gp[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
         }
         if (threadIdx.x == 128) ATRACE(4, i);
-        // P^T(i) / dS^T(i) overwrite S^T(i) / dP^T(i) in place (this half's 32 queries -> 16
-        // packed columns). dV / dK(i-2), the last readers of buffer tb, completed before S^T(i).
-        tmem_st16(tmem + lanes + tb * 64 + half * 16, pp);
-        tmem_st16(tmem + lanes + 128 + tb * 64 + half * 16, gp);
+        // P^T(i) / dS^T(i) overwrite S^T(i) / dP^T(i) in place, each half inside the columns it read
+        // itself (half 0: 0-15 of its 0-31, half 1: 48-63 of its 32-63): the other half reads the
+        // same TMEM lanes without any ordering against this store (packing half 1 at 16-31 made
+        // warps 4-7 read P^T instead of S^T, ~0.1 % of runs). dV / dK(i-2), the last readers of
+        // buffer tb, completed before S^T(i).
+        tmem_st16(tmem + lanes + tb * 64 + half * 48, pp);
+        tmem_st16(tmem + lanes + 128 + tb * 64 + half * 48, gp);
         tmem_st_wait();
       }
       tc_fence_before();
-      mbar_arrive(pd_full);
+      mbar_arrive(pd_full + tb);
       if (threadIdx.x == 128) ATRACE(6, i);
     }
     mbar_wait(fin, 0);
@@ -617,7 +628,8 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // A = dS(j), packed bf16 over the S(j) columns of TMEM buffer tb
-          umma_f16_ts(tmem + 256, tmem + tb * 64 + kk * 8, mnmaj(sK + st * L::kKT, kk, 8192), idG, (j | kk) != 0);
+          umma_f16_ts(tmem + 256, tmem + tb * 64 + kk * 8 + (kk >= 2 ? 32 : 0), mnmaj(sK + st * L::kKT, kk, 8192),
+                      idG, (j | kk) != 0);
         umma_commit(ds_free + tb);
         umma_commit(kv_empty + st);
         if (j + 2 < n) issue_s(j + 2);
@@ -655,9 +667,10 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t packed[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c) packed[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
-        // dS(j) overwrites S(j) in place (this row's 32 keys -> 16 packed columns); dQ(j-2), the
-        // last reader of this buffer, completed before S(j) (tensor-pipe order).
-        tmem_st16(tmem + lanes + st * 64 + half * 16, packed);
+        // dS(j) overwrites S(j) in place, each half inside the columns it read (half 0: 0-15, half 1:
+        // 48-63; see the dK/dV kernel); dQ(j-2), the last reader of this buffer, completed before
+        // S(j) (tensor-pipe order).
+        tmem_st16(tmem + lanes + st * 64 + half * 48, packed);
         tmem_st_wait();
       }
       tc_fence_before();
