@@ -129,5 +129,9 @@ int fill_param(__nv_bfloat16* p, float* master, float v, long long n, cudaStream
 int count_mismatch(const void* a, const void* b, size_t bytes, unsigned long long* d_count, cudaStream_t s);
 int init_normal_bf16(__nv_bfloat16* p, float* master, long long n, float std, uint64_t seed, uint64_t stream_id,
                      cudaStream_t s);
+// Single-GPU stand-in for a collective (exec.comm_standin_us): `ctas` CTAs of 512 threads hold
+// the stream for `ns` nanoseconds of %globaltimer, sleeping between polls. Models the transfer
+// time of an NCCL all-reduce the plan's window capacity assumes; not its SM / HBM traffic.
+int comm_standin(unsigned long long ns, int ctas, cudaStream_t s);
 
 }  // namespace lynx

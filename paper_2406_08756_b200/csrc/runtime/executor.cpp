@@ -184,6 +184,8 @@ void Executor::parse_config(const std::string& text) {
   opt_.probe_fc1 = ex.value("probe_fc1", false);
   opt_.probe_ops = ex.value("probe_ops", false);
   opt_.reserve_pool = ex.value("reserve_pool", true);
+  opt_.comm_standin_us = ex.value("comm_standin_us", 0.0);
+  opt_.comm_standin_ctas = ex.value("comm_standin_ctas", 16);
   cfg_.head_chunk = static_cast<int>(std::min<long long>(ex.value("head_chunk", 4096), cfg_.tokens()));
   if (cfg_.hidden % cfg_.heads || cfg_.heads % cfg_.tp || (cfg_.hidden / cfg_.tp) % 128)
     throw RtError("hidden must split into heads and TP ranks in 128-column tiles", kValidation);
@@ -194,8 +196,15 @@ void Executor::parse_config(const std::string& text) {
   nccl_id_ = par.value("nccl_id", std::string());
   world_rank_ = par.value("world_rank", 0);
   world_size_ = par.value("world_size", 1);
-  if (opt_.standalone && (cfg_.tp != 1 || world_size_ != 1))
-    throw RtError("standalone_stage runs one stage at TP = 1 in a single process", kValidation);
+  if (opt_.standalone && world_size_ != 1)
+    throw RtError("standalone_stage runs one stage in a single process", kValidation);
+  if (opt_.standalone && cfg_.tp != 1 && opt_.comm_standin_us <= 0)
+    throw RtError("standalone_stage at TP > 1 needs exec.comm_standin_us (one TP rank, stand-in all-reduces)",
+                  kValidation);
+  if (opt_.comm_standin_us > 0 && !opt_.standalone)
+    throw RtError("exec.comm_standin_us is a standalone_stage option", kValidation);
+  if (opt_.comm_standin_ctas < 1 || opt_.comm_standin_ctas > 148)
+    throw RtError("exec.comm_standin_ctas must be in [1, 148]", kValidation);
 }
 
 void Executor::init_comms(const std::string& id_hex, int world_rank, int world_size) {
@@ -234,7 +243,8 @@ void Executor::bind_template() {
   }
   const bool tp_tmpl = !L.fwd_comm_ids.empty();
   if (cfg_.tp > 1 && !tp_tmpl) throw RtError("tp > 1 needs the tensor-parallel layer template", kValidation);
-  needs_comms_ = tp_tmpl || cfg_.tp > 1 || (cfg_.pp > 1 && !opt_.standalone);
+  const bool standin = opt_.comm_standin_us > 0;
+  needs_comms_ = (!standin && (tp_tmpl || cfg_.tp > 1)) || (cfg_.pp > 1 && !opt_.standalone);
   tp_tmpl_ = tp_tmpl;
   static const std::vector<Op> t1 = {Op::LN1, Op::QKV, Op::ATTN, Op::PROJ_RES, Op::LN2, Op::FC1,
                                      Op::GELU, Op::FC2_RES, Op::MLP_BWD, Op::ATTN_BWD, Op::LN1_BWD};
@@ -742,7 +752,12 @@ void Executor::comm_element(int mb, bool bwd, int l, const host::Element& e) {
   }
   if (!opt_.dry_run) {
     span_begin(tp_s_, 1, mb, e.op);
-    nccl(ncclAllReduce(buf, buf, static_cast<size_t>(T * h), ncclBfloat16, ncclSum, tp_comm_, tp_s_), "allreduce");
+    if (opt_.comm_standin_us > 0)
+      ck_op(comm_standin(static_cast<unsigned long long>(opt_.comm_standin_us * 1e3), opt_.comm_standin_ctas, tp_s_),
+            "comm stand-in");
+    else
+      nccl(ncclAllReduce(buf, buf, static_cast<size_t>(T * h), ncclBfloat16, ncclSum, tp_comm_, tp_s_),
+           "allreduce");
     span_end(tp_s_);
     cudaEvent_t done = ev();
     ck(cudaEventRecord(done, tp_s_), "event");

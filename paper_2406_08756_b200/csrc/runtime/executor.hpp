@@ -48,6 +48,9 @@ struct ExecOptions {
                                 // time per operator name, gaps included (report "probe_ops")
   bool standalone = false;      // time one pipeline stage alone on one GPU: receives read synthetic
                                 // activations / gradients, sends are skipped (measured partitioning)
+  double comm_standin_us = 0;   // > 0 (standalone only): each TP all-reduce is replaced by a stand-in
+  int comm_standin_ctas = 16;   // kernel holding the TP stream this long, so one GPU runs one TP rank
+                                // of a TP > 1 stage with the plan's comm windows (window overlap)
 };
 
 struct Slot {

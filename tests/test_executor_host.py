@@ -80,3 +80,26 @@ def test_executor_rejects_foreign_templates():
     plan = ex.plan_for(t, 0)
     with pytest.raises(LynxError):
         ex.Executor(t, plan["timeline"], ex.make_config(c, plan["layers_per_stage"], exec_opts={"dry_run": True}))
+
+
+def test_comm_standin_stage_program():
+    """exec.comm_standin_us (tools/emulate_stage.py): one TP rank of a TP2 stage runs alone with
+    stand-in all-reduces; its launch program keeps the TP rank's all-reduce sequence (same windows)
+    and the PP transfers become synthetic. Without a stand-in, or outside a standalone stage, it is
+    rejected."""
+    from paper_2406_08756_b200._native import LynxError
+    c = gp.CONFIGS["1.3b"]
+    progs, plans = dry_programs(c)
+    text = gp.profile_text(c)
+    layers = plans[0]["layers_per_stage"]
+    for s in (0, c.pp - 1):
+        opts = {"dry_run": True, "standalone_stage": True, "comm_standin_us": 500.0}
+        e = ex.Executor(text, plans[s]["timeline"], ex.make_config(c, layers, exec_opts=opts))
+        e.step(None, None)
+        prog = e.program()
+        e.close()
+        assert prog == progs[(s, 0)] and any(o["comm"] == "tp" for o in prog)
+    for opts in ({"dry_run": True, "standalone_stage": True},
+                 {"dry_run": True, "comm_standin_us": 500.0}):
+        with pytest.raises(LynxError):
+            ex.Executor(text, plans[0]["timeline"], ex.make_config(c, layers, exec_opts=opts))

@@ -1,0 +1,120 @@
+"""One TP rank of each TP·PP stage (default the 7B TP2·PP4 headline) on one B200: exposed recompute with the plan's comm windows.
+
+The headline configuration (GPT-7B, micro-batch 32, TP2·PP4, 8 microbatches) needs eight GPUs;
+gpurun has one. This runs each stage's TP-rank-0 executor alone (exec.standalone_stage: pipeline
+receives read synthetic activations / gradients, sends are skipped) with every TP all-reduce
+replaced by a stand-in kernel (exec.comm_standin_us) that holds the TP stream for the transfer
+time the plan's window capacities assume (2(t-1)/t * [T,h] bf16 / NVLINK_BUS_GBS, the profiler's
+comm model). The recompute items the plan files into those windows run on the side stream against
+it, so window overlap, on-demand recompute and waits are measured on real B200 kernels; the SM and
+HBM traffic of a real NCCL all-reduce is not modelled (the stand-in sleeps on 16 CTAs).
+
+Per stage: the HEU plan, the same plan with recompute launches elided (no-recompute floor), and
+Megatron full recompute. Writes one JSON document.
+
+    python tools/emulate_stage.py [--model 7b] [--stages 0,1,2,3] [--out profiles/x.json]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2406_08756_b200 import executor as ex  # noqa: E402
+from paper_2406_08756_b200 import gpt_profile as gp  # noqa: E402
+from paper_2406_08756_b200 import profiler  # noqa: E402
+
+
+def run(text, timeline, c, layers, opts, tok, lab, steps, warmup):
+    cfg = ex.make_config(c, layers, exec_opts={"standalone_stage": True, **opts})
+    e = ex.Executor(text, timeline, cfg)
+    try:
+        for _ in range(warmup):
+            e.step(tok, lab)
+        reps = []
+        for _ in range(steps):
+            e.step(tok, lab)
+            reps.append(e.report())
+    finally:
+        e.close()
+        torch.cuda.empty_cache()
+    r = min(reps, key=lambda x: x["iteration_ms"])
+    keys = ("iteration_ms", "comm_ms", "busy_ms", "exposed_recompute_ms", "recompute_on_demand_ms",
+            "recompute_overlapped_ms", "wait_on_recompute_ms", "recompute_launches", "pool_high_water_bytes")
+    return {k: r[k] for k in keys if k in r} | {"iteration_ms_each": [round(x["iteration_ms"], 3) for x in reps]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="7b")
+    ap.add_argument("--stages", default="0,1,2,3")
+    ap.add_argument("--micro-batch", type=int, default=0)
+    ap.add_argument("--tp", type=int, default=0, help="default: the model config's (7b: TP2 PP4 M8)")
+    ap.add_argument("--pp", type=int, default=0)
+    ap.add_argument("--microbatches", type=int, default=0)
+    ap.add_argument("--budget-gb", type=float, default=0.0,
+                    help="ledger budget per GPU (default: this B200's HBM minus the bench's unmodelled reserve)")
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--ctas", type=int, default=16)
+    ap.add_argument("--out", default="gpurun_out/emulate_tp2pp4.json")
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    base = gp.CONFIGS[a.model]
+    c = gp.GPTConfig(**{**base.__dict__, "tp": a.tp or base.tp, "pp": a.pp or base.pp,
+                        "n_microbatches": a.microbatches or base.n_microbatches, "dropout": 0.1})
+    if a.micro_batch:
+        c.micro_batch = a.micro_batch
+    t0 = time.perf_counter()
+    times = profiler.measure_op_times(c)
+    torch.cuda.empty_cache()
+    prof_s = time.perf_counter() - t0
+    _, total = torch.cuda.mem_get_info()
+    c.mem_budget_bytes = int(a.budget_gb * 1e9) if a.budget_gb else bench.device_budget(c, total)
+    text = gp.profile_text(c, times=times)
+    T, h = c.tokens, c.hidden
+    standin_us = 2.0 * (c.tp - 1) / c.tp * (2 * T * h) / (profiler.NVLINK_BUS_GBS * 1e3)
+    tok, lab = ex.synthetic_batch(c)
+    out = {"workload": f"gpt-{a.model} TP{c.tp}xPP{c.pp}, micro-batch {c.micro_batch}, seq {c.seq}, {c.n_microbatches} "
+                       f"microbatches; TP rank 0 of each stage alone on one B200",
+           "comm_model": {"standin_us_per_allreduce": round(standin_us, 3), "nvlink_bus_gbs": profiler.NVLINK_BUS_GBS,
+                          "bytes": 2 * T * h, "ctas": a.ctas,
+                          "note": "stand-in kernel holds the TP stream for the modelled transfer time; "
+                                  "real NCCL SM/HBM contention not modelled"},
+           "profiler_s": round(prof_s, 2), "ledger_budget_bytes": c.mem_budget_bytes,
+           "budget": "reduced (--budget-gb)" if a.budget_gb else "device HBM minus unmodelled reserve", "stages": {}}
+    std = {"comm_standin_us": standin_us, "comm_standin_ctas": a.ctas}
+    for s in (int(x) for x in a.stages.split(",")):
+        heu = ex.plan_for(text, s, "heu")
+        full = ex.plan_for(text, s, "full")
+        layers = heu["layers_per_stage"]
+        pj = json.loads(heu["plan_json"])
+        row = {"layers_per_stage": layers, "plan": {k: pj[k] for k in ("S", "phase_assignment", "peak_bytes")},
+               "simulated_period_us": heu["period_us"]}
+        row["heu"] = run(text, heu["timeline"], c, layers, std, tok, lab, a.steps, a.warmup)
+        row["elided"] = run(text, heu["timeline"], c, layers, {**std, "elide_recompute": True}, tok, lab,
+                            a.steps, a.warmup)
+        try:
+            row["full_recompute"] = run(text, full["timeline"], c, layers, std, tok, lab, a.steps, a.warmup)
+        except ex.LynxError as err:
+            row["full_recompute"] = {"error": str(err)[:200]}
+        hr, el = row["heu"], row["elided"]
+        row["exposed_fraction_of_iteration"] = round(hr["exposed_recompute_ms"] / hr["iteration_ms"], 4)
+        row["crosscheck_ms"] = round(hr["iteration_ms"] - el["iteration_ms"], 3)
+        rc = hr["recompute_on_demand_ms"] + hr["recompute_overlapped_ms"]
+        row["exposed_fraction_of_recompute"] = round(hr["exposed_recompute_ms"] / rc, 4) if rc else 0.0
+        out["stages"][str(s)] = row
+        print(json.dumps({"stage": s, **{k: row[k] for k in ("exposed_fraction_of_iteration", "crosscheck_ms")},
+                          "heu_ms": hr["iteration_ms"], "elided_ms": el["iteration_ms"],
+                          "full_ms": row["full_recompute"].get("iteration_ms")}), flush=True)
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
