@@ -107,7 +107,8 @@ char* lynx_plan_opt_timeline(const char* profile_json, int stage, const int* lay
  *   "layers_per_stage": [...], "parallel": {tp, tp_rank, world_rank, world_size,
  *   nccl_id (hex, from lynx_rt_nccl_unique_id on rank 0)}, "train": {dropout,
  *   seed, lr, beta1, beta2, eps, weight_decay, init_std}, "exec": {trace,
- *   check_recompute, elide_recompute, dry_run, head_chunk}}.
+ *   check_recompute, elide_recompute, dry_run, head_chunk, probe_fc1, probe_ops,
+ *   reserve_pool, standalone_stage, comm_standin_us, comm_standin_ctas}}.
  * Weights are initialised on the device from Philox streams keyed by seed. */
 typedef struct lynx_rt lynx_rt;
 int lynx_rt_create(const char* profile_json, const char* timeline_json, const char* config_json, lynx_rt** out);
