@@ -160,3 +160,42 @@ def test_selective_plan_is_bit_identical(cuda):
     assert l_sel == l_keep
     for k in g_keep:
         assert np.array_equal(g_keep[k], g_sel[k]), k
+
+
+def test_comm_standin_stage_windows_are_bit_identical(cuda):
+    """One TP rank of a TP2·PP2 stage alone on the GPU (tools/emulate_stage.py): all-reduces become
+    stand-in kernels holding the TP stream for the modelled transfer time, so the HEU plan's window
+    recomputes overlap them on the side stream. Regenerated tensors equal their forward copies, the
+    stage's gradients equal the retain-all run's, and the TP stream is busy at least the modelled
+    time per all-reduce."""
+    from paper_2406_08756_b200 import executor as ex
+    from paper_2406_08756_b200 import gpt_profile as gp
+    base = dict(name="gpt-tiny-tp2pp2", n_layers=4, hidden=512, heads=8, seq=256, micro_batch=2, vocab=50304, tp=2,
+                pp=2, n_microbatches=4, dropout=0.1)
+    c = gp.GPTConfig(**{**base, "mem_budget_bytes": 256 * 2**20})
+    text = gp.profile_text(c)
+    tok, lab = ex.synthetic_batch(c)
+    us = 200.0
+    for s in (0, 1):
+        grads = {}
+        for baseline in ("heu", "retain_all"):
+            plan = ex.plan_for(text, s, baseline)
+            layers = plan["layers_per_stage"]
+            opts = {"standalone_stage": True, "comm_standin_us": us, "check_recompute": baseline == "heu"}
+            e = ex.Executor(text, plan["timeline"], ex.make_config(c, layers, exec_opts=opts))
+            shapes = ex.param_shapes(c, layers[s], s == 0, s == c.pp - 1)
+            e.step(tok, lab)
+            rep = e.report()
+            grads[baseline] = {k: e.get("grad:" + k, int(np.prod(v))) for k, v in shapes.items()}
+            prog = e.program()
+            e.close()
+            n_ar = sum(1 for o in prog if o["comm"] == "tp")
+            assert n_ar >= 4 * layers[s] * c.n_microbatches
+            assert rep["comm_ms"] >= 0.95 * n_ar * us / 1000.0, (rep["comm_ms"], n_ar)
+            if baseline == "heu" and s == 0:
+                assert any(it["host"] == "window" for it in plan["timeline"]["items"])
+                assert rep["recompute_overlapped_ms"] > 0 and rep["recompute_checked"] > 0
+            assert rep["recompute_mismatch_words"] == 0
+        for k in grads["heu"]:
+            assert np.isfinite(grads["heu"][k]).all(), k
+            assert np.array_equal(grads["heu"][k], grads["retain_all"][k]), k
