@@ -292,6 +292,40 @@ def gemm_roofline(c, peaks: dict) -> dict:
             "flops_per_launch": flops}
 
 
+def stage_emulation_summary(args, device_total: int) -> dict:
+    """The headline TP2xPP4 configuration's stage 0 (four microbatches in flight, the most
+    recompute) as TP rank 0 alone on this B200, all-reduces replaced by stand-in kernels that hold
+    the TP stream for the modelled transfer time (paper_2406_08756_b200/stage_emulation.py): the
+    exposed recompute with the plan's comm windows, against the same plan with recompute elided."""
+    import torch
+
+    from paper_2406_08756_b200 import gpt_profile as gp
+    from paper_2406_08756_b200 import profiler
+    from paper_2406_08756_b200 import stage_emulation as se
+    try:
+        torch.cuda.empty_cache()
+        c2 = config_for(8, args)
+        times2 = profiler.measure_op_times(c2) if args.profile == "measured" else None
+        torch.cuda.empty_cache()
+        c2.mem_budget_bytes = device_budget(c2, device_total, args.mem_margin_gib)
+        text2 = gp.profile_text(c2, times=times2)
+        row = se.emulate(c2, text2, [0], variants=("heu", "elided"))["0"]
+        h, el = row["heu"], row["elided"]
+        return {"config": f"stage 0 of {c2.name} TP{c2.tp}xPP{c2.pp}, micro-batch {c2.micro_batch}, "
+                          f"{c2.n_microbatches} microbatches ({row['layers_per_stage'][0]} layers + embedding), TP "
+                          "rank 0 alone on this B200; PP receives synthetic; each TP all-reduce a stand-in kernel "
+                          f"holding the TP stream {se.standin_us(c2):.1f} us (2(t-1)/t [T,h] bf16 at "
+                          f"{profiler.NVLINK_BUS_GBS:g} GB/s; NCCL SM/HBM contention not modelled)",
+                "plan": row["plan"], "iteration_ms": round(h["iteration_ms"], 3),
+                "exposed_recompute_ms": round(h["exposed_recompute_ms"], 3),
+                "exposed_fraction_of_iteration": row["exposed_fraction_of_iteration"],
+                "recompute_overlapped_ms": round(h["recompute_overlapped_ms"], 3),
+                "elided_iteration_ms": round(el["iteration_ms"], 3), "crosscheck_ms": row["crosscheck_ms"],
+                "simulated_iteration_ms": round(float(row["simulated_period_us"]) * c2.n_microbatches / 1000.0, 3)}
+    except Exception as err:  # reported, never fatal for the headline line
+        return {"error": str(err).splitlines()[0][:200]}
+
+
 def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times) -> dict:
     """Same-box comparison runs after the timed region (N=1):
     - "elided": the same plan with every recompute launch skipped (timing only; regenerated
@@ -459,6 +493,13 @@ def run_gpu_arm(args):
         print(json.dumps({"partial": True, "value": value, "ms": dev_ms, "exposed_ms": exposed,
                           "report": rep}), file=sys.stderr, flush=True)
         extra = run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times)
+        e = None
+    emu = None
+    if rank == 0 and ws == 1 and not args.no_stage_emulation:
+        if e is not None:
+            e.close()
+        e = None
+        emu = stage_emulation_summary(args, total)
     if rank != 0:
         return
     step_tflops = c.flops_per_token() * tokens_iter / (dev_ms / 1000.0) / 1e12
@@ -474,6 +515,7 @@ def run_gpu_arm(args):
                       "wait_on_recompute_ms": rep["wait_on_recompute_ms"], "baselines": extra or None,
                       "profile": args.profile, "profiler_s": round(prof_s, 2),
                       "op_times_us": {k: float(v) for k, v in (times or {}).items()}},
+        "tp2pp4_stage_emulation": emu,
         "memory": {"ledger_budget_bytes": c.mem_budget_bytes, "plan_peak_bytes": plan0["peak_bytes"],
                    "margin_gib": margins[len(oom_retries)], "oom_retries": oom_retries,
                    "pool_high_water_bytes": rep["pool_high_water_bytes"],
@@ -532,6 +574,8 @@ def main():
                     help="operator times for the planner: B200-measured (default) or the analytic estimate")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-crosscheck", action="store_true", help="skip the recompute-elided timing run")
+    ap.add_argument("--no-stage-emulation", action="store_true",
+                    help="skip the TP2xPP4 stage-0 run with stand-in all-reduces (N=1)")
     ap.add_argument("--mem-margin-gib", type=float, default=8.0,
                     help="HBM held back from the HEU budget for context and pool fragmentation "
                          "(an OOM retries with 12 and 16 GiB)")

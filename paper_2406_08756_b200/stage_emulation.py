@@ -1,0 +1,81 @@
+"""One TP rank of a TP·PP stage on one B200, with the plan's comm windows (exec.comm_standin_us).
+
+The headline configuration (GPT-7B, micro-batch 32, TP2·PP4, 8 microbatches) needs eight GPUs.
+Each stage's TP-rank-0 executor runs alone (exec.standalone_stage: pipeline receives read synthetic
+activations / gradients, sends are skipped) with every TP all-reduce replaced by a stand-in kernel
+that holds the TP stream for the transfer time the plan's window capacities assume
+(2(t-1)/t * [T,h] bf16 / profiler.NVLINK_BUS_GBS). The recompute items the plan files into those
+windows (expand_plan_to_stage, heusched.cpp:372-405) run on the side stream against it, so window
+overlap, on-demand recompute and waits are measured on real B200 kernels. The SM and HBM traffic of
+a real NCCL all-reduce is not modelled (the stand-in sleeps on `ctas` CTAs).
+"""
+from __future__ import annotations
+
+import json
+
+from . import executor as ex
+from . import gpt_profile as gp
+from . import profiler
+
+
+def standin_us(c: gp.GPTConfig) -> float:
+    """Modelled TP all-reduce time of one [T, h] bf16 tensor (the profiler's comm model)."""
+    return 2.0 * (c.tp - 1) / c.tp * (2 * c.tokens * c.hidden) / (profiler.NVLINK_BUS_GBS * 1e3)
+
+
+def run_stage(text: str, timeline: dict, c: gp.GPTConfig, layers, opts: dict, tok, lab, steps: int = 2,
+              warmup: int = 1) -> dict:
+    """The stage's executor alone: best of `steps` iterations after `warmup`."""
+    import torch
+    cfg = ex.make_config(c, layers, exec_opts={"standalone_stage": True, **opts})
+    e = ex.Executor(text, timeline, cfg)
+    try:
+        for _ in range(warmup):
+            e.step(tok, lab)
+        reps = []
+        for _ in range(steps):
+            e.step(tok, lab)
+            reps.append(e.report())
+    finally:
+        e.close()
+        torch.cuda.empty_cache()
+    r = min(reps, key=lambda x: x["iteration_ms"])
+    keys = ("iteration_ms", "comm_ms", "busy_ms", "exposed_recompute_ms", "recompute_on_demand_ms",
+            "recompute_overlapped_ms", "wait_on_recompute_ms", "recompute_launches", "pool_high_water_bytes")
+    return {k: r[k] for k in keys if k in r} | {"iteration_ms_each": [round(x["iteration_ms"], 3) for x in reps]}
+
+
+def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int = 1, ctas: int = 16,
+            variants=("heu", "elided", "full_recompute")) -> dict:
+    """Per stage: its HEU plan, the same plan with recompute elided (no-recompute floor) and
+    Megatron full recompute, each as one TP rank with stand-in all-reduces."""
+    std = {"comm_standin_us": standin_us(c), "comm_standin_ctas": ctas}
+    tok, lab = ex.synthetic_batch(c)
+    out = {}
+    for s in stages:
+        heu = ex.plan_for(text, s, "heu")
+        layers = heu["layers_per_stage"]
+        pj = json.loads(heu["plan_json"])
+        row = {"layers_per_stage": layers, "plan": {k: pj[k] for k in ("S", "phase_assignment", "peak_bytes")},
+               "simulated_period_us": heu["period_us"]}
+        for v in variants:
+            try:
+                if v == "heu":
+                    row[v] = run_stage(text, heu["timeline"], c, layers, std, tok, lab, steps, warmup)
+                elif v == "elided":
+                    row[v] = run_stage(text, heu["timeline"], c, layers, {**std, "elide_recompute": True}, tok, lab,
+                                       steps, warmup)
+                else:
+                    full = ex.plan_for(text, s, "full")
+                    row[v] = run_stage(text, full["timeline"], c, layers, std, tok, lab, steps, warmup)
+            except ex.LynxError as err:
+                row[v] = {"error": str(err)[:200]}
+        hr = row.get("heu", {})
+        if "iteration_ms" in hr:
+            row["exposed_fraction_of_iteration"] = round(hr["exposed_recompute_ms"] / hr["iteration_ms"], 4)
+            rc = hr["recompute_on_demand_ms"] + hr["recompute_overlapped_ms"]
+            row["exposed_fraction_of_recompute"] = round(hr["exposed_recompute_ms"] / rc, 4) if rc else 0.0
+            if "iteration_ms" in row.get("elided", {}):
+                row["crosscheck_ms"] = round(hr["iteration_ms"] - row["elided"]["iteration_ms"], 3)
+        out[str(s)] = row
+    return out

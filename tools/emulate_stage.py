@@ -1,4 +1,5 @@
-"""One TP rank of each TP·PP stage (default the 7B TP2·PP4 headline) on one B200: exposed recompute with the plan's comm windows.
+"""One TP rank of each TP·PP stage on one B200 (default: the 7B TP2·PP4 headline): exposed
+recompute with the plan's comm windows. CLI over paper_2406_08756_b200/stage_emulation.py.
 
 The headline configuration (GPT-7B, micro-batch 32, TP2·PP4, 8 microbatches) needs eight GPUs;
 gpurun has one. This runs each stage's TP-rank-0 executor alone (exec.standalone_stage: pipeline
@@ -24,28 +25,9 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
-from paper_2406_08756_b200 import executor as ex  # noqa: E402
 from paper_2406_08756_b200 import gpt_profile as gp  # noqa: E402
 from paper_2406_08756_b200 import profiler  # noqa: E402
-
-
-def run(text, timeline, c, layers, opts, tok, lab, steps, warmup):
-    cfg = ex.make_config(c, layers, exec_opts={"standalone_stage": True, **opts})
-    e = ex.Executor(text, timeline, cfg)
-    try:
-        for _ in range(warmup):
-            e.step(tok, lab)
-        reps = []
-        for _ in range(steps):
-            e.step(tok, lab)
-            reps.append(e.report())
-    finally:
-        e.close()
-        torch.cuda.empty_cache()
-    r = min(reps, key=lambda x: x["iteration_ms"])
-    keys = ("iteration_ms", "comm_ms", "busy_ms", "exposed_recompute_ms", "recompute_on_demand_ms",
-            "recompute_overlapped_ms", "wait_on_recompute_ms", "recompute_launches", "pool_high_water_bytes")
-    return {k: r[k] for k in keys if k in r} | {"iteration_ms_each": [round(x["iteration_ms"], 3) for x in reps]}
+from paper_2406_08756_b200 import stage_emulation as se  # noqa: E402
 
 
 def main():
@@ -76,41 +58,22 @@ def main():
     _, total = torch.cuda.mem_get_info()
     c.mem_budget_bytes = int(a.budget_gb * 1e9) if a.budget_gb else bench.device_budget(c, total)
     text = gp.profile_text(c, times=times)
-    T, h = c.tokens, c.hidden
-    standin_us = 2.0 * (c.tp - 1) / c.tp * (2 * T * h) / (profiler.NVLINK_BUS_GBS * 1e3)
-    tok, lab = ex.synthetic_batch(c)
-    out = {"workload": f"gpt-{a.model} TP{c.tp}xPP{c.pp}, micro-batch {c.micro_batch}, seq {c.seq}, {c.n_microbatches} "
-                       f"microbatches; TP rank 0 of each stage alone on one B200",
-           "comm_model": {"standin_us_per_allreduce": round(standin_us, 3), "nvlink_bus_gbs": profiler.NVLINK_BUS_GBS,
-                          "bytes": 2 * T * h, "ctas": a.ctas,
+    out = {"workload": f"gpt-{a.model} TP{c.tp}xPP{c.pp}, micro-batch {c.micro_batch}, seq {c.seq}, "
+                       f"{c.n_microbatches} microbatches; TP rank 0 of each stage alone on one B200",
+           "comm_model": {"standin_us_per_allreduce": round(se.standin_us(c), 3),
+                          "nvlink_bus_gbs": profiler.NVLINK_BUS_GBS, "bytes": 2 * c.tokens * c.hidden, "ctas": a.ctas,
                           "note": "stand-in kernel holds the TP stream for the modelled transfer time; "
                                   "real NCCL SM/HBM contention not modelled"},
            "profiler_s": round(prof_s, 2), "ledger_budget_bytes": c.mem_budget_bytes,
-           "budget": "reduced (--budget-gb)" if a.budget_gb else "device HBM minus unmodelled reserve", "stages": {}}
-    std = {"comm_standin_us": standin_us, "comm_standin_ctas": a.ctas}
+           "budget": "reduced (--budget-gb)" if a.budget_gb else "device HBM minus unmodelled reserve",
+           "stages": {}}
     for s in (int(x) for x in a.stages.split(",")):
-        heu = ex.plan_for(text, s, "heu")
-        full = ex.plan_for(text, s, "full")
-        layers = heu["layers_per_stage"]
-        pj = json.loads(heu["plan_json"])
-        row = {"layers_per_stage": layers, "plan": {k: pj[k] for k in ("S", "phase_assignment", "peak_bytes")},
-               "simulated_period_us": heu["period_us"]}
-        row["heu"] = run(text, heu["timeline"], c, layers, std, tok, lab, a.steps, a.warmup)
-        row["elided"] = run(text, heu["timeline"], c, layers, {**std, "elide_recompute": True}, tok, lab,
-                            a.steps, a.warmup)
-        try:
-            row["full_recompute"] = run(text, full["timeline"], c, layers, std, tok, lab, a.steps, a.warmup)
-        except ex.LynxError as err:
-            row["full_recompute"] = {"error": str(err)[:200]}
-        hr, el = row["heu"], row["elided"]
-        row["exposed_fraction_of_iteration"] = round(hr["exposed_recompute_ms"] / hr["iteration_ms"], 4)
-        row["crosscheck_ms"] = round(hr["iteration_ms"] - el["iteration_ms"], 3)
-        rc = hr["recompute_on_demand_ms"] + hr["recompute_overlapped_ms"]
-        row["exposed_fraction_of_recompute"] = round(hr["exposed_recompute_ms"] / rc, 4) if rc else 0.0
+        row = se.emulate(c, text, [s], steps=a.steps, warmup=a.warmup, ctas=a.ctas)[str(s)]
         out["stages"][str(s)] = row
-        print(json.dumps({"stage": s, **{k: row[k] for k in ("exposed_fraction_of_iteration", "crosscheck_ms")},
-                          "heu_ms": hr["iteration_ms"], "elided_ms": el["iteration_ms"],
-                          "full_ms": row["full_recompute"].get("iteration_ms")}), flush=True)
+        print(json.dumps({"stage": s, "exposed_fraction_of_iteration": row.get("exposed_fraction_of_iteration"),
+                          "crosscheck_ms": row.get("crosscheck_ms"),
+                          **{f"{k}_ms": row[k].get("iteration_ms") for k in ("heu", "elided", "full_recompute")}}),
+              flush=True)
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(out, f, indent=1)
