@@ -313,15 +313,18 @@ def stage_emulation_summary(args, device_total: int) -> dict:
         h, el = row["heu"], row["elided"]
         return {"config": f"stage 0 of {c2.name} TP{c2.tp}xPP{c2.pp}, micro-batch {c2.micro_batch}, "
                           f"{c2.n_microbatches} microbatches ({row['layers_per_stage'][0]} layers + embedding), TP "
-                          "rank 0 alone on this B200; PP receives synthetic; each TP all-reduce a stand-in kernel "
-                          f"holding the TP stream {se.standin_us(c2):.1f} us (2(t-1)/t [T,h] bf16 at "
+                          "rank 0 alone on this B200; PP receives synthetic, each preceded by the stall the "
+                          "simulator predicts for this stage (stand-in kernel); each TP all-reduce a stand-in "
+                          f"kernel holding the TP stream {se.standin_us(c2):.1f} us (2(t-1)/t [T,h] bf16 at "
                           f"{profiler.NVLINK_BUS_GBS:g} GB/s; NCCL SM/HBM contention not modelled)",
                 "plan": row["plan"], "iteration_ms": round(h["iteration_ms"], 3),
                 "exposed_recompute_ms": round(h["exposed_recompute_ms"], 3),
                 "exposed_fraction_of_iteration": row["exposed_fraction_of_iteration"],
                 "recompute_overlapped_ms": round(h["recompute_overlapped_ms"], 3),
                 "elided_iteration_ms": round(el["iteration_ms"], 3), "crosscheck_ms": row["crosscheck_ms"],
-                "simulated_iteration_ms": round(float(row["simulated_period_us"]) * c2.n_microbatches / 1000.0, 3)}
+                "exposed_fraction_of_recompute": row["exposed_fraction_of_recompute"],
+                "pipeline_stall_ms": round(sum(row["grad_wait_us"]) / 1000.0, 3),
+                "simulated_busy_ms": round(float(row["simulated_period_us"]) * c2.n_microbatches / 1000.0, 3)}
     except Exception as err:  # reported, never fatal for the headline line
         return {"error": str(err).splitlines()[0][:200]}
 

@@ -186,6 +186,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.reserve_pool = ex.value("reserve_pool", true);
   opt_.comm_standin_us = ex.value("comm_standin_us", 0.0);
   opt_.comm_standin_ctas = ex.value("comm_standin_ctas", 16);
+  opt_.standin_grad_wait_us = ex.value("standin_grad_wait_us", std::vector<double>());
   cfg_.head_chunk = static_cast<int>(std::min<long long>(ex.value("head_chunk", 4096), cfg_.tokens()));
   if (cfg_.hidden % cfg_.heads || cfg_.heads % cfg_.tp || (cfg_.hidden / cfg_.tp) % 128)
     throw RtError("hidden must split into heads and TP ranks in 128-column tiles", kValidation);
@@ -203,6 +204,8 @@ void Executor::parse_config(const std::string& text) {
                   kValidation);
   if (opt_.comm_standin_us > 0 && !opt_.standalone)
     throw RtError("exec.comm_standin_us is a standalone_stage option", kValidation);
+  if (!opt_.standin_grad_wait_us.empty() && !opt_.standalone)
+    throw RtError("exec.standin_grad_wait_us is a standalone_stage option", kValidation);
   if (opt_.comm_standin_ctas < 1 || opt_.comm_standin_ctas > 148)
     throw RtError("exec.comm_standin_ctas must be in [1, 148]", kValidation);
 }
@@ -1022,6 +1025,18 @@ void Executor::backward_pass(int mb) {
     grad_[mb].dy = alloc(2 * T * h, main_);
     program_.push_back({"recv", "pp_grad", cfg_.pp_rank + 1, static_cast<size_t>(2 * T * h), "B mb" + std::to_string(mb)});
     if (opt_.standalone && !opt_.dry_run) {
+      const double wait_us = mb < static_cast<int>(opt_.standin_grad_wait_us.size()) ? opt_.standin_grad_wait_us[mb] : 0;
+      if (wait_us > 0) {  // the modelled pipeline stall before this gradient arrives
+        cudaEvent_t a = ev();
+        ck(cudaEventRecord(a, main_), "event");
+        ck(cudaStreamWaitEvent(pg_s_, a, 0), "wait");
+        ck_op(comm_standin(static_cast<unsigned long long>(wait_us * 1e3), 1, pg_s_), "recv stand-in");
+        cudaEvent_t b = ev();
+        ck(cudaEventRecord(b, pg_s_), "event");
+        span_begin(main_, 5, mb);
+        ck(cudaStreamWaitEvent(main_, b, 0), "wait");
+        span_end(main_);
+      }
       ck(cudaMemcpyAsync(grad_[mb].dy, syn_grad_, static_cast<size_t>(2 * T * h), cudaMemcpyDeviceToDevice, main_),
          "synthetic gradient");
     } else if (!opt_.dry_run) {

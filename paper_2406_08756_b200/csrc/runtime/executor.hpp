@@ -51,6 +51,10 @@ struct ExecOptions {
   double comm_standin_us = 0;   // > 0 (standalone only): each TP all-reduce is replaced by a stand-in
   int comm_standin_ctas = 16;   // kernel holding the TP stream this long, so one GPU runs one TP rank
                                 // of a TP > 1 stage with the plan's comm windows (window overlap)
+  std::vector<double> standin_grad_wait_us;  // standalone: per microbatch m, the pipeline stall before
+                                             // B(m)'s gradient receive (from the simulator's trace),
+                                             // held by a stand-in kernel so stall-fill recomputes
+                                             // meet the bubble they are planned into
 };
 
 struct Slot {

@@ -8,6 +8,14 @@ that holds the TP stream for the transfer time the plan's window capacities assu
 windows (expand_plan_to_stage, heusched.cpp:372-405) run on the side stream against it, so window
 overlap, on-demand recompute and waits are measured on real B200 kernels. The SM and HBM traffic of
 a real NCCL all-reduce is not modelled (the stand-in sleeps on `ctas` CTAs).
+
+Pipeline bubbles: alone, a stage's receives complete at once, so the cool-down stall-fill items
+(expand_plan_to_stage, heusched.cpp:374-380), planned into the wait for the next gradient, would
+meet no wait. With `bubbles`, the stall the native simulator predicts before each backward's
+gradient receive on this stage (its trace, pipesim.cpp:620-646) is held by a stand-in kernel on
+the gradient stream (exec.standin_grad_wait_us), so the stage runs its pipelined timeline: the
+stall-fill recomputes overlap it, and the iteration includes the stage's warm-up / cool-down
+bubbles. Forward (activation) receive stalls are not emulated.
 """
 from __future__ import annotations
 
@@ -15,12 +23,34 @@ import json
 
 from . import executor as ex
 from . import gpt_profile as gp
+from . import planner
 from . import profiler
 
 
 def standin_us(c: gp.GPTConfig) -> float:
     """Modelled TP all-reduce time of one [T, h] bf16 tensor (the profiler's comm model)."""
     return 2.0 * (c.tp - 1) / c.tp * (2 * c.tokens * c.hidden) / (profiler.NVLINK_BUS_GBS * 1e3)
+
+
+def simulated_grad_waits(text: str, stage: int, n_micro: int) -> list[float]:
+    """Per microbatch m: the stall (µs) the simulator puts on `stage` before B(m) starts (its
+    gradient receive), from the native simulator's CSV trace of the HEU plans."""
+    rows = [r.split(",") for r in planner.simulate_text(text, "heu", fmt="csv").splitlines()[1:]]
+    waits, pending = [0.0] * n_micro, 0.0
+    for r in rows:
+        if r[0] != str(stage):
+            continue
+        kind = r[2]
+        if kind == "stall":
+            pending += float(r[5]) - float(r[4])
+        elif kind in ("p2p", "stall_recompute", "recompute"):
+            continue
+        elif kind in ("bwd", "comm_bwd"):
+            waits[int(r[1])] += pending
+            pending = 0.0
+        else:  # a forward receive stall: not emulated
+            pending = 0.0
+    return waits
 
 
 def run_stage(text: str, timeline: dict, c: gp.GPTConfig, layers, opts: dict, tok, lab, steps: int = 2,
@@ -40,24 +70,27 @@ def run_stage(text: str, timeline: dict, c: gp.GPTConfig, layers, opts: dict, to
         e.close()
         torch.cuda.empty_cache()
     r = min(reps, key=lambda x: x["iteration_ms"])
-    keys = ("iteration_ms", "comm_ms", "busy_ms", "exposed_recompute_ms", "recompute_on_demand_ms",
+    keys = ("iteration_ms", "comm_ms", "busy_ms", "recv_wait_ms", "exposed_recompute_ms", "recompute_on_demand_ms",
             "recompute_overlapped_ms", "wait_on_recompute_ms", "recompute_launches", "pool_high_water_bytes")
     return {k: r[k] for k in keys if k in r} | {"iteration_ms_each": [round(x["iteration_ms"], 3) for x in reps]}
 
 
 def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int = 1, ctas: int = 16,
-            variants=("heu", "elided", "full_recompute")) -> dict:
+            variants=("heu", "elided", "full_recompute"), bubbles: bool = True) -> dict:
     """Per stage: its HEU plan, the same plan with recompute elided (no-recompute floor) and
     Megatron full recompute, each as one TP rank with stand-in all-reduces."""
     std = {"comm_standin_us": standin_us(c), "comm_standin_ctas": ctas}
     tok, lab = ex.synthetic_batch(c)
     out = {}
     for s in stages:
+        waits = simulated_grad_waits(text, s, c.n_microbatches) if bubbles else []
+        std = {**std, "standin_grad_wait_us": waits}
         heu = ex.plan_for(text, s, "heu")
         layers = heu["layers_per_stage"]
         pj = json.loads(heu["plan_json"])
         row = {"layers_per_stage": layers, "plan": {k: pj[k] for k in ("S", "phase_assignment", "peak_bytes")},
-               "simulated_period_us": heu["period_us"]}
+               "simulated_period_us": heu["period_us"],
+               "grad_wait_us": [round(w, 1) for w in waits]}
         for v in variants:
             try:
                 if v == "heu":
