@@ -165,7 +165,8 @@ def test_selective_plan_is_bit_identical(cuda):
 def test_comm_standin_stage_windows_are_bit_identical(cuda):
     """One TP rank of a TP2·PP2 stage alone on the GPU (tools/emulate_stage.py): all-reduces become
     stand-in kernels holding the TP stream for the modelled transfer time, so the HEU plan's window
-    recomputes overlap them on the side stream. Regenerated tensors equal their forward copies, the
+    recomputes overlap them on the side stream; the simulator's pipeline stalls hold the gradient
+    receives (stall-fill recomputes run inside them). Regenerated tensors equal their forward copies, the
     stage's gradients equal the retain-all run's, and the TP stream is busy at least the modelled
     time per all-reduce."""
     from paper_2406_08756_b200 import executor as ex
@@ -176,12 +177,15 @@ def test_comm_standin_stage_windows_are_bit_identical(cuda):
     text = gp.profile_text(c)
     tok, lab = ex.synthetic_batch(c)
     us = 200.0
+    from paper_2406_08756_b200 import stage_emulation as se
     for s in (0, 1):
+        waits = se.simulated_grad_waits(text, s, c.n_microbatches)
         grads = {}
         for baseline in ("heu", "retain_all"):
             plan = ex.plan_for(text, s, baseline)
             layers = plan["layers_per_stage"]
-            opts = {"standalone_stage": True, "comm_standin_us": us, "check_recompute": baseline == "heu"}
+            opts = {"standalone_stage": True, "comm_standin_us": us, "check_recompute": baseline == "heu",
+                    "standin_grad_wait_us": waits}
             e = ex.Executor(text, plan["timeline"], ex.make_config(c, layers, exec_opts=opts))
             shapes = ex.param_shapes(c, layers[s], s == 0, s == c.pp - 1)
             e.step(tok, lab)
@@ -192,6 +196,7 @@ def test_comm_standin_stage_windows_are_bit_identical(cuda):
             n_ar = sum(1 for o in prog if o["comm"] == "tp")
             assert n_ar >= 4 * layers[s] * c.n_microbatches
             assert rep["comm_ms"] >= 0.95 * n_ar * us / 1000.0, (rep["comm_ms"], n_ar)
+            assert rep["recv_wait_ms"] >= 0.95 * sum(waits) / 1000.0, (rep["recv_wait_ms"], waits)
             if baseline == "heu" and s == 0:
                 assert any(it["host"] == "window" for it in plan["timeline"]["items"])
                 assert rep["recompute_overlapped_ms"] > 0 and rep["recompute_checked"] > 0
