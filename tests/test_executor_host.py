@@ -72,7 +72,6 @@ def test_single_gpu_program_has_no_collectives():
 
 def test_executor_rejects_foreign_templates():
     from paper_2406_08756_b200._native import LynxError
-    prof = json.loads(open("/dev/null").read() or "{}") if False else None
     c = gp.CONFIGS["tiny"]
     text = json.loads(gp.profile_text(c))
     text["model"]["layer"]["ops"][1]["name"] = "mystery"
