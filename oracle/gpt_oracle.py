@@ -56,7 +56,7 @@ def gpt_step(params: dict[str, np.ndarray], shapes: dict[str, tuple], tokens: np
         logits = yf @ P["w_head"].t()
         loss = F.cross_entropy(logits, lab[m], reduction="sum") / (T * n_micro)
         loss.backward()
-        total += float(loss)
+        total += float(loss.detach())
     grads = {k: v.grad.numpy().ravel().copy() if v.grad is not None else np.zeros(v.numel(), np.float32)
              for k, v in P.items()}
     return total, grads
