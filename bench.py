@@ -26,6 +26,7 @@ import subprocess
 import sys
 import threading
 import time
+from fractions import Fraction
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -409,7 +410,13 @@ def run_gpu_arm(args):
     peaks = measured_peaks()
     roof = gemm_roofline(c, peaks) if rank == 0 else None  # before the executor owns the HBM
     times, prof_s = None, 0.0
-    if args.profile == "measured":
+    if args.op_times:
+        # Replay the operator times of an earlier run (a bench JSON line or a flat {op: us} map), so a
+        # profiled run (ncu serialises and slows every kernel) plans exactly as the measured run did.
+        doc = json.load(open(args.op_times))
+        doc = doc.get("recompute", {}).get("op_times_us", doc)
+        times = {k: Fraction(str(v)) for k, v in doc.items()}
+    elif args.profile == "measured":
         # B200-measured operator times drive the plan; rank 0 measures and
         # broadcasts so that every rank plans from the same profile document.
         from paper_2406_08756_b200 import profiler
@@ -516,7 +523,7 @@ def run_gpu_arm(args):
                       "launches_per_iter": rep["recompute_launches"],
                       "on_demand_ms": rep["recompute_on_demand_ms"], "overlapped_ms": rep["recompute_overlapped_ms"],
                       "wait_on_recompute_ms": rep["wait_on_recompute_ms"], "baselines": extra or None,
-                      "profile": args.profile, "profiler_s": round(prof_s, 2),
+                      "profile": ("replayed " + args.op_times) if args.op_times else args.profile, "profiler_s": round(prof_s, 2),
                       "op_times_us": {k: float(v) for k, v in (times or {}).items()}},
         "tp2pp4_stage_emulation": emu,
         "memory": {"ledger_budget_bytes": c.mem_budget_bytes, "plan_peak_bytes": plan0["peak_bytes"],
@@ -575,6 +582,7 @@ def main():
     ap.add_argument("--gemm-mode", type=int, default=-1, help="lynx_op_gemm_mode (-1 default, 0 single-CTA, 1 pair)")
     ap.add_argument("--profile", default="measured", choices=["measured", "estimated"],
                     help="operator times for the planner: B200-measured (default) or the analytic estimate")
+    ap.add_argument("--op-times", default="", help="plan from the op times of an earlier bench JSON line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-crosscheck", action="store_true", help="skip the recompute-elided timing run")
     ap.add_argument("--no-stage-emulation", action="store_true",
