@@ -225,6 +225,16 @@ def reference_planner(total_bytes: int, model: str) -> dict | None:
         return {"error": str(e).splitlines()[0][:200]}
 
 
+def load_op_times(path: str) -> dict:
+    """Operator times (µs, exact decimal Fractions) of an earlier run — a bench JSON line or a flat
+    {op: us} map — so a profiled run (ncu serialises and slows every kernel) plans exactly as the
+    measured run did."""
+    with open(path) as f:
+        doc = json.load(f)
+    doc = doc.get("recompute", {}).get("op_times_us", doc)
+    return {k: Fraction(str(v)) for k, v in doc.items()}
+
+
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -411,11 +421,7 @@ def run_gpu_arm(args):
     roof = gemm_roofline(c, peaks) if rank == 0 else None  # before the executor owns the HBM
     times, prof_s = None, 0.0
     if args.op_times:
-        # Replay the operator times of an earlier run (a bench JSON line or a flat {op: us} map), so a
-        # profiled run (ncu serialises and slows every kernel) plans exactly as the measured run did.
-        doc = json.load(open(args.op_times))
-        doc = doc.get("recompute", {}).get("op_times_us", doc)
-        times = {k: Fraction(str(v)) for k, v in doc.items()}
+        times = load_op_times(args.op_times)
     elif args.profile == "measured":
         # B200-measured operator times drive the plan; rank 0 measures and
         # broadcasts so that every rank plans from the same profile document.

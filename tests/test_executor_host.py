@@ -102,3 +102,27 @@ def test_comm_standin_stage_program():
                  {"dry_run": True, "comm_standin_us": 500.0}):
         with pytest.raises(LynxError):
             ex.Executor(text, plans[0]["timeline"], ex.make_config(c, layers, exec_opts=opts))
+
+
+def test_bench_op_times_replay_reproduces_the_measured_plan(tmp_path):
+    """`bench.py --op-times` (used for ncu launch lists): the committed bench line's operator times
+    give back the plan that line ran (same S, phases and exact peak bytes), and a flat map loads too."""
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root))
+    import bench
+    line_path = root / "profiles" / "r01_bench_n1.json"
+    line = json.loads(line_path.read_text())
+    times = bench.load_op_times(str(line_path))
+    flat = tmp_path / "times.json"
+    flat.write_text(json.dumps(line["recompute"]["op_times_us"]))
+    assert bench.load_op_times(str(flat)) == times
+    import argparse
+    c = bench.config_for(1, argparse.Namespace(gpus=1, model="7b", micro_batch=0, microbatches=0, plan="heu"))
+    c.mem_budget_bytes = line["memory"]["ledger_budget_bytes"]
+    plans, _ = bench.plan_all(c, gp.profile_text(c, times=times), "heu")
+    got = json.loads(plans[0]["plan_json"])
+    want = line["recompute"]["plan"]
+    assert (got["S"], got["phase_assignment"], got["peak_bytes"]) == (want["S"], want["phase_assignment"],
+                                                                       want["peak_bytes"])
