@@ -7,8 +7,22 @@ restatement of the model the executor runs (Megatron-style pre-LN GPT block,
 gpt_profile.py templates): token + position embedding, per layer
 LN1 -> QKV -> causal softmax attention -> projection + residual -> LN2 -> FC1
 -> tanh-GeLU -> FC2 + residual, final LN, untied LM head, mean token
-cross-entropy over all microbatches. Dropout is off (p = 0) for parity runs.
-Used only by tests/ and bench.py's cpu_baseline leg.
+cross-entropy over all microbatches.
+
+Dropout (hidden dropout on the embedding and on both residual branches; the
+attention probabilities are not dropped) uses the executor's masks exactly:
+Philox-4x32-10 (Salmon et al., SC'11; the Random123 algorithm, pinned by its
+published known-answer vectors in tests/test_oracle.py) keyed by the step seed,
+with the counter (element group, stream id) and stream ids
+  embedding        (0xFFFF << 32) | mb
+  attention branch ((layer + 1) << 32) | (mb << 8) | 5
+  MLP branch       ((layer + 1) << 32) | (mb << 8) | 11
+(layer = global layer index, mb = microbatch of the step), element e of a
+[tokens, hidden] tensor drawing word e % 4 of group e // 4, kept iff the draw is
+>= floor(p * 2^32); kept values are scaled by 1 / (1 - p) in fp32.
+(executor.cpp drop_stream / kEmbedStream, common.cuh keep_bits8.)
+
+Used only by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg.
 """
 from __future__ import annotations
 
@@ -18,6 +32,53 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
+_M0, _M1 = 0xD2511F53, 0xCD9E8D57
+_W0, _W1 = 0x9E3779B9, 0xBB67AE85
+_U32 = np.uint64(0xFFFFFFFF)
+EMBED_STREAM = 0xFFFF << 32
+SITE_ATTN, SITE_MLP = 5, 11  # Op::PROJ_RES, Op::FC2_RES (runtime/gpt_stage.hpp)
+
+
+def philox4x32_10(ctr: tuple, key: tuple) -> tuple:
+    """Philox-4x32-10 on numpy arrays of uint32 values (held in uint64). ctr = 4 words, key = 2 words."""
+    c0, c1, c2, c3 = (np.asarray(x, dtype=np.uint64) & _U32 for x in ctr)
+    k0, k1 = np.uint64(key[0]) & _U32, np.uint64(key[1]) & _U32
+    m0, m1 = np.uint64(_M0), np.uint64(_M1)
+    for _ in range(10):
+        p0 = m0 * c0
+        p1 = m1 * c2
+        hi0, lo0 = p0 >> np.uint64(32), p0 & _U32
+        hi1, lo1 = p1 >> np.uint64(32), p1 & _U32
+        c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+        k0 = (k0 + np.uint64(_W0)) & _U32
+        k1 = (k1 + np.uint64(_W1)) & _U32
+    return c0, c1, c2, c3
+
+
+def drop_threshold(p: float) -> int:
+    t = float(np.float32(p)) * 4294967296.0
+    return 0xFFFFFFFF if t >= 4294967295.0 else int(t)
+
+
+def keep_mask(seed: int, stream: int, n: int, p: float) -> np.ndarray:
+    """Bool keep-mask of n consecutive elements of dropout stream `stream` (common.cuh keep_bits8)."""
+    if p <= 0:
+        return np.ones(n, dtype=bool)
+    groups = np.arange((n + 3) // 4, dtype=np.uint64)
+    r = philox4x32_10((groups & _U32, groups >> np.uint64(32), np.full_like(groups, stream & 0xFFFFFFFF),
+                       np.full_like(groups, stream >> 32)), (seed & 0xFFFFFFFF, seed >> 32))
+    draws = np.stack(r, axis=1).reshape(-1)[:n]
+    return draws >= np.uint64(drop_threshold(p))
+
+
+def step_seed(seed: int, step: int) -> int:
+    """Dropout key of training step `step` (1-based), executor.cpp."""
+    return seed + step * 1000003
+
+
+def layer_stream(layer: int, mb: int, site: int) -> int:
+    return ((layer + 1) << 32) | (mb << 8) | site
+
 
 def _t(a: np.ndarray, shape) -> torch.Tensor:
     return torch.tensor(np.asarray(a, dtype=np.float32).reshape(shape), requires_grad=True)
@@ -25,8 +86,10 @@ def _t(a: np.ndarray, shape) -> torch.Tensor:
 
 def gpt_step(params: dict[str, np.ndarray], shapes: dict[str, tuple], tokens: np.ndarray, labels: np.ndarray, *,
              n_layers: int, hidden: int, heads: int, seq: int, micro_batch: int, n_micro: int, eps: float = 1e-5,
+             dropout: float = 0.0, seed: int = 42, step: int = 1,
              threads: int | None = None) -> tuple[float, dict[str, np.ndarray]]:
-    """Returns (mean token loss, fp32 gradients by parameter name)."""
+    """Returns (mean token loss, fp32 gradients by parameter name) of one training step on the
+    UNSHARDED model (parameter names as a TP = 1, PP = 1 executor reports them)."""
     if threads:
         torch.set_num_threads(threads)
     P = {k: _t(v, shapes[k]) for k, v in params.items()}
@@ -35,10 +98,19 @@ def gpt_step(params: dict[str, np.ndarray], shapes: dict[str, tuple], tokens: np
     tok = torch.tensor(tokens.reshape(n_micro, T).astype(np.int64))
     lab = torch.tensor(labels.reshape(n_micro, T).astype(np.int64))
     mask = torch.ones(seq, seq, dtype=torch.bool).triu(1)
+    key = step_seed(seed, step)
+    scale = float(np.float32(1.0) / (np.float32(1.0) - np.float32(dropout))) if dropout > 0 else 1.0
+
+    def drop(x: torch.Tensor, stream: int) -> torch.Tensor:
+        if dropout <= 0:
+            return x
+        keep = torch.from_numpy(keep_mask(key, stream, x.numel(), dropout).reshape(x.shape))
+        return torch.where(keep, x * scale, torch.zeros((), dtype=x.dtype))
+
     total = 0.0
     for m in range(n_micro):
         pos = torch.arange(T) % seq
-        x = P["wte"][tok[m]] + P["wpe"][pos]
+        x = drop(P["wte"][tok[m]] + P["wpe"][pos], EMBED_STREAM | m)
         for l in range(n_layers):
             p = f"l{l}."
             y = F.layer_norm(x, (hidden,), P[p + "ln1_g"], P[p + "ln1_b"], eps)
@@ -47,11 +119,11 @@ def gpt_step(params: dict[str, np.ndarray], shapes: dict[str, tuple], tokens: np
             att = (q @ k.transpose(-1, -2)) / math.sqrt(D)
             att = att.masked_fill(mask, float("-inf")).softmax(-1)
             o = (att @ v).permute(0, 2, 1, 3).reshape(T, hidden)
-            res1 = x + o @ P[p + "w_proj"].t() + P[p + "b_proj"]
+            res1 = x + drop(o @ P[p + "w_proj"].t() + P[p + "b_proj"], layer_stream(l, m, SITE_ATTN))
             y2 = F.layer_norm(res1, (hidden,), P[p + "ln2_g"], P[p + "ln2_b"], eps)
             f1 = y2 @ P[p + "w_fc1"].t() + P[p + "b_fc1"]
             g = F.gelu(f1, approximate="tanh")
-            x = res1 + g @ P[p + "w_fc2"].t() + P[p + "b_fc2"]
+            x = res1 + drop(g @ P[p + "w_fc2"].t() + P[p + "b_fc2"], layer_stream(l, m, SITE_MLP))
         yf = F.layer_norm(x, (hidden,), P["lnf_g"], P["lnf_b"], eps)
         logits = yf @ P["w_head"].t()
         loss = F.cross_entropy(logits, lab[m], reduction="sum") / (T * n_micro)

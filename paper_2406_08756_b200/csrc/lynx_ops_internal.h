@@ -129,6 +129,13 @@ int fill_param(__nv_bfloat16* p, float* master, float v, long long n, cudaStream
 int count_mismatch(const void* a, const void* b, size_t bytes, unsigned long long* d_count, cudaStream_t s);
 int init_normal_bf16(__nv_bfloat16* p, float* master, long long n, float std, uint64_t seed, uint64_t stream_id,
                      cudaStream_t s);
+// Shard of an unsharded N(0, std) tensor (values identical to init_normal_bf16 of the full tensor;
+// see ops_elementwise.cu for the index map): Megatron column splits use row_blk (QKV: hp, FC1: 4hp),
+// row splits col_split (projection, FC2).
+int init_normal_sharded_bf16(__nv_bfloat16* p, float* master, long long rows, long long cols, long long row_blk,
+                             int col_split, int tp, int tp_rank, float std, uint64_t seed, uint64_t stream_id,
+                             cudaStream_t s);
+int f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s);
 // Single-GPU stand-in for a collective (exec.comm_standin_us): `ctas` CTAs of 512 threads hold
 // the stream for `ns` nanoseconds of %globaltimer, sleeping between polls. Models the transfer
 // time of an NCCL all-reduce the plan's window capacity assumes; not its SM / HBM traffic.

@@ -125,37 +125,134 @@ __global__ void embedding_fwd_kernel(const int32_t* __restrict__ tok, const BF8*
   }
 }
 
-// d(pre-dropout) for the embedding: masked gradient, then dwte (fp32 atomics,
-// see DESIGN.md) and dwpe (deterministic: reduced over the batch in order).
-__global__ void embedding_wte_bwd_kernel(const int32_t* __restrict__ tok, const BF8* __restrict__ dout,
-                                         float* __restrict__ dwte, float* __restrict__ gmasked, long long nvec,
-                                         int wvec, float p, uint64_t seed, uint64_t stream) {
-  const uint32_t thr = drop_threshold(p);
-  const float scale = p > 0.f ? 1.f / (1.f - p) : 1.f;
-  for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < nvec;
-       v += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long row = v / wvec;
-    const int c = static_cast<int>(v % wvec);
-    float d[8];
-    bf8_to_f(dout[v], d);
-    const uint32_t keep = p > 0.f ? keep_bits8(seed, stream, v, thr) : 0xFFu;
-    float* dst = dwte + static_cast<long long>(tok[row]) * wvec * 8 + c * 8;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float g = ((keep >> j) & 1u) ? d[j] * scale : 0.f;
-      gmasked[v * 8 + j] = g;
-      atomicAdd(dst + j, g);
-    }
+// ---------------------------------------------------------------- embedding backward
+// Deterministic: no floating-point atomics. The microbatch's (token, position) pairs are sorted as
+// 64-bit keys (token << 32 | position) by a bitonic network; each run of equal tokens is then
+// summed by ONE thread block in ascending position order (fixed order, fp32) and added to that
+// token's row of the fp32 accumulator, which no other block touches. wpe's gradient reduces the
+// batch in order. Gradients are bit-reproducible however often tokens collide.
+constexpr int kSortBlock = 2048;  // keys per shared-memory bitonic block (1024 threads, 16 KB)
+
+__device__ __forceinline__ void cmp_swap(uint64_t& a, uint64_t& b, bool up) {
+  if ((a > b) == up) {
+    const uint64_t t = a;
+    a = b;
+    b = t;
   }
 }
 
-__global__ void embedding_wpe_bwd_kernel(const float* __restrict__ gmasked, float* __restrict__ dwpe, int batch,
-                                         int seq, int width) {
-  const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-  if (idx >= static_cast<long long>(seq) * width) return;
-  float s = 0.f;
-  for (int b = 0; b < batch; ++b) s += gmasked[static_cast<long long>(b) * seq * width + idx];
-  dwpe[idx] += s;
+__global__ void sort_keys_init_kernel(const int32_t* __restrict__ tok, uint64_t* __restrict__ keys, long long n,
+                                      long long n_pad) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n_pad;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    keys[i] = i < n ? (static_cast<uint64_t>(static_cast<uint32_t>(tok[i])) << 32) | static_cast<uint64_t>(i)
+                    : ~0ull;
+}
+
+// Bitonic stages k = 2 .. kmax (or the merge steps j < block of stage k = kmax when merge_only),
+// on one shared-memory block of `blk` keys; directions follow the global index, so blocks compose.
+__global__ void __launch_bounds__(kSortBlock / 2) bitonic_block_kernel(uint64_t* __restrict__ keys, int blk,
+                                                                       long long kmax, int merge_only) {
+  __shared__ uint64_t sh[kSortBlock];
+  const long long base = static_cast<long long>(blockIdx.x) * blk;
+  for (int i = threadIdx.x; i < blk; i += blockDim.x) sh[i] = keys[base + i];
+  __syncthreads();
+  const long long k0 = merge_only ? kmax : 2;
+  for (long long k = k0; k <= kmax; k <<= 1) {
+    for (long long j = (merge_only ? blk : k) >> 1; j > 0; j >>= 1) {
+      if (j >= k) continue;
+      for (int t = threadIdx.x; t < blk / 2; t += blockDim.x) {
+        const int lo = static_cast<int>((t / j) * 2 * j + (t % j));
+        const int hi = lo + static_cast<int>(j);
+        const bool up = ((base + lo) & k) == 0;
+        cmp_swap(sh[lo], sh[hi], up);
+      }
+      __syncthreads();
+    }
+    if (merge_only) break;
+  }
+  for (int i = threadIdx.x; i < blk; i += blockDim.x) keys[base + i] = sh[i];
+}
+
+// One global compare-exchange step (stride j >= block) of bitonic stage k.
+__global__ void bitonic_global_kernel(uint64_t* __restrict__ keys, long long n_pad, long long k, long long j) {
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n_pad / 2;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long lo = (t / j) * 2 * j + (t % j);
+    const long long hi = lo + j;
+    uint64_t a = keys[lo], b = keys[hi];
+    cmp_swap(a, b, (lo & k) == 0);
+    keys[lo] = a;
+    keys[hi] = b;
+  }
+}
+
+// Block b handles sorted entry b if it starts a run of equal tokens: the run's dropout-masked
+// output-gradient rows are summed in position order and added to dwte[token].
+__global__ void __launch_bounds__(128) embedding_wte_segsum_kernel(const uint64_t* __restrict__ keys,
+                                                                   const BF8* __restrict__ dout,
+                                                                   float* __restrict__ dwte, long long n, int wvec,
+                                                                   float p, uint64_t seed, uint64_t stream) {
+  const long long i = blockIdx.x;
+  const uint32_t tok = static_cast<uint32_t>(keys[i] >> 32);
+  if (i > 0 && static_cast<uint32_t>(keys[i - 1] >> 32) == tok) return;
+  long long end = i + 1;
+  while (end < n && static_cast<uint32_t>(keys[end] >> 32) == tok) ++end;
+  const uint32_t thr = drop_threshold(p);
+  const float scale = p > 0.f ? 1.f / (1.f - p) : 1.f;
+  for (int c = threadIdx.x; c < wvec; c += blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (long long r = i; r < end; ++r) {
+      const long long pos = static_cast<long long>(keys[r] & 0xFFFFFFFFull);
+      const long long v = pos * wvec + c;
+      float d[8];
+      bf8_to_f(dout[v], d);
+      const uint32_t keep = p > 0.f ? keep_bits8(seed, stream, v, thr) : 0xFFu;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += ((keep >> j) & 1u) ? d[j] * scale : 0.f;
+    }
+    float4* dst = reinterpret_cast<float4*>(dwte + (static_cast<long long>(tok) * wvec + c) * 8);
+    float4 x0 = dst[0], x1 = dst[1];
+    x0.x += acc[0];
+    x0.y += acc[1];
+    x0.z += acc[2];
+    x0.w += acc[3];
+    x1.x += acc[4];
+    x1.y += acc[5];
+    x1.z += acc[6];
+    x1.w += acc[7];
+    dst[0] = x0;
+    dst[1] = x1;
+  }
+}
+
+// dwpe[s, :] += sum_b mask * dout[b, s, :] (batch in order).
+__global__ void embedding_wpe_bwd_kernel(const BF8* __restrict__ dout, float* __restrict__ dwpe, int batch, int seq,
+                                         int wvec, float p, uint64_t seed, uint64_t stream) {
+  const uint32_t thr = drop_threshold(p);
+  const float scale = p > 0.f ? 1.f / (1.f - p) : 1.f;
+  const long long n = static_cast<long long>(seq) * wvec;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < n;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int b = 0; b < batch; ++b) {
+      const long long v = static_cast<long long>(b) * n + idx;
+      float d[8];
+      bf8_to_f(dout[v], d);
+      const uint32_t keep = p > 0.f ? keep_bits8(seed, stream, v, thr) : 0xFFu;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += ((keep >> j) & 1u) ? d[j] * scale : 0.f;
+    }
+    float* dst = dwpe + idx * 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dst[j] += acc[j];
+  }
+}
+
+long long sort_pad(long long n) {
+  long long m = 2;
+  while (m < n) m <<= 1;
+  return m;
 }
 
 // Row-wise cross-entropy over the vocabulary, in place: logits -> dlogits.
@@ -321,7 +418,56 @@ __global__ void init_normal_kernel(__nv_bfloat16* __restrict__ p, float* __restr
   }
 }
 
+// One shard of a tensor whose values are defined on the UNSHARDED index space: element (i, c) of
+// the local [rows, cols] block is element g of the full tensor, with
+//   full row = row_blk ? (i / row_blk) * row_blk * tp + tp_rank * row_blk + i % row_blk : i
+//   full col = col_split ? tp_rank * cols + c : c,   g = full_row * full_cols + full_col,
+// and takes the value init_normal_kernel gives element g (Box-Muller pair g / 2, member g % 2).
+// So a TP rank's column / row slice holds exactly the values of the TP = 1 model.
+__global__ void init_normal_sharded_kernel(__nv_bfloat16* __restrict__ p, float* __restrict__ master, long long rows,
+                                           long long cols, long long row_blk, int col_split, int tp, int tp_rank,
+                                           float std, uint64_t seed, uint64_t stream) {
+  const long long n = rows * cols, full_cols = col_split ? cols * tp : cols;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e / cols, c = e % cols;
+    const long long gr = row_blk ? (i / row_blk) * row_blk * tp + tp_rank * row_blk + i % row_blk : i;
+    const long long gc = col_split ? tp_rank * cols + c : c;
+    const long long g = gr * full_cols + gc;
+    const uint4 r = philox_group(seed, stream, static_cast<uint64_t>(g >> 1));
+    const float u1 = (r.x + 1.0f) * 2.3283064365386963e-10f;  // (0, 1]
+    const float u2 = r.y * 2.3283064365386963e-10f;
+    const float rad = sqrtf(-2.f * logf(u1));
+    const float z = (g & 1) ? rad * sinf(6.283185307179586f * u2) * std : rad * cosf(6.283185307179586f * u2) * std;
+    const __nv_bfloat16 b = f2bf(z);
+    p[e] = b;
+    if (master) master[e] = bf2f(b);
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, long long n) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = f2bf(src[i]);
+}
+
 }  // namespace
+
+int init_normal_sharded_bf16(__nv_bfloat16* p, float* master, long long rows, long long cols, long long row_blk,
+                             int col_split, int tp, int tp_rank, float std, uint64_t seed, uint64_t stream_id,
+                             cudaStream_t s) {
+  if (!rows || !cols) return kOk;
+  if (row_blk && rows % row_blk) return set_error("init_normal_sharded: rows % row_blk", kValidation);
+  init_normal_sharded_kernel<<<grid_for(rows * cols), kBlock, 0, s>>>(p, master, rows, cols, row_blk, col_split, tp,
+                                                                       tp_rank, std, seed, stream_id);
+  return check_launch("init_normal_sharded_bf16");
+}
+
+int f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s) {
+  if (!n) return kOk;
+  f32_to_bf16_kernel<<<grid_for(n), kBlock, 0, s>>>(src, dst, n);
+  return check_launch("f32_to_bf16");
+}
 
 int bias_dropout_residual_fwd(const __nv_bfloat16* y, const __nv_bfloat16* bias, const __nv_bfloat16* res,
                               __nv_bfloat16* out, long long rows, int width, float p, uint64_t seed,
@@ -382,7 +528,8 @@ int embedding_fwd(const int32_t* tokens, const __nv_bfloat16* wte, const __nv_bf
 }
 
 size_t embedding_bwd_workspace(int batch, int seq, int width) {
-  return static_cast<size_t>(batch) * seq * width * sizeof(float);
+  (void)width;
+  return static_cast<size_t>(sort_pad(static_cast<long long>(batch) * seq)) * sizeof(uint64_t);
 }
 
 int embedding_bwd(const int32_t* tokens, const __nv_bfloat16* dout, float* dwte, float* dwpe, float* workspace,
@@ -390,13 +537,30 @@ int embedding_bwd(const int32_t* tokens, const __nv_bfloat16* dout, float* dwte,
                   cudaStream_t s) {
   (void)vocab;
   if (width % 8) return set_error("embedding: width % 8", kValidation);
-  const long long nvec = static_cast<long long>(batch) * seq * width / 8;
-  embedding_wte_bwd_kernel<<<grid_for(nvec), kBlock, 0, s>>>(tokens, reinterpret_cast<const BF8*>(dout), dwte,
-                                                             workspace, nvec, width / 8, p, seed, stream_id);
-  const long long n = static_cast<long long>(seq) * width;
-  embedding_wpe_bwd_kernel<<<static_cast<int>((n + kBlock - 1) / kBlock), kBlock, 0, s>>>(workspace, dwpe, batch,
-                                                                                           seq, width);
-  return check_launch("embedding_bwd", 2);
+  const long long n = static_cast<long long>(batch) * seq;
+  if (!n) return kOk;
+  const long long n_pad = sort_pad(n);
+  auto* keys = reinterpret_cast<uint64_t*>(workspace);
+  int launches = 0;
+  sort_keys_init_kernel<<<grid_for(n_pad), kBlock, 0, s>>>(tokens, keys, n, n_pad);
+  ++launches;
+  const int blk = static_cast<int>(n_pad < kSortBlock ? n_pad : kSortBlock);
+  const unsigned nblk = static_cast<unsigned>(n_pad / blk);
+  bitonic_block_kernel<<<nblk, blk / 2, 0, s>>>(keys, blk, blk, 0);  // every stage that fits a block
+  ++launches;
+  for (long long k = 2LL * blk; k <= n_pad; k <<= 1) {
+    for (long long j = k >> 1; j >= blk; j >>= 1) {
+      bitonic_global_kernel<<<grid_for(n_pad / 2), kBlock, 0, s>>>(keys, n_pad, k, j);
+      ++launches;
+    }
+    bitonic_block_kernel<<<nblk, blk / 2, 0, s>>>(keys, blk, k, 1);  // the strides below one block
+    ++launches;
+  }
+  embedding_wte_segsum_kernel<<<static_cast<unsigned>(n), 128, 0, s>>>(
+      keys, reinterpret_cast<const BF8*>(dout), dwte, n, width / 8, p, seed, stream_id);
+  embedding_wpe_bwd_kernel<<<grid_for(static_cast<long long>(seq) * width / 8), kBlock, 0, s>>>(
+      reinterpret_cast<const BF8*>(dout), dwpe, batch, seq, width / 8, p, seed, stream_id);
+  return check_launch("embedding_bwd", launches + 2);
 }
 
 int xent_fwd_bwd(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows, long long rows, int vocab,

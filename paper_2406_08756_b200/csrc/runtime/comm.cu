@@ -1,0 +1,275 @@
+// NCCL and in-process loopback implementations of the executor's Comms (comm.hpp).
+#include "runtime/comm.hpp"
+
+#include <nccl.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "lynx_ops_internal.h"
+
+namespace lynx::rt {
+
+namespace {
+
+void cuda_ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation) throw RtError(std::string(what) + ": out of device memory", kOutOfMemory);
+  throw RtError(std::string(what) + ": " + cudaGetErrorString(e), kCudaError);
+}
+
+void nccl_ck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw RtError(std::string(what) + ": " + ncclGetErrorString(r), kCudaError);
+}
+
+int hex_val(char c) {
+  if (c >= '0' && c <= '9') return c - '0';
+  if (c >= 'a' && c <= 'f') return c - 'a' + 10;
+  if (c >= 'A' && c <= 'F') return c - 'A' + 10;
+  return -1;
+}
+
+// ------------------------------------------------------------------ NCCL
+class NcclComms final : public Comms {
+ public:
+  NcclComms(const std::string& id_hex, int world_rank, int world_size, int pp_rank, int tp_rank) {
+    ncclUniqueId id;
+    if (id_hex.empty() && world_size == 1) {
+      // Single rank with the TP template: the all-reduce windows run on a
+      // one-rank communicator (identity reduction), exercising the same streams.
+      nccl_ck(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    } else {
+      if (id_hex.size() != 2 * sizeof(ncclUniqueId))
+        throw RtError("parallel.nccl_id must be a hex ncclUniqueId", kValidation);
+      for (size_t i = 0; i < sizeof(id); ++i) {
+        const int hi = hex_val(id_hex[2 * i]), lo = hex_val(id_hex[2 * i + 1]);
+        if (hi < 0 || lo < 0) throw RtError("parallel.nccl_id is not hex", kValidation);
+        id.internal[i] = static_cast<char>(hi * 16 + lo);
+      }
+    }
+    nccl_ck(ncclCommInitRank(&world_, world_size, id, world_rank), "ncclCommInitRank");
+    // TP groups: ranks sharing a pipeline stage; PP groups: ranks sharing a TP rank.
+    // Activations (s -> s+1) and gradients (s+1 -> s) use separate communicators and
+    // streams, so the two directions of 1F1B never wait on each other.
+    nccl_ck(ncclCommSplit(world_, pp_rank, tp_rank, &tp_, nullptr), "split tp");
+    nccl_ck(ncclCommSplit(world_, tp_rank, pp_rank, &pa_, nullptr), "split pp act");
+    nccl_ck(ncclCommSplit(world_, tp_rank, pp_rank, &pg_, nullptr), "split pp grad");
+  }
+  ~NcclComms() override {
+    for (ncclComm_t c : {tp_, pa_, pg_, world_})
+      if (c) ncclCommDestroy(c);
+  }
+  void allreduce_sum_bf16(void* buf, size_t count, cudaStream_t s) override {
+    nccl_ck(ncclAllReduce(buf, buf, count, ncclBfloat16, ncclSum, tp_, s), "allreduce");
+  }
+  void send_bf16(const void* buf, size_t count, int peer, Channel ch, cudaStream_t s) override {
+    nccl_ck(ncclSend(buf, count, ncclBfloat16, peer, ch == Channel::PP_ACT ? pa_ : pg_, s), "send");
+  }
+  void recv_bf16(void* buf, size_t count, int peer, Channel ch, cudaStream_t s) override {
+    nccl_ck(ncclRecv(buf, count, ncclBfloat16, peer, ch == Channel::PP_ACT ? pa_ : pg_, s), "recv");
+  }
+  const char* kind() const override { return "nccl"; }
+
+ private:
+  ncclComm_t world_ = nullptr, tp_ = nullptr, pa_ = nullptr, pg_ = nullptr;
+};
+
+// ------------------------------------------------------------------ loopback
+constexpr int kMaxTp = 8;
+constexpr auto kPeerTimeout = std::chrono::seconds(300);
+
+struct PtrPack {
+  __nv_bfloat16* p[kMaxTp];
+};
+
+// out = bf16(sum_r float(in_r)) in rank order, written to every rank's buffer.
+__global__ void loopback_sum_kernel(PtrPack ptrs, int n, long long nvec, long long count) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; v < nvec; v += stride) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int r = 0; r < n; ++r) {
+      float f[8];
+      bf8_to_f(reinterpret_cast<const BF8*>(ptrs.p[r])[v], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += f[j];
+    }
+    const BF8 o = f_to_bf8(acc);
+    for (int r = 0; r < n; ++r) reinterpret_cast<BF8*>(ptrs.p[r])[v] = o;
+  }
+  for (long long i = 8 * nvec + blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < count; i += stride) {
+    float acc = 0.f;
+    for (int r = 0; r < n; ++r) acc += bf2f(ptrs.p[r][i]);
+    for (int r = 0; r < n; ++r) ptrs.p[r][i] = f2bf(acc);
+  }
+}
+
+struct ArCall {
+  int arrived = 0, left = 0;
+  bool complete = false;
+  size_t count = 0;
+  void* bufs[kMaxTp] = {};
+  cudaEvent_t ready[kMaxTp] = {};
+  cudaEvent_t done = nullptr;
+};
+
+struct TpGroup {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::map<long long, ArCall> calls;
+};
+
+struct Msg {
+  void* staging;
+  size_t bytes;
+  cudaEvent_t ready;
+};
+
+struct Link {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<Msg> q;
+};
+
+struct Grid {
+  int tp = 1, pp = 1;
+  std::vector<std::unique_ptr<TpGroup>> groups;  // one per stage
+  std::mutex links_mu;
+  std::map<std::tuple<int, int, int, int>, std::unique_ptr<Link>> links;  // (channel, src, dst, tp_rank)
+  Link& link(Channel ch, int src, int dst, int tp_rank) {
+    std::lock_guard<std::mutex> g(links_mu);
+    auto& p = links[{static_cast<int>(ch), src, dst, tp_rank}];
+    if (!p) p = std::make_unique<Link>();
+    return *p;
+  }
+};
+
+std::mutex g_grids_mu;
+std::map<std::string, std::weak_ptr<Grid>> g_grids;
+
+class LoopbackComms final : public Comms {
+ public:
+  LoopbackComms(const std::string& name, int tp, int pp, int pp_rank, int tp_rank)
+      : tp_(tp), pp_rank_(pp_rank), tp_rank_(tp_rank) {
+    if (tp < 1 || tp > kMaxTp || pp < 1 || pp_rank < 0 || pp_rank >= pp || tp_rank < 0 || tp_rank >= tp)
+      throw RtError("loopback grid: rank out of range (tp <= 8)", kValidation);
+    std::lock_guard<std::mutex> g(g_grids_mu);
+    grid_ = g_grids[name].lock();
+    if (!grid_) {
+      grid_ = std::make_shared<Grid>();
+      grid_->tp = tp;
+      grid_->pp = pp;
+      for (int s = 0; s < pp; ++s) grid_->groups.push_back(std::make_unique<TpGroup>());
+      g_grids[name] = grid_;
+    } else if (grid_->tp != tp || grid_->pp != pp) {
+      throw RtError("loopback grid '" + name + "' exists with a different tp x pp shape", kValidation);
+    }
+  }
+
+  void allreduce_sum_bf16(void* buf, size_t count, cudaStream_t s) override {
+    if (tp_ == 1) return;
+    TpGroup& g = *grid_->groups[pp_rank_];
+    const long long k = seq_++;
+    cudaEvent_t ready;
+    cuda_ck(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+    cuda_ck(cudaEventRecord(ready, s), "event");
+    std::unique_lock<std::mutex> lk(g.mu);
+    ArCall& c = g.calls[k];
+    if (c.arrived && c.count != count) throw RtError("loopback all-reduce: ranks disagree on the size", kCudaError);
+    c.count = count;
+    c.bufs[tp_rank_] = buf;
+    c.ready[tp_rank_] = ready;
+    if (++c.arrived == tp_) {  // last to arrive reduces for everyone
+      for (int r = 0; r < tp_; ++r) cuda_ck(cudaStreamWaitEvent(s, c.ready[r], 0), "wait");
+      PtrPack pk{};
+      for (int r = 0; r < tp_; ++r) pk.p[r] = static_cast<__nv_bfloat16*>(c.bufs[r]);
+      const long long nvec = static_cast<long long>(count / 8);
+      long long blocks = (nvec + 255) / 256;
+      blocks = blocks < 1 ? 1 : (blocks > 148 * 8 ? 148 * 8 : blocks);
+      loopback_sum_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(pk, tp_, nvec, static_cast<long long>(count));
+      if (check_launch("loopback_allreduce") != kOk) throw RtError(last_error(), kCudaError);
+      cuda_ck(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming), "event");
+      cuda_ck(cudaEventRecord(c.done, s), "event");
+      c.complete = true;
+      g.cv.notify_all();
+    } else {
+      if (!g.cv.wait_for(lk, kPeerTimeout, [&] { return c.complete; }))
+        throw RtError("loopback all-reduce: a TP peer did not arrive", kCudaError);
+      cuda_ck(cudaStreamWaitEvent(s, c.done, 0), "wait");
+    }
+    if (++c.left == tp_) {  // every rank has ordered its stream after the reduction
+      for (int r = 0; r < tp_; ++r) cudaEventDestroy(c.ready[r]);
+      cudaEventDestroy(c.done);
+      g.calls.erase(k);
+    }
+  }
+
+  void send_bf16(const void* buf, size_t count, int peer, Channel ch, cudaStream_t s) override {
+    Link& L = grid_->link(ch, pp_rank_, peer, tp_rank_);
+    const size_t bytes = count * 2;
+    Msg m{nullptr, bytes, nullptr};
+    cuda_ck(cudaMallocAsync(&m.staging, bytes, s), "loopback send staging");
+    cuda_ck(cudaMemcpyAsync(m.staging, buf, bytes, cudaMemcpyDeviceToDevice, s), "loopback send");
+    cuda_ck(cudaEventCreateWithFlags(&m.ready, cudaEventDisableTiming), "event");
+    cuda_ck(cudaEventRecord(m.ready, s), "event");
+    std::lock_guard<std::mutex> g(L.mu);
+    L.q.push_back(m);
+    L.cv.notify_all();
+  }
+
+  void recv_bf16(void* buf, size_t count, int peer, Channel ch, cudaStream_t s) override {
+    Link& L = grid_->link(ch, peer, pp_rank_, tp_rank_);
+    Msg m;
+    {
+      std::unique_lock<std::mutex> lk(L.mu);
+      if (!L.cv.wait_for(lk, kPeerTimeout, [&] { return !L.q.empty(); }))
+        throw RtError("loopback recv: the peer stage never sent", kCudaError);
+      m = L.q.front();
+      L.q.pop_front();
+    }
+    if (m.bytes != count * 2) throw RtError("loopback recv: message size mismatch", kCudaError);
+    cuda_ck(cudaStreamWaitEvent(s, m.ready, 0), "wait");
+    cuda_ck(cudaMemcpyAsync(buf, m.staging, m.bytes, cudaMemcpyDeviceToDevice, s), "loopback recv");
+    cuda_ck(cudaFreeAsync(m.staging, s), "loopback recv free");
+    cudaEventDestroy(m.ready);
+  }
+
+  const char* kind() const override { return "loopback"; }
+
+ private:
+  std::shared_ptr<Grid> grid_;
+  int tp_, pp_rank_, tp_rank_;
+  long long seq_ = 0;
+};
+
+}  // namespace
+
+std::unique_ptr<Comms> make_nccl_comms(const std::string& id_hex, int world_rank, int world_size, int pp_rank,
+                                       int tp_rank) {
+  return std::make_unique<NcclComms>(id_hex, world_rank, world_size, pp_rank, tp_rank);
+}
+
+std::unique_ptr<Comms> make_loopback_comms(const std::string& name, int tp, int pp, int pp_rank, int tp_rank) {
+  return std::make_unique<LoopbackComms>(name, tp, pp, pp_rank, tp_rank);
+}
+
+std::string nccl_unique_id_hex() {
+  ncclUniqueId id;
+  nccl_ck(ncclGetUniqueId(&id), "ncclGetUniqueId");
+  static const char* hx = "0123456789abcdef";
+  std::string out(2 * sizeof(id), '0');
+  for (size_t i = 0; i < sizeof(id); ++i) {
+    const unsigned char c = static_cast<unsigned char>(id.internal[i]);
+    out[2 * i] = hx[c >> 4];
+    out[2 * i + 1] = hx[c & 15];
+  }
+  return out;
+}
+
+}  // namespace lynx::rt

@@ -18,18 +18,7 @@ namespace lynx::rt {
 using Json = nlohmann::ordered_json;
 using host::Recompute;
 
-struct RtError : std::runtime_error {
-  RtError(const std::string& w, int c) : std::runtime_error(w), code(c) {}
-  int code;
-};
-
 namespace {
-int hex_val(char c) {
-  if (c >= '0' && c <= '9') return c - '0';
-  if (c >= 'a' && c <= 'f') return c - 'a' + 10;
-  if (c >= 'A' && c <= 'F') return c - 'A' + 10;
-  return 0;
-}
 constexpr uint64_t kEmbedStream = 0xFFFFull << 32;
 }  // namespace
 
@@ -63,10 +52,6 @@ struct ProbeStream {
   ~ProbeStream() { slot = saved; }
 };
 }  // namespace
-void Executor::nccl(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) throw RtError(std::string(what) + ": " + ncclGetErrorString(r), kCudaError);
-}
-
 Executor::Executor(const std::string& profile_json, const std::string& timeline_json, const std::string& config_json) {
   prof_ = host::parse_profile(profile_json);
   tl_ = host::parse_timeline(timeline_json);
@@ -88,16 +73,27 @@ void Executor::init_device() {
   size_t stack = 0;
   ck(cudaDeviceGetLimit(&stack, cudaLimitStackSize), "stack limit");
   if (stack < 1024) ck(cudaDeviceSetLimit(cudaLimitStackSize, 1024), "stack limit");
-  if (needs_comms_) init_comms(nccl_id_, world_rank_, world_size_);
+  if (needs_comms_) {
+    if (!loopback_.empty())
+      comms_ = make_loopback_comms(loopback_, cfg_.tp, cfg_.pp, cfg_.pp_rank, cfg_.tp_rank);
+    else
+      comms_ = make_nccl_comms(nccl_id_, world_rank_, world_size_, cfg_.pp_rank, cfg_.tp_rank);
+  }
   for (cudaStream_t* s : {&main_, &side_, &tp_s_, &pa_s_, &pg_s_})
     ck(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "stream");
   int dev = 0;
   ck(cudaGetDevice(&dev), "device");
-  ck(cudaDeviceGetDefaultMemPool(&pool_, dev), "mempool");
+  // A private pool: its high-water mark is this executor's alone, several executors can share a
+  // process (the loopback grid), and destroying it returns every byte (the OOM error path).
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  ck(cudaMemPoolCreate(&pool_, &props), "mempool");
   uint64_t thr = UINT64_MAX;
   ck(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
-  uint64_t zero = 0;  // high-water mark of this executor only (the default pool outlives it)
-  ck(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &zero), "mempool attr");
+  int internal = opt_.pool_internal_deps ? 1 : 0;
+  ck(cudaMemPoolSetAttribute(pool_, cudaMemPoolReuseAllowInternalDependencies, &internal), "mempool attr");
   ps_.allocate_and_init(cfg_, main_);
   alloc_persistent();
   if (opt_.reserve_pool) reserve_pool();
@@ -184,6 +180,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.probe_fc1 = ex.value("probe_fc1", false);
   opt_.probe_ops = ex.value("probe_ops", false);
   opt_.reserve_pool = ex.value("reserve_pool", true);
+  opt_.pool_internal_deps = ex.value("pool_internal_deps", false);
   opt_.comm_standin_us = ex.value("comm_standin_us", 0.0);
   opt_.comm_standin_ctas = ex.value("comm_standin_ctas", 16);
   opt_.standin_grad_wait_us = ex.value("standin_grad_wait_us", std::vector<double>());
@@ -195,8 +192,11 @@ void Executor::parse_config(const std::string& text) {
   if (cfg_.vocab % 128) throw RtError("vocab must be padded to a multiple of 128", kValidation);
   ps_.layout(cfg_);
   nccl_id_ = par.value("nccl_id", std::string());
+  loopback_ = par.value("loopback", std::string());
   world_rank_ = par.value("world_rank", 0);
   world_size_ = par.value("world_size", 1);
+  if (!loopback_.empty() && (opt_.standalone || !nccl_id_.empty()))
+    throw RtError("parallel.loopback runs every rank in this process: no nccl_id, no standalone_stage", kValidation);
   if (opt_.standalone && world_size_ != 1)
     throw RtError("standalone_stage runs one stage in a single process", kValidation);
   if (opt_.standalone && cfg_.tp != 1 && opt_.comm_standin_us <= 0)
@@ -208,27 +208,6 @@ void Executor::parse_config(const std::string& text) {
     throw RtError("exec.standin_grad_wait_us is a standalone_stage option", kValidation);
   if (opt_.comm_standin_ctas < 1 || opt_.comm_standin_ctas > 148)
     throw RtError("exec.comm_standin_ctas must be in [1, 148]", kValidation);
-}
-
-void Executor::init_comms(const std::string& id_hex, int world_rank, int world_size) {
-  ncclUniqueId id;
-  if (id_hex.empty() && world_size == 1) {
-    // Single rank with the TP template: the all-reduce windows run on a
-    // one-rank communicator (identity reduction), exercising the same streams.
-    nccl(ncclGetUniqueId(&id), "ncclGetUniqueId");
-  } else {
-    if (id_hex.size() != 2 * sizeof(ncclUniqueId))
-      throw RtError("parallel.nccl_id must be a hex ncclUniqueId", kValidation);
-    for (size_t i = 0; i < sizeof(id); ++i)
-      id.internal[i] = static_cast<char>(hex_val(id_hex[2 * i]) * 16 + hex_val(id_hex[2 * i + 1]));
-  }
-  nccl(ncclCommInitRank(&world_, world_size, id, world_rank), "ncclCommInitRank");
-  // TP groups: ranks sharing a pipeline stage; PP groups: ranks sharing a TP rank.
-  // Activations (s -> s+1) and gradients (s+1 -> s) use separate communicators
-  // and streams, so the two directions of 1F1B never wait on each other.
-  nccl(ncclCommSplit(world_, cfg_.pp_rank, cfg_.tp_rank, &tp_comm_, nullptr), "split tp");
-  nccl(ncclCommSplit(world_, cfg_.tp_rank, cfg_.pp_rank, &pa_comm_, nullptr), "split pp act");
-  nccl(ncclCommSplit(world_, cfg_.tp_rank, cfg_.pp_rank, &pg_comm_, nullptr), "split pp grad");
 }
 
 void Executor::bind_template() {
@@ -343,11 +322,18 @@ Executor::~Executor() {
 }
 
 void Executor::release_all() {
-  cudaDeviceSynchronize();
-  for (auto& s : slots_) {
-    if (s.p) cudaFree(s.p);
-    if (s.shadow) cudaFree(s.shadow);
-  }
+  // Own streams only: other executors of this process (loopback grid) keep running.
+  for (cudaStream_t s : {main_, side_, tp_s_, pa_s_, pg_s_})
+    if (s) cudaStreamSynchronize(s);
+  // Every pool allocation still live — tensors of a step that threw (LYNX_E_OOM), per-microbatch
+  // gradients and staging, forward copies kept for check_recompute — is freed before the pool.
+  for (void* p : live_) cudaFree(p);
+  live_.clear();
+  for (auto& s : slots_) s = Slot{};
+  std::fill(stage_in_.begin(), stage_in_.end(), nullptr);
+  std::fill(head_dy_.begin(), head_dy_.end(), nullptr);
+  std::fill(ln_f_.begin(), ln_f_.end(), nullptr);
+  std::fill(grad_.begin(), grad_.end(), Grad{});
   ps_.release();
   for (void* p : {static_cast<void*>(sc_main_.t_h), static_cast<void*>(sc_main_.t_h2),
                   static_cast<void*>(sc_main_.t_wide), static_cast<void*>(sc_main_.ws),
@@ -356,19 +342,37 @@ void Executor::release_all() {
                   static_cast<void*>(syn_grad_),
                   static_cast<void*>(d_labels_), static_cast<void*>(d_loss_), static_cast<void*>(d_mismatch_)})
     if (p) cudaFree(p);
+  sc_main_ = Scratch{};
+  sc_side_ = Scratch{};
+  d_tokens_ = d_labels_ = nullptr;
+  d_loss_ = nullptr;
+  head_gw32_ = emb_gw32_ = nullptr;
+  syn_act_ = syn_grad_ = nullptr;
+  d_mismatch_ = nullptr;
   cudaFreeHost(h_tokens_);
   cudaFreeHost(h_labels_);
   cudaFreeHost(h_loss_);
+  h_tokens_ = h_labels_ = nullptr;
+  h_loss_ = nullptr;
   for (auto e : ev_pool_) cudaEventDestroy(e);
   for (auto e : act_sent_) cudaEventDestroy(e);
   for (auto e : grad_sent_) cudaEventDestroy(e);
+  ev_pool_.clear();
+  act_sent_.clear();
+  grad_sent_.clear();
+  ev_next_ = 0;
   if (t0_) cudaEventDestroy(t0_);
   if (t1_) cudaEventDestroy(t1_);
-  for (ncclComm_t c : {tp_comm_, pa_comm_, pg_comm_, world_})
-    if (c) ncclCommDestroy(c);
-  for (cudaStream_t s : {main_, side_, tp_s_, pa_s_, pg_s_})
-    if (s) cudaStreamDestroy(s);
-  if (pool_) cudaMemPoolTrimTo(pool_, 0);
+  t0_ = t1_ = nullptr;
+  comms_.reset();
+  for (cudaStream_t* s : {&main_, &side_, &tp_s_, &pa_s_, &pg_s_})
+    if (*s) {
+      cudaStreamDestroy(*s);
+      *s = nullptr;
+    }
+  if (pool_) cudaMemPoolDestroy(pool_);
+  pool_ = nullptr;
+  cudaGetLastError();
 }
 
 // ============================================================ tensors
@@ -393,11 +397,13 @@ void* Executor::alloc(size_t bytes, cudaStream_t s) {
                   kOutOfMemory);
   }
   ck(e, "activation allocation");
+  live_.insert(p);
   return p;
 }
 
 void Executor::release(void* p, cudaStream_t s) {
   if (!p || opt_.dry_run) return;
+  live_.erase(p);
   ck(cudaFreeAsync(p, s), "activation free");
 }
 
@@ -457,9 +463,14 @@ void* Executor::layer_input(int mb, int l, cudaStream_t s) {
   return need(mb, l - 1, ck_pos, s);
 }
 
+// Philox stream of a dropout site: (global layer, microbatch, site). The TP template's all-reduce
+// epilogues (AR1 / AR2) draw the same masks as the TP = 1 fused ops (PROJ_RES / FC2_RES), and no
+// TP rank enters the key, so every TP rank — and a TP = 1 run of the same model — drops the same
+// elements of the replicated residual stream.
 uint64_t Executor::drop_stream(int l, int mb, Op op) const {
+  const Op site = op == Op::AR1 ? Op::PROJ_RES : (op == Op::AR2 ? Op::FC2_RES : op);
   return (static_cast<uint64_t>(cfg_.layer0 + l + 1) << 32) | (static_cast<uint64_t>(mb) << 8) |
-         static_cast<uint64_t>(op);
+         static_cast<uint64_t>(site);
 }
 
 // ============================================================ timing
@@ -759,8 +770,7 @@ void Executor::comm_element(int mb, bool bwd, int l, const host::Element& e) {
       ck_op(comm_standin(static_cast<unsigned long long>(opt_.comm_standin_us * 1e3), opt_.comm_standin_ctas, tp_s_),
             "comm stand-in");
     else
-      nccl(ncclAllReduce(buf, buf, static_cast<size_t>(T * h), ncclBfloat16, ncclSum, tp_comm_, tp_s_),
-           "allreduce");
+      comms_->allreduce_sum_bf16(buf, static_cast<size_t>(T * h), tp_s_);
     span_end(tp_s_);
     cudaEvent_t done = ev();
     ck(cudaEventRecord(done, tp_s_), "event");
@@ -959,7 +969,7 @@ void Executor::forward_pass(int mb) {
       cudaEvent_t a = ev();
       ck(cudaEventRecord(a, main_), "event");  // buffer allocated on main
       ck(cudaStreamWaitEvent(pa_s_, a, 0), "wait");
-      nccl(ncclRecv(stage_in_[mb], static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank - 1, pa_comm_, pa_s_), "recv");
+      comms_->recv_bf16(stage_in_[mb], static_cast<size_t>(T * h), cfg_.pp_rank - 1, Channel::PP_ACT, pa_s_);
       cudaEvent_t b = ev();
       ck(cudaEventRecord(b, pa_s_), "event");
       span_begin(main_, 5, mb);
@@ -995,7 +1005,7 @@ void Executor::forward_pass(int mb) {
       cudaEvent_t a = ev();
       ck(cudaEventRecord(a, main_), "event");
       ck(cudaStreamWaitEvent(pa_s_, a, 0), "wait");
-      nccl(ncclSend(out, static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank + 1, pa_comm_, pa_s_), "send");
+      comms_->send_bf16(out, static_cast<size_t>(T * h), cfg_.pp_rank + 1, Channel::PP_ACT, pa_s_);
       ck(cudaEventRecord(act_sent_[mb], pa_s_), "event");
     }
   }
@@ -1003,8 +1013,9 @@ void Executor::forward_pass(int mb) {
 }
 
 void Executor::backward_pass(int mb) {
-  // The first backward pass of the step writes the layer weight gradients
-  // (fp32 store epilogue); later microbatches accumulate into them.
+  // The first backward pass of the step writes the layer weight gradients (bf16 store
+  // epilogue); later microbatches accumulate into them in bf16 (fp32 sum in the epilogue,
+  // one rounding per microbatch): the 2 B/parameter gradient of the paper's accounting.
   dw_epi_ = bwd_passes_ == 0 ? EPI_BF16 : EPI_ACC_BF16;  // bf16 gradients: store on the first pass
   ++bwd_passes_;
   const long long T = cfg_.tokens();
@@ -1043,7 +1054,7 @@ void Executor::backward_pass(int mb) {
       cudaEvent_t a = ev();
       ck(cudaEventRecord(a, main_), "event");
       ck(cudaStreamWaitEvent(pg_s_, a, 0), "wait");
-      nccl(ncclRecv(grad_[mb].dy, static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank + 1, pg_comm_, pg_s_), "recv");
+      comms_->recv_bf16(grad_[mb].dy, static_cast<size_t>(T * h), cfg_.pp_rank + 1, Channel::PP_GRAD, pg_s_);
       cudaEvent_t b = ev();
       ck(cudaEventRecord(b, pg_s_), "event");
       span_begin(main_, 5, mb);
@@ -1080,7 +1091,7 @@ void Executor::backward_pass(int mb) {
   void* dx = grad_[mb].dy;
   if (cfg_.first()) {
     if (!opt_.dry_run) {
-      void* ws = alloc(static_cast<size_t>(T) * h * 4, main_);
+      void* ws = alloc(embedding_bwd_workspace(cfg_.micro_batch, cfg_.seq, h), main_);
       const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
       ck_op(embedding_bwd(d_tokens_ + mb * T, static_cast<const __nv_bfloat16*>(dx), emb_gw32_,
                           emb_gw32_ + static_cast<size_t>(cfg_.vocab) * h,
@@ -1099,7 +1110,7 @@ void Executor::backward_pass(int mb) {
         cudaEvent_t a = ev();
         ck(cudaEventRecord(a, main_), "event");
         ck(cudaStreamWaitEvent(pg_s_, a, 0), "wait");
-        nccl(ncclSend(dx, static_cast<size_t>(T * h), ncclBfloat16, cfg_.pp_rank - 1, pg_comm_, pg_s_), "send");
+        comms_->send_bf16(dx, static_cast<size_t>(T * h), cfg_.pp_rank - 1, Channel::PP_GRAD, pg_s_);
         ck(cudaEventRecord(grad_sent_[mb], pg_s_), "event");
       }
       release(dx, pg_s_);  // stream-ordered after the send; main never waits on the peer
@@ -1149,7 +1160,7 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   }
   ck(cudaMemsetAsync(ps_.grad, 0, static_cast<size_t>(ps_.count()) * 2, main_), "zero grads");
   head_first_ = true;
-  if (cfg_.first())  // fp32 embedding-gradient accumulator (atomics), folded into the bf16 grads at step end
+  if (cfg_.first())  // fp32 embedding-gradient accumulator (deterministic), folded into the bf16 grads at step end
     ck(cudaMemsetAsync(emb_gw32_, 0, static_cast<size_t>(cfg_.vocab + cfg_.seq) * cfg_.hidden * 4, main_),
        "zero embedding grads");
   for (auto [bwd, mb] : passes) bwd ? backward_pass(mb) : forward_pass(mb);
@@ -1335,9 +1346,7 @@ void Executor::set_tensor(const std::string& name, const void* host, size_t byte
     if (r.name == name) {
       if (bytes != static_cast<size_t>(r.n) * 4) throw RtError("set_tensor expects fp32 values", kValidation);
       ck(cudaMemcpy(ps_.master + r.off, host, bytes, cudaMemcpyHostToDevice), "h2d");
-      ck_op(adam_step(ps_.master + r.off, ps_.param + r.off, ps_.grad + r.off, 1, ps_.m + r.off, ps_.v + r.off, r.n, 0.f,
-                      cfg_.beta1, cfg_.beta2, 1.f, 0.f, 1, 0.f, main_),
-            "copy");  // lr = 0: writes bf16(master) without changing it
+      ck_op(f32_to_bf16(ps_.master + r.off, ps_.param + r.off, r.n, main_), "copy");  // Adam state untouched
       ck(cudaStreamSynchronize(main_), "sync");
       return;
     }
@@ -1420,16 +1429,9 @@ int lynx_rt_set_tensor(lynx_rt* h, const char* name, const void* host, size_t by
 
 int lynx_rt_nccl_unique_id(char* hex_out, size_t len) {
   return guard([&] {
-    ncclUniqueId id;
-    if (ncclGetUniqueId(&id) != ncclSuccess) throw lynx::rt::RtError("ncclGetUniqueId failed", lynx::kCudaError);
-    if (len < 2 * sizeof(id) + 1) throw lynx::rt::RtError("buffer too small", lynx::kValidation);
-    static const char* hx = "0123456789abcdef";
-    for (size_t i = 0; i < sizeof(id); ++i) {
-      const unsigned char c = static_cast<unsigned char>(id.internal[i]);
-      hex_out[2 * i] = hx[c >> 4];
-      hex_out[2 * i + 1] = hx[c & 15];
-    }
-    hex_out[2 * sizeof(id)] = 0;
+    const std::string hex = lynx::rt::nccl_unique_id_hex();
+    if (len < hex.size() + 1) throw lynx::rt::RtError("buffer too small", lynx::kValidation);
+    std::memcpy(hex_out, hex.c_str(), hex.size() + 1);
   });
 }
 

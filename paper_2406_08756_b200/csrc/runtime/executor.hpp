@@ -28,11 +28,13 @@
 
 #include <map>
 #include <memory>
+#include <unordered_set>
 #include <string>
 #include <tuple>
 #include <vector>
 
 #include "host/pipeline.hpp"
+#include "runtime/comm.hpp"
 #include "runtime/gpt_stage.hpp"
 
 namespace lynx::rt {
@@ -44,6 +46,9 @@ struct ExecOptions {
   bool dry_run = false;         // build the launch program only (no device)
   bool probe_fc1 = false;       // CUDA events around every FC1 forward GEMM launch (roofline line)
   bool reserve_pool = true;     // map all free HBM (but 2 GiB) into the activation pool at construction
+  bool pool_internal_deps = false;  // cudaMemPoolReuseAllowInternalDependencies on the activation pool: lets
+                                    // an allocation on one stream reuse memory freed on another by making it
+                                    // wait on the freeing stream (serialises the side stream behind main)
   bool probe_ops = false;       // one CUDA event after every operator launch on its stream: in-step
                                 // time per operator name, gaps included (report "probe_ops")
   bool standalone = false;      // time one pipeline stage alone on one GPU: receives read synthetic
@@ -116,7 +121,6 @@ class Executor {
   void init_device();
   void finish_production(Slot& out, size_t bytes, cudaStream_t s, bool recompute);
   void release_all();
-  void init_comms(const std::string& nccl_id_hex, int world_rank, int world_size);
   void alloc_persistent();
 
   // passes
@@ -149,7 +153,6 @@ class Executor {
   void ck(cudaError_t e, const char* what);
   void ck_op(int status, const char* what);
   void reserve_pool();
-  void nccl(ncclResult_t r, const char* what);
 
   host::Profile prof_;
   host::StageTimeline tl_;
@@ -168,8 +171,10 @@ class Executor {
   std::map<int, std::vector<host::Recompute>> stall_;
 
   cudaStream_t main_ = nullptr, side_ = nullptr, tp_s_ = nullptr, pa_s_ = nullptr, pg_s_ = nullptr;
-  ncclComm_t tp_comm_ = nullptr, pa_comm_ = nullptr, pg_comm_ = nullptr, world_ = nullptr;
-  cudaMemPool_t pool_ = nullptr;
+  std::unique_ptr<Comms> comms_;
+  std::string loopback_;           // parallel.loopback: in-process grid name (all ranks on this GPU)
+  cudaMemPool_t pool_ = nullptr;   // private stream-ordered pool of this executor (activations)
+  std::unordered_set<void*> live_;  // every pool allocation not yet released (freed by release_all)
   ParamStore ps_;
   Scratch sc_main_, sc_side_;
   int *d_tokens_ = nullptr, *d_labels_ = nullptr;
@@ -191,7 +196,7 @@ class Executor {
   StepReport rep_;
   int step_ = 0;
   int bwd_passes_ = 0;
-  int dw_epi_ = 1;  // EPI_ACC_F32
+  int dw_epi_ = 0;  // EPI_BF16 on the step's first backward pass, then EPI_ACC_BF16
   cudaEvent_t t0_ = nullptr, t1_ = nullptr;
   __nv_bfloat16 *syn_act_ = nullptr, *syn_grad_ = nullptr;  // standalone stage: stand-ins for PP receives
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probes_;  // exec.probe_fc1 event pairs of this step
@@ -201,7 +206,7 @@ class Executor {
   std::vector<std::tuple<std::string, long long, double>> op_times_;           // name, launches, ms (last step)
   double op_stream_ms_[2] = {0, 0};                                            // main, side: sum of op times
   float* head_gw32_ = nullptr;  // last stage: LM-head weight gradient, fp32 across chunks / microbatches
-  float* emb_gw32_ = nullptr;   // first stage: wte | wpe gradients, fp32 (scatter-add with atomics)
+  float* emb_gw32_ = nullptr;   // first stage: wte | wpe gradients, fp32 (sorted segment sums, no atomics)
   bool head_first_ = true;
   std::vector<std::tuple<int, int, int, int, double, double>> trace_;  // stage, mb, kind, op, start, end
 };

@@ -118,27 +118,46 @@ void ParamStore::allocate_and_init(const ModelCfg& c, cudaStream_t s) {
   ck(cudaMemsetAsync(v, 0, n * 4, s));
   ck(cudaMemsetAsync(param, 0, n * 2, s));  // alignment padding stays zero
   ck(cudaMemsetAsync(master, 0, n * 4, s));
-  // Weights ~ N(0, std) generated for the *unsharded* tensor index space is not
-  // needed for parity (tests read weights back); streams are keyed by
-  // (global layer, tensor, tp_rank) so every rank/stage is deterministic.
+  // Weights ~ N(0, std) defined on the UNSHARDED tensor: the Philox stream is keyed by
+  // (global layer, tensor kind) only — no TP rank, no stage-local position — and each TP rank
+  // materialises its Megatron slice of the full tensor (init_normal_sharded_bf16). Every TP / PP
+  // layout of a model therefore holds exactly the weights of its TP = 1, PP = 1 run: replicated
+  // tensors (embeddings, LM head, LayerNorms, row-parallel biases) are identical on all TP ranks,
+  // and the unsharded CPU oracle sees the same values.
   const float out_std = c.init_std / std::sqrt(2.0f * c.n_layers_total);
-  uint64_t tensor_id = 0;
+  const long long h = c.hidden, hp = c.hp();
   for (const auto& r : refs_) {
-    ++tensor_id;
     const std::string& nm = r.name;
-    const bool is_gamma = nm.find("_g") != std::string::npos && nm.find("ln") != std::string::npos;
-    const bool is_bias = nm.find(".b_") != std::string::npos || nm.find("_b") == nm.size() - 2;
-    uint64_t layer_global = 0;
-    if (nm[0] == 'l' && nm[1] != 'n') layer_global = c.layer0 + std::stoi(nm.substr(1)) + 1;
-    const uint64_t sid = (layer_global << 24) ^ (tensor_id << 8) ^ static_cast<uint64_t>(c.tp_rank);
-    int st;
-    if (is_gamma) {
+    const size_t dot = nm.find('.');
+    const bool layer = nm[0] == 'l' && dot != std::string::npos;
+    const std::string base = layer ? nm.substr(dot + 1) : nm;
+    const uint64_t layer_global = layer ? static_cast<uint64_t>(c.layer0 + std::stoi(nm.substr(1)) + 1) : 0;
+    int st = 0;
+    if (base == "ln1_g" || base == "ln2_g" || base == "lnf_g") {
       st = fill_param(param + r.off, master + r.off, 1.0f, r.n, s);
-    } else if (is_bias) {
+    } else if (base.rfind("b_", 0) == 0 || base == "ln1_b" || base == "ln2_b" || base == "lnf_b") {
       st = fill_param(param + r.off, master + r.off, 0.0f, r.n, s);
     } else {
-      const bool out_proj = nm.find("w_proj") != std::string::npos || nm.find("w_fc2") != std::string::npos;
-      st = init_normal_bf16(param + r.off, master + r.off, r.n, out_proj ? out_std : c.init_std, c.seed, sid, s);
+      // kind id, local [rows, cols], column-split row block / row-split flag
+      static const struct { const char* name; int kind; } kinds[] = {
+          {"wte", 1}, {"wpe", 2}, {"w_qkv", 3}, {"w_proj", 4}, {"w_fc1", 5}, {"w_fc2", 6}, {"w_head", 7}};
+      int kind = 0;
+      for (const auto& k : kinds)
+        if (base == k.name) kind = k.kind;
+      if (!kind) throw std::runtime_error("parameter init: no rule for " + nm);
+      long long rows = r.n / h, cols = h, row_blk = 0;
+      int col_split = 0;
+      if (base == "w_qkv") row_blk = hp;                      // [3 hp, h]: q | k | v blocks of hp rows
+      if (base == "w_fc1") row_blk = 4 * hp;                  // [4 hp, h]
+      if (base == "w_proj" || base == "w_fc2") {              // [h, hp] / [h, 4 hp]: column slices
+        rows = h;
+        cols = r.n / h;
+        col_split = 1;
+      }
+      const bool out_proj = base == "w_proj" || base == "w_fc2";
+      const uint64_t sid = (layer_global << 24) ^ (static_cast<uint64_t>(kind) << 8);
+      st = init_normal_sharded_bf16(param + r.off, master + r.off, rows, cols, row_blk, col_split, c.tp, c.tp_rank,
+                                    out_proj ? out_std : c.init_std, c.seed, sid, s);
     }
     if (st) throw std::runtime_error(std::string("parameter init: ") + last_error());
   }

@@ -121,13 +121,15 @@ class Executor:
 
 
 def make_config(c: gp.GPTConfig, layers_per_stage, *, tp_rank=0, world_rank=0, world_size=1, nccl_id="",
-                train: dict | None = None, exec_opts: dict | None = None) -> dict:
+                loopback: str = "", train: dict | None = None, exec_opts: dict | None = None) -> dict:
+    par = {"tp": c.tp, "tp_rank": tp_rank, "world_rank": world_rank, "world_size": world_size, "nccl_id": nccl_id}
+    if loopback:
+        par["loopback"] = loopback
     return {
         "model": {"hidden": c.hidden, "heads": c.heads, "seq": c.seq, "micro_batch": c.micro_batch,
                   "vocab": c.vocab},
         "layers_per_stage": list(layers_per_stage),
-        "parallel": {"tp": c.tp, "tp_rank": tp_rank, "world_rank": world_rank, "world_size": world_size,
-                     "nccl_id": nccl_id},
+        "parallel": par,
         "train": {"dropout": c.dropout, "seed": 42, "lr": 1e-4, "beta1": 0.9, "beta2": 0.95, "eps": 1e-8,
                   "weight_decay": 0.1, "init_std": 0.02, **(train or {})},
         "exec": dict(exec_opts or {}),
@@ -164,3 +166,105 @@ def synthetic_batch(c: gp.GPTConfig, seed: int = 1234) -> tuple[np.ndarray, np.n
     rng = np.random.default_rng(seed)
     seqs = rng.integers(0, min(50257, c.vocab), size=(c.n_microbatches * c.micro_batch, c.seq + 1), dtype=np.int64)
     return seqs[:, :-1].astype(np.int32).ravel(), seqs[:, 1:].astype(np.int32).ravel()
+
+
+class LoopbackGrid:
+    """Every (stage, TP rank) executor of a TP x PP configuration inside this process, on one GPU.
+
+    The ranks talk through the executor's in-process loopback Comms (runtime/comm.hpp:
+    parallel.loopback) instead of NCCL, which cannot place two ranks on one device; each
+    rank is driven by its own host thread (ctypes releases the GIL), exactly as one process
+    per GPU drives it under torchrun. This is how the sharded numerics — Megatron column /
+    row splits, the four TP all-reduces per layer, the 1F1B pipeline hand-off, the plan's
+    window recomputes overlapping the all-reduces — are checked against the unsharded CPU
+    oracle on a single B200.
+    """
+
+    _count = 0
+
+    def __init__(self, c: gp.GPTConfig, profile_text: str, plans: list[dict], *, exec_opts: dict | None = None,
+                 train: dict | None = None):
+        LoopbackGrid._count += 1
+        name = f"grid{LoopbackGrid._count}-{id(self):x}"
+        self.c = c
+        self.layers = plans[0]["layers_per_stage"]
+        opts = {"reserve_pool": False, **(exec_opts or {})}
+        self.ranks: dict[tuple[int, int], Executor] = {}
+        try:
+            for s in range(c.pp):
+                for r in range(c.tp):
+                    cfg = make_config(c, self.layers, tp_rank=r, world_rank=s * c.tp + r, world_size=c.tp * c.pp,
+                                      loopback=name, train=train, exec_opts=opts)
+                    self.ranks[(s, r)] = Executor(profile_text, plans[s]["timeline"], cfg)
+        except Exception:
+            self.close()
+            raise
+
+    def step(self, tokens: np.ndarray, labels: np.ndarray) -> dict[tuple[int, int], float]:
+        """One training iteration on every rank concurrently; returns each rank's loss (last stage)."""
+        import threading
+        out: dict[tuple[int, int], float] = {}
+        errs: list[BaseException] = []
+
+        def run(key, e):
+            try:
+                s = key[0]
+                out[key] = e.step(tokens if s == 0 else None, labels if s == self.c.pp - 1 else None)
+            except BaseException as exc:  # noqa: BLE001 - re-raised below
+                errs.append(exc)
+
+        th = [threading.Thread(target=run, args=(k, e)) for k, e in self.ranks.items()]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        if errs:
+            raise errs[0]
+        return out
+
+    def reports(self) -> dict[tuple[int, int], dict]:
+        return {k: e.report() for k, e in self.ranks.items()}
+
+    def rank_tensors(self, grad: bool) -> dict[tuple[int, int], dict[str, np.ndarray]]:
+        """Per rank: its parameters (or fp32 gradients) under GLOBAL layer names."""
+        out = {}
+        l0 = [sum(self.layers[:s]) for s in range(self.c.pp)]
+        for (s, r), e in self.ranks.items():
+            shapes = param_shapes(self.c, self.layers[s], s == 0, s == self.c.pp - 1)
+            d = {}
+            for k, shp in shapes.items():
+                v = e.get(("grad:" if grad else "") + k, int(np.prod(shp))).reshape(shp)
+                if k.startswith("l") and "." in k:
+                    k = f"l{int(k[1:k.index('.')]) + l0[s]}{k[k.index('.'):]}"
+                d[k] = v
+            out[(s, r)] = d
+        return out
+
+    def close(self):
+        for e in self.ranks.values():
+            e.close()
+        self.ranks = {}
+
+
+# Megatron split of each per-layer tensor: (kind, axis, blocks). "rows": column-parallel output rows
+# (QKV's q | k | v blocks of hp rows each, FC1's 4hp rows); "cols": row-parallel input columns.
+_SPLIT = {"w_qkv": ("rows", 3), "b_qkv": ("rows", 3), "w_fc1": ("rows", 1), "b_fc1": ("rows", 1),
+          "w_proj": ("cols", 1), "w_fc2": ("cols", 1)}
+
+
+def unshard(per_rank: list[np.ndarray], name: str) -> np.ndarray:
+    """Reassemble one tensor from its TP-rank slices (rank order); replicated tensors come back from
+    rank 0 (callers check the replicas are identical)."""
+    base = name[name.index(".") + 1:] if name.startswith("l") and "." in name else name
+    if base not in _SPLIT or len(per_rank) == 1:
+        return per_rank[0]
+    kind, blocks = _SPLIT[base]
+    if kind == "cols":
+        return np.concatenate(per_rank, axis=1)
+    parts = [np.split(x, blocks, axis=0) for x in per_rank]  # [rank][block]
+    return np.concatenate([parts[r][b] for b in range(blocks) for r in range(len(per_rank))], axis=0)
+
+
+def is_tp_sharded(name: str) -> bool:
+    base = name[name.index(".") + 1:] if name.startswith("l") and "." in name else name
+    return base in _SPLIT

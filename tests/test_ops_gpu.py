@@ -341,6 +341,43 @@ def test_embedding(ops, cuda):
     assert torch.allclose(dwpe, dout.float().view(B, S, W).sum(0), atol=1e-3)
 
 
+@pytest.mark.parametrize("B,S,W,V,p", [(2, 64, 256, 512, 0.0), (2, 64, 256, 512, 0.1), (1, 300, 64, 7, 0.0),
+                                       (4, 2048, 512, 512, 0.1)])
+def test_embedding_bwd_deterministic_under_collisions(ops, cuda, B, S, W, V, p):
+    """Sorted segment sums (no atomics): bit-identical reruns even when every token repeats many times
+    (V = 7 / 512 over up to 8192 positions), equal to a float64 index_add with the executor's Philox mask."""
+    import numpy as np
+    from oracle import gpt_oracle
+    g = torch.Generator(device=cuda).manual_seed(B * S + V)
+    tok = torch.randint(0, V, (B * S,), device=cuda, dtype=torch.int32, generator=g)
+    dout = torch.randn(B * S, W, device=cuda, generator=g).bfloat16()
+    runs = []
+    for _ in range(3):
+        dwte = torch.zeros(V, W, device=cuda)
+        dwpe = torch.zeros(S, W, device=cuda)
+        ops.embedding_bwd(tok, dout, dwte, dwpe, B, S, p, 77, 5)
+        runs.append((dwte.cpu(), dwpe.cpu()))
+    for a, b in runs[1:]:
+        assert torch.equal(a, runs[0][0]) and torch.equal(b, runs[0][1])
+    keep = torch.from_numpy(gpt_oracle.keep_mask(77, 5, B * S * W, p).reshape(B * S, W))
+    scale = float(np.float32(1) / (np.float32(1) - np.float32(p))) if p > 0 else 1.0
+    d = torch.where(keep, dout.cpu().double() * scale, torch.zeros((), dtype=torch.float64))
+    ref_wte = torch.zeros(V, W, dtype=torch.float64).index_add_(0, tok.cpu().long(), d)
+    ref_wpe = d.view(B, S, W).sum(0)
+    assert (runs[0][0].double() - ref_wte).abs().max().item() < 1e-4 * max(1.0, ref_wte.abs().max().item())
+    assert (runs[0][1].double() - ref_wpe).abs().max().item() < 1e-4 * max(1.0, ref_wpe.abs().max().item())
+
+
+def test_dropout_mask_matches_oracle_philox(ops, cuda):
+    """The device Philox-4x32-10 dropout mask equals the oracle's numpy restatement element for element."""
+    from oracle import gpt_oracle
+    rows, width, p = 64, 1024, 0.1
+    ones = torch.ones(rows, width, device=cuda, dtype=torch.bfloat16)
+    out = ops.dropout_bwd(ones, p, 1000045, (3 << 32) | (1 << 8) | 5)
+    keep = gpt_oracle.keep_mask(1000045, (3 << 32) | (1 << 8) | 5, rows * width, p)
+    assert torch.equal(out.cpu().flatten() != 0, torch.from_numpy(keep))
+
+
 def test_adam_and_init(ops, cuda):
     n = 10000
     p = torch.empty(n, device=cuda, dtype=torch.bfloat16)
