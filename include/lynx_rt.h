@@ -108,7 +108,9 @@ char* lynx_plan_opt_timeline(const char* profile_json, int stage, const int* lay
  *   nccl_id (hex, from lynx_rt_nccl_unique_id on rank 0)}, "train": {dropout,
  *   seed, lr, beta1, beta2, eps, weight_decay, init_std}, "exec": {trace,
  *   check_recompute, elide_recompute, dry_run, head_chunk, probe_fc1, probe_ops,
- *   reserve_pool, standalone_stage, comm_standin_us, comm_standin_ctas}}.
+ *   reserve_pool, pool_internal_deps, standalone_stage, comm_standin_us, comm_standin_ctas,
+ *   standin_grad_wait_us, ledger_pass_start_us}}; parallel.loopback = "<name>" instead of
+ *   nccl_id runs every rank of the grid in this process on one GPU (one thread per rank).
  * Weights are initialised on the device from Philox streams keyed by seed. */
 typedef struct lynx_rt lynx_rt;
 int lynx_rt_create(const char* profile_json, const char* timeline_json, const char* config_json, lynx_rt** out);
@@ -119,11 +121,25 @@ int lynx_rt_create(const char* profile_json, const char* timeline_json, const ch
  * Blocks until the iteration's final event; *loss = mean token loss (last stage). */
 int lynx_rt_step(lynx_rt* h, const int* tokens, const int* labels, float* loss);
 
-/* Measured report of the last step (CUDA events): iteration / busy / comm /
- * recompute on-demand and overlapped / wait-on-recompute / exposed recompute ms,
- * recompute launches, bit-identity check counters, pool high-water bytes. */
+/* Measured report of the last step in the reference's simreport.schema.json shape
+ * (SimReport, proj/include/lynx/pipesim.hpp:68-75, emitted like simreport_to_json,
+ * report_io.cpp:103-143), for this executor's stage: iteration / busy / comm / stall
+ * (pipeline-receive waits) / recompute on-demand (kernels + main-stream waits on the side
+ * stream) / overlapped (window + stall fill) µs from CUDA events; breakdown weighted like
+ * pipesim.cpp:705-720; memory_peaks = the LOGICAL ledger's peak (see lynx_rt_stats_json);
+ * timeline = measured events of kinds fwd|bwd|comm_fwd|comm_bwd|recompute|stall_recompute|
+ * stall (exec.trace, else empty). Arrays hold this stage only. */
 char* lynx_rt_report_json(lynx_rt* h, int* status);
-/* Measured timeline of the last step (exec.trace): 0 Chrome trace JSON, 1 CSV. */
+/* Executor counters of the last step (flat JSON): iteration / busy / comm / recompute
+ * on-demand, overlapped, wait-on-recompute, exposed-recompute ms, launches, bit-identity check
+ * counters, pool high-water bytes, host issue / allocation ms, and "ledger": the logical memory
+ * ledger (pipesim.cpp:143-183, 483-605, 722-736) booked by this executor's own tensor
+ * productions and drops on the plan clock — {memory_peak_bytes, memory_trace [[t_us, bytes]],
+ * plan_clock}; with exec.ledger_pass_start_us = the simulator's pass starts it equals
+ * simulate()'s memory_traces / memory_peaks entry for this stage exactly. */
+char* lynx_rt_stats_json(lynx_rt* h, int* status);
+/* Measured timeline of the last step (exec.trace) in emit_trace's formats
+ * (pipesim.cpp:781-810): 0 Chrome trace JSON, 1 CSV. */
 char* lynx_rt_trace(lynx_rt* h, int format, int* status);
 /* Communication program of the last step (collectives / send / recv in issue order). */
 char* lynx_rt_program_json(lynx_rt* h, int* status);

@@ -112,8 +112,15 @@ def build(clean: bool = False, jobs: int | None = None, verbose: bool = False) -
         return LIB
     LIB.parent.mkdir(parents=True, exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
+    # Export the C-ABI only: the library's C++ symbols (nlohmann / STL template instances, the
+    # planner restatement) stay local, so they cannot interpose on another library loaded into the
+    # same process (e.g. the test oracle oracle/_ref, built from the reference with its own
+    # instances of the same templates).
+    exports = OBJ.parent / "exports.map"
+    exports.parent.mkdir(parents=True, exist_ok=True)
+    exports.write_text("{\n  global: lynx_*;\n  local: *;\n};\n")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs),
-           "-lcudart", *_nccl_link()]
+           "-lcudart", *_nccl_link(), "-Xlinker", f"--version-script={exports}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

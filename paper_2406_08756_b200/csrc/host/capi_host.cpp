@@ -254,6 +254,13 @@ char* lynx_plan_simulate_timelines(const char* profile_json, const int* layers, 
     nlohmann::ordered_json peaks = nlohmann::ordered_json::array();
     for (const auto& pk : r.peaks) peaks.push_back(to_canonical(pk));
     j["memory_peaks"] = peaks;
+    nlohmann::ordered_json starts = nlohmann::ordered_json::array();  // per stage, in pass order
+    for (const auto& st : r.pass_starts) {
+      nlohmann::ordered_json a = nlohmann::ordered_json::array();
+      for (const Rat& t : st) a.push_back(to_canonical(t));
+      starts.push_back(a);
+    }
+    j["pass_start_us"] = starts;
     j["csv"] = trace_csv(r);
     return j.dump();
   });

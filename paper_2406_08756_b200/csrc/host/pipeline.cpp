@@ -139,6 +139,7 @@ struct Lane {  // one pipeline stage
   Rat exposed_comm, first, last;
   bool any = false;
   std::vector<Event>* sink = nullptr;
+  std::vector<Rat> starts;  // pass start times (the executor's ledger clock for this stage)
 
   void event(EvKind k, int mb, int op, const Rat& s, const Rat& e, bool ov) {
     if (sink) sink->push_back(Event{stage, mb, k, op, s, e, ov});
@@ -523,6 +524,7 @@ class Model {
       if (t < start) ln.event(EvKind::Stall, mb, -1, t, start, false);
     }
     ln.started = true;
+    ln.starts.push_back(start);
     const Rat end = bwd ? backward(ln, mb, start) : forward(ln, mb, start);
     (bwd ? ln.bwd_done : ln.fwd_done)[mb] = end;
     ln.free_at = end;
@@ -535,6 +537,8 @@ class Model {
     r.breakdown.assign(S, {});
     r.peaks.assign(S, Rat(0));
     r.traces.assign(S, {});
+    r.pass_starts.assign(S, {});
+    for (int s = 0; s < S; ++s) r.pass_starts[s] = lanes_[s].starts;
     r.iteration_us = Rat(0);
     for (const Event& e : r.events) r.iteration_us = rmax(r.iteration_us, e.end);
     for (const Event& e : r.events) {

@@ -47,6 +47,7 @@ struct PipeResult {
   std::vector<Rat> peaks;
   std::vector<std::vector<std::pair<Rat, Rat>>> traces;
   std::vector<Event> events;
+  std::vector<std::vector<Rat>> pass_starts;  // per stage: start of each pass, in pass order
 };
 
 PipeResult run_pipeline(const Profile& p, const std::vector<int>& layers, const std::vector<StageTimeline>& tls,

@@ -184,6 +184,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.comm_standin_us = ex.value("comm_standin_us", 0.0);
   opt_.comm_standin_ctas = ex.value("comm_standin_ctas", 16);
   opt_.standin_grad_wait_us = ex.value("standin_grad_wait_us", std::vector<double>());
+  opt_.ledger_pass_start_us = ex.value("ledger_pass_start_us", std::vector<std::string>());
   cfg_.head_chunk = static_cast<int>(std::min<long long>(ex.value("head_chunk", 4096), cfg_.tokens()));
   if (cfg_.hidden % cfg_.heads || cfg_.heads % cfg_.tp || (cfg_.hidden / cfg_.tp) % 128)
     throw RtError("hidden must split into heads and TP ranks in 128-column tiles", kValidation);
@@ -271,6 +272,33 @@ void Executor::bind_template() {
     std::stable_sort(kv.second.begin(), kv.second.end(), [](const Recompute& a, const Recompute& b) {
       return std::tie(a.owner_mb, a.owner_layer, a.op) < std::tie(b.owner_mb, b.owner_layer, b.op);
     });
+  // plan clock and logical-ledger tables (pipesim.cpp:83-121 build_layout)
+  bwd_elem_.assign(n_, -1);
+  bwd_last_use_.assign(n_, -1);
+  for (int i = 0; i < n_; ++i) {
+    cost_.push_back(host::op_time(L.ops[i], prof_.hardware));
+    out_bytes_.push_back(L.ops[i].out_bytes);
+  }
+  for (int i = nf_; i < n_; ++i) bwd_elem_[i] = elem_of(bel_, i);
+  for (int i = nf_; i < n_; ++i)
+    for (int d : deps_[i])
+      if (d >= nf_) bwd_last_use_[d] = std::max(bwd_last_use_[d], bwd_elem_[i]);
+  for (const auto& o : prof_.model.embed_ops) {
+    pre_dur_ += o.kind == host::OpKind::Comm ? host::op_time(o, prof_.hardware) : o.time_us;
+    pre_bytes_ += o.out_bytes;
+  }
+  for (const auto& o : prof_.model.head_ops) {
+    post_dur_ += o.kind == host::OpKind::Comm ? host::op_time(o, prof_.hardware) : o.time_us;
+    post_bytes_ += o.out_bytes;
+  }
+  for (const std::string& x : opt_.ledger_pass_start_us) {
+    const auto r = host::parse_rat(x);
+    if (!r) throw RtError("exec.ledger_pass_start_us: '" + x + "' is not a rational", kValidation);
+    lg_.starts.push_back(*r);
+  }
+  lg_.override_starts = !lg_.starts.empty();
+  if (lg_.override_starts && lg_.starts.size() != host::stage_passes(cfg_.pp, cfg_.pp_rank, cfg_.n_micro).size())
+    throw RtError("exec.ledger_pass_start_us needs one start per pass of this stage", kValidation);
   slots_.assign(static_cast<size_t>(cfg_.n_micro) * cfg_.layers * nf_, Slot{});
   stage_in_.assign(cfg_.n_micro, nullptr);
   head_dy_.assign(cfg_.n_micro, nullptr);
@@ -417,6 +445,8 @@ void Executor::mark_ready(Slot& sl, cudaStream_t s) {
 
 void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
   if (!sl.p) return;
+  if (sl.booked) book(-out_bytes_[static_cast<size_t>(&sl - slots_.data()) % nf_]);
+  sl.booked = false;
   if (trace_slots()) {
     const size_t idx = static_cast<size_t>(&sl - slots_.data());
     std::fprintf(stderr, "drop mb%zu l%zu op%zu\n", idx / (cfg_.layers * nf_), (idx / nf_) % cfg_.layers, idx % nf_);
@@ -473,6 +503,58 @@ uint64_t Executor::drop_stream(int l, int mb, Op op) const {
          static_cast<uint64_t>(site);
 }
 
+// ============================================================ logical ledger
+// The reference simulator's memory ledger (pipesim.cpp:143-183, 483-605, 722-736): every
+// forward-template tensor this executor produces or drops books its profile out_bytes at the
+// plan-clock time of the element (or recompute item) doing it; backward-op outputs, the embedding
+// and the head are booked by the same rules (they are executor transients of other sizes). The
+// trace and peak are then formed exactly like the simulator's (stable sort by time, equal
+// timestamps netted), so with the simulator's pass start times (exec.ledger_pass_start_us) the
+// executor's liveness decisions reproduce simulate()'s memory_traces / memory_peaks bit for bit.
+void Executor::book(long long delta) {
+  if (!delta) return;
+  lg_.resident += host::Rat(delta);
+  lg_.deltas.emplace_back(lg_.t, host::Rat(delta));
+}
+
+void Executor::ledger_reset() {
+  lg_.t = lg_.free_at = host::Rat(0);
+  lg_.started = false;
+  lg_.pass = 0;
+  lg_.deltas.clear();
+  lg_.pass_release.clear();
+  lg_.budget = host::Rat(prof_.hardware.mem_budget_bytes);
+  const host::Rat share = host::Rat(prof_.model.static_bytes) * host::Rat(cfg_.layers) / host::Rat(prof_.model.n_layers);
+  lg_.resident = share;
+  lg_.deltas.emplace_back(host::Rat(0), share);
+  deferred_.clear();
+}
+
+host::Rat Executor::ledger_pass_start() {
+  host::Rat s = lg_.free_at;
+  if (lg_.override_starts) s = lg_.starts.at(lg_.pass);
+  ++lg_.pass;
+  return s;
+}
+
+std::pair<host::Rat, std::vector<std::pair<host::Rat, host::Rat>>> Executor::ledger_trace() const {
+  auto d = lg_.deltas;
+  std::stable_sort(d.begin(), d.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  host::Rat res(0), peak(0);
+  std::vector<std::pair<host::Rat, host::Rat>> tr;
+  for (size_t i = 0; i < d.size(); ++i) {
+    res += d[i].second;
+    if (i + 1 < d.size() && d[i + 1].first == d[i].first) continue;
+    if (!tr.empty() && tr.back().first == d[i].first) {
+      tr.back().second = res;
+    } else {
+      tr.emplace_back(d[i].first, res);
+    }
+    peak = host::rmax(peak, res);
+  }
+  return {peak, tr};
+}
+
 // ============================================================ timing
 cudaEvent_t Executor::ev() {
   if (ev_next_ == ev_pool_.size()) {
@@ -485,7 +567,7 @@ cudaEvent_t Executor::ev() {
 
 void Executor::span_begin(cudaStream_t s, int kind, int mb, int op) {
   if (opt_.dry_run) return;
-  TimedSpan sp{ev(), ev(), kind, mb, op, s == side_};
+  TimedSpan sp{ev(), ev(), kind, mb, op, s == side_, cur_bwd_};
   ck(cudaEventRecord(sp.a, s), "event");
   spans_.push_back(sp);
   open_.emplace_back(s, spans_.size() - 1);
@@ -512,7 +594,8 @@ void Executor::collect_spans() {
       case 0: rep_.busy_ms += ms; break;
       case 1: rep_.comm_ms += ms; break;
       case 2: rep_.recompute_on_demand_ms += ms; break;
-      case 3: rep_.recompute_overlapped_ms += ms; break;
+      case 3:
+      case 6: rep_.recompute_overlapped_ms += ms; break;
       case 4: rep_.wait_on_recompute_ms += ms; break;
       case 5: rep_.recv_wait_ms += ms; break;
       default: break;
@@ -521,7 +604,7 @@ void Executor::collect_spans() {
       float s0 = 0.f, s1 = 0.f;
       cudaEventElapsedTime(&s0, t0_, sp.a);
       cudaEventElapsedTime(&s1, t0_, sp.b);
-      trace_.emplace_back(cfg_.pp_rank, sp.mb, sp.kind, sp.op, 1e3 * s0, 1e3 * s1);
+      trace_.emplace_back(cfg_.pp_rank, sp.mb, sp.kind, sp.op, 1e3 * s0, 1e3 * s1, sp.bwd);
     }
   }
 }
@@ -536,6 +619,10 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
   if (out.p) {
     if (out.fused) {  // GeLU already written by the FC1 epilogue of this pass
       out.fused = false;
+      if (!out.booked) {  // a regenerated GeLU is booked at its own item's plan time, like the simulator
+        book(out_bytes_[pos]);
+        out.booked = true;
+      }
       return;
     }
     if (recompute) return;  // already resident (duplicate placement)
@@ -600,6 +687,8 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
   }
   out.p = alloc(bytes, s);
   out.bytes = bytes;
+  out.booked = true;
+  book(out_bytes_[pos]);
   if (recompute) ++rep_.recompute_launches;
   // FC1 with its GeLU fused into the GEMM epilogue when the GeLU tensor is not resident (forward
   // pass, or both discarded and regenerated): the GeLU slot is produced here, its own op call
@@ -611,6 +700,8 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
       gelu_slot = &slot(mb, l, gpos);
       gelu_slot->p = alloc(2 * T * 4 * hp, s);
       gelu_slot->bytes = 2 * T * 4 * hp;
+      gelu_slot->booked = !recompute;  // forward: same element as FC1; recompute: booked by GeLU's item
+      if (!recompute) book(out_bytes_[gpos]);
       if (recompute) ++rep_.recompute_launches;
     }
   }
@@ -704,38 +795,57 @@ void Executor::finish_production(Slot& out, size_t bytes, cudaStream_t s, bool r
   }
 }
 
-void Executor::run_items(const std::vector<Recompute>& items, cudaStream_t s, int span_kind) {
+// Runs recompute items in order on stream s. With a plan clock, each item books its tensor at
+// the clock and advances it by the op's cost (the simulator's item placement).
+void Executor::run_items(const std::vector<Recompute>& items, cudaStream_t s, int span_kind, host::Rat* clock) {
   if (items.empty() || opt_.elide_recompute) return;
   span_begin(s, span_kind, items.front().owner_mb, items.front().op);
   for (const Recompute& it : items) {
+    if (clock) lg_.t = *clock;
     const Op op = op_of_[it.op];
     if (op == Op::AR1 || op == Op::AR2) {
       // A discarded all-reduce output is only ever regenerated on the critical
       // path (heusched.cpp:125): re-issue its producer, then the collective.
-      if (slot(it.owner_mb, it.owner_layer, it.op).p) continue;
-      const int prod = it.op - 1;  // PROJ / FC2 precede their all-reduce
-      fwd_op(it.owner_mb, it.owner_layer, prod, main_, true);
-      host::Element e;
-      e.comm = true;
-      e.op = it.op;
-      comm_element(it.owner_mb, false, it.owner_layer, e);
-      slot(it.owner_mb, it.owner_layer, it.op).regenerated = true;
-      continue;
+      if (!slot(it.owner_mb, it.owner_layer, it.op).p) {
+        const int prod = it.op - 1;  // PROJ / FC2 precede their all-reduce
+        fwd_op(it.owner_mb, it.owner_layer, prod, main_, true);
+        host::Element e;
+        e.comm = true;
+        e.op = it.op;
+        comm_element(it.owner_mb, false, it.owner_layer, e, lg_.t);
+        slot(it.owner_mb, it.owner_layer, it.op).regenerated = true;
+      }
+    } else {
+      fwd_op(it.owner_mb, it.owner_layer, it.op, s, true);
     }
-    fwd_op(it.owner_mb, it.owner_layer, it.op, s, true);
+    if (clock) *clock += cost_[it.op];
   }
   span_end(s);
 }
 
-void Executor::run_critical(const Key4& key) {
+// Critical-path items of an element (plus stall-fill items the plan clock deferred to it), sorted
+// by (owner_mb, owner_layer, op) as the simulator sorts them (pipesim.cpp:426-440).
+void Executor::run_critical(const Key4& key, host::Rat& t) {
   auto f = crit_.find(key);
-  if (f != crit_.end()) run_items(f->second, main_, 2);
+  auto d = deferred_.find(key);
+  if (d == deferred_.end()) {
+    if (f != crit_.end()) run_items(f->second, main_, 2, &t);
+    return;
+  }
+  std::vector<Recompute> all = f != crit_.end() ? f->second : std::vector<Recompute>{};
+  all.insert(all.end(), d->second.begin(), d->second.end());
+  std::stable_sort(all.begin(), all.end(), [](const Recompute& a, const Recompute& b) {
+    return std::tie(a.owner_mb, a.owner_layer, a.op) < std::tie(b.owner_mb, b.owner_layer, b.op);
+  });
+  deferred_.erase(d);
+  run_items(all, main_, 2, &t);
 }
 
 // TP all-reduce element. Window items of (mb, bwd, l, window) are released on
 // the side stream at the same instant, so their kernels overlap the NCCL transfer.
-void Executor::comm_element(int mb, bool bwd, int l, const host::Element& e) {
+host::Rat Executor::comm_element(int mb, bool bwd, int l, const host::Element& e, const host::Rat& t) {
   const Op op = op_of_[e.op];
+  host::Rat busy = t;  // plan clock: window items are packed from the comm start (pipesim.cpp:398-424)
   const long long T = cfg_.tokens();
   const int h = cfg_.hidden;
   void* buf = nullptr;
@@ -761,9 +871,10 @@ void Executor::comm_element(int mb, bool bwd, int l, const host::Element& e) {
     auto w = win_.find({mb, bwd, l, e.window});
     if (w != win_.end() && !opt_.elide_recompute) {
       if (!opt_.dry_run) ck(cudaStreamWaitEvent(side_, go, 0), "wait");
-      run_items(w->second, side_, 3);
+      run_items(w->second, side_, 3, &busy);
     }
   }
+  lg_.t = t;
   if (!opt_.dry_run) {
     span_begin(tp_s_, 1, mb, e.op);
     if (opt_.comm_standin_us > 0)
@@ -776,11 +887,13 @@ void Executor::comm_element(int mb, bool bwd, int l, const host::Element& e) {
     ck(cudaEventRecord(done, tp_s_), "event");
     ck(cudaStreamWaitEvent(main_, done, 0), "wait");
   }
-  if (bwd) return;  // backward partials are reduced in place
+  if (bwd) return busy;  // backward partials are reduced in place
   // forward: bias + dropout + residual epilogue produces the op's tensor
   Slot& out = slot(mb, l, e.op);
   out.p = alloc(2 * T * h, main_);
   out.bytes = 2 * T * h;
+  out.booked = true;
+  book(out_bytes_[e.op]);
   const void* resid = op == Op::AR1 ? layer_input(mb, l, main_) : need(mb, l, pos_of(Op::AR1), main_);
   if (!opt_.dry_run) {
     const LayerParams P = ps_.layer(l);
@@ -795,6 +908,8 @@ void Executor::comm_element(int mb, bool bwd, int l, const host::Element& e) {
   Slot& part = slot(mb, l, pos_of(op == Op::AR1 ? Op::PROJ : Op::FC2));
   release(part.p, main_);
   part.p = nullptr;
+  part.booked = false;
+  return busy;
 }
 
 // ============================================================ backward operators
@@ -951,6 +1066,7 @@ void Executor::head_backward(int mb) {
 
 // ============================================================ passes
 void Executor::forward_pass(int mb) {
+  cur_bwd_ = false;
   const long long T = cfg_.tokens();
   const int h = cfg_.hidden;
   const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
@@ -978,21 +1094,42 @@ void Executor::forward_pass(int mb) {
     }
   }
   span_begin(main_, 0, mb);
+  // plan clock (pipesim.cpp:442-481 expand_fwd): the ledger books at these times
+  const host::Rat start = ledger_pass_start();
+  lg_.started = true;
+  host::Rat t = start;
+  if (cfg_.first()) {
+    t += pre_dur_;
+    lg_.t = start;
+    book(pre_bytes_);
+    lg_.pass_release[mb] += pre_bytes_;
+  }
   for (int l = 0; l < cfg_.layers; ++l) {
     for (size_t ei = 0; ei < fel_.size(); ++ei) {
       const host::Element& e = fel_[ei];
-      run_critical({mb, false, l, static_cast<int>(ei)});
+      run_critical({mb, false, l, static_cast<int>(ei)}, t);
+      host::Rat next = t + e.dur;
       if (e.comm) {
-        comm_element(mb, false, l, e);
+        next = host::rmax(next, comm_element(mb, false, l, e, t));
       } else {
+        lg_.t = t;
         for (int pos : e.ops) fwd_op(mb, l, pos, main_, false);
       }
       // discarded tensors drop after their last forward consumer (pipesim.cpp:496-504)
+      lg_.t = t + e.dur;
       for (int i = 0; i < nf_; ++i)
         if (!tl_.plan.retained[i] && std::max(made_in_[i], last_fwd_use_[i]) == static_cast<int>(ei))
           drop(slot(mb, l, i), main_, true);
+      t = next;
     }
   }
+  if (cfg_.last()) {
+    t += post_dur_;
+    lg_.t = t;
+    book(post_bytes_);
+    lg_.pass_release[mb] += post_bytes_;
+  }
+  lg_.free_at = t;
   if (cfg_.last()) {
     head_forward(mb);
   } else {
@@ -1018,18 +1155,47 @@ void Executor::backward_pass(int mb) {
   // one rounding per microbatch): the 2 B/parameter gradient of the paper's accounting.
   dw_epi_ = bwd_passes_ == 0 ? EPI_BF16 : EPI_ACC_BF16;  // bf16 gradients: store on the first pass
   ++bwd_passes_;
+  cur_bwd_ = true;
   const long long T = cfg_.tokens();
   const int h = cfg_.hidden;
-  // cool-down stall fill: released before the gradient arrives (pipesim.cpp:620-646)
+  const host::Rat start = ledger_pass_start();
+  // cool-down stall fill: released on the side stream before the gradient arrives, so it fills the
+  // bubble the receive leaves (pipesim.cpp:620-646). On the simulator's clock (ledger_pass_start_us)
+  // an item that does not fit the gap or the budget moves to the critical path at element 0 of its
+  // layer, as there; without it every item goes to the bubble (the gap is physical, not modelled).
   auto st = stall_.find(mb);
   if (st != stall_.end() && !opt_.elide_recompute) {
-    if (!opt_.dry_run) {
-      cudaEvent_t a = ev();
-      ck(cudaEventRecord(a, main_), "event");
-      ck(cudaStreamWaitEvent(side_, a, 0), "wait");
+    std::vector<Recompute> fit;
+    host::Rat t = lg_.free_at;
+    if (!lg_.override_starts) {
+      fit = st->second;
+    } else if (start > lg_.free_at && lg_.started) {
+      host::Rat resident = lg_.resident;
+      for (const Recompute& it : st->second) {
+        const host::Rat b(out_bytes_[it.op]);
+        if (t + cost_[it.op] <= start && resident + b <= lg_.budget) {
+          fit.push_back(it);
+          t += cost_[it.op];
+          resident += b;
+        } else {
+          deferred_[{mb, true, it.owner_layer, 0}].push_back(it);
+        }
+      }
+    } else {  // no gap on the simulator's clock: the reference never runs them (pipesim.cpp:620); the
+              // executor still must regenerate them, on the critical path
+      for (const Recompute& it : st->second) deferred_[{mb, true, it.owner_layer, 0}].push_back(it);
     }
-    run_items(st->second, side_, 3);
+    if (!fit.empty()) {
+      if (!opt_.dry_run) {
+        cudaEvent_t a = ev();
+        ck(cudaEventRecord(a, main_), "event");
+        ck(cudaStreamWaitEvent(side_, a, 0), "wait");
+      }
+      host::Rat clock = lg_.free_at;
+      run_items(fit, side_, 6, &clock);
+    }
   }
+  lg_.started = true;
   if (cfg_.last()) {
     head_backward(mb);
   } else {
@@ -1063,22 +1229,46 @@ void Executor::backward_pass(int mb) {
     }
   }
   span_begin(main_, 0, mb);
+  // plan clock (pipesim.cpp:509-605 expand_bwd / release_bwd)
+  host::Rat t = start;
+  long long sink = 0;
   for (int l = cfg_.layers - 1; l >= 0; --l) {
+    bool first_elem = true;
     for (size_t ei = 0; ei < bel_.size(); ++ei) {
       const host::Element& e = bel_[ei];
-      run_critical({mb, true, l, static_cast<int>(ei)});
+      run_critical({mb, true, l, static_cast<int>(ei)}, t);
+      const host::Rat tend = t + e.dur;
+      host::Rat next = tend;
+      lg_.t = t;
       if (e.comm) {
-        comm_element(mb, true, l, e);
+        book(out_bytes_[e.op]);  // logical: the all-reduced gradient (reduced in place here)
+        next = host::rmax(next, comm_element(mb, true, l, e, t));
       } else {
+        long long made = 0;  // logical: backward op outputs (executor transients of other sizes)
+        for (int pos : e.ops) made += out_bytes_[pos];
+        book(made);
         for (int pos : e.ops) bwd_op(mb, l, pos, main_);
       }
       // retained / regenerated tensors drop after their last backward consumer
+      lg_.t = tend;
       for (int i = 0; i < nf_; ++i)
         if (last_bwd_user_[i] == static_cast<int>(ei)) drop(slot(mb, l, i), main_, false);
+      long long out = 0;  // backward transients whose last consumer this element is (the sink crosses layers)
+      for (int o = nf_; o < n_ - 1; ++o)
+        if ((bwd_last_use_[o] >= 0 ? bwd_last_use_[o] : bwd_elem_[o]) == static_cast<int>(ei)) out += out_bytes_[o];
+      book(-out);
+      t = next;
+      if (first_elem) {  // the downstream layer's gradient has now been consumed
+        first_elem = false;
+        lg_.t = t;
+        book(-sink);
+        sink = 0;
+      }
     }
     // end-of-layer sweep (pipesim.cpp:546-569): everything else of (mb, l)
     if (l == cfg_.layers - 1 && !cfg_.last() && !opt_.dry_run)
       ck(cudaStreamWaitEvent(main_, act_sent_[mb], 0), "wait");  // the activation send read it
+    lg_.t = t;
     for (int i = 0; i < nf_; ++i) {
       Slot& sl = slot(mb, l, i);
       drop(sl, main_, false);
@@ -1087,7 +1277,15 @@ void Executor::backward_pass(int mb) {
         sl.shadow = nullptr;
       }
     }
+    if (n_ > nf_) sink = out_bytes_[n_ - 1];
   }
+  lg_.t = t;
+  book(-sink);
+  if (auto pe = lg_.pass_release.find(mb); pe != lg_.pass_release.end()) {
+    book(-pe->second);
+    lg_.pass_release.erase(pe);
+  }
+  lg_.free_at = t;
   void* dx = grad_[mb].dy;
   if (cfg_.first()) {
     if (!opt_.dry_run) {
@@ -1133,6 +1331,7 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   probes_.clear();
   op_events_.clear();
   bwd_passes_ = 0;
+  ledger_reset();
   const long long T = cfg_.tokens();
   const size_t ntok = static_cast<size_t>(cfg_.n_micro) * T;
   const auto passes = host::stage_passes(cfg_.pp, cfg_.pp_rank, cfg_.n_micro);
@@ -1238,7 +1437,7 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
 }
 
 // ============================================================ reports
-std::string Executor::report_json() const {
+std::string Executor::stats_json() const {
   Json j;
   j["stage"] = cfg_.pp_rank;
   j["tp_rank"] = cfg_.tp_rank;
@@ -1276,32 +1475,79 @@ std::string Executor::report_json() const {
   j["layers"] = cfg_.layers;
   j["microbatches"] = cfg_.n_micro;
   j["tokens_per_microbatch"] = cfg_.tokens();
+  // logical ledger of the last step (plan clock): simulate()'s memory_peaks / memory_traces entry for
+  // this stage when exec.ledger_pass_start_us carries the simulator's pass starts
+  const auto [peak, tr] = ledger_trace();
+  Json lt = Json::array();
+  for (const auto& [t, b] : tr) lt.push_back({host::to_canonical(t), host::to_canonical(b)});
+  j["ledger"] = {{"memory_peak_bytes", host::to_canonical(peak)}, {"memory_trace", lt},
+                 {"deltas", lg_.deltas.size()}, {"plan_clock", lg_.override_starts ? "simulator" : "back-to-back"}};
   return j.dump();
 }
 
+// Measured counterpart of simulate()'s SimReport for this stage (pipesim.hpp:68-75): CUDA-event
+// times on the executor's streams, the logical ledger's peak, and (exec.trace) the timeline.
+host::PipeResult Executor::measured_result() const {
+  auto us = [](double v) { return host::Rat::frac(std::llround(v * 1000.0), 1000); };  // ns resolution
+  host::PipeResult r;
+  r.iteration_us = us(rep_.step_ms * 1000.0);
+  host::StageSummary st;
+  st.busy = us(rep_.busy_ms * 1000.0);
+  st.comm = us(rep_.comm_ms * 1000.0);
+  st.stall = us(rep_.recv_wait_ms * 1000.0);
+  st.on_demand = us((rep_.recompute_on_demand_ms + rep_.wait_on_recompute_ms) * 1000.0);
+  st.overlapped = us(rep_.recompute_overlapped_ms * 1000.0);
+  r.stages.push_back(st);
+  host::Rat kept(0);  // tensor-path breakdown, weighted like pipesim.cpp:705-720
+  for (int o = 0; o < nf_; ++o)
+    if (tl_.plan.retained[o]) kept += cost_[o] * host::Rat(cfg_.layers) * host::Rat(cfg_.n_micro);
+  const host::Rat total = kept + st.overlapped + st.on_demand;
+  if (total.sign() == 0)
+    r.breakdown.push_back({host::Rat(1), host::Rat(0), host::Rat(0)});
+  else
+    r.breakdown.push_back({kept / total, st.overlapped / total, st.on_demand / total});
+  const auto lt = ledger_trace();
+  r.peaks.push_back(lt.first);
+  r.traces.push_back(lt.second);
+  for (const auto& [stage, mb, k, op, a, b, bwd] : trace_) {
+    host::Event e;
+    e.stage = stage;
+    e.microbatch = mb;
+    e.op = k == 0 || k == 5 ? -1 : op;
+    e.start = us(a);
+    e.end = us(b);
+    switch (k) {
+      case 0: e.kind = bwd ? host::EvKind::Bwd : host::EvKind::Fwd; break;
+      case 1: e.kind = bwd ? host::EvKind::CommBwd : host::EvKind::CommFwd; break;
+      case 2:
+      case 4: e.kind = host::EvKind::Recompute; break;  // on demand: kernels, or main waiting on the side stream
+      case 3:
+        e.kind = host::EvKind::Recompute;
+        e.overlapped = true;
+        break;
+      case 5: e.kind = host::EvKind::Stall; break;  // waiting for a pipeline receive
+      case 6:
+        e.kind = host::EvKind::StallRecompute;
+        e.overlapped = true;
+        break;
+      default: continue;
+    }
+    r.events.push_back(e);
+  }
+  std::stable_sort(r.events.begin(), r.events.end(), [](const host::Event& a, const host::Event& b) {
+    if (a.start != b.start) return a.start < b.start;
+    if (a.stage != b.stage) return a.stage < b.stage;
+    return static_cast<int>(a.kind) < static_cast<int>(b.kind);
+  });
+  return r;
+}
+
+std::string Executor::report_json() const { return host::simreport_json(measured_result()); }
+
+// emit_trace (pipesim.cpp:781-810) of the measured timeline: 0 Chrome trace, 1 CSV.
 std::string Executor::trace(int format) const {
-  static const char* kinds[] = {"pass", "comm", "recompute", "recompute_overlapped", "wait_recompute", "recv_wait"};
-  std::ostringstream os;
-  if (format == 1) {
-    os << "stage,microbatch,kind,op_id,start_us,end_us\n";
-    for (const auto& [st, mb, k, op, a, b] : trace_)
-      os << st << "," << mb << "," << kinds[k] << "," << (op < 0 ? "" : std::to_string(op)) << "," << a << "," << b
-         << "\n";
-    return os.str();
-  }
-  os << "[";
-  bool first = true;
-  for (const auto& [st, mb, k, op, a, b] : trace_) {
-    if (!first) os << ",";
-    first = false;
-    os << "\n  {\"name\": \"" << kinds[k];
-    if (mb >= 0) os << " mb" << mb;
-    if (op >= 0) os << " op" << op;
-    os << "\", \"ph\": \"X\", \"pid\": " << st << ", \"tid\": \"" << (k == 1 ? "comm" : (k == 3 ? "side" : "compute"))
-       << "\", \"ts\": " << a << ", \"dur\": " << (b - a) << "}";
-  }
-  os << "\n]\n";
-  return os.str();
+  const host::PipeResult r = measured_result();
+  return format == 1 ? host::trace_csv(r) : host::trace_chrome(r);
 }
 
 std::string Executor::program_json() const {
@@ -1401,6 +1647,13 @@ int lynx_rt_step(lynx_rt* h, const int* tokens, const int* labels, float* loss) 
 char* lynx_rt_report_json(lynx_rt* h, int* status) {
   std::string s;
   const int st = guard([&] { s = h->ex->report_json(); });
+  if (status) *status = st;
+  return st ? nullptr : dupstr(s);
+}
+
+char* lynx_rt_stats_json(lynx_rt* h, int* status) {
+  std::string s;
+  const int st = guard([&] { s = h->ex->stats_json(); });
   if (status) *status = st;
   return st ? nullptr : dupstr(s);
 }

@@ -60,6 +60,11 @@ struct ExecOptions {
                                              // B(m)'s gradient receive (from the simulator's trace),
                                              // held by a stand-in kernel so stall-fill recomputes
                                              // meet the bubble they are planned into
+  std::vector<std::string> ledger_pass_start_us;  // plan-clock start of each pass of this stage (exact
+                                                  // rationals, e.g. from lynx_plan_simulate_timelines'
+                                                  // pass_start_us): the logical ledger is then timed on
+                                                  // exactly the simulator's clock; default: passes back
+                                                  // to back from 0
 };
 
 struct Slot {
@@ -69,6 +74,7 @@ struct Slot {
   cudaStream_t stream = nullptr;
   bool regenerated = false;
   bool fused = false;      // produced early by the FC1 + GeLU epilogue; its own op call is a no-op
+  bool booked = false;     // its profile bytes are in the logical ledger
   void* shadow = nullptr;  // check_recompute: forward-produced copy
 };
 
@@ -99,7 +105,9 @@ class Executor {
   Executor(const std::string& profile_json, const std::string& timeline_json, const std::string& config_json);
   ~Executor();
   void step(const int* tokens_host, const int* labels_host, float* loss_out);
-  std::string report_json() const;
+  std::string report_json() const;  // simreport.schema.json document of the last step (measured)
+  std::string stats_json() const;   // executor counters, logical ledger trace, host timings
+  host::PipeResult measured_result() const;
   std::string trace(int format) const;
   std::string program_json() const;
   void get_tensor(const std::string& name, void* host, size_t bytes);
@@ -110,9 +118,11 @@ class Executor {
   using Key4 = std::tuple<int, bool, int, int>;
   struct TimedSpan {
     cudaEvent_t a, b;
-    int kind;  // 0 busy(pass), 1 comm, 2 on-demand recompute, 3 overlapped recompute, 4 wait-on-recompute, 5 recv wait
+    int kind;  // 0 busy(pass), 1 comm, 2 on-demand recompute, 3 window recompute, 4 wait-on-recompute,
+               // 5 recv wait, 6 stall-fill recompute
     int mb = -1, op = -1;
     bool on_side = false;
+    bool bwd = false;
   };
 
   // setup
@@ -126,9 +136,10 @@ class Executor {
   // passes
   void forward_pass(int mb);
   void backward_pass(int mb);
-  void run_items(const std::vector<host::Recompute>& items, cudaStream_t s, int span_kind);
-  void run_critical(const Key4& key);
-  void comm_element(int mb, bool bwd, int l, const host::Element& e);
+  void run_items(const std::vector<host::Recompute>& items, cudaStream_t s, int span_kind, host::Rat* clock);
+  void run_critical(const Key4& key, host::Rat& t);
+  // TP all-reduce element starting at plan-clock time t; returns when its window recomputes end
+  host::Rat comm_element(int mb, bool bwd, int l, const host::Element& e, const host::Rat& t);
   void fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute);
   void bwd_op(int mb, int l, int pos, cudaStream_t s);
   void head_forward(int mb);
@@ -143,6 +154,13 @@ class Executor {
   void drop(Slot& sl, cudaStream_t s, bool keep_shadow);
   void mark_ready(Slot& sl, cudaStream_t s);
   uint64_t drop_stream(int l, int mb, Op op) const;
+
+  // logical ledger (the simulator's memory ledger, pipesim.cpp:143-183 / 483-605 / 722-736), booked
+  // by this executor's own tensor productions and drops on the plan clock
+  void book(long long delta);
+  host::Rat ledger_pass_start();
+  void ledger_reset();
+  std::pair<host::Rat, std::vector<std::pair<host::Rat, host::Rat>>> ledger_trace() const;
 
   // timing
   cudaEvent_t ev();
@@ -208,7 +226,24 @@ class Executor {
   float* head_gw32_ = nullptr;  // last stage: LM-head weight gradient, fp32 across chunks / microbatches
   float* emb_gw32_ = nullptr;   // first stage: wte | wpe gradients, fp32 (sorted segment sums, no atomics)
   bool head_first_ = true;
-  std::vector<std::tuple<int, int, int, int, double, double>> trace_;  // stage, mb, kind, op, start, end
+  std::vector<std::tuple<int, int, int, int, double, double, bool>> trace_;  // stage, mb, kind, op, start, end, bwd
+  bool cur_bwd_ = false;  // direction of the pass being issued (span tags)
+
+  struct Ledger {
+    bool override_starts = false;
+    std::vector<host::Rat> starts;
+    host::Rat t, free_at, resident, budget;
+    bool started = false;
+    size_t pass = 0;
+    std::vector<std::pair<host::Rat, host::Rat>> deltas;  // (plan-clock time, +/- bytes), booking order
+    std::map<int, long long> pass_release;
+  } lg_;
+  std::vector<host::Rat> cost_;        // plan-clock cost of each template op (op_time)
+  std::vector<long long> out_bytes_;   // profile out_bytes of each template op
+  std::vector<int> bwd_elem_, bwd_last_use_;
+  host::Rat pre_dur_, post_dur_;
+  long long pre_bytes_ = 0, post_bytes_ = 0;
+  std::map<Key4, std::vector<host::Recompute>> deferred_;  // stall items the plan clock moves to the critical path
 };
 
 }  // namespace lynx::rt

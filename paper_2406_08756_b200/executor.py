@@ -22,6 +22,7 @@ _SIGS = {
     "lynx_rt_create": (_c.c_int, [_c.c_char_p, _c.c_char_p, _c.c_char_p, _c.POINTER(_c.c_void_p)]),
     "lynx_rt_step": (_c.c_int, [_c.c_void_p, _c.c_void_p, _c.c_void_p, _c.POINTER(_c.c_float)]),
     "lynx_rt_report_json": (_c.c_void_p, [_c.c_void_p, _c.POINTER(_c.c_int)]),
+    "lynx_rt_stats_json": (_c.c_void_p, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "lynx_rt_trace": (_c.c_void_p, [_c.c_void_p, _c.c_int, _c.POINTER(_c.c_int)]),
     "lynx_rt_program_json": (_c.c_void_p, [_c.c_void_p, _c.POINTER(_c.c_int)]),
     "lynx_rt_get_tensor": (_c.c_int, [_c.c_void_p, _c.c_char_p, _c.c_void_p, _c.c_size_t]),
@@ -94,6 +95,12 @@ class Executor:
         return float(loss.value)
 
     def report(self) -> dict:
+        """Executor counters of the last step (lynx_rt_stats_json), incl. the logical ledger."""
+        st = _c.c_int(0)
+        return json.loads(_take(_lib().lynx_rt_stats_json(self._h, _c.byref(st)), st))
+
+    def simreport(self) -> dict:
+        """The last step's measured report in simreport.schema.json shape (lynx_rt_report_json)."""
         st = _c.c_int(0)
         return json.loads(_take(_lib().lynx_rt_report_json(self._h, _c.byref(st)), st))
 
@@ -183,7 +190,7 @@ class LoopbackGrid:
     _count = 0
 
     def __init__(self, c: gp.GPTConfig, profile_text: str, plans: list[dict], *, exec_opts: dict | None = None,
-                 train: dict | None = None):
+                 train: dict | None = None, stage_exec_opts: list[dict] | None = None):
         LoopbackGrid._count += 1
         name = f"grid{LoopbackGrid._count}-{id(self):x}"
         self.c = c
@@ -194,7 +201,8 @@ class LoopbackGrid:
             for s in range(c.pp):
                 for r in range(c.tp):
                     cfg = make_config(c, self.layers, tp_rank=r, world_rank=s * c.tp + r, world_size=c.tp * c.pp,
-                                      loopback=name, train=train, exec_opts=opts)
+                                      loopback=name, train=train,
+                                      exec_opts={**opts, **(stage_exec_opts[s] if stage_exec_opts else {})})
                     self.ranks[(s, r)] = Executor(profile_text, plans[s]["timeline"], cfg)
         except Exception:
             self.close()

@@ -256,3 +256,39 @@ def test_oom_error_path_frees_everything(cuda):
     assert free1 >= free0 - (256 << 20), (free0, free1)
     losses, _, _, rep, _, _, _ = run(tiny(), "full")
     assert np.isfinite(losses[0]) and 0 < rep["pool_high_water_bytes"] <= total
+
+
+def test_real_step_ledger_simreport_and_trace(cuda):
+    """The measured report of a real step: the logical ledger equals simulate()'s memory trace and peak on the
+    simulator's clock; lynx_rt_report_json has the simreport.schema.json shape with a measured timeline
+    (forward / backward passes, all-reduces, window recomputes); lynx_rt_trace emits emit_trace's CSV."""
+    import sys
+    sys.path.insert(0, __file__.rsplit("/", 1)[0])
+    from test_ledger_parity import check_simreport_shape
+    from paper_2406_08756_b200 import executor as ex
+    from paper_2406_08756_b200 import gpt_profile as gp
+    from paper_2406_08756_b200 import planner
+    base = dict(name="gpt-tiny-tp", n_layers=4, hidden=512, heads=8, seq=256, micro_batch=2, vocab=50304, tp=1, pp=1,
+                n_microbatches=2, dropout=0.1, tp_template=True)
+    static = gp.BYTES_PER_PARAM_STATIC * gp.GPTConfig(**base).params()
+    c = gp.GPTConfig(**{**base, "mem_budget_bytes": static + 22 * 2**20})
+    text = gp.profile_text(c)
+    plan = ex.plan_for(text, 0, "heu")
+    sim = planner.simulate_timelines_text(text, plan["layers_per_stage"], [plan["timeline"]])
+    e = ex.Executor(text, plan["timeline"], ex.make_config(
+        c, plan["layers_per_stage"], exec_opts={"trace": True, "ledger_pass_start_us": sim["pass_start_us"][0]}))
+    try:
+        tok, lab = ex.synthetic_batch(c)
+        e.step(tok, lab)
+        rep, doc, csv = e.report(), e.simreport(), e.trace("csv")
+    finally:
+        e.close()
+    assert rep["ledger"]["memory_trace"] == sim["memory_traces"][0]
+    assert rep["ledger"]["memory_peak_bytes"] == sim["memory_peaks"][0]
+    check_simreport_shape(doc)
+    assert doc["memory_peaks"] == sim["memory_peaks"]
+    kinds = {ev["kind"] for ev in doc["timeline"]}
+    assert {"fwd", "bwd", "comm_fwd", "comm_bwd", "recompute"} <= kinds, kinds
+    assert any(ev["kind"] == "recompute" and ev["overlapped"] for ev in doc["timeline"])
+    assert float(doc["iteration_us"]) > 0 and float(doc["per_stage"][0]["busy_us"]) > 0
+    assert csv.splitlines()[0] == "stage,microbatch,kind,op_id,start_us,end_us,overlapped"

@@ -166,7 +166,9 @@ def test_gpt_simulated_ledger_matches(R, key, text):
     tls = [p["timeline"] for p in plans]
     ref = R.simulate_timelines(text, layers, tls, "0")
     mine = pl.simulate_timelines_text(text, layers, tls, "0")
+    starts = mine.pop("pass_start_us")  # the executor's ledger clock: an addition, not in the reference's output
     assert mine == ref
+    assert len(starts) == S and all(len(x) > 0 for x in starts)
 
 
 def _random_profile(rng: random.Random) -> str:

@@ -36,12 +36,14 @@ def cfg(tp=2, pp=1, n_micro=2, dropout=0.1, budget_extra_mib=None, layers=4):
     return gp.GPTConfig(**base)
 
 
-def grid_run(c, baseline="heu", exec_opts=None):
+def grid_run(c, baseline="heu", exec_opts=None, stage_exec_opts=None):
     from paper_2406_08756_b200 import executor as ex
     from paper_2406_08756_b200 import gpt_profile as gp
     text = gp.profile_text(c)
     plans = [ex.plan_for(text, s, baseline) for s in range(c.pp)]
-    g = ex.LoopbackGrid(c, text, plans, exec_opts=exec_opts)
+    if callable(stage_exec_opts):
+        stage_exec_opts = stage_exec_opts(text, plans)
+    g = ex.LoopbackGrid(c, text, plans, exec_opts=exec_opts, stage_exec_opts=stage_exec_opts)
     try:
         params = g.rank_tensors(grad=False)
         tok, lab = ex.synthetic_batch(c)
@@ -167,3 +169,21 @@ def test_tp2pp2_checked_recompute_has_no_mismatch(cuda):
     reps = res["reports"]
     assert sum(r["recompute_checked"] for r in reps.values()) > 0
     assert all(r["recompute_mismatch_words"] == 0 for r in reps.values())
+
+
+def test_tp2pp2_real_step_ledgers_equal_simulator(cuda):
+    """Every rank of a TP2·PP2 HEU run (window, critical and pipeline hand-offs on the B200) books a logical
+    ledger equal to the reference simulator's memory trace / peak of its stage, on the simulator's clock."""
+    from paper_2406_08756_b200 import planner
+    c = cfg(tp=2, pp=2, n_micro=4, dropout=0.1, budget_extra_mib=4)
+    sims = {}
+
+    def opts(text, plans):
+        sims["sim"] = planner.simulate_timelines_text(text, plans[0]["layers_per_stage"], [p["timeline"] for p in plans])
+        return [{"ledger_pass_start_us": sims["sim"]["pass_start_us"][s]} for s in range(c.pp)]
+
+    res = grid_run(c, "heu", stage_exec_opts=opts)
+    sim = sims["sim"]
+    for (s, r), rep in res["reports"].items():
+        assert rep["ledger"]["memory_trace"] == sim["memory_traces"][s], (s, r)
+        assert rep["ledger"]["memory_peak_bytes"] == sim["memory_peaks"][s], (s, r)
