@@ -136,6 +136,8 @@ int init_normal_sharded_bf16(__nv_bfloat16* p, float* master, long long rows, lo
                              int col_split, int tp, int tp_rank, float std, uint64_t seed, uint64_t stream_id,
                              cudaStream_t s);
 int f32_to_bf16(const float* src, __nv_bfloat16* dst, long long n, cudaStream_t s);
+// bytes / 4 words of uniform bf16 pairs in [-1, 1) (timing-only stand-in buffers).
+int fill_noise_bf16(void* p, size_t bytes, uint64_t seed, cudaStream_t s);
 // Single-GPU stand-in for a collective (exec.comm_standin_us): `ctas` CTAs of 512 threads hold
 // the stream for `ns` nanoseconds of %globaltimer, sleeping between polls. Models the transfer
 // time of an NCCL all-reduce the plan's window capacity assumes; not its SM / HBM traffic.

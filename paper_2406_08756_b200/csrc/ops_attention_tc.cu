@@ -1,4 +1,7 @@
-// Causal attention on tcgen05 tensor cores (head_dim 64 / 128, seq % 128 == 0).
+// Causal attention on tcgen05 tensor cores (head_dim 64 / 96 / 112 / 128, seq % 128 == 0).
+// A head of D columns occupies ceil(D / 64) 128-B swizzle atoms in shared memory (the last atom
+// of D = 96 / 112 is loaded whole by TMA and only its first D % 64 columns are read: QK^T runs
+// D / 16 K steps, the D-wide MMAs have N = D); epilogues move D columns in 32 / 16-column pieces.
 //
 // Same contract and layouts as ops_attention.cu (qkv [T, 3*H*D] = [Q|K|V],
 // out [T, H*D], lse [B, H, S] natural log; backward writes dQ|dK|dV with the
@@ -114,6 +117,25 @@ LYNX_DEV float ex2(float x) {
   return y;
 }
 
+// Columns [c0, c1) (multiples of 16) of this thread's TMEM lane, in 32- then 16-column pieces:
+// f(col, values, count) sees the fp32 bits of `count` consecutive columns starting at `col`.
+template <class F>
+LYNX_DEV void tmem_cols(uint32_t taddr, int c0, int c1, F&& f) {
+  int c = c0;
+  for (; c + 32 <= c1; c += 32) {
+    uint32_t o[32];
+    tmem_ld32(taddr + c, o);
+    tmem_ld_wait();
+    f(c, o, 32);
+  }
+  if (c < c1) {
+    uint32_t o[32];
+    tmem_ld16(taddr + c, o);
+    tmem_ld_wait();
+    f(c, o, 16);
+  }
+}
+
 // Per-tile event timeline of CTA (0,0,0) for kernel tuning: build with -DLYNX_ATTN_TRACE
 // (LYNX_BUILD_TRACE=1 python -m paper_2406_08756_b200.build); compiled out otherwise.
 #ifdef LYNX_ATTN_TRACE
@@ -142,7 +164,8 @@ __device__ long long g_atrace[8][64];
 // ============================================================== forward
 template <int D>
 struct FwdL {
-  static constexpr int kTile = 128 * D * 2;  // one 128-row x D tile (D/64 atoms of 16 KB)
+  static constexpr int kAtoms = (D + 63) / 64;
+  static constexpr int kTile = 128 * kAtoms * 64 * 2;  // one 128-row x D tile (ceil(D/64) atoms of 16 KB)
   static constexpr int kQ = 0, kK = kTile, kV = 3 * kTile, kBar = 5 * kTile;  // P lives in TMEM
   static constexpr int kBytes = kBar + 128 + 1024;
 };
@@ -152,7 +175,7 @@ __global__ void __launch_bounds__(256, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ out,
                        float* __restrict__ lse, int S, int H, float scale_log2) {
   using L = FwdL<D>;
-  constexpr int kA = D / 64;
+  constexpr int kA = L::kAtoms;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
@@ -286,15 +309,13 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(pv_done, (j - 1) & 1);
         tc_fence_after();
         if (need) {
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tmem + lanes + 256 + c * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(u2f(o[i]) * corr);
-            tmem_st32(tmem + lanes + 256 + c * 32, o);
-          }
+          tmem_cols(tmem + lanes + 256, 0, D, [&](int c, uint32_t* o, int cnt) {
+            for (int i = 0; i < cnt; ++i) o[i] = __float_as_uint(u2f(o[i]) * corr);
+            if (cnt == 32)
+              tmem_st32(tmem + lanes + 256 + c, o);
+            else
+              tmem_st16(tmem + lanes + 256 + c, o);
+          });
           tmem_st_wait();
         }
       }
@@ -314,17 +335,11 @@ __global__ void __launch_bounds__(256, 1)
     const float inv = 1.f / l_run;
     const int q = qb * 128 + r;
     BF8* orow = reinterpret_cast<BF8*>(out + static_cast<long long>(row0 + q) * HD + h * D);
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32(tmem + lanes + 256 + c * 32, o);
-      tmem_ld_wait();
+    tmem_cols(tmem + lanes + 256, 0, D, [&](int c, const uint32_t* o, int cnt) {
       float f[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]) * inv;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) orow[c * 4 + i] = f_to_bf8(f + 8 * i);
-    }
+      for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * inv;
+      for (int i = 0; i < cnt / 8; ++i) orow[c / 8 + i] = f_to_bf8(f + 8 * i);
+    });
     lse[(static_cast<long long>(b) * H + h) * S + q] = (m_run + log2f(l_run)) / kLog2e;
   }
   tc_fence_before();
@@ -337,8 +352,9 @@ __global__ void __launch_bounds__(256, 1)
 template <int D>
 struct DkvL {
   static constexpr int kStages = 3;        // Q / dO / lse / D ring (each stage is used early and late)
-  static constexpr int kKV = 128 * D * 2;  // K or V tile: D/64 atoms of 16 KB (128 rows)
-  static constexpr int kQT = 64 * D * 2;   // Q or dO tile: D/64 atoms of 8 KB (64 rows)
+  static constexpr int kAtoms = (D + 63) / 64;
+  static constexpr int kKV = 128 * kAtoms * 64 * 2;  // K or V tile: ceil(D/64) atoms of 16 KB (128 rows)
+  static constexpr int kQT = 64 * kAtoms * 64 * 2;   // Q or dO tile: ceil(D/64) atoms of 8 KB (64 rows)
   static constexpr int kK = 0, kV = kKV, kQ = 2 * kKV, kDO = kQ + kStages * kQT;
   static constexpr int kVec = kDO + kStages * kQT;  // lse2[kStages][64], dvec[kStages][64]; P^T / dS^T live in TMEM
   static constexpr int kBar = kVec + 2 * kStages * 256;
@@ -352,7 +368,7 @@ __global__ void __launch_bounds__(384, 1)
                         const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
                         float scale_log2) {
   using L = DkvL<D>;
-  constexpr int kA = D / 64, NS = L::kStages;
+  constexpr int kA = L::kAtoms, NS = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
@@ -514,17 +530,11 @@ __global__ void __launch_bounds__(384, 1)
     const long long grow = static_cast<long long>(row0 + key) * 3 * HD;
     BF8* dst = reinterpret_cast<BF8*>(dqkv + grow + (half ? HD : 2 * HD) + h * D);
     const float mul = half ? scale : 1.f;
-#pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
+    tmem_cols(tmem + lanes + (half ? 384 : 256), 0, D, [&](int c, const uint32_t* o, int cnt) {
       float f[32];
-      tmem_ld32(tmem + lanes + (half ? 384 : 256) + c * 32, o);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]) * mul;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dst[c * 4 + i] = f_to_bf8(f + 8 * i);
-    }
+      for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * mul;
+      for (int i = 0; i < cnt / 8; ++i) dst[c / 8 + i] = f_to_bf8(f + 8 * i);
+    });
   }
   tc_fence_before();
   __syncthreads();
@@ -536,8 +546,9 @@ __global__ void __launch_bounds__(384, 1)
 // ============================================================== backward dQ
 template <int D>
 struct DqL {
-  static constexpr int kQT = 128 * D * 2;  // Q or dO tile (128 rows)
-  static constexpr int kKT = 64 * D * 2;   // K or V tile (64 rows)
+  static constexpr int kAtoms = (D + 63) / 64;
+  static constexpr int kQT = 128 * kAtoms * 64 * 2;  // Q or dO tile (128 rows)
+  static constexpr int kKT = 64 * kAtoms * 64 * 2;   // K or V tile (64 rows)
   static constexpr int kStages = 3;
   static constexpr int kQ = 0, kDO = kQT, kK = 2 * kQT, kV = kK + kStages * kKT;
   static constexpr int kBar = kV + kStages * kKT;  // dS lives in TMEM
@@ -551,7 +562,7 @@ __global__ void __launch_bounds__(384, 1)
                       const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
                       float scale_log2) {
   using L = DqL<D>;
-  constexpr int kA = D / 64, NS = L::kStages;
+  constexpr int kA = L::kAtoms, NS = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
@@ -678,18 +689,13 @@ __global__ void __launch_bounds__(384, 1)
     }
     mbar_wait(fin, 0);
     tc_fence_after();
-    BF8* dqrow = reinterpret_cast<BF8*>(dqkv + static_cast<long long>(row0 + q) * 3 * HD + h * D + half * (D / 2));
-#pragma unroll
-    for (int c = 0; c < D / 64; ++c) {  // each warpgroup writes half of the D columns
-      uint32_t o[32];
+    BF8* dqrow = reinterpret_cast<BF8*>(dqkv + static_cast<long long>(row0 + q) * 3 * HD + h * D);
+    constexpr int kSplit = (D / 2 + 15) / 16 * 16;  // each warpgroup writes its share of the D columns
+    tmem_cols(tmem + lanes + 256, half ? kSplit : 0, half ? D : kSplit, [&](int c, const uint32_t* o, int cnt) {
       float f[32];
-      tmem_ld32(tmem + lanes + 256 + half * (D / 2) + c * 32, o);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) f[i] = u2f(o[i]) * scale;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dqrow[c * 4 + i] = f_to_bf8(f + 8 * i);
-    }
+      for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * scale;
+      for (int i = 0; i < cnt / 8; ++i) dqrow[c / 8 + i] = f_to_bf8(f + 8 * i);
+    });
   }
   tc_fence_before();
   __syncthreads();
@@ -734,18 +740,30 @@ int g_mode = -1;
 void attention_set_mode(int mode) { attn_tc::g_mode = mode; }
 int attention_mode() { return attn_tc::g_mode; }
 bool attention_tc_supported(int seq, int head_dim) {
-  return attn_tc::g_mode != 0 && seq % 128 == 0 && (head_dim == 64 || head_dim == 128);
+  return attn_tc::g_mode != 0 && seq % 128 == 0 &&
+         (head_dim == 64 || head_dim == 96 || head_dim == 112 || head_dim == 128);
 }
 
 int attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, int H, int D,
                      cudaStream_t s) {
-  return D == 64 ? attn_tc::fwd<64>(qkv, out, lse, B, S, H, s) : attn_tc::fwd<128>(qkv, out, lse, B, S, H, s);
+  switch (D) {
+    case 64: return attn_tc::fwd<64>(qkv, out, lse, B, S, H, s);
+    case 96: return attn_tc::fwd<96>(qkv, out, lse, B, S, H, s);   // GPT-20B
+    case 112: return attn_tc::fwd<112>(qkv, out, lse, B, S, H, s);  // GPT-1.3B
+    case 128: return attn_tc::fwd<128>(qkv, out, lse, B, S, H, s);
+    default: return set_error("attention_fwd_tc: head_dim must be 64, 96, 112 or 128", kValidation);
+  }
 }
 
 int attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* dvec,
                      __nv_bfloat16* dqkv, int B, int S, int H, int D, cudaStream_t s) {
-  return D == 64 ? attn_tc::bwd<64>(qkv, dout, lse, dvec, dqkv, B, S, H, s)
-                 : attn_tc::bwd<128>(qkv, dout, lse, dvec, dqkv, B, S, H, s);
+  switch (D) {
+    case 64: return attn_tc::bwd<64>(qkv, dout, lse, dvec, dqkv, B, S, H, s);
+    case 96: return attn_tc::bwd<96>(qkv, dout, lse, dvec, dqkv, B, S, H, s);
+    case 112: return attn_tc::bwd<112>(qkv, dout, lse, dvec, dqkv, B, S, H, s);
+    case 128: return attn_tc::bwd<128>(qkv, dout, lse, dvec, dqkv, B, S, H, s);
+    default: return set_error("attention_bwd_tc: head_dim must be 64, 96, 112 or 128", kValidation);
+  }
 }
 
 }  // namespace lynx

@@ -451,7 +451,28 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16*
     dst[i] = f2bf(src[i]);
 }
 
+// Uniform bf16 noise in [-1, 1) (hash of the index): realistic operand bits for timing-only runs.
+__global__ void fill_noise_kernel(uint32_t* __restrict__ p, long long n, uint64_t seed) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    uint64_t x = (static_cast<uint64_t>(i) + 1) * 0x9E3779B97F4A7C15ull ^ seed;
+    x ^= x >> 31;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    const float a = static_cast<float>(static_cast<uint32_t>(x) >> 8) * 1.1920929e-7f - 1.f;
+    const float b = static_cast<float>(static_cast<uint32_t>(x >> 32) >> 8) * 1.1920929e-7f - 1.f;
+    p[i] = pack_bf16x2(a, b);
+  }
+}
+
 }  // namespace
+
+int fill_noise_bf16(void* p, size_t bytes, uint64_t seed, cudaStream_t s) {
+  const long long n = static_cast<long long>(bytes / 4);
+  if (!n) return kOk;
+  fill_noise_kernel<<<grid_for(n), kBlock, 0, s>>>(static_cast<uint32_t*>(p), n, seed);
+  return check_launch("fill_noise_bf16");
+}
 
 int init_normal_sharded_bf16(__nv_bfloat16* p, float* master, long long rows, long long cols, long long row_blk,
                              int col_split, int tp, int tp_rank, float std, uint64_t seed, uint64_t stream_id,

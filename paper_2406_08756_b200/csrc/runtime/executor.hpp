@@ -43,6 +43,8 @@ struct ExecOptions {
   bool trace = false;           // per-element CUDA-event timeline
   bool check_recompute = false; // keep forward copies, compare regenerated tensors bit-for-bit
   bool elide_recompute = false; // timing-only: skip recompute launches (exposed-recompute cross-check)
+  bool elide_fill = false;      // elided mode: fill each stand-in buffer with uniform bf16 noise (timed apart,
+                                // report elide_fill_ms) so consumers read realistic operands, not stale memory
   bool dry_run = false;         // build the launch program only (no device)
   bool probe_fc1 = false;       // CUDA events around every FC1 forward GEMM launch (roofline line)
   bool reserve_pool = true;     // map all free HBM (but 2 GiB) into the activation pool at construction
@@ -89,6 +91,7 @@ struct StepReport {
   double probe_ms = 0;           // ... and their summed CUDA-event durations
   double alloc_host_ms = 0, alloc_host_max_ms = 0;  // host time inside pool allocations (stall diagnosis)
   double host_issue_ms = 0;                         // host time to issue the step (before the final sync)
+  double elide_fill_ms = 0;                         // exec.elide_fill: device time of the stand-in fills
   size_t pool_reserved = 0;
 };
 
@@ -220,7 +223,8 @@ class Executor {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> probes_;  // exec.probe_fc1 event pairs of this step
   size_t pool_reserved_init_ = 0;  // bytes mapped into the pool by reserve_pool()
   cudaStream_t probe_stream_ = nullptr;  // exec.probe_ops: the stream the current operator launches on
-  std::vector<std::tuple<const char*, cudaStream_t, cudaEvent_t>> op_events_;  // exec.probe_ops, this step
+  std::vector<std::tuple<std::string, cudaStream_t, cudaEvent_t>> op_events_;  // exec.probe_ops, this step
+  bool probe_recompute_ = false;  // exec.probe_ops: the current operator is a regeneration ("re: " prefix)
   std::vector<std::tuple<std::string, long long, double>> op_times_;           // name, launches, ms (last step)
   double op_stream_ms_[2] = {0, 0};                                            // main, side: sum of op times
   float* head_gw32_ = nullptr;  // last stage: LM-head weight gradient, fp32 across chunks / microbatches

@@ -77,8 +77,9 @@ def run_stage(text: str, timeline: dict, c: gp.GPTConfig, layers, opts: dict, to
 
 def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int = 1, ctas: int = 16,
             variants=("heu", "elided", "full_recompute"), bubbles: bool = True) -> dict:
-    """Per stage: its HEU plan, the same plan with recompute elided (no-recompute floor) and
-    Megatron full recompute, each as one TP rank with stand-in all-reduces."""
+    """Per stage: its HEU plan, the same plan with recompute elided (no-recompute floor), Megatron full
+    recompute and (variant "selective") Megatron selective recompute, each as one TP rank with stand-in
+    all-reduces."""
     std = {"comm_standin_us": standin_us(c), "comm_standin_ctas": ctas}
     tok, lab = ex.synthetic_batch(c)
     out = {}
@@ -98,9 +99,9 @@ def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int =
                 elif v == "elided":
                     row[v] = run_stage(text, heu["timeline"], c, layers, {**std, "elide_recompute": True}, tok, lab,
                                        steps, warmup)
-                else:
-                    full = ex.plan_for(text, s, "full")
-                    row[v] = run_stage(text, full["timeline"], c, layers, std, tok, lab, steps, warmup)
+                else:  # Megatron baselines: "full_recompute" (keep the checkpoint only), "selective" (core attention)
+                    base = ex.plan_for(text, s, "full" if v == "full_recompute" else v)
+                    row[v] = run_stage(text, base["timeline"], c, layers, std, tok, lab, steps, warmup)
             except ex.LynxError as err:
                 row[v] = {"error": str(err)[:200]}
         hr = row.get("heu", {})

@@ -284,9 +284,12 @@ def _ref_attention(qkv, B, S, H, D):
 
 @pytest.mark.parametrize("mode", [-1, 0])
 @pytest.mark.parametrize("B,S,H,D", [(2, 128, 2, 64), (1, 256, 3, 128), (2, 192, 2, 96), (1, 128, 2, 112),
-                                     (2, 640, 2, 128), (1, 1024, 1, 64), (1, 256, 4, 64)])
+                                     (2, 640, 2, 128), (1, 1024, 1, 64), (1, 256, 4, 64), (2, 256, 3, 96),
+                                     (1, 384, 2, 112), (1, 2048, 2, 96), (1, 2048, 2, 112)])
 def test_attention(ops, cuda, B, S, H, D, mode):
-    """mode -1: tcgen05 kernels where the shape allows (D 64/128, S % 128 == 0); 0: mma.sync kernels."""
+    """mode -1: tcgen05 kernels where the shape allows (D 64/96/112/128, S % 128 == 0); 0: mma.sync kernels."""
+    from paper_2406_08756_b200._native import lib
+    assert lib().lynx_op_attention_tc_supported(S, D) == (1 if S % 128 == 0 else 0)
     from paper_2406_08756_b200._native import lib
     g = torch.Generator(device=cuda).manual_seed(B * S * H * D)
     qkv = torch.randn(B * S, 3 * H * D, device=cuda, generator=g).bfloat16()

@@ -43,6 +43,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--ctas", type=int, default=16)
+    ap.add_argument("--variants", default="heu,elided,full_recompute",
+                    help="comma list of heu, elided, full_recompute, selective")
     ap.add_argument("--out", default="gpurun_out/emulate_tp2pp4.json")
     a = ap.parse_args()
     torch.cuda.set_device(0)
@@ -68,11 +70,12 @@ def main():
            "budget": "reduced (--budget-gb)" if a.budget_gb else "device HBM minus unmodelled reserve",
            "stages": {}}
     for s in (int(x) for x in a.stages.split(",")):
-        row = se.emulate(c, text, [s], steps=a.steps, warmup=a.warmup, ctas=a.ctas)[str(s)]
+        row = se.emulate(c, text, [s], steps=a.steps, warmup=a.warmup, ctas=a.ctas,
+                         variants=tuple(a.variants.split(",")))[str(s)]
         out["stages"][str(s)] = row
         print(json.dumps({"stage": s, "exposed_fraction_of_iteration": row.get("exposed_fraction_of_iteration"),
                           "crosscheck_ms": row.get("crosscheck_ms"),
-                          **{f"{k}_ms": row[k].get("iteration_ms") for k in ("heu", "elided", "full_recompute")}}),
+                          **{f"{k}_ms": row[k].get("iteration_ms") for k in a.variants.split(",") if k in row}}),
               flush=True)
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
