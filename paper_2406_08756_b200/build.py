@@ -109,6 +109,7 @@ def build(clean: bool = False, jobs: int | None = None, verbose: bool = False) -
                 print(log, file=sys.stderr)
     newest_obj = max(o.stat().st_mtime for o in objs)
     if LIB.exists() and LIB.stat().st_mtime >= newest_obj and not clean:
+        build_cli()
         return LIB
     LIB.parent.mkdir(parents=True, exist_ok=True)
     tmp = LIB.with_suffix(".so.tmp")
@@ -125,7 +126,25 @@ def build(clean: bool = False, jobs: int | None = None, verbose: bool = False) -
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    build_cli()
     return LIB
+
+
+CLI_SRC = PKG / "cli" / "lynx_execute.cpp"
+CLI = PKG / "_lib" / "lynx_execute"
+
+
+def build_cli() -> Path:
+    """`lynx execute` (cli/lynx_execute.cpp): a host C++ program over the C-ABI only."""
+    if CLI.exists() and CLI.stat().st_mtime >= max(CLI_SRC.stat().st_mtime, LIB.stat().st_mtime):
+        return CLI
+    cmd = [CXX, "-O2", "-std=c++17", "-Wall", f"-I{ROOT / 'include'}", f"-I{_nlohmann_include()}", str(CLI_SRC),
+           "-o", str(CLI), f"-L{LIB.parent}", "-l:liblynx_b200.so", "-Wl,-rpath,$ORIGIN",
+           "-Wl,-rpath,/usr/local/cuda/lib64", "-L/usr/local/cuda/lib64", "-lcudart"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"lynx_execute build failed:\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

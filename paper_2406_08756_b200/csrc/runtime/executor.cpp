@@ -180,6 +180,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.standalone = ex.value("standalone_stage", false);
   opt_.probe_fc1 = ex.value("probe_fc1", false);
   opt_.probe_ops = ex.value("probe_ops", false);
+  opt_.op_timing = ex.value("op_timing", false);
   opt_.reserve_pool = ex.value("reserve_pool", true);
   opt_.pool_internal_deps = ex.value("pool_internal_deps", false);
   opt_.comm_standin_us = ex.value("comm_standin_us", 0.0);
@@ -589,6 +590,19 @@ void Executor::span_end(cudaStream_t s) {
     }
 }
 
+template <class F>
+void Executor::timed_op(const char* name, F&& f) {
+  if (!opt_.op_timing || opt_.dry_run) {
+    f();
+    return;
+  }
+  cudaEvent_t a = ev(), b = ev();
+  ck(cudaEventRecord(a, main_), "event");
+  f();
+  ck(cudaEventRecord(b, main_), "event");
+  op_tim_.emplace_back(name, a, b);
+}
+
 void Executor::collect_spans() {
   rep_.busy_ms = rep_.comm_ms = rep_.recompute_on_demand_ms = rep_.recompute_overlapped_ms = 0;
   rep_.wait_on_recompute_ms = rep_.recv_wait_ms = rep_.elide_fill_ms = 0;
@@ -911,10 +925,12 @@ host::Rat Executor::comm_element(int mb, bool bwd, int l, const host::Element& e
   if (!opt_.dry_run) {
     const LayerParams P = ps_.layer(l);
     const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
+    timed_op(op == Op::AR1 ? "ar1_epilogue" : "ar2_epilogue", [&] {
     ck_op(bias_dropout_residual_fwd(static_cast<const __nv_bfloat16*>(buf), op == Op::AR1 ? P.b_proj : P.b_fc2,
                                     static_cast<const __nv_bfloat16*>(resid), static_cast<__nv_bfloat16*>(out.p), T, h,
                                     cfg_.dropout, seed, drop_stream(l, mb, op), main_),
           "residual");
+    });
   }
   mark_ready(out, main_);
   // the partial (PROJ / FC2, 0 bytes in the profile) is consumed
@@ -1086,9 +1102,11 @@ void Executor::forward_pass(int mb) {
   stage_in_[mb] = alloc(2 * T * h, main_);
   if (cfg_.first()) {
     if (!opt_.dry_run)
-      ck_op(embedding_fwd(d_tokens_ + mb * T, ps_.p("wte"), ps_.p("wpe"), static_cast<__nv_bfloat16*>(stage_in_[mb]),
+      timed_op("embed", [&] {
+        ck_op(embedding_fwd(d_tokens_ + mb * T, ps_.p("wte"), ps_.p("wpe"), static_cast<__nv_bfloat16*>(stage_in_[mb]),
                           cfg_.micro_batch, cfg_.seq, h, cfg_.dropout, seed, kEmbedStream | mb, main_),
             "embedding");
+      });
   } else {
     program_.push_back({"recv", "pp_act", cfg_.pp_rank - 1, static_cast<size_t>(2 * T * h), "F mb" + std::to_string(mb)});
     if (opt_.standalone && !opt_.dry_run) {
@@ -1126,7 +1144,7 @@ void Executor::forward_pass(int mb) {
         next = host::rmax(next, comm_element(mb, false, l, e, t));
       } else {
         lg_.t = t;
-        for (int pos : e.ops) fwd_op(mb, l, pos, main_, false);
+        for (int pos : e.ops) timed_op(op_name(op_of_[pos]), [&] { fwd_op(mb, l, pos, main_, false); });
       }
       // discarded tensors drop after their last forward consumer (pipesim.cpp:496-504)
       lg_.t = t + e.dur;
@@ -1144,7 +1162,7 @@ void Executor::forward_pass(int mb) {
   }
   lg_.free_at = t;
   if (cfg_.last()) {
-    head_forward(mb);
+    timed_op("head_fwd", [&] { head_forward(mb); });
   } else {
     void* out = need(mb, cfg_.layers - 1, nf_ - 1, main_);
     program_.push_back({"send", "pp_act", cfg_.pp_rank + 1, static_cast<size_t>(2 * T * h), "F mb" + std::to_string(mb)});
@@ -1210,7 +1228,7 @@ void Executor::backward_pass(int mb) {
   }
   lg_.started = true;
   if (cfg_.last()) {
-    head_backward(mb);
+    timed_op("head_bwd", [&] { head_backward(mb); });
   } else {
     grad_[mb].dy = alloc(2 * T * h, main_);
     program_.push_back({"recv", "pp_grad", cfg_.pp_rank + 1, static_cast<size_t>(2 * T * h), "B mb" + std::to_string(mb)});
@@ -1260,7 +1278,7 @@ void Executor::backward_pass(int mb) {
         long long made = 0;  // logical: backward op outputs (executor transients of other sizes)
         for (int pos : e.ops) made += out_bytes_[pos];
         book(made);
-        for (int pos : e.ops) bwd_op(mb, l, pos, main_);
+        for (int pos : e.ops) timed_op(op_name(op_of_[pos]), [&] { bwd_op(mb, l, pos, main_); });
       }
       // retained / regenerated tensors drop after their last backward consumer
       lg_.t = tend;
@@ -1408,6 +1426,13 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   ck(cudaEventElapsedTime(&ms, t0_, t1_), "elapsed");
   rep_.step_ms = ms;
   collect_spans();
+  op_tim_ms_.clear();
+  for (const auto& [name, a, b] : op_tim_) {
+    float d = 0.f;
+    ck(cudaEventElapsedTime(&d, a, b), "op timing");
+    op_tim_ms_[name].push_back(d);
+  }
+  op_tim_.clear();
   for (const auto& [a, b] : probes_) {
     float pm = 0.f;
     ck(cudaEventElapsedTime(&pm, a, b), "probe");
@@ -1475,6 +1500,7 @@ std::string Executor::stats_json() const {
   j["alloc_host_max_ms"] = rep_.alloc_host_max_ms;
   j["host_issue_ms"] = rep_.host_issue_ms;
   j["elide_fill_ms"] = rep_.elide_fill_ms;
+  if (opt_.op_timing) j["op_timing_ms"] = op_tim_ms_;
   j["pool_reserved_bytes"] = rep_.pool_reserved;
   j["pool_reserved_at_init_bytes"] = pool_reserved_init_;
   if (opt_.probe_ops) {

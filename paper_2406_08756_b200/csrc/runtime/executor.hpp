@@ -51,6 +51,9 @@ struct ExecOptions {
   bool pool_internal_deps = false;  // cudaMemPoolReuseAllowInternalDependencies on the activation pool: lets
                                     // an allocation on one stream reuse memory freed on another by making it
                                     // wait on the freeing stream (serialises the side stream behind main)
+  bool op_timing = false;       // CUDA events around every template operator on the main stream (forward /
+                                // backward ops, all-reduce epilogues, embedding, head): per-op device time
+                                // of exactly the executor's kernel sequence (the profiler's source)
   bool probe_ops = false;       // one CUDA event after every operator launch on its stream: in-step
                                 // time per operator name, gaps included (report "probe_ops")
   bool standalone = false;      // time one pipeline stage alone on one GPU: receives read synthetic
@@ -224,7 +227,11 @@ class Executor {
   size_t pool_reserved_init_ = 0;  // bytes mapped into the pool by reserve_pool()
   cudaStream_t probe_stream_ = nullptr;  // exec.probe_ops: the stream the current operator launches on
   std::vector<std::tuple<std::string, cudaStream_t, cudaEvent_t>> op_events_;  // exec.probe_ops, this step
-  bool probe_recompute_ = false;  // exec.probe_ops: the current operator is a regeneration ("re: " prefix)
+  bool probe_recompute_ = false;
+  std::vector<std::tuple<std::string, cudaEvent_t, cudaEvent_t>> op_tim_;  // exec.op_timing, this step
+  std::map<std::string, std::vector<double>> op_tim_ms_;                  // ... resolved (ms per call)
+  template <class F>
+  void timed_op(const char* name, F&& f);  // exec.probe_ops: the current operator is a regeneration ("re: " prefix)
   std::vector<std::tuple<std::string, long long, double>> op_times_;           // name, launches, ms (last step)
   double op_stream_ms_[2] = {0, 0};                                            // main, side: sum of op times
   float* head_gw32_ = nullptr;  // last stage: LM-head weight gradient, fp32 across chunks / microbatches

@@ -62,7 +62,7 @@ class ParamStore {
   void layout(const ModelCfg& c);
   void allocate_and_init(const ModelCfg& c, cudaStream_t s);
   void release();
-  LayerParams layer(int l) const;
+  LayerParams layer(int l) const { return layers_.at(static_cast<size_t>(l)); }  // resolved once at allocation
   __nv_bfloat16* p(const std::string& name) const;
   __nv_bfloat16* g(const std::string& name) const;
   long long count() const { return total_; }
@@ -74,7 +74,9 @@ class ParamStore {
  private:
   const ParamRef& find(const std::string& name) const;
   long long add(const std::string& name, long long n);
+  LayerParams resolve(int l) const;
   std::vector<ParamRef> refs_;
+  std::vector<LayerParams> layers_;
   long long total_ = 0;
 };
 

@@ -70,7 +70,7 @@ const ParamRef& ParamStore::find(const std::string& name) const {
 __nv_bfloat16* ParamStore::p(const std::string& name) const { return param + find(name).off; }
 __nv_bfloat16* ParamStore::g(const std::string& name) const { return grad + find(name).off; }
 
-LayerParams ParamStore::layer(int l) const {
+LayerParams ParamStore::resolve(int l) const {
   const std::string p = "l" + std::to_string(l) + ".";
   LayerParams L{};
   L.ln1_g = this->p(p + "ln1_g");
@@ -118,6 +118,8 @@ void ParamStore::allocate_and_init(const ModelCfg& c, cudaStream_t s) {
   ck(cudaMemsetAsync(v, 0, n * 4, s));
   ck(cudaMemsetAsync(param, 0, n * 2, s));  // alignment padding stays zero
   ck(cudaMemsetAsync(master, 0, n * 4, s));
+  layers_.clear();
+  for (int l = 0; l < c.layers; ++l) layers_.push_back(resolve(l));
   // Weights ~ N(0, std) defined on the UNSHARDED tensor: the Philox stream is keyed by
   // (global layer, tensor kind) only — no TP rank, no stage-local position — and each TP rank
   // materialises its Megatron slice of the full tensor (init_normal_sharded_bf16). Every TP / PP
@@ -164,6 +166,7 @@ void ParamStore::allocate_and_init(const ModelCfg& c, cudaStream_t s) {
 }
 
 void ParamStore::release() {
+  layers_.clear();
   cudaFree(param);
   cudaFree(master);
   cudaFree(grad);

@@ -116,6 +116,8 @@ def dropout_bwd_colsum(dout, acc, p: float, seed: int, stream_id: int):
 
 def column_sum_acc(x, acc):
     rows, width = x.shape
+    if acc.numel() < width or not acc.is_contiguous():
+        raise ValueError(f"column_sum_acc: accumulator of {acc.numel()} elements for width {width}")
     ws = torch.empty(lib().lynx_op_column_sum_workspace(rows, width) // 4 + 1, device=x.device, dtype=torch.float32)
     call("lynx_op_column_sum_acc", x.data_ptr(), acc.data_ptr(), ws.data_ptr(), rows, width, _s())
     return acc

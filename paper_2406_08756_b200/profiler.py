@@ -2,10 +2,20 @@
 
 The reference's profile carries per-operator times the paper obtains from a
 CUDA-event profiler of the real model (out of the
-reference's own scope). This module measures exactly the kernel
-sequence the executor launches for each template operator (the same C-ABI
-kernels, the same shapes per TP rank) with CUDA events, so that HEU's window
-capacities and recompute costs are B200-true:
+reference's own scope). `measure_op_times` times the EXECUTOR
+itself: a two-layer, two-microbatch standalone stage of the workload's width,
+sequence, micro-batch and TP degree runs training steps with exec.op_timing
+(CUDA events around every template operator on the main stream), so each op's
+time is that of the exact fused kernel sequence the step launches (FC2-dX with
+the GeLU backward epilogue, dropout backward with the bias column sum, bf16
+weight-gradient epilogues, the residual epilogues) under the step's own
+conditions. At TP > 1 every all-reduce is a stand-in kernel holding 16 CTAs
+for the modelled transfer time while the stage runs, as in the stage emulation.
+Ops the step does not launch alone are timed as the kernel the executor
+launches when regenerating them: `fc1` (plain GEMM: a kept GeLU) and `gelu`
+(stand-alone kernel: GeLU regenerated from a kept FC1; in the forward both are
+one fused GEMM). Op times of the other layer template (TP = 1 fused residual
+GEMMs vs TP partial + all-reduce epilogue) come from the isolated kernels.
 
     times = measure_op_times(cfg)            # {op name: Fraction(µs)}
     profile = gpt_profile.profile(cfg, times=times)
@@ -40,7 +50,63 @@ def _time(fn, iters: int = 5, warm: int = 2) -> float:
     return 1000.0 * s.elapsed_time(e) / iters  # µs
 
 
-def measure_op_times(c: gp.GPTConfig, iters: int = 5) -> dict[str, Fraction]:
+def measure_op_times(c: gp.GPTConfig, iters: int = 5, method: str = "executor") -> dict[str, Fraction]:
+    """{op: µs} for the profile of `c`; method "executor" (default, see the module docstring) or "isolated"
+    (each op's kernels launched alone on random operands)."""
+    iso = measure_op_times_isolated(c, iters)
+    if method == "isolated":
+        return iso
+    ms = executor_op_times(c)
+    out = dict(iso)
+    for k in ("qkv", "attn", "mlp_bwd", "attn_bwd", "ln1_bwd", "embed"):
+        out[k] = _us(ms[k])
+    out["ln1"] = out["ln2"] = out["final_ln"] = _us((ms["ln1"] + ms["ln2"]) / 2)
+    if c.tp > 1 or c.tp_template:
+        out["proj"], out["fc2"] = _us(ms["proj"]), _us(ms["fc2"])
+        tw = c.tp_model if c.tp == 1 else c.tp
+        ar_ms = 2.0 * (tw - 1) / tw * (2 * c.tokens * c.hidden) / (NVLINK_BUS_GBS * 1e6)
+        out["ar1"] = _us(ar_ms + ms["ar1_epilogue"])
+        out["ar2"] = _us(ar_ms + ms["ar2_epilogue"])
+    else:
+        out["proj_res"], out["fc2_res"] = _us(ms["proj_res"]), _us(ms["fc2_res"])
+    out["lm_head"] = _us(max(ms["head_fwd"] + ms["head_bwd"] - (ms["ln1"] + ms["ln2"]) / 2, 1e-6))
+    return out
+
+
+def _us(ms: float) -> Fraction:
+    """ms -> µs as an exact Fraction at ns resolution (the profile's rational time_us)."""
+    return Fraction(max(1, round(float(ms) * 1e6)), 1000)
+
+
+def executor_op_times(c: gp.GPTConfig, steps: int = 2) -> dict[str, float]:
+    """Median device time (ms) of each template operator of a two-layer, two-microbatch standalone
+    stage of `c`'s shapes (retain-all plan, exec.op_timing; all-reduces as stand-ins at TP > 1)."""
+    import statistics
+
+    from . import executor as ex
+    from . import stage_emulation as se
+    c2 = gp.GPTConfig(**{**c.__dict__, "n_layers": 2, "pp": 1, "n_microbatches": 2, "mem_budget_bytes": 10**15})
+    text = gp.profile_text(c2)
+    plan = ex.plan_for(text, 0, "retain_all")
+    opts = {"standalone_stage": True, "op_timing": True, "reserve_pool": False}
+    if c2.tp > 1 or c2.tp_template:
+        opts["comm_standin_us"] = max(se.standin_us(c2), 1.0)
+    e = ex.Executor(text, plan["timeline"], ex.make_config(c2, plan["layers_per_stage"], exec_opts=opts))
+    tok, lab = ex.synthetic_batch(c2)
+    try:
+        e.step(tok, lab)  # warm-up (pool growth, first launches)
+        acc: dict[str, list[float]] = {}
+        for _ in range(steps):
+            e.step(tok, lab)
+            for k, v in e.report()["op_timing_ms"].items():
+                acc.setdefault(k, []).extend(v)
+    finally:
+        e.close()
+        torch.cuda.empty_cache()
+    return {k: statistics.median(v) for k, v in acc.items()}
+
+
+def measure_op_times_isolated(c: gp.GPTConfig, iters: int = 5) -> dict[str, Fraction]:
     dev = "cuda"
     T, h, t = c.tokens, c.hidden, c.tp
     hp = h // t
@@ -78,7 +144,7 @@ def measure_op_times(c: gp.GPTConfig, iters: int = 5) -> dict[str, Fraction]:
 
     g_fc2 = torch.zeros(h, 4 * hp, device=dev)
     g_fc1 = torch.zeros(4 * hp, h, device=dev)
-    g_b = torch.zeros(4 * hp, device=dev)
+    g_b = torch.zeros(max(4 * hp, 3 * hp, h), device=dev)  # bias-gradient accumulator wide enough for every use
 
     def mlp_bwd():
         d = ops.dropout_bwd(y, c.dropout, 1, 3)

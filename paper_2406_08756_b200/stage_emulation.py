@@ -53,6 +53,28 @@ def simulated_grad_waits(text: str, stage: int, n_micro: int) -> list[float]:
     return waits
 
 
+def simulated_stage_ms(text: str, stage: int) -> float:
+    """The simulator's prediction of what the emulation measures for `stage` (ms): the stage's span in
+    the native simulator's HEU trace (first to last event) minus the stalls before forward passes
+    (activation receives, which the emulation does not hold)."""
+    rows = [r.split(",") for r in planner.simulate_text(text, "heu", fmt="csv").splitlines()[1:]]
+    mine = [r for r in rows if r[0] == str(stage) and r[2] != "p2p"]
+    if not mine:
+        return 0.0
+    start = min(float(r[4]) for r in mine)
+    end = max(float(r[5]) for r in mine)
+    fwd_stall, pending = 0.0, 0.0
+    for r in mine:
+        if r[2] == "stall":
+            pending += float(r[5]) - float(r[4])
+        elif r[2] in ("fwd", "comm_fwd"):
+            fwd_stall += pending
+            pending = 0.0
+        elif r[2] in ("bwd", "comm_bwd"):
+            pending = 0.0
+    return (end - start - fwd_stall) / 1000.0
+
+
 def run_stage(text: str, timeline: dict, c: gp.GPTConfig, layers, opts: dict, tok, lab, steps: int = 2,
               warmup: int = 1) -> dict:
     """The stage's executor alone: best of `steps` iterations after `warmup`."""
@@ -91,6 +113,7 @@ def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int =
         pj = json.loads(heu["plan_json"])
         row = {"layers_per_stage": layers, "plan": {k: pj[k] for k in ("S", "phase_assignment", "peak_bytes")},
                "simulated_period_us": heu["period_us"],
+               "simulated_stage_ms": round(simulated_stage_ms(text, s), 3),
                "grad_wait_us": [round(w, 1) for w in waits]}
         for v in variants:
             try:
@@ -109,6 +132,8 @@ def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int =
             row["exposed_fraction_of_iteration"] = round(hr["exposed_recompute_ms"] / hr["iteration_ms"], 4)
             rc = hr["recompute_on_demand_ms"] + hr["recompute_overlapped_ms"]
             row["exposed_fraction_of_recompute"] = round(hr["exposed_recompute_ms"] / rc, 4) if rc else 0.0
+            if row["simulated_stage_ms"]:  # simulator fidelity: predicted / measured stage time
+                row["simulated_over_measured"] = round(row["simulated_stage_ms"] / hr["iteration_ms"], 4)
             if "iteration_ms" in row.get("elided", {}):
                 row["crosscheck_ms"] = round(hr["iteration_ms"] - row["elided"]["iteration_ms"], 3)
         out[str(s)] = row
