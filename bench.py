@@ -351,7 +351,10 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
 
     from paper_2406_08756_b200 import executor as ex
     from paper_2406_08756_b200 import gpt_profile as gp
-    variants = [("elided", c, text, plans[0]["timeline"], {"elide_recompute": True})]
+    # elided: the consumers of skipped regenerations read stand-in buffers filled with bf16 noise (the fill is
+    # timed apart and subtracted): stale pool memory made the remaining GEMMs draw less power and run at a
+    # higher clock under the 1 kW cap, which had inflated the cross-check by ~30 % (tools/recompute_accounting.py)
+    variants = [("elided", c, text, plans[0]["timeline"], {"elide_recompute": True, "elide_fill": True})]
     if args.baselines:
         variants.append(("full", c, text, None, {}))
         variants.append(("selective", c, text, None, {"plan": "selective"}))
@@ -380,9 +383,11 @@ def run_variants(args, c, text, plans, cfg, tok, lab, tokens_iter, dev_ms, times
             for _ in range(3):  # the median of three steps (one slow step must not decide the cross-check)
                 be.step(btok, blab)
                 reps.append(be.report())
+            for r in reps:
+                r["iteration_ms"] -= r.get("elide_fill_ms", 0.0)
             br = sorted(reps, key=lambda r: r["iteration_ms"])[1]
             tok_i = cc.tokens * cc.n_microbatches
-            out[name] = {"iteration_ms": round(br["iteration_ms"], 3),
+            out[name] = {"iteration_ms": round(br["iteration_ms"], 3), "elide_fill_ms": round(br.get("elide_fill_ms", 0.0), 3),
                          "exposed_recompute_ms": round(br["exposed_recompute_ms"], 3),
                          "tokens_per_s": round(tok_i / (br["iteration_ms"] / 1000.0), 1),
                          "micro_batch": cc.micro_batch, "recompute_launches": br["recompute_launches"],
@@ -525,6 +530,10 @@ def run_gpu_arm(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic tokens, random-init weights",
         "config": workload_config(c, args),
         "exposed_recompute_ms_per_iter": round(exposed, 3),
+        # T(plan) - T(same plan, recompute elided, stand-in buffers noise-filled): the exposed cost measured as
+        # lost time, including the power-cap clock drop the extra work causes (the span metric above counts
+        # on-demand recompute kernels + main-stream waits only)
+        "exposed_recompute_crosscheck_ms": (extra or {}).get("elided", {}).get("exposed_recompute_crosscheck_ms"),
         "recompute": {"plan": plan0, "items": len(plans[stage]["timeline"]["items"]),
                       "launches_per_iter": rep["recompute_launches"],
                       "on_demand_ms": rep["recompute_on_demand_ms"], "overlapped_ms": rep["recompute_overlapped_ms"],

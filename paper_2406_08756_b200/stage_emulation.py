@@ -93,7 +93,8 @@ def run_stage(text: str, timeline: dict, c: gp.GPTConfig, layers, opts: dict, to
         torch.cuda.empty_cache()
     r = min(reps, key=lambda x: x["iteration_ms"])
     keys = ("iteration_ms", "comm_ms", "busy_ms", "recv_wait_ms", "exposed_recompute_ms", "recompute_on_demand_ms",
-            "recompute_overlapped_ms", "wait_on_recompute_ms", "recompute_launches", "pool_high_water_bytes")
+            "recompute_overlapped_ms", "wait_on_recompute_ms", "recompute_launches", "pool_high_water_bytes",
+            "elide_fill_ms")
     return {k: r[k] for k in keys if k in r} | {"iteration_ms_each": [round(x["iteration_ms"], 3) for x in reps]}
 
 
@@ -119,12 +120,16 @@ def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int =
             try:
                 if v == "heu":
                     row[v] = run_stage(text, heu["timeline"], c, layers, std, tok, lab, steps, warmup)
-                elif v == "elided":
-                    row[v] = run_stage(text, heu["timeline"], c, layers, {**std, "elide_recompute": True}, tok, lab,
-                                       steps, warmup)
+                elif v == "elided":  # stand-in buffers filled with noise (realistic operands), fill time excluded
+                    row[v] = run_stage(text, heu["timeline"], c, layers,
+                                       {**std, "elide_recompute": True, "elide_fill": True}, tok, lab, steps, warmup)
+                    row[v]["iteration_ms"] -= row[v].get("elide_fill_ms", 0.0)
                 else:  # Megatron baselines: "full_recompute" (keep the checkpoint only), "selective" (core attention)
                     base = ex.plan_for(text, s, "full" if v == "full_recompute" else v)
                     row[v] = run_stage(text, base["timeline"], c, layers, std, tok, lab, steps, warmup)
+                    peak = json.loads(base["plan_json"])["peak_bytes"]
+                    row[v]["plan_peak_bytes"] = peak
+                    row[v]["fits_budget"] = int(peak) <= json.loads(text)["hardware"]["mem_budget_bytes"]
             except ex.LynxError as err:
                 row[v] = {"error": str(err)[:200]}
         hr = row.get("heu", {})
