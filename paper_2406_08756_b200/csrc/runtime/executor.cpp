@@ -176,6 +176,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.check_recompute = ex.value("check_recompute", false);
   opt_.elide_recompute = ex.value("elide_recompute", false);
   opt_.elide_fill = ex.value("elide_fill", false);
+  opt_.window_join = ex.value("window_join", true);
   opt_.dry_run = ex.value("dry_run", false);
   opt_.standalone = ex.value("standalone_stage", false);
   opt_.probe_fc1 = ex.value("probe_fc1", false);
@@ -894,11 +895,18 @@ host::Rat Executor::comm_element(int mb, bool bwd, int l, const host::Element& e
     ck(cudaStreamWaitEvent(tp_s_, go, 0), "wait");
   }
   // window items (the reference packs them from the comm start, pipesim.cpp:398-424)
+  cudaEvent_t win_done = nullptr;
+  int win_op = -1;
   if (e.window >= 0) {
     auto w = win_.find({mb, bwd, l, e.window});
     if (w != win_.end() && !opt_.elide_recompute) {
       if (!opt_.dry_run) ck(cudaStreamWaitEvent(side_, go, 0), "wait");
       run_items(w->second, side_, 3, &busy);
+      if (opt_.window_join && !opt_.dry_run) {
+        win_done = ev();
+        ck(cudaEventRecord(win_done, side_), "event");
+        win_op = w->second.front().op;
+      }
     }
   }
   lg_.t = t;
@@ -913,6 +921,14 @@ host::Rat Executor::comm_element(int mb, bool bwd, int l, const host::Element& e
     cudaEvent_t done = ev();
     ck(cudaEventRecord(done, tp_s_), "event");
     ck(cudaStreamWaitEvent(main_, done, 0), "wait");
+    if (win_done) {
+      // The element after the all-reduce starts at max(comm end, window recompute end), as the
+      // reference schedules it (pipesim.cpp:462, 527): a recompute that spills past the window is
+      // waited for (and measured as exposed) instead of contending with the main stream for SMs.
+      span_begin(main_, 4, mb, win_op);
+      ck(cudaStreamWaitEvent(main_, win_done, 0), "wait");
+      span_end(main_);
+    }
   }
   if (bwd) return busy;  // backward partials are reduced in place
   // forward: bias + dropout + residual epilogue produces the op's tensor

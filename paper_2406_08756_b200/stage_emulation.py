@@ -92,18 +92,24 @@ def run_stage(text: str, timeline: dict, c: gp.GPTConfig, layers, opts: dict, to
         e.close()
         torch.cuda.empty_cache()
     r = min(reps, key=lambda x: x["iteration_ms"])
+    import statistics
+    op_ms = {k: round(statistics.median(v), 4) for k, v in r.get("op_timing_ms", {}).items()}
     keys = ("iteration_ms", "comm_ms", "busy_ms", "recv_wait_ms", "exposed_recompute_ms", "recompute_on_demand_ms",
             "recompute_overlapped_ms", "wait_on_recompute_ms", "recompute_launches", "pool_high_water_bytes",
             "elide_fill_ms")
-    return {k: r[k] for k in keys if k in r} | {"iteration_ms_each": [round(x["iteration_ms"], 3) for x in reps]}
+    out = {k: r[k] for k in keys if k in r} | {"iteration_ms_each": [round(x["iteration_ms"], 3) for x in reps]}
+    if op_ms:
+        out["op_timing_median_ms"] = op_ms
+    return out
 
 
 def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int = 1, ctas: int = 16,
-            variants=("heu", "elided", "full_recompute"), bubbles: bool = True) -> dict:
+            variants=("heu", "elided", "full_recompute"), bubbles: bool = True, op_timing: bool = False,
+            extra_opts: dict | None = None) -> dict:
     """Per stage: its HEU plan, the same plan with recompute elided (no-recompute floor), Megatron full
     recompute and (variant "selective") Megatron selective recompute, each as one TP rank with stand-in
     all-reduces."""
-    std = {"comm_standin_us": standin_us(c), "comm_standin_ctas": ctas}
+    std = {"comm_standin_us": standin_us(c), "comm_standin_ctas": ctas, **(extra_opts or {})}
     tok, lab = ex.synthetic_batch(c)
     out = {}
     for s in stages:
@@ -119,7 +125,8 @@ def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int =
         for v in variants:
             try:
                 if v == "heu":
-                    row[v] = run_stage(text, heu["timeline"], c, layers, std, tok, lab, steps, warmup)
+                    row[v] = run_stage(text, heu["timeline"], c, layers, {**std, "op_timing": op_timing}, tok, lab,
+                                       steps, warmup)
                 elif v == "elided":  # stand-in buffers filled with noise (realistic operands), fill time excluded
                     row[v] = run_stage(text, heu["timeline"], c, layers,
                                        {**std, "elide_recompute": True, "elide_fill": True}, tok, lab, steps, warmup)

@@ -25,8 +25,10 @@ def _files(tmp_path, exec_opts):
 def run(tmp_path, *args):
     if not B.CLI.exists():
         pytest.skip("lynx_execute not built")
+    import os
+    env = {**os.environ, "NCCL_DEBUG": "WARN"}  # NCCL's version banner goes to stdout otherwise
     r = subprocess.run([str(B.CLI), str(tmp_path / "p.json"), str(tmp_path / "c.json"), *args],
-                       capture_output=True, text=True, timeout=300)
+                       capture_output=True, text=True, timeout=300, env=env)
     return r.returncode, r.stdout, r.stderr
 
 

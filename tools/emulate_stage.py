@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--ctas", type=int, default=16)
     ap.add_argument("--variants", default="heu,elided,full_recompute",
                     help="comma list of heu, elided, full_recompute, selective")
+    ap.add_argument("--op-timing", action="store_true", help="per-operator device times of the HEU run")
+    ap.add_argument("--window-join", type=int, default=1, help="exec.window_join (1: reference semantics)")
     ap.add_argument("--out", default="gpurun_out/emulate_tp2pp4.json")
     a = ap.parse_args()
     torch.cuda.set_device(0)
@@ -67,11 +69,13 @@ def main():
                           "note": "stand-in kernel holds the TP stream for the modelled transfer time; "
                                   "real NCCL SM/HBM contention not modelled"},
            "profiler_s": round(prof_s, 2), "ledger_budget_bytes": c.mem_budget_bytes,
+           "profile_op_us": {k: float(v) for k, v in times.items()}, "window_join": bool(a.window_join),
            "budget": "reduced (--budget-gb)" if a.budget_gb else "device HBM minus unmodelled reserve",
            "stages": {}}
     for s in (int(x) for x in a.stages.split(",")):
         row = se.emulate(c, text, [s], steps=a.steps, warmup=a.warmup, ctas=a.ctas,
-                         variants=tuple(a.variants.split(",")))[str(s)]
+                         variants=tuple(a.variants.split(",")), op_timing=a.op_timing,
+                         extra_opts={"window_join": bool(a.window_join)})[str(s)]
         out["stages"][str(s)] = row
         print(json.dumps({"stage": s, "exposed_fraction_of_iteration": row.get("exposed_fraction_of_iteration"),
                           "crosscheck_ms": row.get("crosscheck_ms"),
