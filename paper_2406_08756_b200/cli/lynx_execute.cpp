@@ -7,7 +7,7 @@
 // emit_trace's CSV / Chrome trace, or the executor counters).
 //
 //   lynx_execute <profile.json> <config.json> [--mode heu|full|retain_all|selective]
-//                [--stage s] [--steps n] [--format json|csv|chrome|stats]
+//                [--stage s] [--steps n] [--format json|csv|chrome|stats] [--out file]
 //
 // config.json is the executor configuration of lynx_rt_create (model shape, layers_per_stage,
 // parallel, train, exec). Exit codes are the reference CLI's (lynx_main.cpp:30-35: 1 validation,
@@ -53,10 +53,10 @@ uint64_t mix(uint64_t& s) {
 int main(int argc, char** argv) {
   if (argc < 3) {
     std::cerr << "usage: lynx_execute <profile.json> <config.json> [--mode heu|full|retain_all|selective] "
-                 "[--stage s] [--steps n] [--format json|csv|chrome|stats]\n";
+                 "[--stage s] [--steps n] [--format json|csv|chrome|stats] [--out file]\n";
     return 1;
   }
-  std::string mode = "heu", format = "json";
+  std::string mode = "heu", format = "json", out_path;
   int stage = 0, steps = 1;
   for (int i = 3; i + 1 < argc; i += 2) {
     const std::string k = argv[i], v = argv[i + 1];
@@ -64,6 +64,7 @@ int main(int argc, char** argv) {
     else if (k == "--stage") stage = std::stoi(v);
     else if (k == "--steps") steps = std::stoi(v);
     else if (k == "--format") format = v;
+    else if (k == "--out") out_path = v;
     else {
       std::cerr << "unknown option " << k << "\n";
       return 1;
@@ -120,8 +121,19 @@ int main(int argc, char** argv) {
     lynx_rt_destroy(rt);
     return fail(st);
   }
-  std::fputs(out, stdout);
-  if (format == "stats") std::fputs("\n", stdout);
+  if (out_path.empty()) {
+    std::fputs(out, stdout);
+    if (format == "stats") std::fputs("\n", stdout);
+  } else {
+    std::ofstream f(out_path, std::ios::binary);
+    f << out;
+    if (!f) {
+      std::cerr << "cannot write " << out_path << "\n";
+      lynx_free(out);
+      lynx_rt_destroy(rt);
+      return 2;
+    }
+  }
   lynx_free(out);
   lynx_rt_destroy(rt);
   return 0;

@@ -32,6 +32,8 @@
 // gradient is accumulated with atomics: results are bit-reproducible.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "lynx_ops_internal.h"
 
@@ -45,6 +47,7 @@ namespace attn_tc {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescale = 8.f;  // log2 units
 constexpr int kAtom = 128;       // bytes per swizzled row (64 bf16)
+constexpr int kDefaultPoly = 0;  // see poly_every()
 
 LYNX_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -117,6 +120,19 @@ LYNX_DEV float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA / ALU pipes (no MUFU): round-to-nearest split x = j + f by the 1.5 * 2^23 trick,
+// 2^f by a cubic fitted on [-0.5, 0.5] (relative error < 1.2e-4, far below the bf16 rounding of P),
+// 2^j added to the exponent bits. x is clamped at -125 (ex2.approx.ftz flushes below -126 to 0; the
+// clamped value contributes < 2^-125 to sums of terms >= 1). Used for a fixed share of the softmax
+// exponentials so that the MUFU and FMA pipes share the row warps' work.
+LYNX_DEV float ex2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05459282f, f, 0.24221784f), f, 0.6933686f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+
 // Columns [c0, c1) (multiples of 16) of this thread's TMEM lane, in 32- then 16-column pieces:
 // f(col, values, count) sees the fp32 bits of `count` consecutive columns starting at `col`.
 template <class F>
@@ -170,7 +186,7 @@ struct FwdL {
   static constexpr int kBytes = kBar + 128 + 1024;
 };
 
-template <int D>
+template <int D, int kPoly>  // kPoly > 0: every kPoly-th softmax exponential on the FMA pipe (ex2_poly)
 __global__ void __launch_bounds__(256, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ out,
                        float* __restrict__ lse, int S, int H, float scale_log2) {
@@ -297,7 +313,8 @@ __global__ void __launch_bounds__(256, 1)
       float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < 128; ++i) {
-        x[i] = ex2(fmaf(x[i], scale_log2, -m_run));
+        const float a = fmaf(x[i], scale_log2, -m_run);
+        x[i] = (kPoly > 0 && i % (kPoly > 0 ? kPoly : 1) == (kPoly > 0 ? kPoly : 1) - 1) ? ex2_poly(a) : ex2(a);
         rv[i & 7] += x[i];
       }
       const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
@@ -704,12 +721,36 @@ __global__ void __launch_bounds__(384, 1)
 }
 
 // ============================================================== host
+// LYNX_ATTN_POLY: share of the forward softmax exponentials computed on the FMA pipe, as one in N
+// (0: all on MUFU). Read once.
+int poly_every() {
+  static const int n = [] {
+    const char* e = std::getenv("LYNX_ATTN_POLY");
+    return e ? std::atoi(e) : kDefaultPoly;
+  }();
+  return n;
+}
+
+template <int D, int kPoly>
+int fwd_poly(const CUtensorMap& m, __nv_bfloat16* out, float* lse, int B, int S, int H, cudaStream_t s) {
+  auto k = attn_fwd_tc_kernel<D, kPoly>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<D>::kBytes);
+  k<<<dim3(S / 128, H, B), 256, FwdL<D>::kBytes, s>>>(m, out, lse, S, H, kLog2e / sqrtf(static_cast<float>(D)));
+  return check_launch("attention_fwd_tc");
+}
+
 template <int D>
 int fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, int H, cudaStream_t s) {
   CUtensorMap m;
   const long long T = static_cast<long long>(B) * S, ld = 3LL * H * D;
   if (!gemm::make_map(&m, qkv, ld, T, ld, 64, 128)) return set_error("attention: tensor map encode failed");
-  auto k = attn_fwd_tc_kernel<D>;
+  switch (poly_every()) {
+    case 2: return fwd_poly<D, 2>(m, out, lse, B, S, H, s);
+    case 3: return fwd_poly<D, 3>(m, out, lse, B, S, H, s);
+    case 4: return fwd_poly<D, 4>(m, out, lse, B, S, H, s);
+    default: break;
+  }
+  auto k = attn_fwd_tc_kernel<D, 0>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<D>::kBytes);
   k<<<dim3(S / 128, H, B), 256, FwdL<D>::kBytes, s>>>(m, out, lse, S, H, kLog2e / sqrtf(static_cast<float>(D)));
   return check_launch("attention_fwd_tc");

@@ -78,14 +78,14 @@ def _us(ms: float) -> Fraction:
     return Fraction(max(1, round(float(ms) * 1e6)), 1000)
 
 
-def executor_op_times(c: gp.GPTConfig, steps: int = 2) -> dict[str, float]:
-    """Median device time (ms) of each template operator of a two-layer, two-microbatch standalone
+def executor_op_times(c: gp.GPTConfig, steps: int = 2, layers: int = 2, warmup: int = 1) -> dict[str, float]:
+    """Median device time (ms) of each template operator of a `layers`-layer, two-microbatch standalone
     stage of `c`'s shapes (retain-all plan, exec.op_timing; all-reduces as stand-ins at TP > 1)."""
     import statistics
 
     from . import executor as ex
     from . import stage_emulation as se
-    c2 = gp.GPTConfig(**{**c.__dict__, "n_layers": 2, "pp": 1, "n_microbatches": 2, "mem_budget_bytes": 10**15})
+    c2 = gp.GPTConfig(**{**c.__dict__, "n_layers": layers, "pp": 1, "n_microbatches": 2, "mem_budget_bytes": 10**15})
     text = gp.profile_text(c2)
     plan = ex.plan_for(text, 0, "retain_all")
     opts = {"standalone_stage": True, "op_timing": True, "reserve_pool": False}
@@ -94,7 +94,8 @@ def executor_op_times(c: gp.GPTConfig, steps: int = 2) -> dict[str, float]:
     e = ex.Executor(text, plan["timeline"], ex.make_config(c2, plan["layers_per_stage"], exec_opts=opts))
     tok, lab = ex.synthetic_batch(c2)
     try:
-        e.step(tok, lab)  # warm-up (pool growth, first launches)
+        for _ in range(warmup):
+            e.step(tok, lab)  # warm-up (pool growth, first launches)
         acc: dict[str, list[float]] = {}
         for _ in range(steps):
             e.step(tok, lab)
