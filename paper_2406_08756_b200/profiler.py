@@ -3,7 +3,7 @@
 The reference's profile carries per-operator times the paper obtains from a
 CUDA-event profiler of the real model (out of the
 reference's own scope). `measure_op_times` times the EXECUTOR
-itself: a two-layer, two-microbatch standalone stage of the workload's width,
+itself: an eight-layer standalone stage of the workload's width,
 sequence, micro-batch and TP degree runs training steps with exec.op_timing
 (CUDA events around every template operator on the main stream), so each op's
 time is that of the exact fused kernel sequence the step launches (FC2-dX with
@@ -78,14 +78,19 @@ def _us(ms: float) -> Fraction:
     return Fraction(max(1, round(float(ms) * 1e6)), 1000)
 
 
-def executor_op_times(c: gp.GPTConfig, steps: int = 2, layers: int = 2, warmup: int = 1) -> dict[str, float]:
-    """Median device time (ms) of each template operator of a `layers`-layer, two-microbatch standalone
-    stage of `c`'s shapes (retain-all plan, exec.op_timing; all-reduces as stand-ins at TP > 1)."""
+def executor_op_times(c: gp.GPTConfig, steps: int = 2, layers: int = 8, warmup: int = 1,
+                      micro: int = 1) -> dict[str, float]:
+    """Median device time (ms) of each template operator of a `layers`-layer standalone stage of `c`'s
+    shapes, `micro` microbatches (retain-all plan, exec.op_timing; all-reduces as stand-ins at TP > 1).
+    Eight layers: in a two-layer stage the LM head's GEMMs (tens of ms at the board's power cap) dominate
+    the step and the layer ops after them ran ~10 % slower than inside a full stage
+    (profiles/r02_profiler_check.json); with eight they match the stage's own per-op times."""
     import statistics
 
     from . import executor as ex
     from . import stage_emulation as se
-    c2 = gp.GPTConfig(**{**c.__dict__, "n_layers": layers, "pp": 1, "n_microbatches": 2, "mem_budget_bytes": 10**15})
+    c2 = gp.GPTConfig(**{**c.__dict__, "n_layers": layers, "pp": 1, "n_microbatches": micro,
+                         "mem_budget_bytes": 10**15})
     text = gp.profile_text(c2)
     plan = ex.plan_for(text, 0, "retain_all")
     opts = {"standalone_stage": True, "op_timing": True, "reserve_pool": False}
