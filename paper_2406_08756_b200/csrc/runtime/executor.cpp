@@ -57,6 +57,7 @@ Executor::Executor(const std::string& profile_json, const std::string& timeline_
   tl_ = host::parse_timeline(timeline_json);
   parse_config(config_json);
   bind_template();
+  validate_program();
   if (opt_.dry_run) return;
   try {
     init_device();
@@ -64,6 +65,30 @@ Executor::Executor(const std::string& profile_json, const std::string& timeline_
     release_all();  // a throwing constructor runs no destructor: free what was already allocated
     throw;
   }
+}
+
+// Replays the whole step's launch program on the host (dry run, no device work) before anything is
+// allocated: a timeline whose regeneration comes after a consumer of the tensor — or a tensor produced
+// twice — is rejected here, at lynx_rt_create, as the reference rejects it (InconsistentPlan, exit code 2,
+// pipesim.cpp:364-376), instead of in the middle of a step.
+void Executor::validate_program() {
+  const bool dry = opt_.dry_run;
+  const int step0 = step_;
+  opt_.dry_run = true;
+  try {
+    step(nullptr, nullptr, nullptr);
+  } catch (const RtError& e) {
+    opt_.dry_run = dry;
+    step_ = step0;
+    throw RtError(std::string("InconsistentPlan: ") + e.what(), e.code == kValidation ? kValidation : kParse);
+  }
+  opt_.dry_run = dry;
+  step_ = step0;
+  for (auto& sl : slots_) sl = Slot{};
+  std::fill(stage_in_.begin(), stage_in_.end(), nullptr);
+  std::fill(head_dy_.begin(), head_dy_.end(), nullptr);
+  std::fill(ln_f_.begin(), ln_f_.end(), nullptr);
+  std::fill(grad_.begin(), grad_.end(), Grad{});
 }
 
 void Executor::init_device() {

@@ -136,6 +136,7 @@ class Executor {
   // setup
   void parse_config(const std::string& cfg);
   void bind_template();
+  void validate_program();
   void init_device();
   void finish_production(Slot& out, size_t bytes, cudaStream_t s, bool recompute);
   void release_all();

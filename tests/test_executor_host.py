@@ -126,3 +126,27 @@ def test_bench_op_times_replay_reproduces_the_measured_plan(tmp_path):
     want = line["recompute"]["plan"]
     assert (got["S"], got["phase_assignment"], got["peak_bytes"]) == (want["S"], want["phase_assignment"],
                                                                        want["peak_bytes"])
+
+
+def test_non_causal_timeline_is_rejected_at_create():
+    """A timeline whose regeneration of a tensor comes after that tensor's consumer is rejected when the
+    executor is created (InconsistentPlan, the reference's exit code 2), not in the middle of a step."""
+    import copy
+    c = gp.GPTConfig("gpt-tiny", 4, 512, 8, 256, 2, 50304, 1, 1, 2, dropout=0.1)
+    text = gp.profile_text(c)
+    plan = ex.plan_for(text, 0, "full")
+    tl = copy.deepcopy(plan["timeline"])
+    late = None
+    for it in tl["items"]:
+        if it["host"] == "critical" and it["op"] == 1 and it["host_backward"]:  # qkv, consumed by attn_bwd
+            it["host_elem"] = 2  # ln1_bwd's element: after attn_bwd read it
+            late = it
+            break
+    assert late is not None
+    for dry in (True, False):
+        cfg = ex.make_config(c, plan["layers_per_stage"], exec_opts={"dry_run": dry})
+        with pytest.raises(ex.LynxError) as err:
+            ex.Executor(text, tl, cfg)
+        assert err.value.code == 2 and "InconsistentPlan" in str(err.value)
+    e = ex.Executor(text, plan["timeline"], ex.make_config(c, plan["layers_per_stage"], exec_opts={"dry_run": True}))
+    e.close()
