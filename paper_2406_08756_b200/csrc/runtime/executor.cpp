@@ -4,6 +4,7 @@
 #include <chrono>
 #include <map>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <stdexcept>
@@ -99,6 +100,17 @@ void Executor::init_device() {
   ck(cudaDeviceGetLimit(&stack, cudaLimitStackSize), "stack limit");
   if (stack < 1024) ck(cudaDeviceSetLimit(cudaLimitStackSize, 1024), "stack limit");
   if (needs_comms_) {
+    // A plan that regenerates an all-reduce output (phase 5 on ar1 / ar2, heusched.cpp:125) re-issues
+    // the collective; its result must be bit-identical to the first one. Ring / Simple is deterministic
+    // for a fixed communicator and size; the size-dependent choice among NVLS / tree / ring protocols is
+    // pinned so the two calls cannot differ (unless the user set NCCL_ALGO / NCCL_PROTO).
+    bool regen_ar = false;
+    for (const host::Recompute& it : tl_.items)
+      if (op_of_[it.op] == Op::AR1 || op_of_[it.op] == Op::AR2) regen_ar = true;
+    if (regen_ar && loopback_.empty()) {
+      setenv("NCCL_ALGO", "Ring", 0);
+      setenv("NCCL_PROTO", "Simple", 0);
+    }
     if (!loopback_.empty())
       comms_ = make_loopback_comms(loopback_, cfg_.tp, cfg_.pp, cfg_.pp_rank, cfg_.tp_rank);
     else
@@ -1236,6 +1248,8 @@ void Executor::backward_pass(int mb) {
   // an item that does not fit the gap or the budget moves to the critical path at element 0 of its
   // layer, as there; without it every item goes to the bubble (the gap is physical, not modelled).
   auto st = stall_.find(mb);
+  cudaEvent_t stall_done = nullptr;
+  int stall_op = -1;
   if (st != stall_.end() && !opt_.elide_recompute) {
     std::vector<Recompute> fit;
     host::Rat t = lg_.free_at;
@@ -1265,6 +1279,11 @@ void Executor::backward_pass(int mb) {
       }
       host::Rat clock = lg_.free_at;
       run_items(fit, side_, 6, &clock);
+      if (opt_.window_join && !opt_.dry_run) {
+        stall_done = ev();
+        ck(cudaEventRecord(stall_done, side_), "event");
+        stall_op = fit.front().op;
+      }
     }
   }
   lg_.started = true;
@@ -1299,6 +1318,14 @@ void Executor::backward_pass(int mb) {
       ck(cudaStreamWaitEvent(main_, b, 0), "wait");
       span_end(main_);
     }
+  }
+  if (stall_done) {
+    // The pass starts once the stall-fill regenerations are done (they were planned into the bubble
+    // before it, pipesim.cpp:620-646): an overrun is waited for and measured as exposed recompute,
+    // not left to contend with the backward kernels for SMs.
+    span_begin(main_, 4, mb, stall_op);
+    ck(cudaStreamWaitEvent(main_, stall_done, 0), "wait");
+    span_end(main_);
   }
   span_begin(main_, 0, mb);
   // plan clock (pipesim.cpp:509-605 expand_bwd / release_bwd)

@@ -43,8 +43,9 @@ struct ExecOptions {
   bool trace = false;           // per-element CUDA-event timeline
   bool check_recompute = false; // keep forward copies, compare regenerated tensors bit-for-bit
   bool elide_recompute = false; // timing-only: skip recompute launches (exposed-recompute cross-check)
-  bool window_join = true;      // main waits for a window's recomputes before the element after its all-reduce
-                                // (reference semantics); false: they may keep running beside the main stream
+  bool window_join = true;      // main waits for a window's recomputes before the element after its all-reduce,
+                                // and for a backward pass's stall-fill recomputes before the pass (reference
+                                // semantics); false: they may keep running beside the main stream
   bool elide_fill = false;      // elided mode: fill each stand-in buffer with uniform bf16 noise (timed apart,
                                 // report elide_fill_ms) so consumers read realistic operands, not stale memory
   bool dry_run = false;         // build the launch program only (no device)

@@ -25,11 +25,10 @@ def main():
     torch.cuda.set_device(0)
     base = gp.CONFIGS[a.model]
     c = gp.GPTConfig(**{**base.__dict__, "tp": a.tp, "dropout": 0.1})
-    keys = ("qkv", "attn", "mlp_bwd", "attn_bwd", "fc2", "proj", "ln1")
+    keys = ("qkv", "attn", "mlp_bwd", "attn_bwd", "fc2", "proj", "ln1", "head_fwd", "head_bwd", "embed")
     out = {}
-    for name, kw in [("2L_w1", dict(layers=2, warmup=1)), ("2L_w1_again", dict(layers=2, warmup=1)),
-                     ("2L_w4", dict(layers=2, warmup=4)), ("8L_w1", dict(layers=8, warmup=1)),
-                     ("8L_w3_s3", dict(layers=8, warmup=3, steps=3))]:
+    for name, kw in [("8L_m1", dict(layers=8, micro=1)), ("8L_m2", dict(layers=8, micro=2)),
+                     ("8L_m1_w3", dict(layers=8, micro=1, warmup=3, steps=3)), ("4L_m4", dict(layers=4, micro=4))]:
         ms = profiler.executor_op_times(c, **kw)
         out[name] = {k: round(1000 * ms[k], 1) for k in keys if k in ms}
         print(name, json.dumps(out[name]), flush=True)
