@@ -42,59 +42,7 @@ def measured_peaks() -> dict:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
 
 
-class ClockSampler:
-    """SM clocks and throttle reasons sampled through NVML every 200 ms during the timed region
-    (in-process; an nvidia-smi subprocess per sample perturbs the step)."""
-
-    def __init__(self, gpu: int = 0):
-        self.gpu = gpu
-        self.rows: list[tuple] = []
-        self._stop = threading.Event()
-        self._t = None
-        self._nv = self._hnd = self._mx = None
-        self._err = None
-        # NVML is initialised here, before the warm-up steps: nvmlInit running concurrently with the
-        # first timed step stalled it by up to 1.3 s (driver-level contention).
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-            self._nv, self._hnd = nv, nv.nvmlDeviceGetHandleByIndex(gpu)
-            self._mx = nv.nvmlDeviceGetMaxClockInfo(self._hnd, nv.NVML_CLOCK_SM)
-        except Exception as e:  # pragma: no cover
-            self._err = str(e)
-
-    def _run(self):
-        if self._err is not None:  # pragma: no cover
-            self.rows.append(("error", self._err))
-            return
-        nv, hnd, mx = self._nv, self._hnd, self._mx
-        while not self._stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(hnd, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(hnd)
-                self.rows.append((sm, mx, rs))
-            except Exception:
-                pass
-            self._stop.wait(0.2)
-
-    def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-        return self
-
-    def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
-
-    def summary(self) -> dict:
-        rows = [r for r in self.rows if r and r[0] != "error"]
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
-        bits = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
-        reasons = sorted({name for r in rows for bit, name in bits.items() if r[2] & bit})
-        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows), "source": "NVML"}
+from paper_2406_08756_b200.clocks import ClockSampler  # noqa: E402  (NVML clocks during the timed region)
 
 
 def dist_env():
@@ -141,6 +89,29 @@ def plan_all(c, profile_text: str, baseline: str):
     t0 = time.perf_counter()
     plans = [ex.plan_for(profile_text, s, baseline) for s in range(c.pp)]
     return plans, time.perf_counter() - t0
+
+
+def cpu_sample_step(c):
+    """One bounded-sample step of the CPU numerical port (oracle/gpt_oracle.py): fwd + bwd of ONE GPT
+    block of the workload's width and sequence length + the LM head at micro-batch 1, all host cores.
+    Returns (seconds, tokens of the sample, model-FLOP scale to the whole workload)."""
+    import numpy as np
+
+    from oracle import gpt_oracle
+    from paper_2406_08756_b200 import executor as ex
+    from paper_2406_08756_b200 import gpt_profile as gp
+    s = gp.GPTConfig("sample", 1, c.hidden, c.heads, c.seq, 1, c.vocab, 1, 1, 1, dropout=0.0)
+    shapes = ex.param_shapes(s, 1, True, True)
+    rng = np.random.default_rng(0)
+    params = {k: (rng.standard_normal(int(np.prod(v))) * 0.02).astype(np.float32) for k, v in shapes.items()}
+    for k in shapes:
+        if k.endswith("_g"):
+            params[k][:] = 1.0
+    tok, lab = ex.synthetic_batch(s)
+    t0 = time.perf_counter()
+    gpt_oracle.gpt_step(params, shapes, tok, lab, n_layers=1, hidden=s.hidden, heads=s.heads, seq=s.seq,
+                        micro_batch=1, n_micro=1)
+    return time.perf_counter() - t0, s.tokens, s.flops_per_token() / c.flops_per_token()
 
 
 def cpu_baseline(c, budget_s: float = 20.0) -> dict:
@@ -236,20 +207,37 @@ def load_op_times(path: str) -> dict:
 
 
 def run_reference_arm(args):
+    """The reference arm: the CPU implementation of the training step (oracle/gpt_oracle.py; the reference
+    itself only simulates the step, proj/src/pipesim.cpp) on this host's cores. Each step is one bounded
+    sample of the workload — fwd + bwd of one GPT block + LM head at micro-batch 1 — timed on the wall
+    clock, so --steps K of them take K x ms_per_step; `value` is that throughput scaled to the whole
+    workload by model FLOPs per token. The reference's own simulate() runs beside it (its prediction)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    import torch
     from paper_2406_08756_b200 import gpt_profile as gp
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
     c = config_for(max(args.gpus, 1), args)
     c.mem_budget_bytes = 170_000_000_000
     text = gp.profile_text(c)
-    base = cpu_baseline(c, budget_s=min(20.0, 6.0 * max(args.steps, 1)))
-    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "tokens/s", "n_gpus": 0,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "ms_per_step": 1000.0 * c.tokens * c.n_microbatches / base["value"],
-            "config": workload_config(c, args), "dtype": "f32", "data": "synthetic",
-            "cpu_baseline": base,
-            "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    for _ in range(min(args.warmup, 1)):  # one warm-up sample (the rest of W would only repeat it)
+        cpu_sample_step(c)
+    secs, toks, scale = [], 0, 1.0
+    for _ in range(args.steps):
+        dt, toks, scale = cpu_sample_step(c)
+        secs.append(dt)
+    sample_ms = 1000.0 * statistics.mean(secs)
+    value = toks / (sample_ms / 1000.0) * scale
+    sample = (f"one step = torch-CPU fp32 fwd+bwd of 1 GPT block (h={c.hidden}, s={c.seq}, micro-batch 1) + LM head "
+              f"({toks} tokens, {sample_ms:.0f} ms on {threads} threads); value scaled to {c.name} by model "
+              f"FLOPs/token (x{scale:.4g})")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": min(args.warmup, 1), "higher_is_better": True,
+            "ms_per_step": sample_ms, "config": workload_config(c, args), "dtype": "f32", "data": "synthetic",
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "reference_simulate": reference_simulate(c, text), "vs_baseline": None}
     print(json.dumps(line), flush=True)
 

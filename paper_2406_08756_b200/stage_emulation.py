@@ -20,6 +20,7 @@ bubbles. Forward (activation) receive stalls are not emulated.
 from __future__ import annotations
 
 import json
+from fractions import Fraction
 
 from . import executor as ex
 from . import gpt_profile as gp
@@ -80,14 +81,18 @@ def run_stage(text: str, timeline: dict, c: gp.GPTConfig, layers, opts: dict, to
     """The stage's executor alone: best of `steps` iterations after `warmup`."""
     import torch
     cfg = ex.make_config(c, layers, exec_opts={"standalone_stage": True, **opts})
+    from .clocks import ClockSampler
     e = ex.Executor(text, timeline, cfg)
     try:
         for _ in range(warmup):
             e.step(tok, lab)
         reps = []
-        for _ in range(steps):
-            e.step(tok, lab)
-            reps.append(e.report())
+        sampler = ClockSampler(0)
+        with sampler:
+            for _ in range(steps):
+                e.step(tok, lab)
+                reps.append(e.report())
+        clk = sampler.summary()
     finally:
         e.close()
         torch.cuda.empty_cache()
@@ -97,7 +102,8 @@ def run_stage(text: str, timeline: dict, c: gp.GPTConfig, layers, opts: dict, to
     keys = ("iteration_ms", "comm_ms", "busy_ms", "recv_wait_ms", "exposed_recompute_ms", "recompute_on_demand_ms",
             "recompute_overlapped_ms", "wait_on_recompute_ms", "recompute_launches", "pool_high_water_bytes",
             "elide_fill_ms")
-    out = {k: r[k] for k in keys if k in r} | {"iteration_ms_each": [round(x["iteration_ms"], 3) for x in reps]}
+    out = {k: r[k] for k in keys if k in r} | {"iteration_ms_each": [round(x["iteration_ms"], 3) for x in reps],
+                                               "sm_mhz_median": clk.get("sm_mhz")}
     if op_ms:
         out["op_timing_median_ms"] = op_ms
     return out
@@ -139,7 +145,15 @@ def emulate(c: gp.GPTConfig, text: str, stages, *, steps: int = 2, warmup: int =
                     row[v]["fits_budget"] = int(peak) <= json.loads(text)["hardware"]["mem_budget_bytes"]
             except ex.LynxError as err:
                 row[v] = {"error": str(err)[:200]}
+        # contention: the window / stall-fill regenerations' measured side-stream time (beside a 16-CTA
+        # all-reduce stand-in) against their cost in the profile (measured alone)
+        prof = json.loads(text)["model"]["layer"]["ops"]
+        cost_us = {i: float(Fraction(str(o["time_us"]))) for i, o in enumerate(prof)}
+        side_cost = sum(cost_us[it["op"]] for it in heu["timeline"]["items"] if it["host"] in ("window", "stall"))
+        row["side_items_profile_ms"] = round(side_cost / 1000.0, 3)
         hr = row.get("heu", {})
+        if "iteration_ms" in hr and side_cost > 0:
+            row["side_items_measured_over_profile"] = round(hr["recompute_overlapped_ms"] / (side_cost / 1000.0), 4)
         if "iteration_ms" in hr:
             row["exposed_fraction_of_iteration"] = round(hr["exposed_recompute_ms"] / hr["iteration_ms"], 4)
             rc = hr["recompute_on_demand_ms"] + hr["recompute_overlapped_ms"]
