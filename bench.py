@@ -61,7 +61,8 @@ def config_for(n_gpus: int, args):
         tp = 2
         pp = n_gpus // 2
         m = args.microbatches or max(2 * pp, 2)
-    c = gp.GPTConfig(**{**base.__dict__, "tp": tp, "pp": pp, "n_microbatches": m, "dropout": 0.1})
+    c = gp.GPTConfig(**{**base.__dict__, "tp": tp, "pp": pp, "n_microbatches": m, "dropout": 0.1,
+                        "vocab": gp.padded_vocab(tp)})
     if args.micro_batch:
         c.micro_batch = args.micro_batch
     return c

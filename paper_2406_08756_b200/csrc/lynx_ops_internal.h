@@ -102,6 +102,15 @@ size_t embedding_bwd_workspace(int batch, int seq, int width);
 
 int xent_fwd_bwd(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows, long long rows, int vocab,
                  float grad_scale, cudaStream_t s);
+// Vocab-parallel cross-entropy (TP > 1): the rank's logits cover vocabulary columns [v0, v0 + vl);
+// row_max is all-reduced (MAX) after xent_vp_max, sum_target ([2 * rows]: sums, then target logits)
+// (SUM) after xent_vp_sum; xent_vp_finish writes the loss rows and the logit gradients in place.
+int xent_vp_max(const __nv_bfloat16* logits, float* row_max, long long rows, int vl, cudaStream_t s);
+int xent_vp_sum(const __nv_bfloat16* logits, const int32_t* labels, long long v0, const float* row_max,
+                float* sum_target, long long rows, int vl, cudaStream_t s);
+int xent_vp_finish(__nv_bfloat16* logits, const int32_t* labels, long long v0, const float* row_max,
+                   const float* sum_target, float* loss_rows, long long rows, int vl, float grad_scale,
+                   cudaStream_t s);
 
 int attention_fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int batch, int seq, int heads,
                   int head_dim, cudaStream_t s);

@@ -316,6 +316,93 @@ __global__ void __launch_bounds__(kBlock) xent_kernel(__nv_bfloat16* __restrict_
   if (threadIdx.x == 0) loss_rows[row] = lse - target;
 }
 
+// ---------------------------------------------------------------- vocab-parallel cross-entropy
+// TP > 1 (Megatron): each rank holds the logits of vocabulary columns [v0, v0 + Vl). Three kernels
+// around two all-reduces over the TP group (executor.cpp head_forward):
+//   xent_vp_max     m_r[row] = max_j logit                                    -> all-reduce MAX
+//   xent_vp_sum     s_r[row] = sum_j exp(logit - m), t_r[row] = logit[label]
+//                   if the label is local, else 0                            -> all-reduce SUM
+//   xent_vp_finish  loss[row] = m + log(s) - t; logits <- (softmax - onehot) * grad_scale
+// Same arithmetic as xent_kernel, which they reproduce at TP = 1 up to summation order.
+template <class F>
+LYNX_DEV float block_reduce(float v, F op, float* red, float* bcast) {
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = red[0];
+    for (int i = 1; i < kBlock / 32; ++i) t = op(t, red[i]);
+    *bcast = t;
+  }
+  __syncthreads();
+  const float r = *bcast;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kBlock) xent_vp_max_kernel(const __nv_bfloat16* __restrict__ logits,
+                                                             float* __restrict__ row_max, int vl) {
+  __shared__ float red[kBlock / 32];
+  __shared__ float bcast;
+  const BF8* lr = reinterpret_cast<const BF8*>(logits + static_cast<long long>(blockIdx.x) * vl);
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < vl / 8; c += kBlock) {
+    float a[8];
+    bf8_to_f(lr[c], a);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) mx = fmaxf(mx, a[j]);
+  }
+  mx = block_reduce(mx, [](float x, float y) { return fmaxf(x, y); }, red, &bcast);
+  if (threadIdx.x == 0) row_max[blockIdx.x] = mx;
+}
+
+__global__ void __launch_bounds__(kBlock) xent_vp_sum_kernel(const __nv_bfloat16* __restrict__ logits,
+                                                             const int32_t* __restrict__ labels, long long v0,
+                                                             const float* __restrict__ row_max,
+                                                             float* __restrict__ sum_target, int vl, int rows) {
+  __shared__ float red[kBlock / 32];
+  __shared__ float bcast;
+  const int row = blockIdx.x;
+  const BF8* lr = reinterpret_cast<const BF8*>(logits + static_cast<long long>(row) * vl);
+  const float mx = row_max[row];
+  float s = 0.f;
+  for (int c = threadIdx.x; c < vl / 8; c += kBlock) {
+    float a[8];
+    bf8_to_f(lr[c], a);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += __expf(a[j] - mx);
+  }
+  s = block_reduce(s, [](float x, float y) { return x + y; }, red, &bcast);
+  if (threadIdx.x == 0) {
+    const long long lab = labels[row] - v0;
+    sum_target[row] = s;
+    sum_target[rows + row] = (lab >= 0 && lab < vl) ? bf2f(logits[static_cast<long long>(row) * vl + lab]) : 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) xent_vp_finish_kernel(__nv_bfloat16* __restrict__ logits,
+                                                                const int32_t* __restrict__ labels, long long v0,
+                                                                const float* __restrict__ row_max,
+                                                                const float* __restrict__ sum_target,
+                                                                float* __restrict__ loss_rows, int vl, int rows,
+                                                                float grad_scale) {
+  const int row = blockIdx.x;
+  BF8* lr = reinterpret_cast<BF8*>(logits + static_cast<long long>(row) * vl);
+  const float lse = row_max[row] + logf(sum_target[row]);
+  const long long lab = labels[row] - v0;
+  for (int c = threadIdx.x; c < vl / 8; c += kBlock) {
+    float a[8];
+    bf8_to_f(lr[c], a);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float pj = __expf(a[j] - lse);
+      a[j] = (pj - ((c * 8 + j) == lab ? 1.f : 0.f)) * grad_scale;
+    }
+    lr[c] = f_to_bf8(a);
+  }
+  if (threadIdx.x == 0) loss_rows[row] = lse - sum_target[rows + row];
+}
+
 LYNX_DEV float grad_at(const float* g, long long i) { return g[i]; }
 LYNX_DEV float grad_at(const __nv_bfloat16* g, long long i) { return bf2f(g[i]); }
 
@@ -590,6 +677,33 @@ int xent_fwd_bwd(__nv_bfloat16* logits, const int32_t* labels, float* loss_rows,
   if (!rows) return kOk;
   xent_kernel<<<static_cast<unsigned>(rows), kBlock, 0, s>>>(logits, labels, loss_rows, vocab, grad_scale);
   return check_launch("xent_fwd_bwd");
+}
+
+int xent_vp_max(const __nv_bfloat16* logits, float* row_max, long long rows, int vl, cudaStream_t s) {
+  if (vl % 8) return set_error("xent_vp: local vocab % 8", kValidation);
+  if (!rows) return kOk;
+  xent_vp_max_kernel<<<static_cast<unsigned>(rows), kBlock, 0, s>>>(logits, row_max, vl);
+  return check_launch("xent_vp_max");
+}
+
+int xent_vp_sum(const __nv_bfloat16* logits, const int32_t* labels, long long v0, const float* row_max,
+                float* sum_target, long long rows, int vl, cudaStream_t s) {
+  if (vl % 8) return set_error("xent_vp: local vocab % 8", kValidation);
+  if (!rows) return kOk;
+  xent_vp_sum_kernel<<<static_cast<unsigned>(rows), kBlock, 0, s>>>(logits, labels, v0, row_max, sum_target, vl,
+                                                                    static_cast<int>(rows));
+  return check_launch("xent_vp_sum");
+}
+
+int xent_vp_finish(__nv_bfloat16* logits, const int32_t* labels, long long v0, const float* row_max,
+                   const float* sum_target, float* loss_rows, long long rows, int vl, float grad_scale,
+                   cudaStream_t s) {
+  if (vl % 8) return set_error("xent_vp: local vocab % 8", kValidation);
+  if (!rows) return kOk;
+  xent_vp_finish_kernel<<<static_cast<unsigned>(rows), kBlock, 0, s>>>(logits, labels, v0, row_max, sum_target,
+                                                                       loss_rows, vl, static_cast<int>(rows),
+                                                                       grad_scale);
+  return check_launch("xent_vp_finish");
 }
 
 int adam_step(float* master, __nv_bfloat16* param, const void* grad, int grad_bf16, float* m, float* v, long long n,

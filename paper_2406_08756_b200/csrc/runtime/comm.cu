@@ -69,6 +69,9 @@ class NcclComms final : public Comms {
   void allreduce_sum_bf16(void* buf, size_t count, cudaStream_t s) override {
     nccl_ck(ncclAllReduce(buf, buf, count, ncclBfloat16, ncclSum, tp_, s), "allreduce");
   }
+  void allreduce_f32(float* buf, size_t count, bool max, cudaStream_t s) override {
+    nccl_ck(ncclAllReduce(buf, buf, count, ncclFloat32, max ? ncclMax : ncclSum, tp_, s), "allreduce f32");
+  }
   void send_bf16(const void* buf, size_t count, int peer, Channel ch, cudaStream_t s) override {
     nccl_ck(ncclSend(buf, count, ncclBfloat16, peer, ch == Channel::PP_ACT ? pa_ : pg_, s), "send");
   }
@@ -110,10 +113,25 @@ __global__ void loopback_sum_kernel(PtrPack ptrs, int n, long long nvec, long lo
   }
 }
 
+struct PtrPackF {
+  float* p[kMaxTp];
+};
+
+// fp32 MAX / SUM over the ranks in rank order, written to every rank's buffer.
+__global__ void loopback_f32_kernel(PtrPackF ptrs, int n, long long count, int is_max) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float acc = ptrs.p[0][i];
+    for (int r = 1; r < n; ++r) acc = is_max ? fmaxf(acc, ptrs.p[r][i]) : acc + ptrs.p[r][i];
+    for (int r = 0; r < n; ++r) ptrs.p[r][i] = acc;
+  }
+}
+
 struct ArCall {
   int arrived = 0, left = 0;
   bool complete = false;
   size_t count = 0;
+  int kind = 0;
   void* bufs[kMaxTp] = {};
   cudaEvent_t ready[kMaxTp] = {};
   cudaEvent_t done = nullptr;
@@ -172,7 +190,14 @@ class LoopbackComms final : public Comms {
     }
   }
 
-  void allreduce_sum_bf16(void* buf, size_t count, cudaStream_t s) override {
+  void allreduce_sum_bf16(void* buf, size_t count, cudaStream_t s) override { reduce(buf, count, 0, s); }
+  void allreduce_f32(float* buf, size_t count, bool max, cudaStream_t s) override {
+    reduce(buf, count, max ? 2 : 1, s);
+  }
+
+  // kind 0: bf16 SUM (fp32 accumulation), 1: fp32 SUM, 2: fp32 MAX. Every rank of the TP group calls
+  // its collectives in the same order (identical programs), so the k-th call of each rank matches.
+  void reduce(void* buf, size_t count, int kind, cudaStream_t s) {
     if (tp_ == 1) return;
     TpGroup& g = *grid_->groups[pp_rank_];
     const long long k = seq_++;
@@ -181,18 +206,29 @@ class LoopbackComms final : public Comms {
     cuda_ck(cudaEventRecord(ready, s), "event");
     std::unique_lock<std::mutex> lk(g.mu);
     ArCall& c = g.calls[k];
-    if (c.arrived && c.count != count) throw RtError("loopback all-reduce: ranks disagree on the size", kCudaError);
+    if (c.arrived && (c.count != count || c.kind != kind))
+      throw RtError("loopback all-reduce: ranks disagree on the size or type", kCudaError);
     c.count = count;
+    c.kind = kind;
     c.bufs[tp_rank_] = buf;
     c.ready[tp_rank_] = ready;
     if (++c.arrived == tp_) {  // last to arrive reduces for everyone
       for (int r = 0; r < tp_; ++r) cuda_ck(cudaStreamWaitEvent(s, c.ready[r], 0), "wait");
-      PtrPack pk{};
-      for (int r = 0; r < tp_; ++r) pk.p[r] = static_cast<__nv_bfloat16*>(c.bufs[r]);
-      const long long nvec = static_cast<long long>(count / 8);
-      long long blocks = (nvec + 255) / 256;
-      blocks = blocks < 1 ? 1 : (blocks > 148 * 8 ? 148 * 8 : blocks);
-      loopback_sum_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(pk, tp_, nvec, static_cast<long long>(count));
+      if (kind == 0) {
+        PtrPack pk{};
+        for (int r = 0; r < tp_; ++r) pk.p[r] = static_cast<__nv_bfloat16*>(c.bufs[r]);
+        const long long nvec = static_cast<long long>(count / 8);
+        long long blocks = (nvec + 255) / 256;
+        blocks = blocks < 1 ? 1 : (blocks > 148 * 8 ? 148 * 8 : blocks);
+        loopback_sum_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(pk, tp_, nvec, static_cast<long long>(count));
+      } else {
+        PtrPackF pk{};
+        for (int r = 0; r < tp_; ++r) pk.p[r] = static_cast<float*>(c.bufs[r]);
+        long long blocks = (static_cast<long long>(count) + 255) / 256;
+        blocks = blocks < 1 ? 1 : (blocks > 148 * 8 ? 148 * 8 : blocks);
+        loopback_f32_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(pk, tp_, static_cast<long long>(count),
+                                                                     kind == 2 ? 1 : 0);
+      }
       if (check_launch("loopback_allreduce") != kOk) throw RtError(last_error(), kCudaError);
       cuda_ck(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming), "event");
       cuda_ck(cudaEventRecord(c.done, s), "event");

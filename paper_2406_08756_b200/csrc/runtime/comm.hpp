@@ -36,6 +36,9 @@ class Comms {
   virtual ~Comms() = default;
   // In-place sum over the TP group of `count` bf16 elements, stream-ordered on s.
   virtual void allreduce_sum_bf16(void* buf, size_t count, cudaStream_t s) = 0;
+  // In-place fp32 MAX (max = true) or SUM over the TP group (the vocab-parallel cross-entropy's row
+  // statistics), stream-ordered on s.
+  virtual void allreduce_f32(float* buf, size_t count, bool max, cudaStream_t s) = 0;
   // Pipeline hand-off of `count` bf16 elements to / from stage `peer` (same TP rank).
   virtual void send_bf16(const void* buf, size_t count, int peer, Channel ch, cudaStream_t s) = 0;
   virtual void recv_bf16(void* buf, size_t count, int peer, Channel ch, cudaStream_t s) = 0;

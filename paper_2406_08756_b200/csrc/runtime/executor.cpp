@@ -363,8 +363,12 @@ void Executor::alloc_persistent() {
   sc_main_.ws = static_cast<float*>(m(ws));
   sc_main_.ws_bytes = ws;
   if (cfg_.last()) {
-    sc_main_.logits = static_cast<__nv_bfloat16*>(m(static_cast<size_t>(cfg_.head_chunk) * cfg_.vocab * 2));
-    head_gw32_ = static_cast<float*>(m(static_cast<size_t>(cfg_.vocab) * h * 4));
+    sc_main_.logits = static_cast<__nv_bfloat16*>(m(static_cast<size_t>(cfg_.head_chunk) * cfg_.vocab_rank() * 2));
+    head_gw32_ = static_cast<float*>(m(static_cast<size_t>(cfg_.vocab_rank()) * h * 4));
+    if (cfg_.vocab_parallel()) {
+      xent_max_ = static_cast<float*>(m(static_cast<size_t>(cfg_.head_chunk) * 4));
+      xent_st_ = static_cast<float*>(m(static_cast<size_t>(cfg_.head_chunk) * 8));
+    }
   }
   if (cfg_.first()) emb_gw32_ = static_cast<float*>(m(static_cast<size_t>(cfg_.vocab + cfg_.seq) * h * 4));
   if (opt_.standalone) {  // activations ~ N(0, 1), gradients ~ N(0, 1e-2): realistic operands for timing
@@ -407,9 +411,10 @@ void Executor::release_all() {
                   static_cast<void*>(sc_main_.t_wide), static_cast<void*>(sc_main_.ws),
                   static_cast<void*>(sc_main_.logits), static_cast<void*>(sc_side_.t_h), static_cast<void*>(d_tokens_),
                   static_cast<void*>(head_gw32_), static_cast<void*>(emb_gw32_), static_cast<void*>(syn_act_),
-                  static_cast<void*>(syn_grad_),
+                  static_cast<void*>(syn_grad_), static_cast<void*>(xent_max_), static_cast<void*>(xent_st_),
                   static_cast<void*>(d_labels_), static_cast<void*>(d_loss_), static_cast<void*>(d_mismatch_)})
     if (p) cudaFree(p);
+  xent_max_ = xent_st_ = nullptr;
   sc_main_ = Scratch{};
   sc_side_ = Scratch{};
   d_tokens_ = d_labels_ = nullptr;
@@ -1101,10 +1106,19 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
 // ============================================================ head / embedding
 void Executor::head_forward(int mb) {
   const long long T = cfg_.tokens();
-  const int h = cfg_.hidden, V = cfg_.vocab, C = cfg_.head_chunk;
+  const int h = cfg_.hidden, C = cfg_.head_chunk;
+  const int V = cfg_.vocab_rank();  // this rank's vocabulary rows (all of them unless vocab-parallel)
+  const bool vp = cfg_.vocab_parallel();
   void* x = need(mb, cfg_.layers - 1, nf_ - 1, main_);
   ln_f_[mb] = alloc(2 * T * h + 8 * T, main_);
   head_dy_[mb] = alloc(2 * T * h, main_);
+  if (vp) {  // the launch program's collectives (dry runs record them too)
+    for (long long c0 = 0; c0 < T; c0 += C) {
+      program_.push_back({"allreduce", "tp", -1, static_cast<size_t>(C) * 4, "xent max mb" + std::to_string(mb)});
+      program_.push_back({"allreduce", "tp", -1, static_cast<size_t>(C) * 8, "xent sum mb" + std::to_string(mb)});
+    }
+    program_.push_back({"allreduce", "tp", -1, static_cast<size_t>(T * h * 2), "head dX mb" + std::to_string(mb)});
+  }
   if (opt_.dry_run) return;
   auto* y = static_cast<__nv_bfloat16*>(ln_f_[mb]);
   auto* mean = reinterpret_cast<float*>(static_cast<char*>(ln_f_[mb]) + 2 * T * h);
@@ -1114,11 +1128,24 @@ void Executor::head_forward(int mb) {
   const __nv_bfloat16* w = ps_.p("w_head");
   float* gw = head_gw32_;  // fp32 across chunks and microbatches, added to the bf16 gradient at step end
   const float scale = 1.0f / static_cast<float>(T * cfg_.n_micro);
+  const long long v0 = vp ? static_cast<long long>(cfg_.tp_rank) * V : 0;
   for (long long c0 = 0; c0 < T; c0 += C) {
     const __nv_bfloat16* yc = y + c0 * h;
+    const int* lab = d_labels_ + mb * T + c0;
     GemmDesc lg{yc, h, false, w, h, false, sc_main_.logits, V, C, V, h, nullptr, EPI_BF16};
     ck_op(gemm_run(lg, main_), "lm_head");
-    ck_op(xent_fwd_bwd(sc_main_.logits, d_labels_ + mb * T + c0, d_loss_ + mb * T + c0, C, V, scale, main_), "xent");
+    if (!vp) {
+      ck_op(xent_fwd_bwd(sc_main_.logits, lab, d_loss_ + mb * T + c0, C, V, scale, main_), "xent");
+    } else {
+      // Megatron vocab-parallel cross-entropy: row max and (sum of exp, target logit) all-reduced over the
+      // TP group between the three kernels. Standalone (one TP rank alone) skips them: timing only.
+      ck_op(xent_vp_max(sc_main_.logits, xent_max_, C, V, main_), "xent max");
+      if (comms_) comms_->allreduce_f32(xent_max_, static_cast<size_t>(C), true, main_);
+      ck_op(xent_vp_sum(sc_main_.logits, lab, v0, xent_max_, xent_st_, C, V, main_), "xent sum");
+      if (comms_) comms_->allreduce_f32(xent_st_, static_cast<size_t>(2 * C), false, main_);
+      ck_op(xent_vp_finish(sc_main_.logits, lab, v0, xent_max_, xent_st_, d_loss_ + mb * T + c0, C, V, scale, main_),
+            "xent finish");
+    }
     GemmDesc dw{sc_main_.logits, V, true, yc, h, true, gw, h, V, h, C, nullptr,
                 head_first_ ? EPI_STORE_F32 : EPI_ACC_F32};
     head_first_ = false;
@@ -1126,6 +1153,13 @@ void Executor::head_forward(int mb) {
     GemmDesc dx{sc_main_.logits, V, false, w, h, true, static_cast<__nv_bfloat16*>(head_dy_[mb]) + c0 * h, h, C, h, V,
                 nullptr, EPI_BF16};
     ck_op(gemm_run(dx, main_), "lm_head dX");
+  }
+  if (vp) {  // the rows' gradient w.r.t. the final LayerNorm output: partial per vocabulary slice
+    if (comms_)
+      comms_->allreduce_sum_bf16(head_dy_[mb], static_cast<size_t>(T * h), main_);
+    else if (opt_.comm_standin_us > 0)
+      ck_op(comm_standin(static_cast<unsigned long long>(opt_.comm_standin_us * 1e3), opt_.comm_standin_ctas, main_),
+            "head dX stand-in");
   }
 }
 
@@ -1473,7 +1507,8 @@ void Executor::step(const int* tokens, const int* labels, float* loss_out) {
   // moved) so the weights, and the next steps' forward activations, stay valid.
   const size_t hsz = static_cast<size_t>(cfg_.hidden);
   if (cfg_.last() && !head_first_)
-    ck_op(add_f32_to_bf16(head_gw32_, ps_.g("w_head"), static_cast<long long>(cfg_.vocab) * hsz, main_), "head grad");
+    ck_op(add_f32_to_bf16(head_gw32_, ps_.g("w_head"), static_cast<long long>(cfg_.vocab_rank()) * hsz, main_),
+          "head grad");
   if (cfg_.first()) {
     ck_op(add_f32_to_bf16(emb_gw32_, ps_.g("wte"), static_cast<long long>(cfg_.vocab) * hsz, main_), "wte grad");
     ck_op(add_f32_to_bf16(emb_gw32_ + cfg_.vocab * hsz, ps_.g("wpe"), static_cast<long long>(cfg_.seq) * hsz, main_),

@@ -239,6 +239,7 @@ class Executor {
   std::vector<std::tuple<std::string, long long, double>> op_times_;           // name, launches, ms (last step)
   double op_stream_ms_[2] = {0, 0};                                            // main, side: sum of op times
   float* head_gw32_ = nullptr;  // last stage: LM-head weight gradient, fp32 across chunks / microbatches
+  float *xent_max_ = nullptr, *xent_st_ = nullptr;  // vocab-parallel cross-entropy row statistics (one chunk)
   float* emb_gw32_ = nullptr;   // first stage: wte | wpe gradients, fp32 (sorted segment sums, no atomics)
   bool head_first_ = true;
   std::vector<std::tuple<int, int, int, int, double, double, bool>> trace_;  // stage, mb, kind, op, start, end, bwd

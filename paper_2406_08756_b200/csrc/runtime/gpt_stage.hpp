@@ -41,6 +41,10 @@ struct ModelCfg {
   bool last() const { return pp_rank == pp - 1; }
   long long tokens() const { return static_cast<long long>(micro_batch) * seq; }
   int hp() const { return hidden / tp; }  // per-rank attention width
+  // Megatron vocab-parallel LM head + cross-entropy (TP > 1, vocabulary padded to 128 * tp rows):
+  // each TP rank holds vocab / tp rows of the head; otherwise the head is replicated.
+  bool vocab_parallel() const { return tp > 1 && vocab % (128 * tp) == 0; }
+  int vocab_rank() const { return vocab_parallel() ? vocab / tp : vocab; }
   int heads_rank() const { return heads / tp; }
 };
 

@@ -57,7 +57,7 @@ void ParamStore::layout(const ModelCfg& c) {
   if (c.last()) {
     add("lnf_g", h);
     add("lnf_b", h);
-    add("w_head", static_cast<long long>(c.vocab) * h);
+    add("w_head", static_cast<long long>(c.vocab_rank()) * h);
   }
 }
 
@@ -151,6 +151,7 @@ void ParamStore::allocate_and_init(const ModelCfg& c, cudaStream_t s) {
       int col_split = 0;
       if (base == "w_qkv") row_blk = hp;                      // [3 hp, h]: q | k | v blocks of hp rows
       if (base == "w_fc1") row_blk = 4 * hp;                  // [4 hp, h]
+      if (base == "w_head" && c.vocab_parallel()) row_blk = c.vocab_rank();  // [V / tp, h]: vocab rows
       if (base == "w_proj" || base == "w_fc2") {              // [h, hp] / [h, 4 hp]: column slices
         rows = h;
         cols = r.n / h;

@@ -163,7 +163,7 @@ def param_shapes(c: gp.GPTConfig, layers: int, first: bool, last: bool) -> dict[
     if last:
         d["lnf_g"] = (h,)
         d["lnf_b"] = (h,)
-        d["w_head"] = (c.vocab, h)
+        d["w_head"] = (c.vocab // c.tp if c.vocab_parallel else c.vocab, h)
     return d
 
 
@@ -260,10 +260,13 @@ _SPLIT = {"w_qkv": ("rows", 3), "b_qkv": ("rows", 3), "w_fc1": ("rows", 1), "b_f
           "w_proj": ("cols", 1), "w_fc2": ("cols", 1)}
 
 
-def unshard(per_rank: list[np.ndarray], name: str) -> np.ndarray:
+def unshard(per_rank: list[np.ndarray], name: str, vocab_parallel: bool = False) -> np.ndarray:
     """Reassemble one tensor from its TP-rank slices (rank order); replicated tensors come back from
-    rank 0 (callers check the replicas are identical)."""
+    rank 0 (callers check the replicas are identical). With `vocab_parallel` the LM head is split by
+    vocabulary rows."""
     base = name[name.index(".") + 1:] if name.startswith("l") and "." in name else name
+    if base == "w_head" and vocab_parallel and len(per_rank) > 1:
+        return np.concatenate(per_rank, axis=0)
     if base not in _SPLIT or len(per_rank) == 1:
         return per_rank[0]
     kind, blocks = _SPLIT[base]
@@ -273,6 +276,6 @@ def unshard(per_rank: list[np.ndarray], name: str) -> np.ndarray:
     return np.concatenate([parts[r][b] for b in range(blocks) for r in range(len(per_rank))], axis=0)
 
 
-def is_tp_sharded(name: str) -> bool:
+def is_tp_sharded(name: str, vocab_parallel: bool = False) -> bool:
     base = name[name.index(".") + 1:] if name.startswith("l") and "." in name else name
-    return base in _SPLIT
+    return base in _SPLIT or (vocab_parallel and base == "w_head")

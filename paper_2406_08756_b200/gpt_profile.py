@@ -58,6 +58,12 @@ class GPTConfig:
     def tokens(self) -> int:
         return self.micro_batch * self.seq
 
+    @property
+    def vocab_parallel(self) -> bool:
+        """Megatron vocab-parallel LM head + cross-entropy: TP > 1 and the vocabulary padded to 128 * tp
+        rows (runtime/gpt_stage.hpp ModelCfg::vocab_parallel); otherwise the head is replicated."""
+        return self.tp > 1 and self.vocab % (128 * self.tp) == 0
+
     def layer_params(self) -> int:
         h = self.hidden
         return 12 * h * h + 13 * h
@@ -70,6 +76,14 @@ class GPTConfig:
         """Model FLOPs per token, fwd + bwd, no recompute (Megatron count)."""
         L, h, s, V = self.n_layers, self.hidden, self.seq, self.vocab
         return 72.0 * L * h * h + 12.0 * L * s * h + 6.0 * h * V
+
+
+def padded_vocab(tp: int, vocab: int = 50257) -> int:
+    """GPT-2's 50257 tokens padded to a multiple of 128 * tp: every TP rank then holds an
+    equal, 128-aligned slice of the vocab-parallel LM head (50304 at TP1, 50432 at TP2, 50688 at TP4,
+    51200 at TP8)."""
+    m = 128 * tp
+    return (vocab + m - 1) // m * m
 
 
 CONFIGS = {

@@ -81,6 +81,7 @@ def _worker(rank: int, world: int, port: int, cfg_kw: dict, out_dir: str) -> Non
 
 @pytest.mark.parametrize("name,kw", [
     ("tp2", dict(tp=2, pp=1, n_microbatches=2)),
+    ("tp2_vocab_parallel", dict(tp=2, pp=1, n_microbatches=2, vocab=50432)),
     ("pp2", dict(tp=1, pp=2, n_microbatches=4)),
 ])
 def test_two_rank_programs_replay_over_gloo(tmp_path, name, kw):

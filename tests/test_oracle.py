@@ -89,3 +89,14 @@ def test_oracle_step_with_dropout_differs_from_without():
     l2, g2 = go.gpt_step(params, shapes, tok, lab, dropout=0.1, **kw)
     assert l0 != l1 and l1 == l2
     assert all(np.array_equal(g1[k], g2[k]) for k in g1)
+
+
+def test_vocab_parallel_head_unshards_by_rows():
+    from paper_2406_08756_b200 import executor as ex
+    from paper_2406_08756_b200 import gpt_profile as gp
+    c = gp.GPTConfig("t", 2, 512, 8, 256, 2, 50432, tp=2)
+    assert c.vocab_parallel and not gp.GPTConfig("t", 2, 512, 8, 256, 2, 50304, tp=2).vocab_parallel
+    assert ex.param_shapes(c, 2, False, True)["w_head"] == (25216, 512)
+    full = np.arange(8 * 3, dtype=np.float32).reshape(8, 3)
+    assert ex.is_tp_sharded("w_head", True) and not ex.is_tp_sharded("w_head", False)
+    assert np.array_equal(ex.unshard([full[:4], full[4:]], "w_head", True), full)

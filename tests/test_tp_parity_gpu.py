@@ -26,10 +26,10 @@ GRAD_MAXREL = 5e-2
 GRAD_COS = 0.999
 
 
-def cfg(tp=2, pp=1, n_micro=2, dropout=0.1, budget_extra_mib=None, layers=4):
+def cfg(tp=2, pp=1, n_micro=2, dropout=0.1, budget_extra_mib=None, layers=4, vocab=50304):
     from paper_2406_08756_b200 import gpt_profile as gp
     base = dict(name=f"gpt-tiny-tp{tp}pp{pp}", n_layers=layers, hidden=512, heads=8, seq=256, micro_batch=2,
-                vocab=50304, tp=tp, pp=pp, n_microbatches=n_micro, dropout=dropout)
+                vocab=vocab, tp=tp, pp=pp, n_microbatches=n_micro, dropout=dropout)
     if budget_extra_mib is not None:
         static = gp.BYTES_PER_PARAM_STATIC * gp.GPTConfig(**base).params() // tp
         base["mem_budget_bytes"] = static // pp + budget_extra_mib * 2**20
@@ -63,10 +63,10 @@ def assemble(c, per_rank):
         names = per_rank[(s, 0)].keys()
         for k in names:
             slices = [per_rank[(s, r)][k] for r in range(c.tp)]
-            if not ex.is_tp_sharded(k):
+            if not ex.is_tp_sharded(k, c.vocab_parallel):
                 for r in range(1, c.tp):
                     assert np.array_equal(slices[0], slices[r]), f"replicated {k} differs on TP rank {r}"
-            out[k] = ex.unshard(slices, k)
+            out[k] = ex.unshard(slices, k, c.vocab_parallel)
     return out
 
 
@@ -130,17 +130,22 @@ def test_tp2_weights_are_slices_of_the_unsharded_model(cuda):
         assert np.array_equal(p1[k], p2[k]), k
 
 
-@pytest.mark.parametrize("tp,pp,n_micro,dropout,baseline", [
-    (2, 1, 2, 0.0, "retain_all"),
-    (2, 1, 2, 0.1, "full"),
-    (2, 1, 8, 0.1, "retain_all"),
-    (2, 2, 4, 0.1, "heu"),
+@pytest.mark.parametrize("tp,pp,n_micro,dropout,baseline,vocab", [
+    (2, 1, 2, 0.0, "retain_all", 50304),
+    (2, 1, 2, 0.1, "full", 50304),
+    (2, 1, 8, 0.1, "retain_all", 50304),
+    (2, 2, 4, 0.1, "heu", 50304),
+    (2, 1, 2, 0.1, "retain_all", 50432),   # vocab padded to 128 * tp: vocab-parallel head + cross-entropy
+    (4, 2, 4, 0.1, "heu", 50688),          # TP4·PP2, vocab-parallel over 4 ranks
 ])
-def test_sharded_step_matches_unsharded_oracle(cuda, tp, pp, n_micro, dropout, baseline):
-    c = cfg(tp=tp, pp=pp, n_micro=n_micro, dropout=dropout, budget_extra_mib=8 if baseline == "heu" else None)
+def test_sharded_step_matches_unsharded_oracle(cuda, tp, pp, n_micro, dropout, baseline, vocab):
+    c = cfg(tp=tp, pp=pp, n_micro=n_micro, dropout=dropout, budget_extra_mib=8 if baseline == "heu" else None,
+            vocab=vocab)
+    assert c.vocab_parallel == (vocab % (128 * tp) == 0)
     res = grid_run(c, baseline)
     worst = compare_with_oracle(c, res)
-    print(f"tp{tp} pp{pp} M{n_micro} p{dropout} {baseline}: worst max-rel {worst[0]:.3e} cos {worst[1]:.6f} ({worst[2]})")
+    print(f"tp{tp} pp{pp} M{n_micro} p{dropout} {baseline} V{vocab}: worst max-rel {worst[0]:.3e} cos {worst[1]:.6f} "
+          f"({worst[2]})")
 
 
 def test_tp1_step_matches_oracle_with_dropout_and_8_microbatches(cuda):

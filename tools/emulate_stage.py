@@ -51,7 +51,8 @@ def main():
     a = ap.parse_args()
     torch.cuda.set_device(0)
     base = gp.CONFIGS[a.model]
-    c = gp.GPTConfig(**{**base.__dict__, "tp": a.tp or base.tp, "pp": a.pp or base.pp,
+    tp = a.tp or base.tp
+    c = gp.GPTConfig(**{**base.__dict__, "tp": tp, "pp": a.pp or base.pp, "vocab": gp.padded_vocab(tp),
                         "n_microbatches": a.microbatches or base.n_microbatches, "dropout": 0.1})
     if a.micro_batch:
         c.micro_batch = a.micro_batch
