@@ -1,7 +1,7 @@
 """Summarise an ncu launch list (`--metrics gpu__time_duration.sum --csv`) of `bench.py`.
 
-Takes the LAST complete training step: the launches from the embedding forward that follows the
-second-to-last Adam launch through the last Adam launch. Writes the step's launches
+Takes the longest complete training step: the launches from an embedding forward that follows an
+Adam launch through the next Adam launch. Writes the step's launches
 (`--csv-out`, id,kernel,ns) and a per-kernel summary (`--json-out`).
 
     python tools/launch_summary.py gpurun_out/launches.csv --csv-out profiles/r01_launches_7b_step.csv \
@@ -41,8 +41,14 @@ def main():
     adam = [i for i, (_, k, _) in enumerate(rows) if "adam" in k]
     if len(adam) < 2:
         raise SystemExit("need two optimizer launches to delimit a step")
-    start = next(i for i in range(adam[-2] + 1, adam[-1]) if "embedding_fwd" in rows[i][1])
-    step = rows[start:adam[-1] + 1]
+    # the complete steps (embedding forward after one optimizer launch through the next); the longest
+    # one is the workload's (bench.py ends with a short tiny-config run)
+    steps = []
+    for a, b in zip(adam, adam[1:]):
+        start = next((i for i in range(a + 1, b) if "embedding_fwd" in rows[i][1]), None)
+        if start is not None:
+            steps.append(rows[start:b + 1])
+    step = max(steps, key=lambda st: sum(ns for _, _, ns in st))
     with open(args.csv_out, "w") as f:
         if args.cmd:
             f.write(f"# {args.cmd}\n")
