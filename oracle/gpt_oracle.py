@@ -13,13 +13,13 @@ Dropout (hidden dropout on the embedding and on both residual branches; the
 attention probabilities are not dropped) uses the executor's masks exactly:
 Philox-4x32-10 (Salmon et al., SC'11; the Random123 algorithm, pinned by its
 published known-answer vectors in tests/test_oracle.py) keyed by the step seed,
-with the counter (element group, stream id) and stream ids
+with the counter (group of 8 elements, stream id) and stream ids
   embedding        (0xFFFF << 32) | mb
   attention branch ((layer + 1) << 32) | (mb << 8) | 5
   MLP branch       ((layer + 1) << 32) | (mb << 8) | 11
 (layer = global layer index, mb = microbatch of the step), element e of a
-[tokens, hidden] tensor drawing word e % 4 of group e // 4, kept iff the draw is
->= floor(p * 2^32); kept values are scaled by 1 / (1 - p) in fp32.
+[tokens, hidden] tensor drawing the 16-bit half e % 2 of word (e % 8) // 2 of group e // 8,
+kept iff the draw is >= floor(p * 2^16); kept values are scaled by 1 / (1 - p) in fp32.
 (executor.cpp drop_stream / kEmbedStream, common.cuh keep_bits8.)
 
 Used only by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg.
@@ -56,18 +56,22 @@ def philox4x32_10(ctr: tuple, key: tuple) -> tuple:
 
 
 def drop_threshold(p: float) -> int:
-    t = float(np.float32(p)) * 4294967296.0
-    return 0xFFFFFFFF if t >= 4294967295.0 else int(t)
+    """16-bit keep threshold (common.cuh drop_threshold16)."""
+    t = float(np.float32(p)) * 65536.0
+    return 65536 if t >= 65536.0 else int(t)
 
 
 def keep_mask(seed: int, stream: int, n: int, p: float) -> np.ndarray:
-    """Bool keep-mask of n consecutive elements of dropout stream `stream` (common.cuh keep_bits8)."""
+    """Bool keep-mask of n consecutive elements of dropout stream `stream` (common.cuh keep_bits8):
+    element e draws the 16-bit half e % 2 (low first) of word (e % 8) // 2 of Philox group e // 8."""
     if p <= 0:
         return np.ones(n, dtype=bool)
-    groups = np.arange((n + 3) // 4, dtype=np.uint64)
+    groups = np.arange((n + 7) // 8, dtype=np.uint64)
     r = philox4x32_10((groups & _U32, groups >> np.uint64(32), np.full_like(groups, stream & 0xFFFFFFFF),
                        np.full_like(groups, stream >> 32)), (seed & 0xFFFFFFFF, seed >> 32))
-    draws = np.stack(r, axis=1).reshape(-1)[:n]
+    words = np.stack(r, axis=1)                                     # [groups, 4]
+    halves = np.stack([words & np.uint64(0xFFFF), words >> np.uint64(16)], axis=2)  # [groups, 4, 2]
+    draws = halves.reshape(-1)[:n]
     return draws >= np.uint64(drop_threshold(p))
 
 

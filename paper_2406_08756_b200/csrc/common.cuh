@@ -245,21 +245,24 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N, bool a_mn_m
          | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-// Dropout keep threshold for probability p (keep iff draw >= threshold).
-LYNX_DEV uint32_t drop_threshold(float p) {
-  const double t = static_cast<double>(p) * 4294967296.0;
-  return t >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(t);
+// Dropout keep threshold for probability p on 16-bit draws (keep iff draw >= threshold).
+__host__ __device__ inline uint32_t drop_threshold16(float p) {
+  const double t = static_cast<double>(p) * 65536.0;
+  return t >= 65536.0 ? 65536u : static_cast<uint32_t>(t);
 }
+LYNX_DEV uint32_t drop_threshold(float p) { return drop_threshold16(p); }
 
 // keep-mask bits for elements [8v, 8v+8) of a dropout stream (shared by the dropout kernels
-// and the fused GEMM residual epilogue: a regenerated activation must draw the same mask)
+// and the fused GEMM residual epilogue: a regenerated activation must draw the same mask).
+// One Philox-4x32-10 call per 8 elements: element j draws the 16-bit half j % 2 (low first) of
+// word j / 2 of the counter (v, stream) — half the Philox work of one 32-bit draw per element,
+// which bounded the dropout-backward kernels; p is resolved to 1/65536.
 LYNX_DEV uint32_t keep_bits8(uint64_t seed, uint64_t stream, long long v, uint32_t thr) {
-  const uint4 a = philox_group(seed, stream, static_cast<uint64_t>(2 * v));
-  const uint4 b = philox_group(seed, stream, static_cast<uint64_t>(2 * v + 1));
-  const uint32_t r[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  const uint4 a = philox_group(seed, stream, static_cast<uint64_t>(v));
+  const uint32_t w[4] = {a.x, a.y, a.z, a.w};
   uint32_t bits = 0;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) bits |= (r[j] >= thr ? 1u : 0u) << j;
+  for (int j = 0; j < 8; ++j) bits |= (((w[j >> 1] >> (16 * (j & 1))) & 0xFFFFu) >= thr ? 1u : 0u) << j;
   return bits;
 }
 

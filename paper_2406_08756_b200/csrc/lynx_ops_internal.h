@@ -121,6 +121,8 @@ size_t attention_bwd_workspace(int batch, int seq, int heads);
 // tcgen05 attention (ops_attention_tc.cu): head_dim 64/128, seq % 128 == 0.
 // attention_set_mode: -1 (default) tcgen05 kernels where the shape allows, 0 mma.sync kernels only.
 void attention_set_mode(int mode);
+// tcgen05 backward kernels: 2 or 4 row warpgroups (0: default).
+void attention_set_bwd_warpgroups(int n);
 int attention_mode();
 bool attention_tc_supported(int seq, int head_dim);
 int attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int batch, int seq, int heads,

@@ -48,6 +48,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescale = 8.f;  // log2 units
 constexpr int kAtom = 128;       // bytes per swizzled row (64 bf16)
 constexpr int kDefaultPoly = 0;  // see poly_every()
+constexpr int kDefaultBwdWG = 4;  // see bwd_warpgroups()
 
 LYNX_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -68,6 +69,32 @@ LYNX_DEV void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+LYNX_DEV void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+// kCols consecutive 32-bit TMEM columns of this thread's lane (16 or 32).
+template <int kCols>
+LYNX_DEV void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
+  if constexpr (kCols == 32) tmem_ld32(taddr, r);
+  else tmem_ld16(taddr, r);
+}
+template <int kCols>
+LYNX_DEV void tmem_st_cols(uint32_t taddr, const uint32_t* r) {
+  if constexpr (kCols == 16) tmem_st16(taddr, r);
+  else tmem_st8(taddr, r);
+}
+// Row-warpgroup split of a 64-column (query or key) tile: warpgroup wg of kWG owns columns
+// [wg * 64 / kWG, (wg + 1) * 64 / kWG) and packs its bf16 results (half as many 32-bit columns) at the
+// start of that range — never into columns another warpgroup still reads. K step kk (16 columns) of
+// the A-from-TMEM MMA then sits at:
+template <int kWG>
+LYNX_DEV constexpr uint32_t packed_col(int kk) {
+  constexpr int CW = 64 / kWG;
+  return static_cast<uint32_t>((16 * kk / CW) * CW + (16 * kk % CW) / 2);
+}
+
 // D[tmem] (+)= A[tmem] * B[smem]^T: A (128 rows x 16 K, bf16 pairs packed per 32-bit TMEM cell,
 // one row per lane, 8 columns per K step) is read from tensor memory, so a row warp can hand
 // its P / dS tile to the tensor core with tcgen05.st — no shared-memory round trip and no
@@ -378,8 +405,8 @@ struct DkvL {
   static constexpr int kBytes = kBar + 128 + 1024;
 };
 
-template <int D>
-__global__ void __launch_bounds__(384, 1)
+template <int D, int kWG>  // kWG row warpgroups (2 or 4), each owning 64 / kWG query columns of a tile
+__global__ void __launch_bounds__(128 + 128 * kWG, 1)
     attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
                         const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
                         const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
@@ -408,7 +435,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
-      mbar_init(pd_full + i, 256);
+      mbar_init(pd_full + i, 128 * kWG);
     }
     mbar_init(mma_done, 1);
     mbar_init(fin, 1);
@@ -473,7 +500,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t tb = static_cast<uint32_t>(i & 1);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // A = P^T / dS^T, packed bf16 over S^T / dP^T in TMEM buffer tb
-          const uint32_t ac = tb * 64 + kk * 8 + (kk >= 2 ? 32 : 0);  // queries 0-31: cols 0-15, 32-63: 48-63
+          const uint32_t ac = tb * 64 + packed_col<kWG>(kk);
           umma_f16_ts(tmem + 256, tmem + ac, mnmaj(sDO + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
           umma_f16_ts(tmem + 384, tmem + 128 + ac, mnmaj(sQ + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
         }
@@ -484,11 +511,12 @@ __global__ void __launch_bounds__(384, 1)
       umma_commit(fin);
     }
   } else if (warp >= 4) {
-    // Two row warpgroups: warps 4-7 take query columns 0-31 of each 64-query tile, warps 8-11
-    // columns 32-63 (same key rows / TMEM lanes). The work is elementwise, so the halves never
-    // exchange data; two warps per SM sub-partition hide the latencies one row warp cannot (a
-    // clock64 trace showed ~1500 cycles of row work per tile against ~1000 of MMA).
-    const int half = warp >= 8 ? 1 : 0;
+    // kWG row warpgroups split each 64-query tile's columns (warpgroup wg: columns wg * CW ...
+    // + CW) on the same key rows / TMEM lanes. The work is elementwise, so they never exchange data;
+    // more warps per SM sub-partition hide the TMEM-load / MUFU latencies of the per-tile row work
+    // (a clock64 trace showed ~1500 cycles of it per tile against ~1000 of MMA with two warpgroups).
+    constexpr int CW = 64 / kWG;
+    const int wg = (warp - 4) / 4;
     const int k = (warp % 4) * 32 + lane;  // key row of the tile
     const int key = kb * 128 + k;
     const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
@@ -498,43 +526,42 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(s_full + tb, (i >> 1) & 1);
       if (threadIdx.x == 128) ATRACE(3, i);
       tc_fence_after();
-      const float* sl = reinterpret_cast<const float*>(smem + L::kVec + st * 256) + half * 32;
-      const float* sd = reinterpret_cast<const float*>(smem + L::kVec + (NS + st) * 256) + half * 32;
+      const float* sl = reinterpret_cast<const float*>(smem + L::kVec + st * 256) + wg * CW;
+      const float* sd = reinterpret_cast<const float*>(smem + L::kVec + (NS + st) * 256) + wg * CW;
       {
-        uint32_t sr[32], dp[32];
-        tmem_ld32(tmem + lanes + tb * 64 + half * 32, sr);
-        tmem_ld32(tmem + lanes + 128 + tb * 64 + half * 32, dp);
+        uint32_t sr[CW], dp[CW];
+        tmem_ld_cols<CW>(tmem + lanes + tb * 64 + wg * CW, sr);
+        tmem_ld_cols<CW>(tmem + lanes + 128 + tb * 64 + wg * CW, dp);
         tmem_ld_wait();
-        float p[32], g[32], lv[32], dv[32];
+        float p[CW], g[CW], lv[CW], dv[CW];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < CW / 4; ++c) {
           const float4 a = lds128(sl + 4 * c), d4 = lds128(sd + 4 * c);
           lv[4 * c] = a.x, lv[4 * c + 1] = a.y, lv[4 * c + 2] = a.z, lv[4 * c + 3] = a.w;
           dv[4 * c] = d4.x, dv[4 * c + 1] = d4.y, dv[4 * c + 2] = d4.z, dv[4 * c + 3] = d4.w;
         }
 #pragma unroll
-        for (int c = 0; c < 32; ++c) p[c] = ex2(fmaf(u2f(sr[c]), scale_log2, -lv[c]));
+        for (int c = 0; c < CW; ++c) p[c] = ex2(fmaf(u2f(sr[c]), scale_log2, -lv[c]));
         if (i < 2) {  // the two 64-query tiles that meet the diagonal of this 128-key tile
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (key > q0 + half * 32 + c) p[c] = 0.f;
+          for (int c = 0; c < CW; ++c)
+            if (key > q0 + wg * CW + c) p[c] = 0.f;
         }
 #pragma unroll
-        for (int c = 0; c < 32; ++c) g[c] = p[c] * (u2f(dp[c]) - dv[c]);
-        uint32_t pp[16], gp[16];
+        for (int c = 0; c < CW; ++c) g[c] = p[c] * (u2f(dp[c]) - dv[c]);
+        uint32_t pp[CW / 2], gp[CW / 2];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
+        for (int c = 0; c < CW / 2; ++c) {
           pp[c] = pack_bf16x2(p[2 * c], p[2 * c + 1]);
           gp[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
         }
         if (threadIdx.x == 128) ATRACE(4, i);
-        // P^T(i) / dS^T(i) overwrite S^T(i) / dP^T(i) in place, each half inside the columns it read
-        // itself (half 0: 0-15 of its 0-31, half 1: 48-63 of its 32-63): the other half reads the
-        // same TMEM lanes without any ordering against this store (packing half 1 at 16-31 made
-        // warps 4-7 read P^T instead of S^T, ~0.1 % of runs). dV / dK(i-2), the last readers of
-        // buffer tb, completed before S^T(i).
-        tmem_st16(tmem + lanes + tb * 64 + half * 48, pp);
-        tmem_st16(tmem + lanes + 128 + tb * 64 + half * 48, gp);
+        // P^T(i) / dS^T(i) overwrite S^T(i) / dP^T(i) in place, each warpgroup inside the columns it
+        // read itself (packed_col): the others read the same TMEM lanes without any ordering against
+        // this store (packing outside its own range once made warps read P^T instead of S^T, ~0.1 %
+        // of runs). dV / dK(i-2), the last readers of buffer tb, completed before S^T(i).
+        tmem_st_cols<CW / 2>(tmem + lanes + tb * 64 + wg * CW, pp);
+        tmem_st_cols<CW / 2>(tmem + lanes + 128 + tb * 64 + wg * CW, gp);
         tmem_st_wait();
       }
       tc_fence_before();
@@ -543,11 +570,16 @@ __global__ void __launch_bounds__(384, 1)
     }
     mbar_wait(fin, 0);
     tc_fence_after();
-    // epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled)
+    // epilogue: the first half of the warpgroups writes dV, the second dK (scaled), each warpgroup a
+    // 16-aligned share of the D columns
+    constexpr int kPer = kWG / 2, kSplit = (D / 16 + kPer - 1) / kPer * 16;
+    const bool is_dk = wg >= kPer;
+    const int part = wg % kPer;
     const long long grow = static_cast<long long>(row0 + key) * 3 * HD;
-    BF8* dst = reinterpret_cast<BF8*>(dqkv + grow + (half ? HD : 2 * HD) + h * D);
-    const float mul = half ? scale : 1.f;
-    tmem_cols(tmem + lanes + (half ? 384 : 256), 0, D, [&](int c, const uint32_t* o, int cnt) {
+    BF8* dst = reinterpret_cast<BF8*>(dqkv + grow + (is_dk ? HD : 2 * HD) + h * D);
+    const float mul = is_dk ? scale : 1.f;
+    const int c_lo = part * kSplit < D ? part * kSplit : D, c_hi = (part + 1) * kSplit < D ? (part + 1) * kSplit : D;
+    tmem_cols(tmem + lanes + (is_dk ? 384 : 256), c_lo, c_hi, [&](int c, const uint32_t* o, int cnt) {
       float f[32];
       for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * mul;
       for (int i = 0; i < cnt / 8; ++i) dst[c / 8 + i] = f_to_bf8(f + 8 * i);
@@ -572,8 +604,8 @@ struct DqL {
   static constexpr int kBytes = kBar + 128 + 1024;
 };
 
-template <int D>
-__global__ void __launch_bounds__(384, 1)
+template <int D, int kWG>  // kWG row warpgroups (2 or 4), each owning 64 / kWG key columns of a tile
+__global__ void __launch_bounds__(128 + 128 * kWG, 1)
     attn_dq_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                       const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
                       const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
@@ -598,7 +630,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
-      mbar_init(ds_full + i, 256);
+      mbar_init(ds_full + i, 128 * kWG);
       mbar_init(ds_free + i, 1);
     }
     mbar_init(fin, 1);
@@ -656,7 +688,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // A = dS(j), packed bf16 over the S(j) columns of TMEM buffer tb
-          umma_f16_ts(tmem + 256, tmem + tb * 64 + kk * 8 + (kk >= 2 ? 32 : 0), mnmaj(sK + st * L::kKT, kk, 8192),
+          umma_f16_ts(tmem + 256, tmem + tb * 64 + packed_col<kWG>(kk), mnmaj(sK + st * L::kKT, kk, 8192),
                       idG, (j | kk) != 0);
         umma_commit(ds_free + tb);
         umma_commit(kv_empty + st);
@@ -665,8 +697,9 @@ __global__ void __launch_bounds__(384, 1)
       umma_commit(fin);
     }
   } else if (warp >= 4) {
-    // Two row warpgroups split each 64-key tile's columns (0-31 / 32-63), as in dK/dV.
-    const int half = warp >= 8 ? 1 : 0;
+    // kWG row warpgroups split each 64-key tile's columns, as in dK/dV.
+    constexpr int CW = 64 / kWG;
+    const int wg = (warp - 4) / 4;
     const int r = (warp % 4) * 32 + lane;
     const int q = qb * 128 + r;
     const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
@@ -678,27 +711,26 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
       const bool diag = j >= 2 * qb;
       {
-        uint32_t s[32], dp[32];
-        tmem_ld32(tmem + lanes + st * 64 + half * 32, s);
-        tmem_ld32(tmem + lanes + 128 + st * 64 + half * 32, dp);
+        uint32_t s[CW], dp[CW];
+        tmem_ld_cols<CW>(tmem + lanes + st * 64 + wg * CW, s);
+        tmem_ld_cols<CW>(tmem + lanes + 128 + st * 64 + wg * CW, dp);
         tmem_ld_wait();
-        float g[32];
+        float g[CW];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) g[c] = ex2(fmaf(u2f(s[c]), scale_log2, -l2));
+        for (int c = 0; c < CW; ++c) g[c] = ex2(fmaf(u2f(s[c]), scale_log2, -l2));
         if (diag) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (j * 64 + half * 32 + c > q) g[c] = 0.f;
+          for (int c = 0; c < CW; ++c)
+            if (j * 64 + wg * CW + c > q) g[c] = 0.f;
         }
 #pragma unroll
-        for (int c = 0; c < 32; ++c) g[c] *= u2f(dp[c]) - dq;
-        uint32_t packed[16];
+        for (int c = 0; c < CW; ++c) g[c] *= u2f(dp[c]) - dq;
+        uint32_t packed[CW / 2];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) packed[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
-        // dS(j) overwrites S(j) in place, each half inside the columns it read (half 0: 0-15, half 1:
-        // 48-63; see the dK/dV kernel); dQ(j-2), the last reader of this buffer, completed before
-        // S(j) (tensor-pipe order).
-        tmem_st16(tmem + lanes + st * 64 + half * 48, packed);
+        for (int c = 0; c < CW / 2; ++c) packed[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
+        // dS(j) overwrites S(j) in place, each warpgroup inside the columns it read (packed_col; see
+        // the dK/dV kernel); dQ(j-2), the last reader of this buffer, completed before S(j).
+        tmem_st_cols<CW / 2>(tmem + lanes + st * 64 + wg * CW, packed);
         tmem_st_wait();
       }
       tc_fence_before();
@@ -707,8 +739,9 @@ __global__ void __launch_bounds__(384, 1)
     mbar_wait(fin, 0);
     tc_fence_after();
     BF8* dqrow = reinterpret_cast<BF8*>(dqkv + static_cast<long long>(row0 + q) * 3 * HD + h * D);
-    constexpr int kSplit = (D / 2 + 15) / 16 * 16;  // each warpgroup writes its share of the D columns
-    tmem_cols(tmem + lanes + 256, half ? kSplit : 0, half ? D : kSplit, [&](int c, const uint32_t* o, int cnt) {
+    constexpr int kSplit = (D / 16 + kWG - 1) / kWG * 16;  // each warpgroup writes its share of the D columns
+    const int c_lo = wg * kSplit < D ? wg * kSplit : D, c_hi = (wg + 1) * kSplit < D ? (wg + 1) * kSplit : D;
+    tmem_cols(tmem + lanes + 256, c_lo, c_hi, [&](int c, const uint32_t* o, int cnt) {
       float f[32];
       for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * scale;
       for (int i = 0; i < cnt / 8; ++i) dqrow[c / 8 + i] = f_to_bf8(f + 8 * i);
@@ -756,6 +789,33 @@ int fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, 
   return check_launch("attention_fwd_tc");
 }
 
+// Row warpgroups of the backward kernels (2 or 4): attention_set_bwd_warpgroups, else LYNX_ATTN_BWD_WG,
+// else kDefaultBwdWG. Both give bit-identical gradients (same MMA order, same per-element math).
+int g_bwd_wg = 0;
+int bwd_warpgroups() {
+  if (g_bwd_wg) return g_bwd_wg;
+  static const int n = [] {
+    const char* e = std::getenv("LYNX_ATTN_BWD_WG");
+    return e && std::atoi(e) == 2 ? 2 : kDefaultBwdWG;
+  }();
+  return n;
+}
+
+template <int D, int kWG>
+int bwd_launch(const CUtensorMap& m128, const CUtensorMap& m64, const CUtensorMap& d64, const CUtensorMap& d128,
+               const float* lse, const float* dvec, __nv_bfloat16* dqkv, int B, int S, int H, float scale,
+               float scale_log2, cudaStream_t s) {
+  auto k1 = attn_dkdv_tc_kernel<D, kWG>;
+  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvL<D>::kBytes);
+  k1<<<dim3(S / 128, H, B), 128 + 128 * kWG, DkvL<D>::kBytes, s>>>(m128, m64, d64, lse, dvec, dqkv, S, H, scale,
+                                                                   scale_log2);
+  auto k2 = attn_dq_tc_kernel<D, kWG>;
+  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, DqL<D>::kBytes);
+  k2<<<dim3(S / 128, H, B), 128 + 128 * kWG, DqL<D>::kBytes, s>>>(m128, m64, d128, lse, dvec, dqkv, S, H, scale,
+                                                                  scale_log2);
+  return check_launch("attention_bwd_tc", 2);
+}
+
 template <int D>
 int bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* dvec,
         __nv_bfloat16* dqkv, int B, int S, int H, cudaStream_t s) {
@@ -765,13 +825,9 @@ int bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, c
             gemm::make_map(&d64, dout, hd, T, hd, 64, 64) && gemm::make_map(&d128, dout, hd, T, hd, 64, 128);
   if (!ok) return set_error("attention: tensor map encode failed");
   const float scale = 1.f / sqrtf(static_cast<float>(D)), scale_log2 = scale * kLog2e;
-  auto k1 = attn_dkdv_tc_kernel<D>;
-  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvL<D>::kBytes);
-  k1<<<dim3(S / 128, H, B), 384, DkvL<D>::kBytes, s>>>(m128, m64, d64, lse, dvec, dqkv, S, H, scale, scale_log2);
-  auto k2 = attn_dq_tc_kernel<D>;
-  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, DqL<D>::kBytes);
-  k2<<<dim3(S / 128, H, B), 384, DqL<D>::kBytes, s>>>(m128, m64, d128, lse, dvec, dqkv, S, H, scale, scale_log2);
-  return check_launch("attention_bwd_tc", 2);
+  if (bwd_warpgroups() == 2)
+    return bwd_launch<D, 2>(m128, m64, d64, d128, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
+  return bwd_launch<D, 4>(m128, m64, d64, d128, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
 }
 
 int g_mode = -1;
@@ -779,6 +835,7 @@ int g_mode = -1;
 }  // namespace attn_tc
 
 void attention_set_mode(int mode) { attn_tc::g_mode = mode; }
+void attention_set_bwd_warpgroups(int n) { attn_tc::g_bwd_wg = n == 2 || n == 4 ? n : 0; }
 int attention_mode() { return attn_tc::g_mode; }
 bool attention_tc_supported(int seq, int head_dim) {
   return attn_tc::g_mode != 0 && seq % 128 == 0 &&

@@ -869,8 +869,7 @@ Args make_args(const GemmDesc& g, bool tma_out) {
   Args a{g.c, g.bias, g.ldc, g.M, g.N, g.K, g.epi, group_size(), cache_hint(0), cache_hint(1), cache_hint(2),
          tma_out ? 1 : 0, g.c2,
          g.res, g.drop_p, g.drop_p > 0.f ? 1.f / (1.f - g.drop_p) : 1.f, 0u, g.drop_seed, g.drop_stream};
-  const double t = static_cast<double>(g.drop_p) * 4294967296.0;  // == drop_threshold(p)
-  a.drop_thr = t >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(t);
+  a.drop_thr = drop_threshold16(g.drop_p);  // the dropout kernels' threshold (common.cuh)
   return a;
 }
 

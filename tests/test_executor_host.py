@@ -150,3 +150,27 @@ def test_non_causal_timeline_is_rejected_at_create():
         assert err.value.code == 2 and "InconsistentPlan" in str(err.value)
     e = ex.Executor(text, plan["timeline"], ex.make_config(c, plan["layers_per_stage"], exec_opts={"dry_run": True}))
     e.close()
+
+
+def test_reference_inconsistent_plan_is_rejected_like_the_reference():
+    """A HEU plan whose expansion (expand_plan_to_stage) regenerates a tensor's consumer before the tensor
+    itself: the reference's own simulate() rejects it (InconsistentPlan, exit code 2) and so does
+    lynx_rt_create — the same plan, the same verdict. (TP4·PP2 tiny GPT, budget static/2 + 8 MiB: ln1 of
+    (mb 1, layer 1) is regenerated in F(2) but its consumer qkv in B(0), which runs first.)"""
+    from paper_2406_08756_b200 import planner
+    base = dict(name="t", n_layers=4, hidden=512, heads=8, seq=256, micro_batch=2, vocab=50688, tp=4, pp=2,
+                n_microbatches=4, dropout=0.1)
+    static = gp.BYTES_PER_PARAM_STATIC * gp.GPTConfig(**base).params() // 4
+    c = gp.GPTConfig(**{**base, "mem_budget_bytes": static // 2 + 8 * 2**20})
+    text = gp.profile_text(c)
+    plans = [ex.plan_for(text, s) for s in range(2)]
+    with pytest.raises(ex.LynxError) as ref_err:
+        planner.simulate_timelines_text(text, plans[0]["layers_per_stage"], [p["timeline"] for p in plans])
+    with pytest.raises(ex.LynxError) as ours:
+        ex.Executor(text, plans[0]["timeline"], ex.make_config(c, plans[0]["layers_per_stage"],
+                                                               exec_opts={"dry_run": True}))
+    assert ref_err.value.code == ours.value.code == 2
+    from oracle import ref as oref
+    if oref.available():
+        with pytest.raises(RuntimeError):
+            oref.RefLib().simulate_timelines(text, plans[0]["layers_per_stage"], [p["timeline"] for p in plans])

@@ -314,6 +314,26 @@ def _check_attention(ops, cuda, qkv, g, B, S, H, D):
     assert torch.equal(dqkv, dqkv2)
 
 
+@pytest.mark.parametrize("B,S,H,D", [(2, 512, 3, 128), (1, 1024, 2, 64), (2, 384, 2, 112), (1, 256, 2, 96)])
+def test_attention_bwd_warpgroup_variants_are_bit_identical(ops, cuda, B, S, H, D):
+    """The tcgen05 backward kernels with 2 or 4 row warpgroups (64 / kWG columns each) issue the same MMAs
+    in the same order on the same per-element values: dQ, dK, dV are bit-identical."""
+    from paper_2406_08756_b200._native import lib
+    g = torch.Generator(device=cuda).manual_seed(S + D)
+    qkv = torch.randn(B * S, 3 * H * D, device=cuda, generator=g).bfloat16()
+    dout = torch.randn(B * S, H * D, device=cuda, generator=g).bfloat16()
+    out, lse = ops.attention_fwd(qkv, B, S, H, D)
+    res = {}
+    try:
+        for wg in (2, 4):
+            lib().lynx_op_attention_bwd_warpgroups(wg)
+            res[wg] = ops.attention_bwd(qkv, out, dout, lse, B, S, H, D)
+    finally:
+        lib().lynx_op_attention_bwd_warpgroups(0)
+    torch.cuda.synchronize()
+    assert torch.equal(res[2], res[4])
+
+
 def test_xent(ops, cuda):
     rows, V = 256, 1024
     logits = torch.randn(rows, V, device=cuda).bfloat16()

@@ -34,7 +34,7 @@ def test_keep_mask_rate_and_purity():
     other = go.keep_mask(go.step_seed(42, 1), go.layer_stream(3, 2, go.SITE_ATTN), 1 << 18, 0.1)
     assert (m != other).mean() > 0.1
     assert go.keep_mask(1, 2, 100, 0.0).all()
-    assert go.drop_threshold(0.1) == int(float(np.float32(0.1)) * 2**32)
+    assert go.drop_threshold(0.1) == int(float(np.float32(0.1)) * 2**16) == 6553
 
 
 def _shard(full: np.ndarray, base: str, tp: int, r: int) -> np.ndarray:

@@ -139,8 +139,8 @@ def test_tp2_weights_are_slices_of_the_unsharded_model(cuda):
     (4, 2, 4, 0.1, "heu", 50688),          # TP4·PP2, vocab-parallel over 4 ranks
 ])
 def test_sharded_step_matches_unsharded_oracle(cuda, tp, pp, n_micro, dropout, baseline, vocab):
-    c = cfg(tp=tp, pp=pp, n_micro=n_micro, dropout=dropout, budget_extra_mib=8 if baseline == "heu" else None,
-            vocab=vocab)
+    extra = (8 if tp == 2 else 4) if baseline == "heu" else None  # TP4·PP2 at +8 MiB: see test_executor_host
+    c = cfg(tp=tp, pp=pp, n_micro=n_micro, dropout=dropout, budget_extra_mib=extra, vocab=vocab)
     assert c.vocab_parallel == (vocab % (128 * tp) == 0)
     res = grid_run(c, baseline)
     worst = compare_with_oracle(c, res)

@@ -40,6 +40,12 @@ def main():
         print(f"mode {mode:2d}: fwd {tf:7.3f} ms {f_fwd / tf / 1e9:7.1f} TF/s | bwd {tb:7.3f} ms "
               f"{2.5 * f_fwd / tb / 1e9:7.1f} TF/s", flush=True)
     lib().lynx_op_attention_mode(-1)
+    out, lse = ops.attention_fwd(qkv, B, S, H, D)
+    for wg in (2, 4):  # row warpgroups of the tcgen05 backward kernels
+        lib().lynx_op_attention_bwd_warpgroups(wg)
+        tb = timeit(lambda: ops.attention_bwd(qkv, out, dout, lse, B, S, H, D))
+        print(f"tcgen05 bwd, {wg} row warpgroups: {tb:7.3f} ms {2.5 * f_fwd / tb / 1e9:7.1f} TF/s", flush=True)
+    lib().lynx_op_attention_bwd_warpgroups(0)
     for i, name in enumerate(["out", "dqkv"]):
         a, b = res[-1][i], res[0][i]
         print(name, "rel diff tc vs mma:", ((a - b).norm() / b.norm()).item())
