@@ -113,8 +113,10 @@ int lynx_op_attention_bwd(const void* qkv, const void* out, const void* dout, co
 /* Attention kernel selection: -1 (default) the tcgen05 kernels (TMEM accumulators, TMA tiles) when
  * head_dim is 64 or 128 and seq % 128 == 0, else the mma.sync kernels; 0 mma.sync kernels only. */
 void lynx_op_attention_mode(int mode);
-/* Row warpgroups of the tcgen05 attention backward kernels: 2 or 4 (0: the default, 4). */
+/* Row warpgroups of the tcgen05 attention backward kernels: 2 or 4 (0: the default, 2). */
 void lynx_op_attention_bwd_warpgroups(int n);
+/* Query tiles per CTA of the tcgen05 attention forward: 1 or 2 (0: the default, 2). */
+void lynx_op_attention_fwd_tiles(int n);
 /* 1 when attention of this shape runs on the tcgen05 kernels (head_dim 64/96/112/128, seq % 128 == 0). */
 int lynx_op_attention_tc_supported(int seq, int head_dim);
 

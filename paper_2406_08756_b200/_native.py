@@ -29,6 +29,7 @@ _SIGNATURES: dict[str, tuple] = {
     "lynx_op_gemm_mode": (None, [_i]),
     "lynx_op_attention_mode": (None, [_i]),
     "lynx_op_attention_bwd_warpgroups": (None, [_i]),
+    "lynx_op_attention_fwd_tiles": (None, [_i]),
     "lynx_op_attention_tc_supported": (_i, [_i, _i]),
     "lynx_op_layernorm_fwd": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _f, _vp]),
     "lynx_op_layernorm_bwd_workspace": (_sz, [_i, _i]),

@@ -80,6 +80,7 @@ int lynx_op_gemm_gelu_bwd(const void* a, long long lda, const void* b, long long
 void lynx_op_gemm_mode(int mode) { gemm_set_mode(mode); }
 void lynx_op_attention_mode(int mode) { attention_set_mode(mode); }
 void lynx_op_attention_bwd_warpgroups(int n) { attention_set_bwd_warpgroups(n); }
+void lynx_op_attention_fwd_tiles(int n) { attention_set_fwd_tiles(n); }
 int lynx_op_attention_tc_supported(int seq, int head_dim) { return attention_tc_supported(seq, head_dim) ? 1 : 0; }
 
 int lynx_op_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean, float* rstd,

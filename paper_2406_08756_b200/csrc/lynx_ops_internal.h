@@ -123,6 +123,8 @@ size_t attention_bwd_workspace(int batch, int seq, int heads);
 void attention_set_mode(int mode);
 // tcgen05 backward kernels: 2 or 4 row warpgroups (0: default).
 void attention_set_bwd_warpgroups(int n);
+// tcgen05 forward: 1 or 2 query tiles per CTA (0: default, 2).
+void attention_set_fwd_tiles(int n);
 int attention_mode();
 bool attention_tc_supported(int seq, int head_dim);
 int attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int batch, int seq, int heads,

@@ -48,7 +48,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kRescale = 8.f;  // log2 units
 constexpr int kAtom = 128;       // bytes per swizzled row (64 bf16)
 constexpr int kDefaultPoly = 0;  // see poly_every()
-constexpr int kDefaultBwdWG = 4;  // see bwd_warpgroups()
+constexpr int kDefaultBwdWG = 2;  // see bwd_warpgroups(): 4 measured no faster (profiles/r02_attention.md)
 
 LYNX_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -385,6 +385,217 @@ __global__ void __launch_bounds__(256, 1)
       for (int i = 0; i < cnt / 8; ++i) orow[c / 8 + i] = f_to_bf8(f + 8 * i);
     });
     lse[(static_cast<long long>(b) * H + h) * S + q] = (m_run + log2f(l_run)) / kLog2e;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// ============================================================== forward, two query tiles per CTA
+// Query tiles 2p and 2p+1 share each K / V tile; two softmax warpgroups (warps 4-7: tile 0, warps
+// 8-11: tile 1) each own one tile's S / P and O in TMEM (S_t at columns 128 t, O_t at 256 + 128 t).
+// The MMA warp ping-pongs: PV_0(j), S_0(j+1), PV_1(j), S_1(j+1) — while one warpgroup's softmax of
+// tile j runs, the tensor core works for the other — so every SM sub-partition has two softmax warps
+// to hide the TMEM-load / MUFU latencies that bound the one-tile kernel (tensor pipe ~39 % there).
+// Per-row arithmetic, warp-to-row mapping and the lazy-rescale decisions are those of
+// attn_fwd_tc_kernel, so O and lse are bit-identical to it.
+template <int D>
+struct Fwd2L {
+  static constexpr int kTile = FwdL<D>::kTile;
+  static constexpr int kQ = 0, kK = 2 * kTile, kV = 4 * kTile, kBar = 6 * kTile;
+  static constexpr int kBytes = kBar + 128 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ out,
+                        float* __restrict__ lse, int S, int H, float scale_log2) {
+  using L = Fwd2L<D>;
+  constexpr int kA = FwdL<D>::kAtoms;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5, *v_empty = bar + 7,
+           *s_full = bar + 9, *p_full = bar + 11, *pv_done = bar + 13;  // s / p / pv: one per query tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
+  const int pair = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n_qt = S / 128;
+  const bool has1 = 2 * pair + 1 < n_qt;
+  const int n0 = 2 * pair + 1, n1 = has1 ? 2 * pair + 2 : 0, n = has1 ? n1 : n0;
+  const int HD = H * D, row0 = b * S;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(p_full + i, 128);
+      mbar_init(pv_done + i, 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // Register split by warpgroup (setmaxnreg, executed at the top of each role): the control warpgroup
+  // (TMA, MMA, TMEM) gives registers to the two softmax warpgroups, whose 128-column rows need them.
+
+  if (warp == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (elect_one()) {
+      tma_prefetch_desc(&map_qkv);
+      mbar_arrive_expect_tx(q_full, (has1 ? 2 : 1) * L::kTile);
+      for (int t = 0; t < (has1 ? 2 : 1); ++t)
+        for (int a = 0; a < kA; ++a)
+          tma_load_2d(&map_qkv, q_full, smem + L::kQ + t * L::kTile + a * 16384, h * D + 64 * a,
+                      row0 + (2 * pair + t) * 128, kEvictFirst);
+      for (int j = 0; j < n; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(k_empty + st, ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(k_full + st, L::kTile);
+        for (int a = 0; a < kA; ++a)
+          tma_load_2d(&map_qkv, k_full + st, smem + L::kK + st * L::kTile + a * 16384, HD + h * D + 64 * a,
+                      row0 + j * 128, kEvictLast);
+        if (j >= 2) mbar_wait(v_empty + st, ((j >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(v_full + st, L::kTile);
+        for (int a = 0; a < kA; ++a)
+          tma_load_2d(&map_qkv, v_full + st, smem + L::kV + st * L::kTile + a * 16384, 2 * HD + h * D + 64 * a,
+                      row0 + j * 128, kEvictLast);
+      }
+    }
+  } else if (warp == 1) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (elect_one()) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idO = umma_idesc_bf16(128, D, false, true);
+      const uint32_t sQ = smem_u32(smem + L::kQ), sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV);
+      auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
+        const int st = j & 1;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16(tmem + t * 128, kmaj(sQ + t * L::kTile, kk, 16384), kmaj(sK + st * L::kTile, kk, 16384), idS,
+                   kk > 0);
+        umma_commit(s_full + t);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P packed bf16 over S_t in TMEM
+        const int st = j & 1;
+        mbar_wait(p_full + t, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj(sV + st * L::kTile, kk, 16384), idO,
+                      (j | kk) != 0);
+        umma_commit(pv_done + t);
+      };
+      auto wait_k = [&](int j) {
+        mbar_wait(k_full + (j & 1), (j >> 1) & 1);
+        tc_fence_after();
+      };
+      mbar_wait(q_full, 0);
+      wait_k(0);
+      issue_s(0, 0);
+      if (n1 > 0) issue_s(1, 0);
+      umma_commit(k_empty);
+      for (int j = 0; j < n; ++j) {
+        const int st = j & 1;
+        mbar_wait(v_full + st, (j >> 1) & 1);
+        tc_fence_after();
+        if (j < n0) issue_pv(0, j);
+        if (j + 1 < n) wait_k(j + 1);
+        if (j + 1 < n0) issue_s(0, j + 1);
+        if (j < n1) issue_pv(1, j);
+        umma_commit(v_empty + st);
+        if (j + 1 < n1) issue_s(1, j + 1);
+        if (j + 1 < n) umma_commit(k_empty + ((j + 1) & 1));
+      }
+    }
+  } else if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    const int t = (warp - 4) / 4;  // query tile of this warpgroup (warp w reads TMEM lanes 32 (w % 4) ...)
+    if (t == 0 || has1) {
+      const int qb = 2 * pair + t, nt = t ? n1 : n0;
+      const int r = (warp % 4) * 32 + lane;
+      const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
+      const uint32_t s_col = tmem + lanes + t * 128, o_col = tmem + lanes + 256 + t * 128;
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < nt; ++j) {
+        mbar_wait(s_full + t, j & 1);
+        tc_fence_after();
+        float x[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(s_col + c * 32, reinterpret_cast<uint32_t*>(x + c * 32));
+        tmem_ld_wait();
+        if (j == qb) {  // diagonal tile: causal mask (warp-uniform branch)
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i > r) x[i] = -INFINITY;
+        }
+        float mv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mv[i] = x[i];
+#pragma unroll
+        for (int i = 8; i < 128; ++i) mv[i & 7] = fmaxf(mv[i & 7], x[i]);
+        const float mt =
+            fmaxf(fmaxf(fmaxf(mv[0], mv[1]), fmaxf(mv[2], mv[3])), fmaxf(fmaxf(mv[4], mv[5]), fmaxf(mv[6], mv[7])));
+        const float m_new = fmaxf(m_run, mt * scale_log2);
+        const bool need = __any_sync(0xffffffffu, m_new > m_run + kRescale);
+        float corr = 1.f;
+        if (need) {
+          corr = exp2f(m_run - m_new);
+          m_run = m_new;
+        }
+        float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          x[i] = ex2(fmaf(x[i], scale_log2, -m_run));
+          rv[i & 7] += x[i];
+        }
+        const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
+        l_run = l_run * corr + rs;
+        if (j > 0 && need) {  // O_t rescale after PV_t(j-1) completes (PV_t(j) needs this tile's P)
+          mbar_wait(pv_done + t, (j - 1) & 1);
+          tc_fence_after();
+          tmem_cols(o_col, 0, D, [&](int c, uint32_t* o, int cnt) {
+            for (int i = 0; i < cnt; ++i) o[i] = __float_as_uint(u2f(o[i]) * corr);
+            if (cnt == 32)
+              tmem_st32(o_col + c, o);
+            else
+              tmem_st16(o_col + c, o);
+          });
+          tmem_st_wait();
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(x[32 * c + 2 * i], x[32 * c + 2 * i + 1]);
+          tmem_st16(s_col + c * 16, packed);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(p_full + t);
+      }
+      mbar_wait(pv_done + t, (nt - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l_run;
+      const int q = qb * 128 + r;
+      BF8* orow = reinterpret_cast<BF8*>(out + static_cast<long long>(row0 + q) * HD + h * D);
+      tmem_cols(o_col, 0, D, [&](int c, const uint32_t* o, int cnt) {
+        float f[32];
+        for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * inv;
+        for (int i = 0; i < cnt / 8; ++i) orow[c / 8 + i] = f_to_bf8(f + 8 * i);
+      });
+      lse[(static_cast<long long>(b) * H + h) * S + q] = (m_run + log2f(l_run)) / kLog2e;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -772,11 +983,29 @@ int fwd_poly(const CUtensorMap& m, __nv_bfloat16* out, float* lse, int B, int S,
   return check_launch("attention_fwd_tc");
 }
 
+// Forward kernel variant: 2 (default) = two query tiles per CTA (attn_fwd2_tc_kernel), 1 = one tile.
+int g_fwd_tiles = 0;
+int fwd_tiles() {
+  if (g_fwd_tiles) return g_fwd_tiles;
+  static const int n = [] {
+    const char* e = std::getenv("LYNX_ATTN_FWD_TILES");
+    return e && std::atoi(e) == 1 ? 1 : 2;
+  }();
+  return n;
+}
+
 template <int D>
 int fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, int H, cudaStream_t s) {
   CUtensorMap m;
   const long long T = static_cast<long long>(B) * S, ld = 3LL * H * D;
   if (!gemm::make_map(&m, qkv, ld, T, ld, 64, 128)) return set_error("attention: tensor map encode failed");
+  if (fwd_tiles() == 2 && poly_every() <= 1) {
+    auto k = attn_fwd2_tc_kernel<D>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2L<D>::kBytes);
+    k<<<dim3((S / 128 + 1) / 2, H, B), 384, Fwd2L<D>::kBytes, s>>>(m, out, lse, S, H,
+                                                                   kLog2e / sqrtf(static_cast<float>(D)));
+    return check_launch("attention_fwd_tc");
+  }
   switch (poly_every()) {
     case 2: return fwd_poly<D, 2>(m, out, lse, B, S, H, s);
     case 3: return fwd_poly<D, 3>(m, out, lse, B, S, H, s);
@@ -836,6 +1065,7 @@ int g_mode = -1;
 
 void attention_set_mode(int mode) { attn_tc::g_mode = mode; }
 void attention_set_bwd_warpgroups(int n) { attn_tc::g_bwd_wg = n == 2 || n == 4 ? n : 0; }
+void attention_set_fwd_tiles(int n) { attn_tc::g_fwd_tiles = n == 1 || n == 2 ? n : 0; }
 int attention_mode() { return attn_tc::g_mode; }
 bool attention_tc_supported(int seq, int head_dim) {
   return attn_tc::g_mode != 0 && seq % 128 == 0 &&

@@ -334,6 +334,25 @@ def test_attention_bwd_warpgroup_variants_are_bit_identical(ops, cuda, B, S, H, 
     assert torch.equal(res[2], res[4])
 
 
+@pytest.mark.parametrize("B,S,H,D", [(2, 512, 3, 128), (1, 384, 2, 64), (2, 640, 2, 112), (1, 128, 2, 96),
+                                     (1, 2048, 2, 128)])
+def test_attention_fwd_two_tile_kernel_is_bit_identical(ops, cuda, B, S, H, D):
+    """The two-query-tile forward (two softmax warpgroups ping-ponging on the tensor core) computes every row
+    exactly as the one-tile kernel: O and lse are bit-identical, odd tile counts included."""
+    from paper_2406_08756_b200._native import lib
+    g = torch.Generator(device=cuda).manual_seed(S * D + H)
+    qkv = torch.randn(B * S, 3 * H * D, device=cuda, generator=g).bfloat16()
+    res = {}
+    try:
+        for tiles in (1, 2):
+            lib().lynx_op_attention_fwd_tiles(tiles)
+            res[tiles] = ops.attention_fwd(qkv, B, S, H, D)
+    finally:
+        lib().lynx_op_attention_fwd_tiles(0)
+    torch.cuda.synchronize()
+    assert torch.equal(res[1][0], res[2][0]) and torch.equal(res[1][1], res[2][1])
+
+
 def test_xent(ops, cuda):
     rows, V = 256, 1024
     logits = torch.randn(rows, V, device=cuda).bfloat16()
