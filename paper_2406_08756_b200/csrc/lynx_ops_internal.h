@@ -132,6 +132,25 @@ int attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, i
 int attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* dvec,
                      __nv_bfloat16* dqkv, int batch, int seq, int heads, int head_dim, cudaStream_t s);
 
+// ---- fused tensor-parallel reductions (ops_tp.cu): every rank's row-parallel partial read in place
+constexpr int kMaxTpRanks = 8;
+struct TpPartials {
+  const __nv_bfloat16* p[kMaxTpRanks];  // rank order
+  int n;
+};
+struct TpFlags {
+  unsigned long long* f[kMaxTpRanks];  // every rank's flag array (peer mappings), rank order
+};
+// out = res + dropout(bias + bf16(sum of partials)) with bias_dropout_residual_fwd's mask and rounding.
+int tp_reduce_residual(const TpPartials& parts, const __nv_bfloat16* bias, const __nv_bfloat16* res,
+                       __nv_bfloat16* out, long long rows, int width, float p, uint64_t seed, uint64_t stream_id,
+                       cudaStream_t s);
+// out = bf16(sum of partials), n elements.
+int tp_reduce(const TpPartials& parts, __nv_bfloat16* out, long long n, cudaStream_t s);
+// Cross-process "partials of call k are written" barrier over device flags (k + 1 = value).
+int tp_signal_wait(const TpFlags& peers, const unsigned long long* my_flags, int n, int me, unsigned long long value,
+                   cudaStream_t s);
+
 // grad is fp32 (grad_bf16 = 0) or bf16 (grad_bf16 = 1).
 int adam_step(float* master, __nv_bfloat16* param, const void* grad, int grad_bf16, float* m, float* v, long long n,
               float lr, float beta1, float beta2, float eps, float weight_decay, int step, float grad_scale,

@@ -62,10 +62,6 @@ class NcclComms final : public Comms {
     nccl_ck(ncclCommSplit(world_, tp_rank, pp_rank, &pa_, nullptr), "split pp act");
     nccl_ck(ncclCommSplit(world_, tp_rank, pp_rank, &pg_, nullptr), "split pp grad");
   }
-  ~NcclComms() override {
-    for (ncclComm_t c : {tp_, pa_, pg_, world_})
-      if (c) ncclCommDestroy(c);
-  }
   void allreduce_sum_bf16(void* buf, size_t count, cudaStream_t s) override {
     nccl_ck(ncclAllReduce(buf, buf, count, ncclBfloat16, ncclSum, tp_, s), "allreduce");
   }
@@ -80,8 +76,75 @@ class NcclComms final : public Comms {
   }
   const char* kind() const override { return "nccl"; }
 
+  // Staging slots and flags in cudaMalloc'd memory, exchanged as CUDA-IPC handles over the TP
+  // communicator (ncclAllGather of the handle bytes) and opened as peer mappings.
+  void fused_setup(size_t bytes) override {
+    if (base_) return;
+    bytes_ = bytes;
+    int n = 0, me = 0;
+    nccl_ck(ncclCommCount(tp_, &n), "comm count");
+    nccl_ck(ncclCommUserRank(tp_, &me), "comm rank");
+    if (n > kMaxTpRanks) throw RtError("tp_fused supports up to 8 TP ranks", kValidation);
+    n_ = n;
+    me_ = me;
+    cuda_ck(cudaMalloc(&base_, 2 * bytes), "fused staging");
+    cuda_ck(cudaMalloc(&flags_, kMaxTpRanks * sizeof(unsigned long long)), "fused flags");
+    cuda_ck(cudaMemset(flags_, 0, kMaxTpRanks * sizeof(unsigned long long)), "fused flags");
+    cudaIpcMemHandle_t h[2];
+    cuda_ck(cudaIpcGetMemHandle(&h[0], base_), "ipc handle");
+    cuda_ck(cudaIpcGetMemHandle(&h[1], flags_), "ipc handle");
+    void *d_send = nullptr, *d_recv = nullptr;
+    cuda_ck(cudaMalloc(&d_send, sizeof(h)), "ipc exchange");
+    cuda_ck(cudaMalloc(&d_recv, sizeof(h) * n), "ipc exchange");
+    cuda_ck(cudaMemcpy(d_send, h, sizeof(h), cudaMemcpyHostToDevice), "ipc exchange");
+    nccl_ck(ncclAllGather(d_send, d_recv, sizeof(h), ncclUint8, tp_, nullptr), "ipc allgather");
+    cuda_ck(cudaStreamSynchronize(nullptr), "ipc exchange");
+    std::vector<cudaIpcMemHandle_t> all(2 * n);
+    cuda_ck(cudaMemcpy(all.data(), d_recv, sizeof(h) * n, cudaMemcpyDeviceToHost), "ipc exchange");
+    cudaFree(d_send);
+    cudaFree(d_recv);
+    for (int r = 0; r < n; ++r) {
+      if (r == me) {
+        peer_base_[r] = base_;
+        peer_flags_.f[r] = static_cast<unsigned long long*>(flags_);
+        continue;
+      }
+      cuda_ck(cudaIpcOpenMemHandle(&peer_base_[r], all[2 * r], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+      void* f = nullptr;
+      cuda_ck(cudaIpcOpenMemHandle(&f, all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess), "ipc open");
+      peer_flags_.f[r] = static_cast<unsigned long long*>(f);
+    }
+  }
+  void* fused_slot(int slot) override { return static_cast<char*>(base_) + slot * bytes_; }
+  std::vector<const void*> fused_peers(int slot) override {
+    std::vector<const void*> v;
+    for (int r = 0; r < n_; ++r) v.push_back(static_cast<const char*>(peer_base_[r]) + slot * bytes_);
+    return v;
+  }
+  void fused_barrier(long long k, cudaStream_t s) override {
+    if (tp_signal_wait(peer_flags_, static_cast<const unsigned long long*>(flags_), n_, me_,
+                       static_cast<unsigned long long>(k + 1), s) != kOk)
+      throw RtError(last_error(), kCudaError);
+  }
+  ~NcclComms() override {
+    for (int r = 0; r < n_; ++r)
+      if (r != me_) {
+        if (peer_base_[r]) cudaIpcCloseMemHandle(peer_base_[r]);
+        if (peer_flags_.f[r]) cudaIpcCloseMemHandle(peer_flags_.f[r]);
+      }
+    if (base_) cudaFree(base_);
+    if (flags_) cudaFree(flags_);
+    for (ncclComm_t c : {tp_, pa_, pg_, world_})
+      if (c) ncclCommDestroy(c);
+  }
+
  private:
   ncclComm_t world_ = nullptr, tp_ = nullptr, pa_ = nullptr, pg_ = nullptr;
+  void *base_ = nullptr, *flags_ = nullptr;
+  size_t bytes_ = 0;
+  int n_ = 0, me_ = 0;
+  void* peer_base_[kMaxTpRanks] = {};
+  TpFlags peer_flags_{};
 };
 
 // ------------------------------------------------------------------ loopback
@@ -158,6 +221,7 @@ struct Link {
 struct Grid {
   int tp = 1, pp = 1;
   std::vector<std::unique_ptr<TpGroup>> groups;  // one per stage
+  std::vector<std::vector<void*>> fused;          // [stage][tp rank]: staging base (exec.tp_fused)
   std::mutex links_mu;
   std::map<std::tuple<int, int, int, int>, std::unique_ptr<Link>> links;  // (channel, src, dst, tp_rank)
   Link& link(Channel ch, int src, int dst, int tp_rank) {
@@ -184,6 +248,7 @@ class LoopbackComms final : public Comms {
       grid_->tp = tp;
       grid_->pp = pp;
       for (int s = 0; s < pp; ++s) grid_->groups.push_back(std::make_unique<TpGroup>());
+      grid_->fused.assign(pp, std::vector<void*>(tp, nullptr));
       g_grids[name] = grid_;
     } else if (grid_->tp != tp || grid_->pp != pp) {
       throw RtError("loopback grid '" + name + "' exists with a different tp x pp shape", kValidation);
@@ -195,7 +260,41 @@ class LoopbackComms final : public Comms {
     reduce(buf, count, max ? 2 : 1, s);
   }
 
-  // kind 0: bf16 SUM (fp32 accumulation), 1: fp32 SUM, 2: fp32 MAX. Every rank of the TP group calls
+  void fused_setup(size_t bytes) override {
+    if (base_) return;
+    bytes_ = bytes;
+    cuda_ck(cudaMalloc(&base_, 2 * bytes), "fused staging");
+    TpGroup& g = *grid_->groups[pp_rank_];
+    std::lock_guard<std::mutex> lk(g.mu);
+    grid_->fused[pp_rank_][tp_rank_] = base_;
+    g.cv.notify_all();
+  }
+  void* fused_slot(int slot) override { return static_cast<char*>(base_) + slot * bytes_; }
+  std::vector<const void*> fused_peers(int slot) override {
+    TpGroup& g = *grid_->groups[pp_rank_];
+    std::unique_lock<std::mutex> lk(g.mu);
+    auto& row = grid_->fused[pp_rank_];
+    if (!g.cv.wait_for(lk, kPeerTimeout, [&] {
+          for (void* p : row)
+            if (!p) return false;
+          return true;
+        }))
+      throw RtError("loopback tp_fused: a TP peer never set up its staging", kCudaError);
+    std::vector<const void*> v;
+    for (void* p : row) v.push_back(static_cast<const char*>(p) + slot * bytes_);
+    return v;
+  }
+  // every rank's stream waits for every rank's partial of call k (events only; no kernel)
+  void fused_barrier(long long k, cudaStream_t s) override { reduce(nullptr, 0, 3, s); }
+  ~LoopbackComms() override {
+    if (base_) {
+      cudaDeviceSynchronize();  // peers may still read this rank's slots
+      cudaFree(base_);
+    }
+  }
+
+  // kind 0: bf16 SUM (fp32 accumulation), 1: fp32 SUM, 2: fp32 MAX, 3: barrier only. Every rank of the
+  // TP group calls
   // its collectives in the same order (identical programs), so the k-th call of each rank matches.
   void reduce(void* buf, size_t count, int kind, cudaStream_t s) {
     if (tp_ == 1) return;
@@ -214,7 +313,9 @@ class LoopbackComms final : public Comms {
     c.ready[tp_rank_] = ready;
     if (++c.arrived == tp_) {  // last to arrive reduces for everyone
       for (int r = 0; r < tp_; ++r) cuda_ck(cudaStreamWaitEvent(s, c.ready[r], 0), "wait");
-      if (kind == 0) {
+      if (kind == 3) {
+        // barrier: the waits above are the whole operation
+      } else if (kind == 0) {
         PtrPack pk{};
         for (int r = 0; r < tp_; ++r) pk.p[r] = static_cast<__nv_bfloat16*>(c.bufs[r]);
         const long long nvec = static_cast<long long>(count / 8);
@@ -229,7 +330,7 @@ class LoopbackComms final : public Comms {
         loopback_f32_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(pk, tp_, static_cast<long long>(count),
                                                                      kind == 2 ? 1 : 0);
       }
-      if (check_launch("loopback_allreduce") != kOk) throw RtError(last_error(), kCudaError);
+      if (kind != 3 && check_launch("loopback_allreduce") != kOk) throw RtError(last_error(), kCudaError);
       cuda_ck(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming), "event");
       cuda_ck(cudaEventRecord(c.done, s), "event");
       c.complete = true;
@@ -282,6 +383,8 @@ class LoopbackComms final : public Comms {
   std::shared_ptr<Grid> grid_;
   int tp_, pp_rank_, tp_rank_;
   long long seq_ = 0;
+  void* base_ = nullptr;
+  size_t bytes_ = 0;
 };
 
 }  // namespace

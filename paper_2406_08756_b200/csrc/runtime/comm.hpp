@@ -21,6 +21,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 namespace lynx::rt {
 
@@ -43,6 +44,18 @@ class Comms {
   virtual void send_bf16(const void* buf, size_t count, int peer, Channel ch, cudaStream_t s) = 0;
   virtual void recv_bf16(void* buf, size_t count, int peer, Channel ch, cudaStream_t s) = 0;
   virtual const char* kind() const = 0;
+
+  // Fused row-parallel reductions (exec.tp_fused): two staging slots of `bytes` per rank that every rank
+  // of the TP group can read in place (the same device in the loopback grid, CUDA-IPC peer mappings over
+  // NVLink across processes). A rank writes its partial into its own slot (call k uses slot k % 2); after
+  // fused_barrier(k, s) — stream-ordered on s, no host wait on the device — every rank's slot of call k
+  // is complete and readable. Two slots suffice: a rank rewrites slot k % 2 at call k + 2 only after its
+  // own reduction of call k + 1, which waited for every peer's call k + 1 partial, written after that
+  // peer's reduction of call k (stream order) had finished reading the slot.
+  virtual void fused_setup(size_t bytes) = 0;
+  virtual void* fused_slot(int slot) = 0;
+  virtual std::vector<const void*> fused_peers(int slot) = 0;  // every rank's slot, rank order
+  virtual void fused_barrier(long long k, cudaStream_t s) = 0;
 };
 
 // id_hex: hex ncclUniqueId ("" with world_size 1: a private one-rank world).

@@ -115,6 +115,7 @@ void Executor::init_device() {
       comms_ = make_loopback_comms(loopback_, cfg_.tp, cfg_.pp, cfg_.pp_rank, cfg_.tp_rank);
     else
       comms_ = make_nccl_comms(nccl_id_, world_rank_, world_size_, cfg_.pp_rank, cfg_.tp_rank);
+    if (fused_) comms_->fused_setup(static_cast<size_t>(cfg_.tokens()) * cfg_.hidden * 2);
   }
   for (cudaStream_t* s : {&main_, &side_, &tp_s_, &pa_s_, &pg_s_})
     ck(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking), "stream");
@@ -214,6 +215,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.elide_recompute = ex.value("elide_recompute", false);
   opt_.elide_fill = ex.value("elide_fill", false);
   opt_.window_join = ex.value("window_join", true);
+  opt_.tp_fused = ex.value("tp_fused", false);
   opt_.dry_run = ex.value("dry_run", false);
   opt_.standalone = ex.value("standalone_stage", false);
   opt_.probe_fc1 = ex.value("probe_fc1", false);
@@ -312,6 +314,15 @@ void Executor::bind_template() {
     std::stable_sort(kv.second.begin(), kv.second.end(), [](const Recompute& a, const Recompute& b) {
       return std::tie(a.owner_mb, a.owner_layer, a.op) < std::tie(b.owner_mb, b.owner_layer, b.op);
     });
+  fused_ = opt_.tp_fused && tp_tmpl_ && cfg_.tp > 1;
+  if (fused_) {
+    if (opt_.standalone) throw RtError("exec.tp_fused needs every TP rank (not standalone_stage)", kValidation);
+    for (const Recompute& it : tl_.items)
+      if (op_of_[it.op] == Op::AR1 || op_of_[it.op] == Op::AR2)
+        throw RtError("exec.tp_fused: the plan regenerates an all-reduce output (phase 5 on ar1 / ar2); run it "
+                      "without tp_fused",
+                      kValidation);
+  }
   // plan clock and logical-ledger tables (pipesim.cpp:83-121 build_layout)
   bwd_elem_.assign(n_, -1);
   bwd_last_use_.assign(n_, -1);
@@ -496,11 +507,14 @@ void Executor::drop(Slot& sl, cudaStream_t s, bool keep_shadow) {
     const size_t idx = static_cast<size_t>(&sl - slots_.data());
     std::fprintf(stderr, "drop mb%zu l%zu op%zu\n", idx / (cfg_.layers * nf_), (idx / nf_) % cfg_.layers, idx % nf_);
   }
-  if (keep_shadow && opt_.check_recompute && !sl.shadow) {
+  if (sl.external) {
+    // a staging slot (exec.tp_fused): owned by the communicator
+  } else if (keep_shadow && opt_.check_recompute && !sl.shadow) {
     sl.shadow = sl.p;  // forward-produced copy, compared against the regeneration
   } else {
     release(sl.p, s);
   }
+  sl.external = false;
   sl.p = nullptr;
   sl.ready = nullptr;
   sl.regenerated = false;
@@ -551,6 +565,10 @@ uint64_t Executor::drop_stream(int l, int mb, Op op) const {
   const Op site = op == Op::AR1 ? Op::PROJ_RES : (op == Op::AR2 ? Op::FC2_RES : op);
   return (static_cast<uint64_t>(cfg_.layer0 + l + 1) << 32) | (static_cast<uint64_t>(mb) << 8) |
          static_cast<uint64_t>(site);
+}
+
+void* Executor::fused_partial() {
+  return opt_.dry_run ? reinterpret_cast<void*>(0x2000) : comms_->fused_slot(static_cast<int>(fused_seq_ % 2));
 }
 
 // ============================================================ logical ledger
@@ -755,7 +773,12 @@ void Executor::fwd_op(int mb, int l, int pos, cudaStream_t s, bool recompute) {
       break;
     default: throw RtError(std::string("operator ") + op_name(op) + " is not a compute forward op", kParse);
   }
-  out.p = alloc(bytes, s);
+  if (fused_ && (op == Op::PROJ || op == Op::FC2)) {  // row-parallel partial: into this rank's staging slot
+    out.p = opt_.dry_run ? reinterpret_cast<void*>(0x2000) : comms_->fused_slot(static_cast<int>(fused_seq_ % 2));
+    out.external = true;
+  } else {
+    out.p = alloc(bytes, s);
+  }
   out.bytes = bytes;
   out.booked = true;
   book(out_bytes_[pos]);
@@ -924,17 +947,21 @@ host::Rat Executor::comm_element(int mb, bool bwd, int l, const host::Element& e
       if (op_of_[i] == o) return i;
     return -1;
   };
-  if (op == Op::AR1) buf = need(mb, l, pos_of(Op::PROJ), main_);
-  if (op == Op::AR2) buf = need(mb, l, pos_of(Op::FC2), main_);
-  if (op == Op::AR_B1) buf = grad_[mb].dln2;
-  if (op == Op::AR_B2) buf = grad_[mb].dln1;
+  if (!fused_) {
+    if (op == Op::AR1) buf = need(mb, l, pos_of(Op::PROJ), main_);
+    if (op == Op::AR2) buf = need(mb, l, pos_of(Op::FC2), main_);
+    if (op == Op::AR_B1) buf = grad_[mb].dln2;
+    if (op == Op::AR_B2) buf = grad_[mb].dln1;
+  } else if (!bwd) {
+    need(mb, l, pos_of(op == Op::AR1 ? Op::PROJ : Op::FC2), main_);  // the partial, in this rank's staging slot
+  }
   program_.push_back({"allreduce", "tp", -1, static_cast<size_t>(T * h * 2),
                       std::string(op_name(op)) + " mb" + std::to_string(mb) + " l" + std::to_string(l)});
   cudaEvent_t go = nullptr;
   if (!opt_.dry_run) {
     go = ev();
     ck(cudaEventRecord(go, main_), "event");
-    ck(cudaStreamWaitEvent(tp_s_, go, 0), "wait");
+    if (!fused_) ck(cudaStreamWaitEvent(tp_s_, go, 0), "wait");
   }
   // window items (the reference packs them from the comm start, pipesim.cpp:398-424)
   cudaEvent_t win_done = nullptr;
@@ -952,7 +979,37 @@ host::Rat Executor::comm_element(int mb, bool bwd, int l, const host::Element& e
     }
   }
   lg_.t = t;
-  if (!opt_.dry_run) {
+  // The element after the all-reduce starts at max(comm end, window recompute end), as the reference
+  // schedules it (pipesim.cpp:462, 527): a recompute that spills past the window is waited for (and
+  // measured as exposed) instead of contending with the main stream for SMs.
+  auto join_window = [&] {
+    if (!win_done) return;
+    span_begin(main_, 4, mb, win_op);
+    ck(cudaStreamWaitEvent(main_, win_done, 0), "wait");
+    span_end(main_);
+  };
+  TpPartials parts{};
+  if (fused_ && !opt_.dry_run) {
+    // exec.tp_fused: every rank's partial is read in place from its staging slot by one kernel on the main
+    // stream that also does the consumer's elementwise work (ops_tp.cu) — no separate collective
+    const long long k = fused_seq_++;
+    span_begin(main_, 1, mb, e.op);
+    comms_->fused_barrier(k, main_);
+    const auto peers = comms_->fused_peers(static_cast<int>(k % 2));
+    parts.n = static_cast<int>(peers.size());
+    for (int r = 0; r < parts.n; ++r) parts.p[r] = static_cast<const __nv_bfloat16*>(peers[r]);
+    if (bwd) {
+      void* dst = alloc(T * h * 2, main_);
+      ck_op(tp_reduce(parts, static_cast<__nv_bfloat16*>(dst), T * h, main_), "tp reduce");
+      (op == Op::AR_B1 ? grad_[mb].dln2 : grad_[mb].dln1) = dst;
+      span_end(main_);
+      join_window();
+      return busy;
+    }
+  } else if (fused_) {  // dry run: the reduced gradient buffer of a backward element
+    if (bwd) (op == Op::AR_B1 ? grad_[mb].dln2 : grad_[mb].dln1) = alloc(T * h * 2, main_);
+    if (bwd) return busy;
+  } else if (!opt_.dry_run) {
     span_begin(tp_s_, 1, mb, e.op);
     if (opt_.comm_standin_us > 0)
       ck_op(comm_standin(static_cast<unsigned long long>(opt_.comm_standin_us * 1e3), opt_.comm_standin_ctas, tp_s_),
@@ -963,14 +1020,7 @@ host::Rat Executor::comm_element(int mb, bool bwd, int l, const host::Element& e
     cudaEvent_t done = ev();
     ck(cudaEventRecord(done, tp_s_), "event");
     ck(cudaStreamWaitEvent(main_, done, 0), "wait");
-    if (win_done) {
-      // The element after the all-reduce starts at max(comm end, window recompute end), as the
-      // reference schedules it (pipesim.cpp:462, 527): a recompute that spills past the window is
-      // waited for (and measured as exposed) instead of contending with the main stream for SMs.
-      span_begin(main_, 4, mb, win_op);
-      ck(cudaStreamWaitEvent(main_, win_done, 0), "wait");
-      span_end(main_);
-    }
+    join_window();
   }
   if (bwd) return busy;  // backward partials are reduced in place
   // forward: bias + dropout + residual epilogue produces the op's tensor
@@ -983,19 +1033,29 @@ host::Rat Executor::comm_element(int mb, bool bwd, int l, const host::Element& e
   if (!opt_.dry_run) {
     const LayerParams P = ps_.layer(l);
     const uint64_t seed = cfg_.seed + static_cast<uint64_t>(step_) * 1000003ull;
-    timed_op(op == Op::AR1 ? "ar1_epilogue" : "ar2_epilogue", [&] {
-    ck_op(bias_dropout_residual_fwd(static_cast<const __nv_bfloat16*>(buf), op == Op::AR1 ? P.b_proj : P.b_fc2,
-                                    static_cast<const __nv_bfloat16*>(resid), static_cast<__nv_bfloat16*>(out.p), T, h,
-                                    cfg_.dropout, seed, drop_stream(l, mb, op), main_),
-          "residual");
-    });
+    if (fused_) {
+      ck_op(tp_reduce_residual(parts, op == Op::AR1 ? P.b_proj : P.b_fc2, static_cast<const __nv_bfloat16*>(resid),
+                               static_cast<__nv_bfloat16*>(out.p), T, h, cfg_.dropout, seed, drop_stream(l, mb, op),
+                               main_),
+            "tp reduce + residual");
+      span_end(main_);
+      join_window();
+    } else {
+      timed_op(op == Op::AR1 ? "ar1_epilogue" : "ar2_epilogue", [&] {
+        ck_op(bias_dropout_residual_fwd(static_cast<const __nv_bfloat16*>(buf), op == Op::AR1 ? P.b_proj : P.b_fc2,
+                                        static_cast<const __nv_bfloat16*>(resid), static_cast<__nv_bfloat16*>(out.p),
+                                        T, h, cfg_.dropout, seed, drop_stream(l, mb, op), main_),
+              "residual");
+      });
+    }
   }
   mark_ready(out, main_);
   // the partial (PROJ / FC2, 0 bytes in the profile) is consumed
   Slot& part = slot(mb, l, pos_of(op == Op::AR1 ? Op::PROJ : Op::FC2));
-  release(part.p, main_);
+  if (!part.external) release(part.p, main_);
   part.p = nullptr;
   part.booked = false;
+  part.external = false;
   return busy;
 }
 
@@ -1046,8 +1106,10 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
       }
       colsum(sc.t_wide, P.g_b_fc1, 4 * hp);
       gemm(sc.t_wide, 4 * hp, true, y2, h, true, P.g_w_fc1, h, 4 * hp, h, T, dw_epi_);       // dW_fc1 += dfc1^T y2
-      G.dln2 = alloc(T * h * 2, s);
-      gemm(sc.t_wide, 4 * hp, false, P.w_fc1, h, true, G.dln2, h, T, h, 4 * hp, EPI_BF16);     // dln2 = dfc1 W_fc1
+      // dln2 = dfc1 W_fc1: a partial over the TP ranks, all-reduced by AR_B1 (exec.tp_fused: written into
+      // this rank's staging slot and reduced into a fresh buffer by the fused reduction)
+      void* d2 = fused_ ? fused_partial() : (G.dln2 = alloc(T * h * 2, s));
+      gemm(sc.t_wide, 4 * hp, false, P.w_fc1, h, true, d2, h, T, h, 4 * hp, EPI_BF16);
       break;
     }
     case Op::ATTN_BWD: {
@@ -1078,8 +1140,8 @@ void Executor::bwd_op(int mb, int l, int pos, cudaStream_t s) {
               "attention_bwd");
       colsum(sc.t_wide, P.g_b_qkv, 3 * hp);
       gemm(sc.t_wide, 3 * hp, true, ln1, h, true, P.g_w_qkv, h, 3 * hp, h, T, dw_epi_);    // dW_qkv += dqkv^T y1
-      G.dln1 = alloc(T * h * 2, s);
-      gemm(sc.t_wide, 3 * hp, false, P.w_qkv, h, true, G.dln1, h, T, h, 3 * hp, EPI_BF16);   // dln1 = dqkv W_qkv
+      void* d1 = fused_ ? fused_partial() : (G.dln1 = alloc(T * h * 2, s));
+      gemm(sc.t_wide, 3 * hp, false, P.w_qkv, h, true, d1, h, T, h, 3 * hp, EPI_BF16);  // dln1 = dqkv W_qkv
       break;
     }
     case Op::LN1_BWD: {

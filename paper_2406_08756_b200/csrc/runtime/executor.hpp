@@ -46,6 +46,9 @@ struct ExecOptions {
   bool window_join = true;      // main waits for a window's recomputes before the element after its all-reduce,
                                 // and for a backward pass's stall-fill recomputes before the pass (reference
                                 // semantics); false: they may keep running beside the main stream
+  bool tp_fused = false;        // TP all-reduces fused into their consumers over peer memory (ops_tp.cu): the
+                                // row-parallel partials go to symmetric staging slots, one kernel per site reads
+                                // every rank's slot, sums and applies the epilogue
   bool elide_fill = false;      // elided mode: fill each stand-in buffer with uniform bf16 noise (timed apart,
                                 // report elide_fill_ms) so consumers read realistic operands, not stale memory
   bool dry_run = false;         // build the launch program only (no device)
@@ -83,6 +86,7 @@ struct Slot {
   bool regenerated = false;
   bool fused = false;      // produced early by the FC1 + GeLU epilogue; its own op call is a no-op
   bool booked = false;     // its profile bytes are in the logical ledger
+  bool external = false;   // a communicator staging slot (exec.tp_fused), not a pool allocation
   void* shadow = nullptr;  // check_recompute: forward-produced copy
 };
 
@@ -138,6 +142,7 @@ class Executor {
   void parse_config(const std::string& cfg);
   void bind_template();
   void validate_program();
+  void* fused_partial();
   void init_device();
   void finish_production(Slot& out, size_t bytes, cudaStream_t s, bool recompute);
   void release_all();
@@ -244,6 +249,8 @@ class Executor {
   bool head_first_ = true;
   std::vector<std::tuple<int, int, int, int, double, double, bool>> trace_;  // stage, mb, kind, op, start, end, bwd
   bool cur_bwd_ = false;  // direction of the pass being issued (span tags)
+  bool fused_ = false;          // exec.tp_fused in effect
+  long long fused_seq_ = 0;     // fused reductions issued so far (identical on every TP rank): staging slot = seq % 2
 
   struct Ledger {
     bool override_starts = false;

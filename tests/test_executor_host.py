@@ -174,3 +174,34 @@ def test_reference_inconsistent_plan_is_rejected_like_the_reference():
     if oref.available():
         with pytest.raises(RuntimeError):
             oref.RefLib().simulate_timelines(text, plans[0]["layers_per_stage"], [p["timeline"] for p in plans])
+
+
+def test_tp_fused_keeps_the_collective_program_and_rejects_what_it_cannot_run():
+    c = gp.GPTConfig("t", 4, 512, 8, 256, 2, 50432, tp=2, pp=2, n_microbatches=4, dropout=0.1,
+                     mem_budget_bytes=gp.BYTES_PER_PARAM_STATIC * gp.GPTConfig("t", 4, 512, 8, 256, 2, 50432,
+                                                                               tp=2).params() // 4 + 8 * 2**20)
+    text = gp.profile_text(c)
+    plans = [ex.plan_for(text, s) for s in range(2)]
+    for s in range(2):
+        progs = []
+        for fused in (False, True):
+            cfg = ex.make_config(c, plans[0]["layers_per_stage"], exec_opts={"dry_run": True, "tp_fused": fused})
+            e = ex.Executor(text, plans[s]["timeline"], cfg)
+            e.step(None, None)
+            progs.append(e.program())
+            e.close()
+        assert progs[0] == progs[1]  # same exchanges, same order: only how they run changes
+    cfg = ex.make_config(c, plans[0]["layers_per_stage"],
+                         exec_opts={"tp_fused": True, "standalone_stage": True, "comm_standin_us": 10})
+    with pytest.raises(ex.LynxError) as err:
+        ex.Executor(text, plans[0]["timeline"], cfg)
+    assert err.value.code == 1
+    # a plan that regenerates an all-reduce output (phase 5 on ar1) cannot run fused
+    import copy
+    tl = copy.deepcopy(plans[0]["timeline"])
+    tl["items"].append({"owner_mb": 0, "owner_layer": 0, "op": 4, "host": "critical", "host_mb": 0,
+                        "host_backward": True, "host_layer": 0, "host_window": 0, "host_elem": 0})
+    with pytest.raises(ex.LynxError) as err:
+        ex.Executor(text, tl, ex.make_config(c, plans[0]["layers_per_stage"],
+                                             exec_opts={"dry_run": True, "tp_fused": True}))
+    assert err.value.code == 1 and "tp_fused" in str(err.value)

@@ -192,3 +192,23 @@ def test_tp2pp2_real_step_ledgers_equal_simulator(cuda):
     for (s, r), rep in res["reports"].items():
         assert rep["ledger"]["memory_trace"] == sim["memory_traces"][s], (s, r)
         assert rep["ledger"]["memory_peak_bytes"] == sim["memory_peaks"][s], (s, r)
+
+
+@pytest.mark.parametrize("tp,pp,n_micro,baseline,vocab", [(2, 1, 2, "heu", 50432), (2, 2, 4, "heu", 50432),
+                                                          (4, 1, 2, "retain_all", 50688)])
+def test_fused_tp_reduction_is_bit_identical_and_matches_oracle(cuda, tp, pp, n_micro, baseline, vocab):
+    """exec.tp_fused: the row-parallel partials go to symmetric staging slots and one kernel
+    per all-reduce site reads every rank's slot in place, sums in rank order and applies the consumer's
+    epilogue — no separate collective. Loss and every gradient equal the collective path's bit for bit, and
+    the oracle's within tolerance; window recomputes still overlap the (fused) reductions."""
+    extra = 8 if baseline == "heu" else None
+    c = cfg(tp=tp, pp=pp, n_micro=n_micro, dropout=0.1, budget_extra_mib=extra, vocab=vocab)
+    plain = grid_run(c, baseline)
+    fused = grid_run(c, baseline, exec_opts={"tp_fused": True})
+    assert plain["losses"] == fused["losses"]
+    for key in plain["grads"]:
+        for k in plain["grads"][key]:
+            assert np.array_equal(plain["grads"][key][k], fused["grads"][key][k]), (key, k)
+    compare_with_oracle(c, fused)
+    if baseline == "heu":
+        assert any(r["recompute_overlapped_ms"] > 0 for r in fused["reports"].values())
