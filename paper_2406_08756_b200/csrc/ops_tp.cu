@@ -23,8 +23,12 @@ __device__ __forceinline__ void sum_ranks(const TpPartials& parts, long long v, 
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.f;
   for (int r = 0; r < parts.n; ++r) {
+    // .cg: not through L1 — a peer's staging slot is rewritten every second call
+    const uint4 raw = __ldcg(reinterpret_cast<const uint4*>(parts.p[r]) + v);
+    BF8 x;
+    x.w[0] = raw.x, x.w[1] = raw.y, x.w[2] = raw.z, x.w[3] = raw.w;
     float f[8];
-    bf8_to_f(reinterpret_cast<const BF8*>(parts.p[r])[v], f);
+    bf8_to_f(x, f);
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] += f[j];
   }
