@@ -182,7 +182,7 @@ LYNX_DEV void tmem_cols(uint32_t taddr, int c0, int c1, F&& f) {
 // Per-tile event timeline of CTA (0,0,0) for kernel tuning: build with -DLYNX_ATTN_TRACE
 // (LYNX_BUILD_TRACE=1 python -m paper_2406_08756_b200.build); compiled out otherwise.
 #ifdef LYNX_ATTN_TRACE
-__device__ long long g_atrace[8][64];
+__device__ long long g_atrace[16][64];
 #define ATRACE(tag, j)                                                              \
   do {                                                                              \
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 64)          \
@@ -191,7 +191,7 @@ __device__ long long g_atrace[8][64];
 #define ATRACE_DUMP(n)                                                              \
   do {                                                                              \
     if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)  \
-      for (int t_ = 0; t_ < 8; ++t_)                                                \
+      for (int t_ = 0; t_ < 16; ++t_)                                                \
         for (int j_ = 0; j_ < (n) && j_ < 64; ++j_)                                 \
           printf("T %d %d %lld\n", t_, j_, g_atrace[t_][j_]);                       \
   } while (0)
@@ -407,7 +407,7 @@ struct Fwd2L {
   static constexpr int kBytes = kBar + 128 + 1024;
 };
 
-template <int D>
+template <int D, int kPoly>  // kPoly: as attn_fwd_tc_kernel (every kPoly-th exponential on the FMA pipe)
 __global__ void __launch_bounds__(384, 1)
     attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ out,
                         float* __restrict__ lse, int S, int H, float scale_log2) {
@@ -483,10 +483,12 @@ __global__ void __launch_bounds__(384, 1)
           umma_f16(tmem + t * 128, kmaj(sQ + t * L::kTile, kk, 16384), kmaj(sK + st * L::kTile, kk, 16384), idS,
                    kk > 0);
         umma_commit(s_full + t);
+        ATRACE(t ? 7 : 0, j);
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P packed bf16 over S_t in TMEM
         const int st = j & 1;
         mbar_wait(p_full + t, j & 1);
+        ATRACE(t ? 6 : 1, j);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
@@ -529,11 +531,13 @@ __global__ void __launch_bounds__(384, 1)
       float m_run = -INFINITY, l_run = 0.f;
       for (int j = 0; j < nt; ++j) {
         mbar_wait(s_full + t, j & 1);
+        if (warp % 4 == 0 && lane == 0) ATRACE(t ? 4 : 2, j);
         tc_fence_after();
         float x[128];
 #pragma unroll
         for (int c = 0; c < 4; ++c) tmem_ld32(s_col + c * 32, reinterpret_cast<uint32_t*>(x + c * 32));
         tmem_ld_wait();
+        if (t == 0 && warp == 4 && lane == 0) ATRACE(8, j);
         if (j == qb) {  // diagonal tile: causal mask (warp-uniform branch)
 #pragma unroll
           for (int i = 0; i < 128; ++i)
@@ -547,6 +551,7 @@ __global__ void __launch_bounds__(384, 1)
         const float mt =
             fmaxf(fmaxf(fmaxf(mv[0], mv[1]), fmaxf(mv[2], mv[3])), fmaxf(fmaxf(mv[4], mv[5]), fmaxf(mv[6], mv[7])));
         const float m_new = fmaxf(m_run, mt * scale_log2);
+        if (t == 0 && warp == 4 && lane == 0) ATRACE(9, j);
         const bool need = __any_sync(0xffffffffu, m_new > m_run + kRescale);
         float corr = 1.f;
         if (need) {
@@ -556,11 +561,13 @@ __global__ void __launch_bounds__(384, 1)
         float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int i = 0; i < 128; ++i) {
-          x[i] = ex2(fmaf(x[i], scale_log2, -m_run));
+          const float a = fmaf(x[i], scale_log2, -m_run);
+          x[i] = (kPoly > 0 && i % (kPoly > 0 ? kPoly : 1) == (kPoly > 0 ? kPoly : 1) - 1) ? ex2_poly(a) : ex2(a);
           rv[i & 7] += x[i];
         }
         const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
         l_run = l_run * corr + rs;
+        if (t == 0 && warp == 4 && lane == 0) ATRACE(10, j);
         if (j > 0 && need) {  // O_t rescale after PV_t(j-1) completes (PV_t(j) needs this tile's P)
           mbar_wait(pv_done + t, (j - 1) & 1);
           tc_fence_after();
@@ -580,9 +587,12 @@ __global__ void __launch_bounds__(384, 1)
           for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(x[32 * c + 2 * i], x[32 * c + 2 * i + 1]);
           tmem_st16(s_col + c * 16, packed);
         }
+        if (t == 0 && warp == 4 && lane == 0) ATRACE(11, j);
         tmem_st_wait();
+        if (t == 0 && warp == 4 && lane == 0) ATRACE(12, j);
         tc_fence_before();
         mbar_arrive(p_full + t);
+        if (warp % 4 == 0 && lane == 0) ATRACE(t ? 5 : 3, j);
       }
       mbar_wait(pv_done + t, (nt - 1) & 1);
       tc_fence_after();
@@ -600,20 +610,26 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  ATRACE_DUMP(n);
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
 // ============================================================== backward dK / dV
 template <int D>
 struct DkvL {
-  static constexpr int kStages = 3;        // Q / dO / lse / D ring (each stage is used early and late)
+  // Q / dO / lse / D ring. A stage is held from S^T(i) to dV / dK(i), about two tile periods, and its
+  // reload takes ~1000 cycles from L2: with 3 stages the load of tile i + 3 could only start when
+  // dV / dK(i) completed and S^T(i + 3) waited for it (a clock64 trace: 1460-cycle tile period for
+  // 1024 cycles of MMA, the row warps idle 500 cycles per tile). 4 stages fill 195 KB at D = 128.
+  static constexpr int kStages = D <= 64 ? 6 : 4;
   static constexpr int kAtoms = (D + 63) / 64;
   static constexpr int kKV = 128 * kAtoms * 64 * 2;  // K or V tile: ceil(D/64) atoms of 16 KB (128 rows)
   static constexpr int kQT = 64 * kAtoms * 64 * 2;   // Q or dO tile: ceil(D/64) atoms of 8 KB (64 rows)
   static constexpr int kK = 0, kV = kKV, kQ = 2 * kKV, kDO = kQ + kStages * kQT;
   static constexpr int kVec = kDO + kStages * kQT;  // lse2[kStages][64], dvec[kStages][64]; P^T / dS^T live in TMEM
   static constexpr int kBar = kVec + 2 * kStages * 256;
-  static constexpr int kBytes = kBar + 128 + 1024;
+  static constexpr int kBytes = kBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
 template <int D, int kWG>  // kWG row warpgroups (2 or 4), each owning 64 / kWG query columns of a tile
@@ -804,21 +820,26 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
 }
 
 // ============================================================== backward dQ
+// Q and dO are the same for every key tile of a CTA, so they sit in TMEM as the A operands of
+// S = Q K^T and dP = dO V^T (packed bf16 pairs, one row per lane, written once by the row warps
+// from global memory). An SS MMA of 128 x 64 x 16 reads 6 KB of shared memory per 32-cycle
+// instruction, 1.5x the 128 B/clk the SM's shared memory delivers, so with Q / dO in shared memory
+// S and dP ran smem-bound at ~48 cycles per instruction; from TMEM only the 2-KB K / V slice is read.
 template <int D>
 struct DqL {
   static constexpr int kAtoms = (D + 63) / 64;
-  static constexpr int kQT = 128 * kAtoms * 64 * 2;  // Q or dO tile (128 rows)
   static constexpr int kKT = 64 * kAtoms * 64 * 2;   // K or V tile (64 rows)
-  static constexpr int kStages = 3;
-  static constexpr int kQ = 0, kDO = kQT, kK = 2 * kQT, kV = kK + kStages * kKT;
-  static constexpr int kBar = kV + kStages * kKT;  // dS lives in TMEM
-  static constexpr int kBytes = kBar + 128 + 1024;
+  static constexpr int kStages = D <= 64 ? 8 : 6;    // K / V ring (see DkvL::kStages)
+  static constexpr int kK = 0, kV = kStages * kKT;
+  static constexpr int kBar = kV + kStages * kKT;  // Q, dO and dS live in TMEM
+  static constexpr int kBytes = kBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
 template <int D, int kWG>  // kWG row warpgroups (2 or 4), each owning 64 / kWG key columns of a tile
 __global__ void __launch_bounds__(128 + 128 * kWG, 1)
-    attn_dq_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
-                      const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
+    attn_dq_tc_kernel(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ dout,
+                      const __grid_constant__ CUtensorMap map_kv, const float* __restrict__ lse2,
                       const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
                       float scale_log2) {
   using L = DqL<D>;
@@ -826,7 +847,7 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = kv_full + NS, *s_full = kv_empty + NS,
+  uint64_t *a_full = bar, *kv_full = bar + 1, *kv_empty = kv_full + NS, *s_full = kv_empty + NS,
            *ds_full = s_full + 2, *ds_free = ds_full + 2, *fin = ds_free + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
   const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -834,7 +855,7 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
   const int n = 2 * (qb + 1), HD = H * D, row0 = b * S;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
+    mbar_init(a_full, 128 * kWG);
     for (int i = 0; i < NS; ++i) {
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
@@ -851,19 +872,15 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  // TMEM: S[2] at 0 / 64, dP[2] at 128 / 192, dQ at 256.
+  // TMEM: S[2] at 0 / 64, dP[2] at 128 / 192, dQ at 256, Q at 384, dO at 448 (D / 2 packed columns each).
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (elect_one()) {
-      mbar_arrive_expect_tx(q_full, 2 * L::kQT);
-      for (int a = 0; a < kA; ++a) {
-        tma_load_2d(&map_q, q_full, smem + L::kQ + a * 16384, h * D + 64 * a, row0 + qb * 128, kEvictFirst);
-        tma_load_2d(&map_do, q_full, smem + L::kDO + a * 16384, h * D + 64 * a, row0 + qb * 128, kEvictFirst);
-      }
       for (int j = 0; j < n; ++j) {
         const int st = j % NS;
         if (j >= NS) mbar_wait(kv_empty + st, ((j / NS) - 1) & 1);
+        ATRACE(0, j);
         mbar_arrive_expect_tx(kv_full + st, 2 * L::kKT);
         for (int a = 0; a < kA; ++a) {
           tma_load_2d(&map_kv, kv_full + st, smem + L::kK + st * L::kKT + a * 8192, HD + h * D + 64 * a,
@@ -877,25 +894,27 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
     if (elect_one()) {
       constexpr uint32_t idS = umma_idesc_bf16(128, 64, false, false);
       constexpr uint32_t idG = umma_idesc_bf16(128, D, false, true);
-      const uint32_t sQ = smem_u32(smem + L::kQ), sDO = smem_u32(smem + L::kDO), sK = smem_u32(smem + L::kK),
-                     sV = smem_u32(smem + L::kV);
+      const uint32_t sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV);
       auto issue_s = [&](int j) {
         const int st = j % NS, tb = j & 1;
         mbar_wait(kv_full + st, (j / NS) & 1);
+        ATRACE(1, j);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          umma_f16(tmem + tb * 64, kmaj(sQ, kk, 16384), kmaj(sK + st * L::kKT, kk, 8192), idS, kk > 0);
-          umma_f16(tmem + 128 + tb * 64, kmaj(sDO, kk, 16384), kmaj(sV + st * L::kKT, kk, 8192), idS, kk > 0);
+          umma_f16_ts(tmem + tb * 64, tmem + 384 + kk * 8, kmaj(sK + st * L::kKT, kk, 8192), idS, kk > 0);
+          umma_f16_ts(tmem + 128 + tb * 64, tmem + 448 + kk * 8, kmaj(sV + st * L::kKT, kk, 8192), idS, kk > 0);
         }
         umma_commit(s_full + tb);
       };
-      mbar_wait(q_full, 0);
+      mbar_wait(a_full, 0);
+      tc_fence_after();
       issue_s(0);
       issue_s(1);
       for (int j = 0; j < n; ++j) {
         const int st = j % NS, tb = j & 1;
         mbar_wait(ds_full + tb, (j >> 1) & 1);
+        ATRACE(2, j);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // A = dS(j), packed bf16 over the S(j) columns of TMEM buffer tb
@@ -914,11 +933,34 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
     const int r = (warp % 4) * 32 + lane;
     const int q = qb * 128 + r;
     const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    {  // this thread's row of Q (even warpgroups) or dO (odd) into TMEM, 16-element granules split over
+       // the kWG / 2 warpgroups of each kind
+      constexpr int kG = D / 16, kParts = kWG / 2, kPer = (kG + kParts - 1) / kParts;
+      const bool is_do = wg & 1;
+      const int part = wg >> 1;
+      const uint4* src = reinterpret_cast<const uint4*>(
+          is_do ? dout + static_cast<long long>(row0 + q) * HD + h * D
+                : qkv + static_cast<long long>(row0 + q) * 3 * HD + h * D);
+      const uint32_t dst = tmem + lanes + (is_do ? 448 : 384);
+#pragma unroll
+      for (int g = 0; g < kPer; ++g) {
+        const int gg = part * kPer + g;
+        if (gg < kG) {
+          const uint4 lo = __ldg(src + 2 * gg), hi = __ldg(src + 2 * gg + 1);
+          const uint32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+          tmem_st8(dst + 8 * gg, v);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(a_full);
+    }
     const long long vi = (static_cast<long long>(b) * H + h) * S + q;
     const float l2 = lse2[vi], dq = dvec[vi];
     for (int j = 0; j < n; ++j) {
       const int st = j & 1;
       mbar_wait(s_full + st, (j >> 1) & 1);
+      if (threadIdx.x == 128) ATRACE(3, j);
       tc_fence_after();
       const bool diag = j >= 2 * qb;
       {
@@ -939,6 +981,7 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
         uint32_t packed[CW / 2];
 #pragma unroll
         for (int c = 0; c < CW / 2; ++c) packed[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
+        if (threadIdx.x == 128) ATRACE(4, j);
         // dS(j) overwrites S(j) in place, each warpgroup inside the columns it read (packed_col; see
         // the dK/dV kernel); dQ(j-2), the last reader of this buffer, completed before S(j).
         tmem_st_cols<CW / 2>(tmem + lanes + st * 64 + wg * CW, packed);
@@ -946,6 +989,7 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
       }
       tc_fence_before();
       mbar_arrive(ds_full + st);
+      if (threadIdx.x == 128) ATRACE(6, j);
     }
     mbar_wait(fin, 0);
     tc_fence_after();
@@ -961,6 +1005,7 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  ATRACE_DUMP(n);
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
@@ -999,8 +1044,12 @@ int fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, 
   CUtensorMap m;
   const long long T = static_cast<long long>(B) * S, ld = 3LL * H * D;
   if (!gemm::make_map(&m, qkv, ld, T, ld, 64, 128)) return set_error("attention: tensor map encode failed");
-  if (fwd_tiles() == 2 && poly_every() <= 1) {
-    auto k = attn_fwd2_tc_kernel<D>;
+  if (fwd_tiles() == 2) {
+    const int poly = poly_every();
+    auto k = poly == 2 ? attn_fwd2_tc_kernel<D, 2>
+             : poly == 3 ? attn_fwd2_tc_kernel<D, 3>
+             : poly == 4 ? attn_fwd2_tc_kernel<D, 4>
+                         : attn_fwd2_tc_kernel<D, 0>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2L<D>::kBytes);
     k<<<dim3((S / 128 + 1) / 2, H, B), 384, Fwd2L<D>::kBytes, s>>>(m, out, lse, S, H,
                                                                    kLog2e / sqrtf(static_cast<float>(D)));
@@ -1025,14 +1074,14 @@ int bwd_warpgroups() {
   if (g_bwd_wg) return g_bwd_wg;
   static const int n = [] {
     const char* e = std::getenv("LYNX_ATTN_BWD_WG");
-    return e && std::atoi(e) == 2 ? 2 : kDefaultBwdWG;
+    return e ? (std::atoi(e) == 4 ? 4 : 2) : kDefaultBwdWG;
   }();
   return n;
 }
 
 template <int D, int kWG>
-int bwd_launch(const CUtensorMap& m128, const CUtensorMap& m64, const CUtensorMap& d64, const CUtensorMap& d128,
-               const float* lse, const float* dvec, __nv_bfloat16* dqkv, int B, int S, int H, float scale,
+int bwd_launch(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const CUtensorMap& m128, const CUtensorMap& m64,
+               const CUtensorMap& d64, const float* lse, const float* dvec, __nv_bfloat16* dqkv, int B, int S, int H, float scale,
                float scale_log2, cudaStream_t s) {
   auto k1 = attn_dkdv_tc_kernel<D, kWG>;
   cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvL<D>::kBytes);
@@ -1040,7 +1089,7 @@ int bwd_launch(const CUtensorMap& m128, const CUtensorMap& m64, const CUtensorMa
                                                                    scale_log2);
   auto k2 = attn_dq_tc_kernel<D, kWG>;
   cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, DqL<D>::kBytes);
-  k2<<<dim3(S / 128, H, B), 128 + 128 * kWG, DqL<D>::kBytes, s>>>(m128, m64, d128, lse, dvec, dqkv, S, H, scale,
+  k2<<<dim3(S / 128, H, B), 128 + 128 * kWG, DqL<D>::kBytes, s>>>(qkv, dout, m64, lse, dvec, dqkv, S, H, scale,
                                                                   scale_log2);
   return check_launch("attention_bwd_tc", 2);
 }
@@ -1048,15 +1097,15 @@ int bwd_launch(const CUtensorMap& m128, const CUtensorMap& m64, const CUtensorMa
 template <int D>
 int bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* dvec,
         __nv_bfloat16* dqkv, int B, int S, int H, cudaStream_t s) {
-  CUtensorMap m128, m64, d64, d128;
+  CUtensorMap m128, m64, d64;
   const long long T = static_cast<long long>(B) * S, ld = 3LL * H * D, hd = static_cast<long long>(H) * D;
   bool ok = gemm::make_map(&m128, qkv, ld, T, ld, 64, 128) && gemm::make_map(&m64, qkv, ld, T, ld, 64, 64) &&
-            gemm::make_map(&d64, dout, hd, T, hd, 64, 64) && gemm::make_map(&d128, dout, hd, T, hd, 64, 128);
+            gemm::make_map(&d64, dout, hd, T, hd, 64, 64);
   if (!ok) return set_error("attention: tensor map encode failed");
   const float scale = 1.f / sqrtf(static_cast<float>(D)), scale_log2 = scale * kLog2e;
   if (bwd_warpgroups() == 2)
-    return bwd_launch<D, 2>(m128, m64, d64, d128, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
-  return bwd_launch<D, 4>(m128, m64, d64, d128, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
+    return bwd_launch<D, 2>(qkv, dout, m128, m64, d64, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
+  return bwd_launch<D, 4>(qkv, dout, m128, m64, d64, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
 }
 
 int g_mode = -1;
