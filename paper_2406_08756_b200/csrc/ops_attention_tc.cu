@@ -41,6 +41,7 @@ namespace lynx {
 namespace gemm {
 bool make_map(CUtensorMap* m, const void* base, long long inner, long long outer, long long ld, int box_inner,
               int box_outer);
+int num_sms();
 }
 namespace attn_tc {
 
@@ -614,30 +615,257 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ============================================================== forward, 64-key blocks, P apart from S
+// The two-tile kernel's per-tile chain is serial: P_t(j) overwrites S_t(j) in TMEM, so S_t(j+1) can only
+// be issued after PV_t(j) has read P_t(j), and each tile alternates ~2200 cycles of softmax with ~1100
+// of its own MMAs (a clock64 trace: 3600-cycle period per 128 keys for 2048 cycles of tensor work).
+// Here each tile keeps a separate P region: S_t (64 columns, one 64-key block), P_t (32 packed
+// columns) and O_t (D columns) fit twice into 512 columns. A softmax warp releases S_t as soon as its
+// tcgen05.ld completed, so S_t(j+1) runs while it computes P_t(j); every tile has its own MMA issuer
+// thread (warps 1 and 3; tcgen05.commit tracks the issuing thread's MMAs), so neither tile's MMAs wait
+// behind the other's. K / V blocks of 64 rows, 4-stage ring released by both issuers.
+// Online softmax per 64-key block with the same lazy rescale rule as attn_fwd_tc_kernel.
+template <int D>
+struct Fwd3L {
+  static constexpr int kAtoms = (D + 63) / 64;
+  static constexpr int kQT = 128 * kAtoms * 64 * 2;  // Q tile, 128 rows
+  static constexpr int kBT = 64 * kAtoms * 64 * 2;   // K or V block, 64 rows
+  static constexpr int kStages = D <= 64 ? 8 : 4;
+  static constexpr int kQ = 0, kK = 2 * kQT, kV = kK + kStages * kBT, kBar = kV + kStages * kBT;
+  static constexpr int kBytes = kBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per CTA");
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd3_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                        __nv_bfloat16* __restrict__ out, float* __restrict__ lse, int S, int H, float scale_log2) {
+  using L = Fwd3L<D>;
+  constexpr int kA = L::kAtoms, NS = L::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = kv_full + NS, *s_full = kv_empty + NS,
+           *s_free = s_full + 2, *p_full = s_free + 2, *pv_done = p_full + 2;  // s / p / pv: one per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  const int pair = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n_qt = S / 128;
+  const bool has1 = 2 * pair + 1 < n_qt;
+  // 64-key blocks per tile: query tile qb attends blocks 0 .. 2 qb + 1
+  const int n0 = 4 * pair + 2, n1 = has1 ? 4 * pair + 4 : 0, n = has1 ? n1 : n0;
+  const int HD = H * D, row0 = b * S;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, has1 ? 2 : 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(s_free + i, 128);
+      mbar_init(p_full + i, 128);
+      mbar_init(pv_done + i, 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  // TMEM: S_t at 64 t, P_t at 128 + 32 t, O_t at 256 + 128 t.
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (elect_one()) {
+      mbar_arrive_expect_tx(q_full, (has1 ? 2 : 1) * L::kQT);
+      for (int t = 0; t < (has1 ? 2 : 1); ++t)
+        for (int a = 0; a < kA; ++a)
+          tma_load_2d(&map_q, q_full, smem + L::kQ + t * L::kQT + a * 16384, h * D + 64 * a,
+                      row0 + (2 * pair + t) * 128, kEvictFirst);
+      for (int j = 0; j < n; ++j) {
+        const int st = j % NS;
+        if (j >= NS) mbar_wait(kv_empty + st, ((j / NS) - 1) & 1);
+        mbar_arrive_expect_tx(kv_full + st, 2 * L::kBT);
+        for (int a = 0; a < kA; ++a) {
+          tma_load_2d(&map_kv, kv_full + st, smem + L::kK + st * L::kBT + a * 8192, HD + h * D + 64 * a,
+                      row0 + j * 64, kEvictLast);
+          tma_load_2d(&map_kv, kv_full + st, smem + L::kV + st * L::kBT + a * 8192, 2 * HD + h * D + 64 * a,
+                      row0 + j * 64, kEvictLast);
+        }
+      }
+    }
+  } else if (warp == 1 || warp == 3) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    const int t = warp == 3;
+    const int nt = t ? n1 : n0;
+    if (nt > 0 && elect_one()) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, 64, false, false);
+      constexpr uint32_t idO = umma_idesc_bf16(128, D, false, true);
+      const uint32_t sQ = smem_u32(smem + L::kQ + t * L::kQT), sK = smem_u32(smem + L::kK),
+                     sV = smem_u32(smem + L::kV);
+      const uint32_t s_tm = tmem + 64 * t, p_tm = tmem + 128 + 32 * t, o_tm = tmem + 256 + 128 * t;
+      auto issue_pv = [&](int j) {  // O_t += P_t(j) V_j
+        const int st = j % NS;
+        mbar_wait(p_full + t, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_f16_ts(o_tm, p_tm + kk * 8, mnmaj(sV + st * L::kBT, kk, 8192), idO, (j | kk) != 0);
+        umma_commit(pv_done + t);
+        umma_commit(kv_empty + st);
+      };
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < nt; ++j) {
+        const int st = j % NS;
+        mbar_wait(kv_full + st, (j / NS) & 1);
+        if (j > 0) mbar_wait(s_free + t, (j - 1) & 1);
+        ATRACE(t ? 4 : 0, j);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_f16(s_tm, kmaj(sQ, kk, 16384), kmaj(sK + st * L::kBT, kk, 8192), idS, kk > 0);
+        umma_commit(s_full + t);
+        if (j > 0) issue_pv(j - 1);
+        if (j > 0) ATRACE(t ? 5 : 1, j - 1);
+      }
+      issue_pv(nt - 1);
+    }
+  } else if (warp == 2) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    const int t = (warp - 4) / 4;
+    if (t == 0 || has1) {
+      const int qb = 2 * pair + t, nt = t ? n1 : n0;
+      const int r = (warp % 4) * 32 + lane;
+      const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
+      const uint32_t s_col = tmem + lanes + 64 * t, p_col = tmem + lanes + 128 + 32 * t,
+                     o_col = tmem + lanes + 256 + 128 * t;
+      const int q = qb * 128 + r;
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < nt; ++j) {
+        mbar_wait(s_full + t, j & 1);
+        if (warp % 4 == 0 && lane == 0) ATRACE(t ? 6 : 2, j);
+        tc_fence_after();
+        float x[64];
+        tmem_ld32(s_col, reinterpret_cast<uint32_t*>(x));
+        tmem_ld32(s_col + 32, reinterpret_cast<uint32_t*>(x + 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(s_free + t);  // S_t(j + 1) may overwrite the block now
+        if (j >= 2 * qb) {  // the two blocks that meet the diagonal (warp-uniform branch)
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (j * 64 + i > q) x[i] = -INFINITY;
+        }
+        float mv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mv[i] = x[i];
+#pragma unroll
+        for (int i = 8; i < 64; ++i) mv[i & 7] = fmaxf(mv[i & 7], x[i]);
+        const float mt =
+            fmaxf(fmaxf(fmaxf(mv[0], mv[1]), fmaxf(mv[2], mv[3])), fmaxf(fmaxf(mv[4], mv[5]), fmaxf(mv[6], mv[7])));
+        const float m_new = fmaxf(m_run, mt * scale_log2);
+        const bool need = __any_sync(0xffffffffu, m_new > m_run + kRescale);
+        float corr = 1.f;
+        if (need) {
+          corr = exp2f(m_run - m_new);
+          m_run = m_new;
+        }
+        float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          x[i] = ex2(fmaf(x[i], scale_log2, -m_run));
+          rv[i & 7] += x[i];
+        }
+        const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
+        l_run = l_run * corr + rs;
+        uint32_t packed[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) packed[i] = pack_bf16x2(x[2 * i], x[2 * i + 1]);
+        if (j > 0) {  // PV_t(j-1) read P_t(j-1) and wrote O_t
+          mbar_wait(pv_done + t, (j - 1) & 1);
+          tc_fence_after();
+          if (need) {
+            tmem_cols(o_col, 0, D, [&](int c, uint32_t* o, int cnt) {
+              for (int i = 0; i < cnt; ++i) o[i] = __float_as_uint(u2f(o[i]) * corr);
+              if (cnt == 32)
+                tmem_st32(o_col + c, o);
+              else
+                tmem_st16(o_col + c, o);
+            });
+          }
+        }
+        tmem_st32(p_col, packed);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(p_full + t);
+        if (warp % 4 == 0 && lane == 0) ATRACE(t ? 7 : 3, j);
+      }
+      mbar_wait(pv_done + t, (nt - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l_run;
+      BF8* orow = reinterpret_cast<BF8*>(out + static_cast<long long>(row0 + q) * HD + h * D);
+      tmem_cols(o_col, 0, D, [&](int c, const uint32_t* o, int cnt) {
+        float f[32];
+        for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * inv;
+        for (int i = 0; i < cnt / 8; ++i) orow[c / 8 + i] = f_to_bf8(f + 8 * i);
+      });
+      lse[(static_cast<long long>(b) * H + h) * S + q] = (m_run + log2f(l_run)) / kLog2e;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  ATRACE_DUMP(n);
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
 // ============================================================== backward dK / dV
+// Persistent, like the dQ kernel: grid = min(work items, SMs), work item w = (key tile, head, batch) in
+// head-major, longest-first order. K / V of the next item are loaded as soon as the current item's
+// last S^T / dP^T MMAs (their only readers) completed, ~2 tile periods before the item ends; the Q / dO
+// ring runs on across items. dV / dK leave through a 32-KB shared-memory staging tile with coalesced
+// global stores. As one CTA per item, each item paid ~5500 cycles before its first S^T and ~3000 of
+// row-per-thread stores after its last tile, against ~1500 cycles per tile.
 template <int D>
 struct DkvL {
-  // Q / dO / lse / D ring. A stage is held from S^T(i) to dV / dK(i), about two tile periods, and its
-  // reload takes ~1000 cycles from L2: with 3 stages the load of tile i + 3 could only start when
-  // dV / dK(i) completed and S^T(i + 3) waited for it (a clock64 trace: 1460-cycle tile period for
-  // 1024 cycles of MMA, the row warps idle 500 cycles per tile). 4 stages fill 195 KB at D = 128.
-  static constexpr int kStages = D <= 64 ? 6 : 4;
+  // Q / dO / lse / D ring: a stage is held from S^T(i) to dV / dK(i), about two tile periods (4 stages
+  // were measured no faster than 3: the tile period is set by the smem-bound S^T / dP^T MMAs).
+  static constexpr int kStages = D <= 64 ? 6 : 3;
   static constexpr int kAtoms = (D + 63) / 64;
   static constexpr int kKV = 128 * kAtoms * 64 * 2;  // K or V tile: ceil(D/64) atoms of 16 KB (128 rows)
   static constexpr int kQT = 64 * kAtoms * 64 * 2;   // Q or dO tile: ceil(D/64) atoms of 8 KB (64 rows)
   static constexpr int kK = 0, kV = kKV, kQ = 2 * kKV, kDO = kQ + kStages * kQT;
   static constexpr int kVec = kDO + kStages * kQT;  // lse2[kStages][64], dvec[kStages][64]; P^T / dS^T live in TMEM
-  static constexpr int kBar = kVec + 2 * kStages * 256;
+  static constexpr int kOut = kVec + 2 * kStages * 256;  // epilogue staging: 128 rows x 256 B (XOR-swizzled)
+  static constexpr int kBar = kOut + 128 * 256;
   static constexpr int kBytes = kBar + 256 + 1024;
   static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
+
+struct DkvItem {
+  int kb, h, b, n;
+};
+LYNX_DEV DkvItem dkv_item(int w, int nk, int S, int H) {
+  const int hb = w / nk;
+  DkvItem it;
+  it.kb = w % nk;
+  it.h = hb % H;
+  it.b = hb / H;
+  it.n = S / 64 - 2 * it.kb;
+  return it;
+}
 
 template <int D, int kWG>  // kWG row warpgroups (2 or 4), each owning 64 / kWG query columns of a tile
 __global__ void __launch_bounds__(128 + 128 * kWG, 1)
     attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
                         const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
-                        const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
-                        float scale_log2) {
+                        const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, int B,
+                        float scale, float scale_log2) {
   using L = DkvL<D>;
   constexpr int kA = L::kAtoms, NS = L::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -646,16 +874,15 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
   // pd_full is double-buffered by tile parity (see the forward kernel's p_full: one barrier let a
   // row warp's arrival for tile i+1 complete tile i's phase before a slower warp had written its
   // P^T / dS^T rows, and dV / dK of those 32 keys picked up stale values, ~3 % of runs).
-  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = q_full + NS, *s_full = q_empty + NS, *pd_full = s_full + 2,
-           *mma_done = pd_full + 2, *fin = mma_done + 1;
+  uint64_t *kv_full = bar, *kv_free = bar + 1, *q_full = bar + 2, *q_empty = q_full + NS, *s_full = q_empty + NS,
+           *pd_full = s_full + 2, *fin = pd_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
-  const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int i0 = 2 * kb, n = S / 64 - i0, HD = H * D, row0 = b * S;
-  const long long vec0 = (static_cast<long long>(b) * H + h) * S;
+  const int nk = S / 128, HD = H * D, n_items = nk * H * B;
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
+    mbar_init(kv_free, 1);
     for (int i = 0; i < NS; ++i) {
       mbar_init(q_full + i, 1);
       mbar_init(q_empty + i, 1);
@@ -664,7 +891,6 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
       mbar_init(s_full + i, 1);
       mbar_init(pd_full + i, 128 * kWG);
     }
-    mbar_init(mma_done, 1);
     mbar_init(fin, 1);
     fence_barrier_init();
   }
@@ -677,25 +903,33 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      mbar_arrive_expect_tx(kv_full, 2 * L::kKV);
-      for (int a = 0; a < kA; ++a) {
-        tma_load_2d(&map_kv, kv_full, smem + L::kK + a * 16384, HD + h * D + 64 * a, row0 + kb * 128, kEvictFirst);
-        tma_load_2d(&map_kv, kv_full, smem + L::kV + a * 16384, 2 * HD + h * D + 64 * a, row0 + kb * 128,
-                    kEvictFirst);
-      }
-      for (int i = 0; i < n; ++i) {
-        const int st = i % NS, q0 = (i0 + i) * 64;
-        if (i >= NS) mbar_wait(q_empty + st, ((i / NS) - 1) & 1);
-        ATRACE(0, i);
-        mbar_arrive_expect_tx(q_full + st, 2 * L::kQT + 512);
+      int g = 0, k = 0;  // Q / dO tile counter over this CTA's items, item counter
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+        const DkvItem it = dkv_item(w, nk, S, H);
+        const int row0 = it.b * S, i0 = 2 * it.kb;
+        const long long vec0 = (static_cast<long long>(it.b) * H + it.h) * S;
+        if (k > 0) mbar_wait(kv_free, (k - 1) & 1);  // the previous item's last S^T / dP^T completed
+        mbar_arrive_expect_tx(kv_full, 2 * L::kKV);
         for (int a = 0; a < kA; ++a) {
-          tma_load_2d(&map_q, q_full + st, smem + L::kQ + st * L::kQT + a * 8192, h * D + 64 * a, row0 + q0,
-                      kEvictLast);
-          tma_load_2d(&map_do, q_full + st, smem + L::kDO + st * L::kQT + a * 8192, h * D + 64 * a, row0 + q0,
-                      kEvictLast);
+          tma_load_2d(&map_kv, kv_full, smem + L::kK + a * 16384, HD + it.h * D + 64 * a, row0 + it.kb * 128,
+                      kEvictFirst);
+          tma_load_2d(&map_kv, kv_full, smem + L::kV + a * 16384, 2 * HD + it.h * D + 64 * a, row0 + it.kb * 128,
+                      kEvictFirst);
         }
-        bulk_load(smem + L::kVec + st * 256, lse2 + vec0 + q0, 256, q_full + st);
-        bulk_load(smem + L::kVec + (NS + st) * 256, dvec + vec0 + q0, 256, q_full + st);
+        for (int i = 0; i < it.n; ++i, ++g) {
+          const int st = g % NS, q0 = (i0 + i) * 64;
+          if (g >= NS) mbar_wait(q_empty + st, ((g / NS) - 1) & 1);
+          ATRACE(0, k == 0 ? i : 64);
+          mbar_arrive_expect_tx(q_full + st, 2 * L::kQT + 512);
+          for (int a = 0; a < kA; ++a) {
+            tma_load_2d(&map_q, q_full + st, smem + L::kQ + st * L::kQT + a * 8192, it.h * D + 64 * a, row0 + q0,
+                        kEvictLast);
+            tma_load_2d(&map_do, q_full + st, smem + L::kDO + st * L::kQT + a * 8192, it.h * D + 64 * a,
+                        row0 + q0, kEvictLast);
+          }
+          bulk_load(smem + L::kVec + st * 256, lse2 + vec0 + q0, 256, q_full + st);
+          bulk_load(smem + L::kVec + (NS + st) * 256, dvec + vec0 + q0, 256, q_full + st);
+        }
       }
     }
   } else if (warp == 1) {
@@ -704,10 +938,9 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
       constexpr uint32_t idG = umma_idesc_bf16(128, D, false, true);
       const uint32_t sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV), sQ = smem_u32(smem + L::kQ),
                      sDO = smem_u32(smem + L::kDO);
-      auto issue_s = [&](int i) {
-        const int st = i % NS, tb = i & 1;
-        mbar_wait(q_full + st, (i / NS) & 1);
-        ATRACE(1, i);
+      auto issue_s = [&](int g) {  // S^T / dP^T of the CTA's g-th tile
+        const int st = g % NS, tb = g & 1;
+        mbar_wait(q_full + st, (g / NS) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -716,146 +949,220 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
         }
         umma_commit(s_full + tb);
       };
-      mbar_wait(kv_full, 0);
-      issue_s(0);
-      if (n > 1) issue_s(1);
-      for (int i = 0; i < n; ++i) {
-        const int st = i % NS;
-        mbar_wait(pd_full + (i & 1), (i >> 1) & 1);
-        ATRACE(2, i);
-        tc_fence_after();
-        const uint32_t tb = static_cast<uint32_t>(i & 1);
+      int g = 0, k = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+        const int n = dkv_item(w, nk, S, H).n;
+        mbar_wait(kv_full, k & 1);
+        ATRACE(10, k);
+        issue_s(g);
+        issue_s(g + 1);
+        if (n == 2) umma_commit(kv_free);
+        for (int i = 0; i < n; ++i) {
+          const int gg = g + i, st = gg % NS;
+          mbar_wait(pd_full + (gg & 1), (gg >> 1) & 1);
+          ATRACE(2, k == 0 ? i : 64);
+          tc_fence_after();
+          const uint32_t tb = static_cast<uint32_t>(gg & 1);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {  // A = P^T / dS^T, packed bf16 over S^T / dP^T in TMEM buffer tb
-          const uint32_t ac = tb * 64 + packed_col<kWG>(kk);
-          umma_f16_ts(tmem + 256, tmem + ac, mnmaj(sDO + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
-          umma_f16_ts(tmem + 384, tmem + 128 + ac, mnmaj(sQ + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
+          for (int kk = 0; kk < 4; ++kk) {  // A = P^T / dS^T, packed bf16 over S^T / dP^T in TMEM buffer tb
+            const uint32_t ac = tb * 64 + packed_col<kWG>(kk);
+            umma_f16_ts(tmem + 256, tmem + ac, mnmaj(sDO + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
+            umma_f16_ts(tmem + 384, tmem + 128 + ac, mnmaj(sQ + st * L::kQT, kk, 8192), idG, (i | kk) != 0);
+          }
+          umma_commit(q_empty + st);
+          if (i + 2 < n) {
+            issue_s(gg + 2);
+            if (i + 3 == n) umma_commit(kv_free);  // K / V have no reader left in this item
+          }
         }
-        umma_commit(mma_done);
-        umma_commit(q_empty + st);
-        if (i + 2 < n) issue_s(i + 2);
+        umma_commit(fin);
+        ATRACE(12, k);
+        g += n;
       }
-      umma_commit(fin);
     }
   } else if (warp >= 4) {
     // kWG row warpgroups split each 64-query tile's columns (warpgroup wg: columns wg * CW ...
-    // + CW) on the same key rows / TMEM lanes. The work is elementwise, so they never exchange data;
-    // more warps per SM sub-partition hide the TMEM-load / MUFU latencies of the per-tile row work
-    // (a clock64 trace showed ~1500 cycles of it per tile against ~1000 of MMA with two warpgroups).
+    // + CW) on the same key rows / TMEM lanes. The work is elementwise, so they never exchange data.
     constexpr int CW = 64 / kWG;
     const int wg = (warp - 4) / 4;
-    const int k = (warp % 4) * 32 + lane;  // key row of the tile
-    const int key = kb * 128 + k;
+    const int kr = (warp % 4) * 32 + lane;  // key row of the tile
     const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
-    for (int i = 0; i < n; ++i) {
-      const int st = i % NS, tb = i & 1, q0 = (i0 + i) * 64;
-      mbar_wait(q_full + st, (i / NS) & 1);
-      mbar_wait(s_full + tb, (i >> 1) & 1);
-      if (threadIdx.x == 128) ATRACE(3, i);
-      tc_fence_after();
-      const float* sl = reinterpret_cast<const float*>(smem + L::kVec + st * 256) + wg * CW;
-      const float* sd = reinterpret_cast<const float*>(smem + L::kVec + (NS + st) * 256) + wg * CW;
-      {
-        uint32_t sr[CW], dp[CW];
-        tmem_ld_cols<CW>(tmem + lanes + tb * 64 + wg * CW, sr);
-        tmem_ld_cols<CW>(tmem + lanes + 128 + tb * 64 + wg * CW, dp);
-        tmem_ld_wait();
-        float p[CW], g[CW], lv[CW], dv[CW];
+    constexpr int kChunks = D / 8, kIter = (128 * kChunks + 128 * kWG - 1) / (128 * kWG);
+    uint8_t* stg = smem + L::kOut;
+    // dV (first half of the warpgroups) then dK (second half, scaled): TMEM -> bf16 rows in the staging
+    // tile (row r's 16-B chunk c at r * 256 + (c ^ (r % 16)) * 16) -> coalesced global stores
+    auto epilogue = [&](const DkvItem& it) {
+      constexpr int kPer = kWG / 2, kSplit = (D / 16 + kPer - 1) / kPer * 16;
+      const int part = wg % kPer;
+      const int c_lo = part * kSplit < D ? part * kSplit : D, c_hi = (part + 1) * kSplit < D ? (part + 1) * kSplit : D;
+      for (int pass = 0; pass < 2; ++pass) {  // 0: dV, 1: dK
+        if ((wg >= kPer) == (pass == 1)) {
+          const float mul = pass ? scale : 1.f;
+          tmem_cols(tmem + lanes + (pass ? 384 : 256), c_lo, c_hi, [&](int c, const uint32_t* o, int cnt) {
+            float f[32];
+            for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * mul;
+            for (int i = 0; i < cnt / 8; ++i)
+              *reinterpret_cast<BF8*>(stg + kr * 256 + (((c / 8 + i) ^ (kr & 15)) * 16)) = f_to_bf8(f + 8 * i);
+          });
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(128 * kWG) : "memory");
+        BF8* dst = reinterpret_cast<BF8*>(dqkv + (static_cast<long long>(it.b) * S + it.kb * 128) * 3 * HD +
+                                          (pass ? HD : 2 * HD) + it.h * D);
+        BF8 v[kIter];
 #pragma unroll
-        for (int c = 0; c < CW / 4; ++c) {
-          const float4 a = lds128(sl + 4 * c), d4 = lds128(sd + 4 * c);
-          lv[4 * c] = a.x, lv[4 * c + 1] = a.y, lv[4 * c + 2] = a.z, lv[4 * c + 3] = a.w;
-          dv[4 * c] = d4.x, dv[4 * c + 1] = d4.y, dv[4 * c + 2] = d4.z, dv[4 * c + 3] = d4.w;
+        for (int x = 0; x < kIter; ++x) {
+          const int i = static_cast<int>(threadIdx.x) - 128 + x * 128 * kWG, rr = i / kChunks, cc = i % kChunks;
+          if (i < 128 * kChunks) v[x] = *reinterpret_cast<const BF8*>(stg + rr * 256 + ((cc ^ (rr & 15)) * 16));
         }
 #pragma unroll
-        for (int c = 0; c < CW; ++c) p[c] = ex2(fmaf(u2f(sr[c]), scale_log2, -lv[c]));
-        if (i < 2) {  // the two 64-query tiles that meet the diagonal of this 128-key tile
-#pragma unroll
-          for (int c = 0; c < CW; ++c)
-            if (key > q0 + wg * CW + c) p[c] = 0.f;
+        for (int x = 0; x < kIter; ++x) {
+          const int i = static_cast<int>(threadIdx.x) - 128 + x * 128 * kWG, rr = i / kChunks, cc = i % kChunks;
+          if (i < 128 * kChunks) dst[static_cast<long long>(rr) * (3 * HD / 8) + cc] = v[x];
         }
-#pragma unroll
-        for (int c = 0; c < CW; ++c) g[c] = p[c] * (u2f(dp[c]) - dv[c]);
-        uint32_t pp[CW / 2], gp[CW / 2];
-#pragma unroll
-        for (int c = 0; c < CW / 2; ++c) {
-          pp[c] = pack_bf16x2(p[2 * c], p[2 * c + 1]);
-          gp[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
-        }
-        if (threadIdx.x == 128) ATRACE(4, i);
-        // P^T(i) / dS^T(i) overwrite S^T(i) / dP^T(i) in place, each warpgroup inside the columns it
-        // read itself (packed_col): the others read the same TMEM lanes without any ordering against
-        // this store (packing outside its own range once made warps read P^T instead of S^T, ~0.1 %
-        // of runs). dV / dK(i-2), the last readers of buffer tb, completed before S^T(i).
-        tmem_st_cols<CW / 2>(tmem + lanes + tb * 64 + wg * CW, pp);
-        tmem_st_cols<CW / 2>(tmem + lanes + 128 + tb * 64 + wg * CW, gp);
-        tmem_st_wait();
+        asm volatile("bar.sync 1, %0;" ::"r"(128 * kWG) : "memory");  // the staging tile is read: reusable
       }
-      tc_fence_before();
-      mbar_arrive(pd_full + tb);
-      if (threadIdx.x == 128) ATRACE(6, i);
+    };
+    int g = 0, k = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+      const DkvItem it = dkv_item(w, nk, S, H);
+      const int key = it.kb * 128 + kr, i0 = 2 * it.kb;
+      if (threadIdx.x == 128) ATRACE(8, k);
+      for (int i = 0; i < it.n; ++i) {
+        const int gg = g + i, st = gg % NS, tb = gg & 1, q0 = (i0 + i) * 64;
+        mbar_wait(q_full + st, (gg / NS) & 1);
+        mbar_wait(s_full + tb, (gg >> 1) & 1);
+        if (threadIdx.x == 128) ATRACE(3, k == 0 ? i : 64);
+        if (threadIdx.x == 128 && i == 0) ATRACE(13, k);
+        tc_fence_after();
+        const float* sl = reinterpret_cast<const float*>(smem + L::kVec + st * 256) + wg * CW;
+        const float* sd = reinterpret_cast<const float*>(smem + L::kVec + (NS + st) * 256) + wg * CW;
+        {
+          uint32_t sr[CW], dp[CW];
+          tmem_ld_cols<CW>(tmem + lanes + tb * 64 + wg * CW, sr);
+          tmem_ld_cols<CW>(tmem + lanes + 128 + tb * 64 + wg * CW, dp);
+          tmem_ld_wait();
+          float p[CW], gd[CW], lv[CW], dv[CW];
+#pragma unroll
+          for (int c = 0; c < CW / 4; ++c) {
+            const float4 a = lds128(sl + 4 * c), d4 = lds128(sd + 4 * c);
+            lv[4 * c] = a.x, lv[4 * c + 1] = a.y, lv[4 * c + 2] = a.z, lv[4 * c + 3] = a.w;
+            dv[4 * c] = d4.x, dv[4 * c + 1] = d4.y, dv[4 * c + 2] = d4.z, dv[4 * c + 3] = d4.w;
+          }
+#pragma unroll
+          for (int c = 0; c < CW; ++c) p[c] = ex2(fmaf(u2f(sr[c]), scale_log2, -lv[c]));
+          if (i < 2) {  // the two 64-query tiles that meet the diagonal of this 128-key tile
+#pragma unroll
+            for (int c = 0; c < CW; ++c)
+              if (key > q0 + wg * CW + c) p[c] = 0.f;
+          }
+#pragma unroll
+          for (int c = 0; c < CW; ++c) gd[c] = p[c] * (u2f(dp[c]) - dv[c]);
+          uint32_t pp[CW / 2], gp[CW / 2];
+#pragma unroll
+          for (int c = 0; c < CW / 2; ++c) {
+            pp[c] = pack_bf16x2(p[2 * c], p[2 * c + 1]);
+            gp[c] = pack_bf16x2(gd[2 * c], gd[2 * c + 1]);
+          }
+          if (threadIdx.x == 128) ATRACE(4, k == 0 ? i : 64);
+          // P^T(i) / dS^T(i) overwrite S^T(i) / dP^T(i) in place, each warpgroup inside the columns it
+          // read itself (packed_col): the others read the same TMEM lanes without any ordering against
+          // this store (packing outside its own range once made warps read P^T instead of S^T, ~0.1 %
+          // of runs). dV / dK(i-2), the last readers of buffer tb, completed before S^T(i).
+          tmem_st_cols<CW / 2>(tmem + lanes + tb * 64 + wg * CW, pp);
+          tmem_st_cols<CW / 2>(tmem + lanes + 128 + tb * 64 + wg * CW, gp);
+          tmem_st_wait();
+        }
+        tc_fence_before();
+        mbar_arrive(pd_full + tb);
+        if (threadIdx.x == 128) ATRACE(6, k == 0 ? i : 64);
+      }
+      g += it.n;
+      if (threadIdx.x == 128) ATRACE(7, k);
+      // dV / dK complete; the next item's first dV / dK MMA (accumulate = 0) waits for this thread's first
+      // hand-off of that item, i.e. after the epilogue
+      mbar_wait(fin, k & 1);
+      tc_fence_after();
+      if (threadIdx.x == 128) ATRACE(9, k);
+      epilogue(it);
+      if (threadIdx.x == 128) ATRACE(11, k);
     }
-    mbar_wait(fin, 0);
-    tc_fence_after();
-    // epilogue: the first half of the warpgroups writes dV, the second dK (scaled), each warpgroup a
-    // 16-aligned share of the D columns
-    constexpr int kPer = kWG / 2, kSplit = (D / 16 + kPer - 1) / kPer * 16;
-    const bool is_dk = wg >= kPer;
-    const int part = wg % kPer;
-    const long long grow = static_cast<long long>(row0 + key) * 3 * HD;
-    BF8* dst = reinterpret_cast<BF8*>(dqkv + grow + (is_dk ? HD : 2 * HD) + h * D);
-    const float mul = is_dk ? scale : 1.f;
-    const int c_lo = part * kSplit < D ? part * kSplit : D, c_hi = (part + 1) * kSplit < D ? (part + 1) * kSplit : D;
-    tmem_cols(tmem + lanes + (is_dk ? 384 : 256), c_lo, c_hi, [&](int c, const uint32_t* o, int cnt) {
-      float f[32];
-      for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * mul;
-      for (int i = 0; i < cnt / 8; ++i) dst[c / 8 + i] = f_to_bf8(f + 8 * i);
-    });
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  ATRACE_DUMP(n);
+  ATRACE_DUMP(64);
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
 // ============================================================== backward dQ
-// Q and dO are the same for every key tile of a CTA, so they sit in TMEM as the A operands of
-// S = Q K^T and dP = dO V^T (packed bf16 pairs, one row per lane, written once by the row warps
-// from global memory). An SS MMA of 128 x 64 x 16 reads 6 KB of shared memory per 32-cycle
-// instruction, 1.5x the 128 B/clk the SM's shared memory delivers, so with Q / dO in shared memory
-// S and dP ran smem-bound at ~48 cycles per instruction; from TMEM only the 2-KB K / V slice is read.
+// Q and dO are the same for every key tile of a work item, so they sit in TMEM as the A operands of
+// S = Q K^T and dP = dO V^T (packed bf16 pairs, one row per lane). An SS MMA of 128 x 64 x 16 reads
+// 6 KB of shared memory per 32-cycle instruction, 1.5x the 128 B/clk the SM's shared memory delivers,
+// so with Q / dO in shared memory S and dP ran smem-bound at ~48 cycles per instruction; from TMEM only
+// the 2-KB K / V slice is read (tile period 1232 -> 975 cycles in a clock64 trace).
+//
+// Persistent: grid = min(work items, SMs); each CTA walks the work items (query tile, head, batch)
+// blockIdx.x, + gridDim.x, ... in longest-first order. The producer TMA-loads the next item's Q / dO
+// into a staging buffer while the current item runs and keeps the K / V ring going across items; the
+// MMA thread moves Q / dO into TMEM with tcgen05.cp (in issue order with its MMAs, so after the
+// previous item's last S / dP). As one CTA per item, each item paid ~7000 cycles of prologue (TMEM
+// allocation, barriers, Q / dO and K / V loads) against ~975 cycles per key tile.
 template <int D>
 struct DqL {
   static constexpr int kAtoms = (D + 63) / 64;
+  static constexpr int kQT = 128 * kAtoms * 64 * 2;  // Q or dO tile (128 rows): the staging buffer
   static constexpr int kKT = 64 * kAtoms * 64 * 2;   // K or V tile (64 rows)
-  static constexpr int kStages = D <= 64 ? 8 : 6;    // K / V ring (see DkvL::kStages)
-  static constexpr int kK = 0, kV = kStages * kKT;
-  static constexpr int kBar = kV + kStages * kKT;  // Q, dO and dS live in TMEM
+  static constexpr int kStages = D <= 64 ? 8 : 4;    // K / V ring (see DkvL::kStages)
+  static constexpr int kQ = 0, kDO = kQT, kK = 2 * kQT, kV = kK + kStages * kKT;
+  static constexpr int kOut = kV + kStages * kKT;  // dQ epilogue staging: 128 rows x 256 B (XOR-swizzled chunks)
+  static constexpr int kBar = kOut + 128 * 256;
   static constexpr int kBytes = kBar + 256 + 1024;
   static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
 
+struct DqItem {
+  int qb, h, b, n;
+};
+// Work item w: head (w / nq) and query tile nq - 1 - w % nq, so the CTAs that run at the same time
+// work on the same few heads and share their K / V tiles in L2 (qb-major order made every CTA stream
+// its own head's K / V from HBM: ~4.5 GB per call at the 7B shape). CTA c meets the query tiles
+// 15 - c % 16, 15 - (c + 148) % 16, ...: balanced over the ~55 items per CTA.
+LYNX_DEV DqItem dq_item(int w, int nq, int H, int B) {
+  const int hb = w / nq;
+  DqItem it;
+  it.qb = nq - 1 - w % nq;
+  it.h = hb % H;
+  it.b = hb / H;
+  it.n = 2 * (it.qb + 1);
+  return it;
+}
+
+// 128 rows x 32 bytes (16 bf16 of each row: one K step) from a K-major SW128 operand in shared memory
+// into 8 TMEM columns of lanes 0-127 — the packed layout an A-from-TMEM MMA reads.
+LYNX_DEV void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
+
 template <int D, int kWG>  // kWG row warpgroups (2 or 4), each owning 64 / kWG key columns of a tile
 __global__ void __launch_bounds__(128 + 128 * kWG, 1)
-    attn_dq_tc_kernel(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ dout,
-                      const __grid_constant__ CUtensorMap map_kv, const float* __restrict__ lse2,
-                      const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, float scale,
-                      float scale_log2) {
+    attn_dq_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                      const __grid_constant__ CUtensorMap map_do, const float* __restrict__ lse2,
+                      const float* __restrict__ dvec, __nv_bfloat16* __restrict__ dqkv, int S, int H, int B,
+                      float scale, float scale_log2) {
   using L = DqL<D>;
   constexpr int kA = L::kAtoms, NS = L::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t *a_full = bar, *kv_full = bar + 1, *kv_empty = kv_full + NS, *s_full = kv_empty + NS,
-           *ds_full = s_full + 2, *ds_free = ds_full + 2, *fin = ds_free + 2;
+  uint64_t *q_full = bar, *q_empty = bar + 1, *kv_full = bar + 2, *kv_empty = kv_full + NS, *s_full = kv_empty + NS,
+           *ds_full = s_full + 2, *fin = ds_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin + 1);
-  const int qb = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int n = 2 * (qb + 1), HD = H * D, row0 = b * S;
+  const int nq = S / 128, HD = H * D, n_items = nq * H * B;
 
   if (threadIdx.x == 0) {
-    mbar_init(a_full, 128 * kWG);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < NS; ++i) {
       mbar_init(kv_full + i, 1);
       mbar_init(kv_empty + i, 1);
@@ -863,7 +1170,6 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + i, 1);
       mbar_init(ds_full + i, 128 * kWG);
-      mbar_init(ds_free + i, 1);
     }
     mbar_init(fin, 1);
     fence_barrier_init();
@@ -877,16 +1183,36 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      for (int j = 0; j < n; ++j) {
-        const int st = j % NS;
-        if (j >= NS) mbar_wait(kv_empty + st, ((j / NS) - 1) & 1);
-        ATRACE(0, j);
-        mbar_arrive_expect_tx(kv_full + st, 2 * L::kKT);
+      auto load_q = [&](int w, int k) {  // Q / dO of this CTA's k-th item into the staging buffer
+        const DqItem it = dq_item(w, nq, H, B);
+        if (k > 0) mbar_wait(q_empty, (k - 1) & 1);  // item k - 1's Q / dO are in TMEM
+        mbar_arrive_expect_tx(q_full, 2 * L::kQT);
         for (int a = 0; a < kA; ++a) {
-          tma_load_2d(&map_kv, kv_full + st, smem + L::kK + st * L::kKT + a * 8192, HD + h * D + 64 * a,
-                      row0 + j * 64, kEvictLast);
-          tma_load_2d(&map_kv, kv_full + st, smem + L::kV + st * L::kKT + a * 8192, 2 * HD + h * D + 64 * a,
-                      row0 + j * 64, kEvictLast);
+          tma_load_2d(&map_q, q_full, smem + L::kQ + a * 16384, it.h * D + 64 * a, it.b * S + it.qb * 128,
+                      kEvictFirst);
+          tma_load_2d(&map_do, q_full, smem + L::kDO + a * 16384, it.h * D + 64 * a, it.b * S + it.qb * 128,
+                      kEvictFirst);
+        }
+      };
+      load_q(blockIdx.x, 0);
+      int g = 0, k = 0;  // K / V tile counter over this CTA's items, item counter
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+        const DqItem it = dq_item(w, nq, H, B);
+        const int row0 = it.b * S;
+        for (int j = 0; j < it.n; ++j, ++g) {
+          const int st = g % NS;
+          if (g >= NS) mbar_wait(kv_empty + st, ((g / NS) - 1) & 1);
+          ATRACE(0, w == static_cast<int>(blockIdx.x) ? j : 64);
+          mbar_arrive_expect_tx(kv_full + st, 2 * L::kKT);
+          for (int a = 0; a < kA; ++a) {
+            tma_load_2d(&map_kv, kv_full + st, smem + L::kK + st * L::kKT + a * 8192, HD + it.h * D + 64 * a,
+                        row0 + j * 64, kEvictLast);
+            tma_load_2d(&map_kv, kv_full + st, smem + L::kV + st * L::kKT + a * 8192, 2 * HD + it.h * D + 64 * a,
+                        row0 + j * 64, kEvictLast);
+          }
+          // the next item's Q / dO once this item's copy into TMEM is done (a few tiles in)
+          if (j == (it.n < 4 ? it.n - 1 : 3) && w + static_cast<int>(gridDim.x) < n_items)
+            load_q(w + gridDim.x, k + 1);
         }
       }
     }
@@ -894,11 +1220,11 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
     if (elect_one()) {
       constexpr uint32_t idS = umma_idesc_bf16(128, 64, false, false);
       constexpr uint32_t idG = umma_idesc_bf16(128, D, false, true);
-      const uint32_t sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV);
-      auto issue_s = [&](int j) {
-        const int st = j % NS, tb = j & 1;
-        mbar_wait(kv_full + st, (j / NS) & 1);
-        ATRACE(1, j);
+      const uint32_t sQ = smem_u32(smem + L::kQ), sDO = smem_u32(smem + L::kDO), sK = smem_u32(smem + L::kK),
+                     sV = smem_u32(smem + L::kV);
+      auto issue_s = [&](int g) {  // S / dP of the CTA's g-th tile
+        const int st = g % NS, tb = g & 1;
+        mbar_wait(kv_full + st, (g / NS) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -907,105 +1233,143 @@ __global__ void __launch_bounds__(128 + 128 * kWG, 1)
         }
         umma_commit(s_full + tb);
       };
-      mbar_wait(a_full, 0);
-      tc_fence_after();
-      issue_s(0);
-      issue_s(1);
-      for (int j = 0; j < n; ++j) {
-        const int st = j % NS, tb = j & 1;
-        mbar_wait(ds_full + tb, (j >> 1) & 1);
-        ATRACE(2, j);
+      int g = 0, k = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+        const int n = dq_item(w, nq, H, B).n;
+        mbar_wait(q_full, k & 1);
+        ATRACE(10, k);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // A = dS(j), packed bf16 over the S(j) columns of TMEM buffer tb
-          umma_f16_ts(tmem + 256, tmem + tb * 64 + packed_col<kWG>(kk), mnmaj(sK + st * L::kKT, kk, 8192),
-                      idG, (j | kk) != 0);
-        umma_commit(ds_free + tb);
-        umma_commit(kv_empty + st);
-        if (j + 2 < n) issue_s(j + 2);
+        for (int kk = 0; kk < D / 16; ++kk) {  // after the previous item's MMAs (tcgen05 issue order)
+          tmem_cp_128x256b(tmem + 384 + kk * 8, kmaj(sQ, kk, 16384));
+          tmem_cp_128x256b(tmem + 448 + kk * 8, kmaj(sDO, kk, 16384));
+        }
+        umma_commit(q_empty);
+        issue_s(g);
+        issue_s(g + 1);
+        for (int j = 0; j < n; ++j) {
+          const int gg = g + j, st = gg % NS, tb = gg & 1;
+          mbar_wait(ds_full + tb, (gg >> 1) & 1);
+          ATRACE(2, k == 0 ? j : 64);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)  // A = dS(j), packed bf16 over the S(j) columns of TMEM buffer tb
+            umma_f16_ts(tmem + 256, tmem + tb * 64 + packed_col<kWG>(kk), mnmaj(sK + st * L::kKT, kk, 8192),
+                        idG, (j | kk) != 0);
+          umma_commit(kv_empty + st);
+          if (j + 2 < n) issue_s(gg + 2);
+        }
+        umma_commit(fin);
+        ATRACE(12, k);
+        g += n;
       }
-      umma_commit(fin);
     }
   } else if (warp >= 4) {
     // kWG row warpgroups split each 64-key tile's columns, as in dK/dV.
     constexpr int CW = 64 / kWG;
     const int wg = (warp - 4) / 4;
     const int r = (warp % 4) * 32 + lane;
-    const int q = qb * 128 + r;
     const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
-    {  // this thread's row of Q (even warpgroups) or dO (odd) into TMEM, 16-element granules split over
-       // the kWG / 2 warpgroups of each kind
-      constexpr int kG = D / 16, kParts = kWG / 2, kPer = (kG + kParts - 1) / kParts;
-      const bool is_do = wg & 1;
-      const int part = wg >> 1;
-      const uint4* src = reinterpret_cast<const uint4*>(
-          is_do ? dout + static_cast<long long>(row0 + q) * HD + h * D
-                : qkv + static_cast<long long>(row0 + q) * 3 * HD + h * D);
-      const uint32_t dst = tmem + lanes + (is_do ? 448 : 384);
+    // dQ of item w: TMEM -> scaled bf16 rows in a shared-memory staging tile (row r's 16-B chunk c at
+    // r * 256 + (c ^ (r % 16)) * 16: conflict-free row-per-thread stores) -> coalesced 16-B global stores,
+    // all loads of a thread issued before its stores. Written per thread straight from TMEM (one 128-B
+    // row piece per thread, 32 rows per warp instruction) the stores took ~3800 cycles per item.
+    constexpr int kChunks = D / 8, kIter = (128 * kChunks + 128 * kWG - 1) / (128 * kWG);
+    uint8_t* stg = smem + L::kOut;
+    auto epilogue = [&](int w, int k) {
+      const DqItem it = dq_item(w, nq, H, B);
+      constexpr int kSplit = (D / 16 + kWG - 1) / kWG * 16;  // each warpgroup stages its share of the D columns
+      const int c_lo = wg * kSplit < D ? wg * kSplit : D, c_hi = (wg + 1) * kSplit < D ? (wg + 1) * kSplit : D;
+      tmem_cols(tmem + lanes + 256, c_lo, c_hi, [&](int c, const uint32_t* o, int cnt) {
+        float f[32];
+        for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * scale;
+        for (int i = 0; i < cnt / 8; ++i)
+          *reinterpret_cast<BF8*>(stg + r * 256 + (((c / 8 + i) ^ (r & 15)) * 16)) = f_to_bf8(f + 8 * i);
+      });
+      if (threadIdx.x == 128) ATRACE(15, k);
+      asm volatile("bar.sync 1, %0;" ::"r"(128 * kWG) : "memory");
+      if (threadIdx.x == 128) ATRACE(5, k);
+      BF8* dst = reinterpret_cast<BF8*>(dqkv + (static_cast<long long>(it.b) * S + it.qb * 128) * 3 * HD + it.h * D);
+      BF8 v[kIter];
 #pragma unroll
-      for (int g = 0; g < kPer; ++g) {
-        const int gg = part * kPer + g;
-        if (gg < kG) {
-          const uint4 lo = __ldg(src + 2 * gg), hi = __ldg(src + 2 * gg + 1);
-          const uint32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-          tmem_st8(dst + 8 * gg, v);
-        }
+      for (int x = 0; x < kIter; ++x) {
+        const int i = static_cast<int>(threadIdx.x) - 128 + x * 128 * kWG, rr = i / kChunks, cc = i % kChunks;
+        if (i < 128 * kChunks) v[x] = *reinterpret_cast<const BF8*>(stg + rr * 256 + ((cc ^ (rr & 15)) * 16));
       }
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(a_full);
-    }
-    const long long vi = (static_cast<long long>(b) * H + h) * S + q;
-    const float l2 = lse2[vi], dq = dvec[vi];
-    for (int j = 0; j < n; ++j) {
-      const int st = j & 1;
-      mbar_wait(s_full + st, (j >> 1) & 1);
-      if (threadIdx.x == 128) ATRACE(3, j);
+#pragma unroll
+      for (int x = 0; x < kIter; ++x) {
+        const int i = static_cast<int>(threadIdx.x) - 128 + x * 128 * kWG, rr = i / kChunks, cc = i % kChunks;
+        if (i < 128 * kChunks) dst[static_cast<long long>(rr) * (3 * HD / 8) + cc] = v[x];
+      }
+      // the next epilogue rewrites the tile only after a whole item of dS hand-offs: every row thread has
+      // long finished reading it
+    };
+    auto vec_index = [&](int w) {
+      const DqItem it = dq_item(w, nq, H, B);
+      return (static_cast<long long>(it.b) * H + it.h) * S + it.qb * 128 + r;
+    };
+    float l2 = lse2[vec_index(blockIdx.x)], dq = dvec[vec_index(blockIdx.x)];
+    int g = 0, k = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+      const DqItem it = dq_item(w, nq, H, B);
+      const int q = it.qb * 128 + r;
+      if (threadIdx.x == 128) ATRACE(8, k);
+      // the next item's row statistics, loaded a whole item ahead (issued at the item's end they were still
+      // in flight ~2600 cycles later under the K / V stream)
+      const int wn = w + gridDim.x;
+      float l2n = 0.f, dqn = 0.f;
+      if (wn < n_items) l2n = lse2[vec_index(wn)], dqn = dvec[vec_index(wn)];
+      for (int j = 0; j < it.n; ++j) {
+        const int gg = g + j, st = gg & 1;
+        mbar_wait(s_full + st, (gg >> 1) & 1);
+        if (threadIdx.x == 128) ATRACE(3, k == 0 ? j : 64);
+        if (threadIdx.x == 128 && j == 0) ATRACE(13, k);
+        tc_fence_after();
+        const bool diag = j >= 2 * it.qb;
+        {
+          uint32_t sv[CW], dp[CW];
+          tmem_ld_cols<CW>(tmem + lanes + st * 64 + wg * CW, sv);
+          tmem_ld_cols<CW>(tmem + lanes + 128 + st * 64 + wg * CW, dp);
+          tmem_ld_wait();
+          float gr[CW];
+#pragma unroll
+          for (int c = 0; c < CW; ++c) gr[c] = ex2(fmaf(u2f(sv[c]), scale_log2, -l2));
+          if (diag) {
+#pragma unroll
+            for (int c = 0; c < CW; ++c)
+              if (j * 64 + wg * CW + c > q) gr[c] = 0.f;
+          }
+#pragma unroll
+          for (int c = 0; c < CW; ++c) gr[c] *= u2f(dp[c]) - dq;
+          uint32_t packed[CW / 2];
+#pragma unroll
+          for (int c = 0; c < CW / 2; ++c) packed[c] = pack_bf16x2(gr[2 * c], gr[2 * c + 1]);
+          if (threadIdx.x == 128) ATRACE(4, k == 0 ? j : 64);
+          // dS(j) overwrites S(j) in place, each warpgroup inside the columns it read (packed_col; see
+          // the dK/dV kernel); dQ(j-2), the last reader of this buffer, completed before S(j).
+          tmem_st_cols<CW / 2>(tmem + lanes + st * 64 + wg * CW, packed);
+          tmem_st_wait();
+        }
+        tc_fence_before();
+        mbar_arrive(ds_full + st);
+        if (threadIdx.x == 128) ATRACE(6, k == 0 ? j : 64);
+      }
+      g += it.n;
+      if (threadIdx.x == 128) ATRACE(7, k);
+      // this item's dQ is complete; the next item's first dQ MMA (which overwrites the accumulator) waits
+      // for the dS hand-off below, i.e. after this epilogue
+      mbar_wait(fin, k & 1);
       tc_fence_after();
-      const bool diag = j >= 2 * qb;
-      {
-        uint32_t s[CW], dp[CW];
-        tmem_ld_cols<CW>(tmem + lanes + st * 64 + wg * CW, s);
-        tmem_ld_cols<CW>(tmem + lanes + 128 + st * 64 + wg * CW, dp);
-        tmem_ld_wait();
-        float g[CW];
-#pragma unroll
-        for (int c = 0; c < CW; ++c) g[c] = ex2(fmaf(u2f(s[c]), scale_log2, -l2));
-        if (diag) {
-#pragma unroll
-          for (int c = 0; c < CW; ++c)
-            if (j * 64 + wg * CW + c > q) g[c] = 0.f;
-        }
-#pragma unroll
-        for (int c = 0; c < CW; ++c) g[c] *= u2f(dp[c]) - dq;
-        uint32_t packed[CW / 2];
-#pragma unroll
-        for (int c = 0; c < CW / 2; ++c) packed[c] = pack_bf16x2(g[2 * c], g[2 * c + 1]);
-        if (threadIdx.x == 128) ATRACE(4, j);
-        // dS(j) overwrites S(j) in place, each warpgroup inside the columns it read (packed_col; see
-        // the dK/dV kernel); dQ(j-2), the last reader of this buffer, completed before S(j).
-        tmem_st_cols<CW / 2>(tmem + lanes + st * 64 + wg * CW, packed);
-        tmem_st_wait();
-      }
-      tc_fence_before();
-      mbar_arrive(ds_full + st);
-      if (threadIdx.x == 128) ATRACE(6, j);
+      if (threadIdx.x == 128) ATRACE(9, k);
+      epilogue(w, k);
+      if (threadIdx.x == 128) ATRACE(11, k);
+      l2 = l2n, dq = dqn;
     }
-    mbar_wait(fin, 0);
-    tc_fence_after();
-    BF8* dqrow = reinterpret_cast<BF8*>(dqkv + static_cast<long long>(row0 + q) * 3 * HD + h * D);
-    constexpr int kSplit = (D / 16 + kWG - 1) / kWG * 16;  // each warpgroup writes its share of the D columns
-    const int c_lo = wg * kSplit < D ? wg * kSplit : D, c_hi = (wg + 1) * kSplit < D ? (wg + 1) * kSplit : D;
-    tmem_cols(tmem + lanes + 256, c_lo, c_hi, [&](int c, const uint32_t* o, int cnt) {
-      float f[32];
-      for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * scale;
-      for (int i = 0; i < cnt / 8; ++i) dqrow[c / 8 + i] = f_to_bf8(f + 8 * i);
-    });
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  ATRACE_DUMP(n);
+  ATRACE_DUMP(64);
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
@@ -1034,7 +1398,8 @@ int fwd_tiles() {
   if (g_fwd_tiles) return g_fwd_tiles;
   static const int n = [] {
     const char* e = std::getenv("LYNX_ATTN_FWD_TILES");
-    return e && std::atoi(e) == 1 ? 1 : 2;
+    const int v = e ? std::atoi(e) : 2;
+    return v == 1 || v == 3 ? v : 2;
   }();
   return n;
 }
@@ -1044,6 +1409,15 @@ int fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, 
   CUtensorMap m;
   const long long T = static_cast<long long>(B) * S, ld = 3LL * H * D;
   if (!gemm::make_map(&m, qkv, ld, T, ld, 64, 128)) return set_error("attention: tensor map encode failed");
+  if (fwd_tiles() == 3) {
+    CUtensorMap m64;
+    if (!gemm::make_map(&m64, qkv, ld, T, ld, 64, 64)) return set_error("attention: tensor map encode failed");
+    auto k = attn_fwd3_tc_kernel<D>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3L<D>::kBytes);
+    k<<<dim3((S / 128 + 1) / 2, H, B), 384, Fwd3L<D>::kBytes, s>>>(m, m64, out, lse, S, H,
+                                                                   kLog2e / sqrtf(static_cast<float>(D)));
+    return check_launch("attention_fwd_tc");
+  }
   if (fwd_tiles() == 2) {
     const int poly = poly_every();
     auto k = poly == 2 ? attn_fwd2_tc_kernel<D, 2>
@@ -1080,32 +1454,32 @@ int bwd_warpgroups() {
 }
 
 template <int D, int kWG>
-int bwd_launch(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const CUtensorMap& m128, const CUtensorMap& m64,
-               const CUtensorMap& d64, const float* lse, const float* dvec, __nv_bfloat16* dqkv, int B, int S, int H, float scale,
+int bwd_launch(const CUtensorMap& m128, const CUtensorMap& m64, const CUtensorMap& d64, const CUtensorMap& d128,
+               const float* lse, const float* dvec, __nv_bfloat16* dqkv, int B, int S, int H, float scale,
                float scale_log2, cudaStream_t s) {
   auto k1 = attn_dkdv_tc_kernel<D, kWG>;
   cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvL<D>::kBytes);
-  k1<<<dim3(S / 128, H, B), 128 + 128 * kWG, DkvL<D>::kBytes, s>>>(m128, m64, d64, lse, dvec, dqkv, S, H, scale,
-                                                                   scale_log2);
+  const int items1 = S / 128 * H * B, grid1 = items1 < gemm::num_sms() ? items1 : gemm::num_sms();
+  k1<<<grid1, 128 + 128 * kWG, DkvL<D>::kBytes, s>>>(m128, m64, d64, lse, dvec, dqkv, S, H, B, scale, scale_log2);
   auto k2 = attn_dq_tc_kernel<D, kWG>;
   cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, DqL<D>::kBytes);
-  k2<<<dim3(S / 128, H, B), 128 + 128 * kWG, DqL<D>::kBytes, s>>>(qkv, dout, m64, lse, dvec, dqkv, S, H, scale,
-                                                                  scale_log2);
+  const int items = S / 128 * H * B, grid2 = items < gemm::num_sms() ? items : gemm::num_sms();
+  k2<<<grid2, 128 + 128 * kWG, DqL<D>::kBytes, s>>>(m128, m64, d128, lse, dvec, dqkv, S, H, B, scale, scale_log2);
   return check_launch("attention_bwd_tc", 2);
 }
 
 template <int D>
 int bwd(const __nv_bfloat16* qkv, const __nv_bfloat16* dout, const float* lse, const float* dvec,
         __nv_bfloat16* dqkv, int B, int S, int H, cudaStream_t s) {
-  CUtensorMap m128, m64, d64;
+  CUtensorMap m128, m64, d64, d128;
   const long long T = static_cast<long long>(B) * S, ld = 3LL * H * D, hd = static_cast<long long>(H) * D;
   bool ok = gemm::make_map(&m128, qkv, ld, T, ld, 64, 128) && gemm::make_map(&m64, qkv, ld, T, ld, 64, 64) &&
-            gemm::make_map(&d64, dout, hd, T, hd, 64, 64);
+            gemm::make_map(&d64, dout, hd, T, hd, 64, 64) && gemm::make_map(&d128, dout, hd, T, hd, 64, 128);
   if (!ok) return set_error("attention: tensor map encode failed");
   const float scale = 1.f / sqrtf(static_cast<float>(D)), scale_log2 = scale * kLog2e;
   if (bwd_warpgroups() == 2)
-    return bwd_launch<D, 2>(qkv, dout, m128, m64, d64, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
-  return bwd_launch<D, 4>(qkv, dout, m128, m64, d64, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
+    return bwd_launch<D, 2>(m128, m64, d64, d128, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
+  return bwd_launch<D, 4>(m128, m64, d64, d128, lse, dvec, dqkv, B, S, H, scale, scale_log2, s);
 }
 
 int g_mode = -1;
@@ -1114,7 +1488,7 @@ int g_mode = -1;
 
 void attention_set_mode(int mode) { attn_tc::g_mode = mode; }
 void attention_set_bwd_warpgroups(int n) { attn_tc::g_bwd_wg = n == 2 || n == 4 ? n : 0; }
-void attention_set_fwd_tiles(int n) { attn_tc::g_fwd_tiles = n == 1 || n == 2 ? n : 0; }
+void attention_set_fwd_tiles(int n) { attn_tc::g_fwd_tiles = n >= 1 && n <= 3 ? n : 0; }
 int attention_mode() { return attn_tc::g_mode; }
 bool attention_tc_supported(int seq, int head_dim) {
   return attn_tc::g_mode != 0 && seq % 128 == 0 &&
