@@ -853,7 +853,7 @@ struct DkvItem {
 LYNX_DEV DkvItem dkv_item(int w, int nk, int S, int H) {
   const int hb = w / nk;
   DkvItem it;
-  it.kb = w % nk;
+  it.kb = (w % nk + hb) % nk;  // rotated by head: see dq_item
   it.h = hb % H;
   it.b = hb / H;
   it.n = S / 64 - 2 * it.kb;
@@ -1123,14 +1123,15 @@ struct DqL {
 struct DqItem {
   int qb, h, b, n;
 };
-// Work item w: head (w / nq) and query tile nq - 1 - w % nq, so the CTAs that run at the same time
-// work on the same few heads and share their K / V tiles in L2 (qb-major order made every CTA stream
-// its own head's K / V from HBM: ~4.5 GB per call at the 7B shape). CTA c meets the query tiles
-// 15 - c % 16, 15 - (c + 148) % 16, ...: balanced over the ~55 items per CTA.
+// Work item w: head w / nq, so the CTAs that run at the same time work on the same few heads and share
+// their K / V tiles in L2 (qb-major order made every CTA stream its own head's K / V from HBM: ~4.5 GB
+// per call at the 7B shape). The query tile is rotated by the head index: without it CTA c (items c,
+// c + 148, ...) met only the tiles (c + 4 k) % 16 — four of the sixteen lengths, up to 43 % more work
+// than another CTA — with it, (c + 13.25 k) % 16 cycles through all of them.
 LYNX_DEV DqItem dq_item(int w, int nq, int H, int B) {
   const int hb = w / nq;
   DqItem it;
-  it.qb = nq - 1 - w % nq;
+  it.qb = nq - 1 - (w % nq + hb) % nq;
   it.h = hb % H;
   it.b = hb / H;
   it.n = 2 * (it.qb + 1);
