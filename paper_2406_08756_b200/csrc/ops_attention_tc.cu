@@ -401,34 +401,53 @@ __global__ void __launch_bounds__(256, 1)
 // to hide the TMEM-load / MUFU latencies that bound the one-tile kernel (tensor pipe ~39 % there).
 // Per-row arithmetic, warp-to-row mapping and the lazy-rescale decisions are those of
 // attn_fwd_tc_kernel, so O and lse are bit-identical to it.
+//
+// Persistent (like the backward kernels): grid = min(work items, SMs); work item w = (tile pair, head,
+// batch), head-major with the pair rotated by the head (dq_item). The K / V ring runs on across items;
+// the next item's Q tiles are loaded as soon as the current item's last S MMAs completed; O leaves
+// through a 16-KB shared-memory staging tile per warpgroup with coalesced stores.
 template <int D>
 struct Fwd2L {
   static constexpr int kTile = FwdL<D>::kTile;
-  static constexpr int kQ = 0, kK = 2 * kTile, kV = 4 * kTile, kBar = 6 * kTile;
-  static constexpr int kBytes = kBar + 128 + 1024;
+  static constexpr int kQ = 0, kK = 2 * kTile, kV = 4 * kTile, kOut = 6 * kTile;  // kOut: 2 x 128 rows x 128 B
+  static constexpr int kBar = kOut + 2 * 16384;
+  static constexpr int kBytes = kBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per CTA");
 };
+
+struct FwdItem {
+  int pair, h, b, n0, n1;  // n0 / n1: key tiles of query tile 2 pair / 2 pair + 1 (0: absent)
+};
+LYNX_DEV FwdItem fwd_item(int w, int np, int n_qt, int H) {
+  const int hb = w / np;
+  FwdItem it;
+  it.pair = (w % np + hb) % np;
+  it.h = hb % H;
+  it.b = hb / H;
+  it.n0 = 2 * it.pair + 1;
+  it.n1 = 2 * it.pair + 1 < n_qt ? 2 * it.pair + 2 : 0;
+  return it;
+}
 
 template <int D, int kPoly>  // kPoly: as attn_fwd_tc_kernel (every kPoly-th exponential on the FMA pipe)
 __global__ void __launch_bounds__(384, 1)
     attn_fwd2_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, __nv_bfloat16* __restrict__ out,
-                        float* __restrict__ lse, int S, int H, float scale_log2) {
+                        float* __restrict__ lse, int S, int H, int B, float scale_log2) {
   using L = Fwd2L<D>;
   constexpr int kA = FwdL<D>::kAtoms;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5, *v_empty = bar + 7,
-           *s_full = bar + 9, *p_full = bar + 11, *pv_done = bar + 13;  // s / p / pv: one per query tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
-  const int pair = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  uint64_t *q_full = bar, *q_free = bar + 1, *k_full = bar + 2, *k_empty = bar + 4, *v_full = bar + 6,
+           *v_empty = bar + 8, *s_full = bar + 10, *p_full = bar + 12, *pv_done = bar + 14;  // s/p/pv: per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int n_qt = S / 128;
-  const bool has1 = 2 * pair + 1 < n_qt;
-  const int n0 = 2 * pair + 1, n1 = has1 ? 2 * pair + 2 : 0, n = has1 ? n1 : n0;
-  const int HD = H * D, row0 = b * S;
+  const int n_qt = S / 128, np = (n_qt + 1) / 2, n_items = np * H * B;
+  const int HD = H * D;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_free, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(k_full + i, 1);
       mbar_init(k_empty + i, 1);
@@ -446,99 +465,119 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // Register split by warpgroup (setmaxnreg, executed at the top of each role): the control warpgroup
-  // (TMA, MMA, TMEM) gives registers to the two softmax warpgroups, whose 128-column rows need them.
+  // (TMA, MMA, TMEM) gives registers to the two softmax warpgroups, whose 128-column rows need them:
+  // 128 x 72 + 256 x 216 = the 168 x 384 the launch allocates.
 
   if (warp == 0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
     if (elect_one()) {
       tma_prefetch_desc(&map_qkv);
-      mbar_arrive_expect_tx(q_full, (has1 ? 2 : 1) * L::kTile);
-      for (int t = 0; t < (has1 ? 2 : 1); ++t)
-        for (int a = 0; a < kA; ++a)
-          tma_load_2d(&map_qkv, q_full, smem + L::kQ + t * L::kTile + a * 16384, h * D + 64 * a,
-                      row0 + (2 * pair + t) * 128, kEvictFirst);
-      for (int j = 0; j < n; ++j) {
-        const int st = j & 1;
-        if (j >= 2) mbar_wait(k_empty + st, ((j >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(k_full + st, L::kTile);
-        for (int a = 0; a < kA; ++a)
-          tma_load_2d(&map_qkv, k_full + st, smem + L::kK + st * L::kTile + a * 16384, HD + h * D + 64 * a,
-                      row0 + j * 128, kEvictLast);
-        if (j >= 2) mbar_wait(v_empty + st, ((j >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(v_full + st, L::kTile);
-        for (int a = 0; a < kA; ++a)
-          tma_load_2d(&map_qkv, v_full + st, smem + L::kV + st * L::kTile + a * 16384, 2 * HD + h * D + 64 * a,
-                      row0 + j * 128, kEvictLast);
+      int g = 0, k = 0;  // K / V tile counter over this CTA's items, item counter
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+        const FwdItem it = fwd_item(w, np, n_qt, H);
+        const int row0 = it.b * S, nq = it.n1 ? 2 : 1, n = it.n1 ? it.n1 : it.n0;
+        if (k > 0) mbar_wait(q_free, (k - 1) & 1);  // the previous item's last S MMAs completed
+        mbar_arrive_expect_tx(q_full, nq * L::kTile);
+        for (int t = 0; t < nq; ++t)
+          for (int a = 0; a < kA; ++a)
+            tma_load_2d(&map_qkv, q_full, smem + L::kQ + t * L::kTile + a * 16384, it.h * D + 64 * a,
+                        row0 + (2 * it.pair + t) * 128, kEvictFirst);
+        for (int j = 0; j < n; ++j, ++g) {
+          const int st = g & 1;
+          if (g >= 2) mbar_wait(k_empty + st, ((g >> 1) - 1) & 1);
+          mbar_arrive_expect_tx(k_full + st, L::kTile);
+          for (int a = 0; a < kA; ++a)
+            tma_load_2d(&map_qkv, k_full + st, smem + L::kK + st * L::kTile + a * 16384, HD + it.h * D + 64 * a,
+                        row0 + j * 128, kEvictLast);
+          if (g >= 2) mbar_wait(v_empty + st, ((g >> 1) - 1) & 1);
+          mbar_arrive_expect_tx(v_full + st, L::kTile);
+          for (int a = 0; a < kA; ++a)
+            tma_load_2d(&map_qkv, v_full + st, smem + L::kV + st * L::kTile + a * 16384, 2 * HD + it.h * D + 64 * a,
+                        row0 + j * 128, kEvictLast);
+        }
       }
     }
   } else if (warp == 1) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
     if (elect_one()) {
       constexpr uint32_t idS = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idO = umma_idesc_bf16(128, D, false, true);
       const uint32_t sQ = smem_u32(smem + L::kQ), sK = smem_u32(smem + L::kK), sV = smem_u32(smem + L::kV);
-      auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
-        const int st = j & 1;
+      int g = 0, k = 0, cp0 = 0, cp1 = 0;  // K / V tiles, items, P hand-offs of query tile 0 / 1
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+        const FwdItem it = fwd_item(w, np, n_qt, H);
+        const int n0 = it.n0, n1 = it.n1, n = n1 ? n1 : n0;
+        auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
+          const int st = (g + j) & 1;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_f16(tmem + t * 128, kmaj(sQ + t * L::kTile, kk, 16384), kmaj(sK + st * L::kTile, kk, 16384), idS,
-                   kk > 0);
-        umma_commit(s_full + t);
-        ATRACE(t ? 7 : 0, j);
-      };
-      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P packed bf16 over S_t in TMEM
-        const int st = j & 1;
-        mbar_wait(p_full + t, j & 1);
-        ATRACE(t ? 6 : 1, j);
-        tc_fence_after();
+          for (int kk = 0; kk < D / 16; ++kk)
+            umma_f16(tmem + t * 128, kmaj(sQ + t * L::kTile, kk, 16384), kmaj(sK + st * L::kTile, kk, 16384), idS,
+                     kk > 0);
+          umma_commit(s_full + t);
+          if (k == 0) ATRACE(t ? 7 : 0, j);
+        };
+        auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P packed bf16 over S_t in TMEM
+          const int st = (g + j) & 1;
+          mbar_wait(p_full + t, (t ? cp1 : cp0) & 1);
+          if (t) ++cp1; else ++cp0;
+          if (k == 0) ATRACE(t ? 6 : 1, j);
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj(sV + st * L::kTile, kk, 16384), idO,
-                      (j | kk) != 0);
-        umma_commit(pv_done + t);
-      };
-      auto wait_k = [&](int j) {
-        mbar_wait(k_full + (j & 1), (j >> 1) & 1);
-        tc_fence_after();
-      };
-      mbar_wait(q_full, 0);
-      wait_k(0);
-      issue_s(0, 0);
-      if (n1 > 0) issue_s(1, 0);
-      umma_commit(k_empty);
-      for (int j = 0; j < n; ++j) {
-        const int st = j & 1;
-        mbar_wait(v_full + st, (j >> 1) & 1);
-        tc_fence_after();
-        if (j < n0) issue_pv(0, j);
-        if (j + 1 < n) wait_k(j + 1);
-        if (j + 1 < n0) issue_s(0, j + 1);
-        if (j < n1) issue_pv(1, j);
-        umma_commit(v_empty + st);
-        if (j + 1 < n1) issue_s(1, j + 1);
-        if (j + 1 < n) umma_commit(k_empty + ((j + 1) & 1));
+          for (int kk = 0; kk < 8; ++kk)
+            umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj(sV + st * L::kTile, kk, 16384), idO,
+                        (j | kk) != 0);
+          umma_commit(pv_done + t);
+        };
+        auto wait_k = [&](int j) {
+          mbar_wait(k_full + ((g + j) & 1), ((g + j) >> 1) & 1);
+          tc_fence_after();
+        };
+        mbar_wait(q_full, k & 1);
+        wait_k(0);
+        issue_s(0, 0);
+        if (n1 > 0) issue_s(1, 0);
+        if (n == 1) umma_commit(q_free);
+        umma_commit(k_empty + (g & 1));
+        for (int j = 0; j < n; ++j) {
+          const int st = (g + j) & 1;
+          mbar_wait(v_full + st, ((g + j) >> 1) & 1);
+          tc_fence_after();
+          if (j < n0) issue_pv(0, j);
+          if (j + 1 < n) wait_k(j + 1);
+          if (j + 1 < n0) issue_s(0, j + 1);
+          if (j < n1) issue_pv(1, j);
+          umma_commit(v_empty + st);
+          if (j + 1 < n1) issue_s(1, j + 1);
+          if (j + 2 == n) umma_commit(q_free);  // the item's last S MMAs are issued: Q may be replaced
+          if (j + 1 < n) umma_commit(k_empty + ((g + j + 1) & 1));
+        }
+        g += n;
       }
     }
   } else if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
     const int t = (warp - 4) / 4;  // query tile of this warpgroup (warp w reads TMEM lanes 32 (w % 4) ...)
-    if (t == 0 || has1) {
-      const int qb = 2 * pair + t, nt = t ? n1 : n0;
-      const int r = (warp % 4) * 32 + lane;
-      const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
-      const uint32_t s_col = tmem + lanes + t * 128, o_col = tmem + lanes + 256 + t * 128;
+    const int r = (warp % 4) * 32 + lane, tr = threadIdx.x - 128 - 128 * t;  // tile row, thread in warpgroup
+    const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    const uint32_t s_col = tmem + lanes + t * 128, o_col = tmem + lanes + 256 + t * 128;
+    uint8_t* stg = smem + L::kOut + t * 16384;  // this warpgroup's O staging: 128 rows x 64 columns
+    int c = 0, k = 0;                           // S_t tiles consumed, items
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++k) {
+      const FwdItem it = fwd_item(w, np, n_qt, H);
+      const int nt = t ? it.n1 : it.n0;
+      if (nt == 0) continue;
+      const int qb = 2 * it.pair + t;
       float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < nt; ++j) {
-        mbar_wait(s_full + t, j & 1);
-        if (warp % 4 == 0 && lane == 0) ATRACE(t ? 4 : 2, j);
+      for (int j = 0; j < nt; ++j, ++c) {
+        mbar_wait(s_full + t, c & 1);
+        if (k == 0 && warp % 4 == 0 && lane == 0) ATRACE(t ? 4 : 2, j);
         tc_fence_after();
         float x[128];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(s_col + c * 32, reinterpret_cast<uint32_t*>(x + c * 32));
+        for (int cc = 0; cc < 4; ++cc) tmem_ld32(s_col + cc * 32, reinterpret_cast<uint32_t*>(x + cc * 32));
         tmem_ld_wait();
-        if (t == 0 && warp == 4 && lane == 0) ATRACE(8, j);
         if (j == qb) {  // diagonal tile: causal mask (warp-uniform branch)
 #pragma unroll
           for (int i = 0; i < 128; ++i)
@@ -552,7 +591,6 @@ __global__ void __launch_bounds__(384, 1)
         const float mt =
             fmaxf(fmaxf(fmaxf(mv[0], mv[1]), fmaxf(mv[2], mv[3])), fmaxf(fmaxf(mv[4], mv[5]), fmaxf(mv[6], mv[7])));
         const float m_new = fmaxf(m_run, mt * scale_log2);
-        if (t == 0 && warp == 4 && lane == 0) ATRACE(9, j);
         const bool need = __any_sync(0xffffffffu, m_new > m_run + kRescale);
         float corr = 1.f;
         if (need) {
@@ -568,50 +606,60 @@ __global__ void __launch_bounds__(384, 1)
         }
         const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
         l_run = l_run * corr + rs;
-        if (t == 0 && warp == 4 && lane == 0) ATRACE(10, j);
         if (j > 0 && need) {  // O_t rescale after PV_t(j-1) completes (PV_t(j) needs this tile's P)
-          mbar_wait(pv_done + t, (j - 1) & 1);
+          mbar_wait(pv_done + t, (c - 1) & 1);
           tc_fence_after();
-          tmem_cols(o_col, 0, D, [&](int c, uint32_t* o, int cnt) {
+          tmem_cols(o_col, 0, D, [&](int col, uint32_t* o, int cnt) {
             for (int i = 0; i < cnt; ++i) o[i] = __float_as_uint(u2f(o[i]) * corr);
             if (cnt == 32)
-              tmem_st32(o_col + c, o);
+              tmem_st32(o_col + col, o);
             else
-              tmem_st16(o_col + c, o);
+              tmem_st16(o_col + col, o);
           });
           tmem_st_wait();
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int cc = 0; cc < 4; ++cc) {
           uint32_t packed[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(x[32 * c + 2 * i], x[32 * c + 2 * i + 1]);
-          tmem_st16(s_col + c * 16, packed);
+          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(x[32 * cc + 2 * i], x[32 * cc + 2 * i + 1]);
+          tmem_st16(s_col + cc * 16, packed);
         }
-        if (t == 0 && warp == 4 && lane == 0) ATRACE(11, j);
         tmem_st_wait();
-        if (t == 0 && warp == 4 && lane == 0) ATRACE(12, j);
         tc_fence_before();
         mbar_arrive(p_full + t);
-        if (warp % 4 == 0 && lane == 0) ATRACE(t ? 5 : 3, j);
+        if (k == 0 && warp % 4 == 0 && lane == 0) ATRACE(t ? 5 : 3, j);
       }
-      mbar_wait(pv_done + t, (nt - 1) & 1);
+      mbar_wait(pv_done + t, (c - 1) & 1);
       tc_fence_after();
+      // O_t / l -> bf16 through the staging tile (row r's 16-B chunk ch at r * 128 + (ch ^ (r % 8)) * 16),
+      // 64 columns per round, then coalesced 16-B stores (8 threads per 128-B row piece). The next item's
+      // first PV_t (which overwrites O_t) waits for this warpgroup's first P hand-off, i.e. after this.
       const float inv = 1.f / l_run;
-      const int q = qb * 128 + r;
-      BF8* orow = reinterpret_cast<BF8*>(out + static_cast<long long>(row0 + q) * HD + h * D);
-      tmem_cols(o_col, 0, D, [&](int c, const uint32_t* o, int cnt) {
-        float f[32];
-        for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * inv;
-        for (int i = 0; i < cnt / 8; ++i) orow[c / 8 + i] = f_to_bf8(f + 8 * i);
-      });
-      lse[(static_cast<long long>(b) * H + h) * S + q] = (m_run + log2f(l_run)) / kLog2e;
+      const long long orow0 = static_cast<long long>(it.b) * S + qb * 128;
+      for (int c0 = 0; c0 < D; c0 += 64) {
+        const int cw = D - c0 < 64 ? D - c0 : 64, nch = cw / 8;
+        tmem_cols(o_col, c0, c0 + cw, [&](int col, const uint32_t* o, int cnt) {
+          float f[32];
+          for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * inv;
+          for (int i = 0; i < cnt / 8; ++i)
+            *reinterpret_cast<BF8*>(stg + r * 128 + ((((col - c0) / 8 + i) ^ (r & 7)) * 16)) = f_to_bf8(f + 8 * i);
+        });
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + t) : "memory");
+        for (int i = tr; i < 128 * nch; i += 128) {
+          const int rr = i / nch, ch = i % nch;
+          const BF8 v = *reinterpret_cast<const BF8*>(stg + rr * 128 + ((ch ^ (rr & 7)) * 16));
+          reinterpret_cast<BF8*>(out + (orow0 + rr) * HD + it.h * D + c0)[ch] = v;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + t) : "memory");  // staging read: reusable
+      }
+      lse[(static_cast<long long>(it.b) * H + it.h) * S + qb * 128 + r] = (m_run + log2f(l_run)) / kLog2e;
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  ATRACE_DUMP(n);
+  ATRACE_DUMP(16);
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
@@ -1426,8 +1474,8 @@ int fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, 
              : poly == 4 ? attn_fwd2_tc_kernel<D, 4>
                          : attn_fwd2_tc_kernel<D, 0>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2L<D>::kBytes);
-    k<<<dim3((S / 128 + 1) / 2, H, B), 384, Fwd2L<D>::kBytes, s>>>(m, out, lse, S, H,
-                                                                   kLog2e / sqrtf(static_cast<float>(D)));
+    const int items = (S / 128 + 1) / 2 * H * B, grid = items < gemm::num_sms() ? items : gemm::num_sms();
+    k<<<grid, 384, Fwd2L<D>::kBytes, s>>>(m, out, lse, S, H, B, kLog2e / sqrtf(static_cast<float>(D)));
     return check_launch("attention_fwd_tc");
   }
   switch (poly_every()) {
