@@ -872,6 +872,303 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+// ============================================================== forward, CTA pair (cta_group::2), D = 128
+// Two CTAs of a cluster (two SMs) own query tiles 2p (rank 0) and 2p + 1 (rank 1); the leader issues
+// M = 256 MMAs over both: S = Q K_j^T with each CTA's Q tile as its half of A and each CTA holding half
+// of K_j's 128 keys (B is split along N), O += P V_j with P from each CTA's TMEM and each CTA holding
+// half of V_j's D columns. Per CTA this halves the K / V shared-memory traffic of an S MMA (6 KB per
+// 64-cycle instruction instead of 8 KB per 64 cycles) and frees TMEM: two 128-column S buffers, a
+// separate 64-column P and the 128-column O fit in 512, so S(j+1) is computed while the softmax of S(j)
+// runs and P(j) never overwrites S — the per-tile softmax -> PV -> S chain of the two-tile kernel is
+// gone. Each CTA's 128 x 128 score tile is split over two softmax warpgroups (64 key columns each,
+// row max exchanged through shared memory), so each SM sub-partition has two warps issuing
+// exponentials: 1024 MUFU cycles per tile per SM against 1024 tensor cycles.
+// Query tile 2p needs one key tile less than 2p + 1: rank 0 writes P = 0 for it.
+struct Fwd4L {
+  static constexpr int kQT = 128 * 128 * 2;   // Q tile: 2 atoms of 16 KB
+  static constexpr int kKH = 64 * 128 * 2;    // K half: 64 keys x 128 columns (2 atoms of 8 KB)
+  static constexpr int kVH = 128 * 64 * 2;    // V half: 128 keys x 64 columns (1 atom of 16 KB)
+  static constexpr int kStage = kKH + kVH;
+  static constexpr int kStages = 4;
+  static constexpr int kQ = 0, kKV = kQT, kOut = kKV + kStages * kStage;  // kOut: 2 x 16 KB O staging
+  static constexpr int kRed = kOut + 2 * 16384;                          // row max / sum exchange: 2 x 2 x 128 f32
+  static constexpr int kBar = kRed + 2 * 2 * 128 * 4;
+  static constexpr int kBytes = kBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per CTA");
+};
+constexpr uint32_t kPeerMask2 = 0xFEFFFFFFu;  // shared::cluster address of the leader's copy
+LYNX_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+LYNX_DEV void cluster_sync2() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Relaxed remote arrive: the .release.cluster form compiles to MEMBAR.ALL.GPU, ~1000 cycles on the
+// softmax's critical path. What an arrival here hands over is TMEM (S read / P written), and those
+// tcgen05.ld / st have completed (wait::ld / wait::st) before the local arrivals this one forwards.
+LYNX_DEV void arrive_leader2(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerMask2)
+               : "memory");
+}
+LYNX_DEV void tma_load_pair(const void* desc, uint64_t* bar, void* smem, int c0, int c1, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar) & kPeerMask2), "r"(c0), "r"(c1), "l"(hint)
+      : "memory");
+}
+LYNX_DEV void umma_pair_ss(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+LYNX_DEV void umma_pair_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+LYNX_DEV void commit_pair(uint64_t* bar) {  // arrive on `bar` in both CTAs when the leader's MMAs complete
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+template <int kPoly>  // every kPoly-th exponential on the FMA pipe (ex2_poly), 0: none
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    attn_fwd4_tc_kernel(const __grid_constant__ CUtensorMap map128, const __grid_constant__ CUtensorMap map64,
+                        __nv_bfloat16* __restrict__ out, float* __restrict__ lse, int S, int H, float scale_log2) {
+  using L = Fwd4L;
+  constexpr int D = 128, NS = L::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1k(smem_raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = kv_full + NS, *s_full = kv_empty + NS, *s_free = s_full + 2,
+           *p_full = s_free + 2, *pv_done = p_full + 1, *s_free_loc = pv_done + 1, *p_full_loc = s_free_loc + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_full_loc + 1);
+  float* red = reinterpret_cast<float*>(smem + L::kRed);  // [2 buffers][2 warpgroups][128 rows]
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = gridDim.x / 2 - 1 - blockIdx.x / 2, h = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qt = 2 * pair + static_cast<int>(rank);  // this CTA's query tile
+  const int n = 2 * pair + 2;                        // key tiles of the pair (rank 0's last one is masked out)
+  const int HD = H * D, row0 = b * S;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(kv_full + i, 1);
+      mbar_init(kv_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(s_free + i, 2);      // one forwarded arrival per CTA (on the leader)
+      mbar_init(s_free_loc + i, 8);  // this CTA's 8 softmax warps
+    }
+    mbar_init(p_full, 2);
+    mbar_init(p_full_loc, 8);
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync2();
+  tc_fence_after();
+  // TMEM (each CTA, its own 128 rows): S[2] at 0 / 128, P at 256 (64 packed columns), O at 384.
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    if (elect_one()) {
+      if (leader) mbar_arrive_expect_tx(q_full, 2 * L::kQT);
+      for (int a = 0; a < 2; ++a)
+        tma_load_pair(&map128, q_full, smem + L::kQ + a * 16384, h * D + 64 * a, row0 + qt * 128, kEvictFirst);
+      for (int j = 0; j < n; ++j) {
+        const int st = j % NS;
+        if (j >= NS) mbar_wait(kv_empty + st, ((j / NS) - 1) & 1);
+        uint8_t* sk = smem + L::kKV + st * L::kStage;
+        if (leader) mbar_arrive_expect_tx(kv_full + st, 2 * L::kStage);
+        for (int a = 0; a < 2; ++a)  // K: keys j * 128 + 64 rank ... + 63, all 128 columns
+          tma_load_pair(&map64, kv_full + st, sk + a * 8192, HD + h * D + 64 * a, row0 + j * 128 + 64 * rank,
+                        kEvictLast);
+        // V: all 128 keys, columns 64 rank ... + 63
+        tma_load_pair(&map128, kv_full + st, sk + L::kKH, 2 * HD + h * D + 64 * rank, row0 + j * 128, kEvictLast);
+      }
+    }
+  } else if (warp == 1) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    if (leader && elect_one()) {
+      constexpr uint32_t idS = umma_idesc_bf16(256, 128, false, false);
+      constexpr uint32_t idO = umma_idesc_bf16(256, D, false, true);
+      const uint32_t sQ = smem_u32(smem + L::kQ), sKV = smem_u32(smem + L::kKV);
+      auto issue_s = [&](int j) {  // S(j) into buffer j & 1 (both CTAs' rows)
+        const int st = j % NS;
+        mbar_wait(kv_full + st, (j / NS) & 1);
+        if (j >= 2) mbar_wait(s_free + (j & 1), ((j >> 1) - 1) & 1);  // the softmax read S(j - 2)
+        tc_fence_after();
+        const uint32_t sk = sKV + st * L::kStage;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_pair_ss(tmem + (j & 1) * 128, kmaj(sQ, kk, 16384), kmaj(sk, kk, 8192), idS, kk > 0);
+        commit_pair(s_full + (j & 1));
+        ATRACE(0, j);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      if (n > 1) issue_s(1);
+      for (int j = 0; j < n; ++j) {
+        const int st = j % NS;
+        mbar_wait(p_full, j & 1);
+        ATRACE(1, j);
+        tc_fence_after();
+        const uint32_t sv = sKV + st * L::kStage + L::kKH;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // A = P (both CTAs' TMEM), B = V half per CTA (MN-major)
+          umma_pair_ts(tmem + 384, tmem + 256 + kk * 8, mnmaj(sv, kk, 16384), idO, (j | kk) != 0);
+        commit_pair(pv_done);
+        commit_pair(kv_empty + st);
+        if (j + 2 < n) issue_s(j + 2);
+      }
+    }
+  } else if (warp == 3) {
+    // Forwarder: the softmax warps arrive on this CTA's barriers (a cluster-scope remote arrive from each
+    // of them cost ~1200 cycles on their critical path); one thread passes each phase on to the leader.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+    if (elect_one()) {
+      for (int j = 0; j < n; ++j) {
+        mbar_wait(s_free_loc + (j & 1), (j >> 1) & 1);
+        arrive_leader2(s_free + (j & 1));
+        mbar_wait(p_full_loc, j & 1);
+        arrive_leader2(p_full);
+      }
+    }
+  } else if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+    const int wg = (warp - 4) / 4;  // key columns 64 wg ... + 63 of every tile
+    const int r = (warp % 4) * 32 + lane, tr = threadIdx.x - 128 - 128 * wg;
+    const uint32_t lanes = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    const uint32_t o_col = tmem + lanes + 384 + 64 * wg;  // this warpgroup's half of O
+    const int q = qt * 128 + r;
+    float m_run = -INFINITY, l_run = 0.f;  // l_run: this warpgroup's half of the row sum
+    for (int j = 0; j < n; ++j) {
+      mbar_wait(s_full + (j & 1), (j >> 1) & 1);
+      if (warp % 4 == 0 && lane == 0) ATRACE(wg ? 4 : 2, j);
+      tc_fence_after();
+      float x[64];
+      const uint32_t s_col = tmem + lanes + (j & 1) * 128 + 64 * wg;
+      tmem_ld32(s_col, reinterpret_cast<uint32_t*>(x));
+      tmem_ld32(s_col + 32, reinterpret_cast<uint32_t*>(x + 32));
+      tmem_ld_wait();
+      if (warp == 4 && lane == 0) ATRACE(8, j);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_free_loc + (j & 1));
+      const bool dead = j > qt;  // rank 0's extra key tile: every key is after every query
+      if (j == qt) {             // diagonal tile: causal mask (warp-uniform branch)
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (64 * wg + i > r) x[i] = -INFINITY;
+      }
+      float mv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mv[i] = x[i];
+#pragma unroll
+      for (int i = 8; i < 64; ++i) mv[i & 7] = fmaxf(mv[i & 7], x[i]);
+      float mt =
+          fmaxf(fmaxf(fmaxf(mv[0], mv[1]), fmaxf(mv[2], mv[3])), fmaxf(fmaxf(mv[4], mv[5]), fmaxf(mv[6], mv[7])));
+      float* rb = red + (j & 1) * 256;
+      rb[wg * 128 + r] = mt;
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      mt = fmaxf(mt, rb[(1 - wg) * 128 + r]);
+      if (warp == 4 && lane == 0) ATRACE(9, j);
+      uint32_t packed[32];
+      bool need = false;
+      float corr = 1.f;
+      if (dead) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) packed[i] = 0u;
+      } else {
+        const float m_new = fmaxf(m_run, mt * scale_log2);
+        need = __any_sync(0xffffffffu, m_new > m_run + kRescale);
+        if (need) {
+          corr = exp2f(m_run - m_new);
+          m_run = m_new;
+        }
+        float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float a = fmaf(x[i], scale_log2, -m_run);
+          x[i] = (kPoly > 0 && i % (kPoly > 0 ? kPoly : 1) == (kPoly > 0 ? kPoly : 1) - 1) ? ex2_poly(a) : ex2(a);
+          rv[i & 7] += x[i];
+        }
+        const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
+        l_run = l_run * corr + rs;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) packed[i] = pack_bf16x2(x[2 * i], x[2 * i + 1]);
+      }
+      if (warp == 4 && lane == 0) ATRACE(10, j);
+      if (j > 0) {  // PV(j - 1) read P and wrote O
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        if (need) {
+          tmem_cols(o_col, 0, 64, [&](int c, uint32_t* o, int cnt) {
+            for (int i = 0; i < cnt; ++i) o[i] = __float_as_uint(u2f(o[i]) * corr);
+            tmem_st32(o_col + c, o);
+          });
+        }
+      }
+      if (warp == 4 && lane == 0) ATRACE(11, j);
+      tmem_st32(tmem + lanes + 256 + 32 * wg, packed);
+      tmem_st_wait();
+      if (warp == 4 && lane == 0) ATRACE(12, j);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full_loc);
+      if (warp % 4 == 0 && lane == 0) ATRACE(wg ? 5 : 3, j);
+    }
+    mbar_wait(pv_done, (n - 1) & 1);
+    tc_fence_after();
+    // row sum = both warpgroups' halves
+    red[wg * 128 + r] = l_run;  // exchange buffer 0: its last readers (tile n - 2, n even) passed tile n - 1's barrier
+    asm volatile("bar.sync 2, 256;" ::: "memory");
+    const float l = l_run + red[(1 - wg) * 128 + r];
+    const float inv = 1.f / l;
+    uint8_t* stg = smem + L::kOut + wg * 16384;
+    tmem_cols(o_col, 0, 64, [&](int c, const uint32_t* o, int cnt) {
+      float f[32];
+      for (int i = 0; i < cnt; ++i) f[i] = u2f(o[i]) * inv;
+      for (int i = 0; i < cnt / 8; ++i)
+        *reinterpret_cast<BF8*>(stg + r * 128 + (((c / 8 + i) ^ (r & 7)) * 16)) = f_to_bf8(f + 8 * i);
+    });
+    asm volatile("bar.sync %0, 128;" ::"r"(3 + wg) : "memory");
+    const long long orow0 = static_cast<long long>(row0) + qt * 128;
+    for (int i = tr; i < 128 * 8; i += 128) {
+      const int rr = i / 8, ch = i % 8;
+      const BF8 v = *reinterpret_cast<const BF8*>(stg + rr * 128 + ((ch ^ (rr & 7)) * 16));
+      reinterpret_cast<BF8*>(out + (orow0 + rr) * HD + h * D + 64 * wg)[ch] = v;
+    }
+    if (wg == 0) lse[(static_cast<long long>(b) * H + h) * S + q] = (m_run + log2f(l)) / kLog2e;
+  }
+  tc_fence_before();
+  cluster_sync2();
+  ATRACE_DUMP(32);
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
 // ============================================================== backward dK / dV
 // Persistent, like the dQ kernel: grid = min(work items, SMs), work item w = (key tile, head, batch) in
 // head-major, longest-first order. K / V of the next item are loaded as soon as the current item's
@@ -1448,7 +1745,7 @@ int fwd_tiles() {
   static const int n = [] {
     const char* e = std::getenv("LYNX_ATTN_FWD_TILES");
     const int v = e ? std::atoi(e) : 2;
-    return v == 1 || v == 3 ? v : 2;
+    return v == 1 || v == 3 || v == 4 ? v : 2;
   }();
   return n;
 }
@@ -1458,6 +1755,16 @@ int fwd(const __nv_bfloat16* qkv, __nv_bfloat16* out, float* lse, int B, int S, 
   CUtensorMap m;
   const long long T = static_cast<long long>(B) * S, ld = 3LL * H * D;
   if (!gemm::make_map(&m, qkv, ld, T, ld, 64, 128)) return set_error("attention: tensor map encode failed");
+  if (fwd_tiles() == 4 && D == 128 && (S / 128) % 2 == 0) {
+    CUtensorMap m64;
+    if (!gemm::make_map(&m64, qkv, ld, T, ld, 64, 64)) return set_error("attention: tensor map encode failed");
+    const int poly = poly_every();
+    auto k = poly == 2 ? attn_fwd4_tc_kernel<2> : poly == 3 ? attn_fwd4_tc_kernel<3>
+             : poly == 4 ? attn_fwd4_tc_kernel<4> : attn_fwd4_tc_kernel<0>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd4L::kBytes);
+    k<<<dim3(S / 128, H, B), 384, Fwd4L::kBytes, s>>>(m, m64, out, lse, S, H, kLog2e / sqrtf(static_cast<float>(D)));
+    return check_launch("attention_fwd_tc");
+  }
   if (fwd_tiles() == 3) {
     CUtensorMap m64;
     if (!gemm::make_map(&m64, qkv, ld, T, ld, 64, 64)) return set_error("attention: tensor map encode failed");
@@ -1537,7 +1844,7 @@ int g_mode = -1;
 
 void attention_set_mode(int mode) { attn_tc::g_mode = mode; }
 void attention_set_bwd_warpgroups(int n) { attn_tc::g_bwd_wg = n == 2 || n == 4 ? n : 0; }
-void attention_set_fwd_tiles(int n) { attn_tc::g_fwd_tiles = n >= 1 && n <= 3 ? n : 0; }
+void attention_set_fwd_tiles(int n) { attn_tc::g_fwd_tiles = n >= 1 && n <= 4 ? n : 0; }
 int attention_mode() { return attn_tc::g_mode; }
 bool attention_tc_supported(int seq, int head_dim) {
   return attn_tc::g_mode != 0 && seq % 128 == 0 &&

@@ -353,12 +353,13 @@ def test_attention_fwd_two_tile_kernel_is_bit_identical(ops, cuda, B, S, H, D):
     assert torch.equal(res[1][0], res[2][0]) and torch.equal(res[1][1], res[2][1])
 
 
-@pytest.mark.parametrize("tiles", [1, 3])
+@pytest.mark.parametrize("tiles", [1, 3, 4])
 @pytest.mark.parametrize("B,S,H,D", [(2, 512, 3, 128), (1, 384, 2, 64), (2, 640, 2, 112), (1, 128, 2, 96),
                                      (1, 2048, 2, 128), (1, 2048, 2, 96), (3, 256, 1, 64)])
 def test_attention_fwd_variants_match_reference(ops, cuda, B, S, H, D, tiles):
-    """The one-tile and the 64-key-block forward (attn_fwd3_tc_kernel: separate P region, one MMA issuer
-    per query tile) against fp32 PyTorch, forward and backward (the backward consumes their lse), odd
+    """The one-tile, the 64-key-block (attn_fwd3_tc_kernel: separate P region, one MMA issuer per query
+    tile) and the CTA-pair forward (attn_fwd4_tc_kernel, D = 128 with an even tile count; other shapes run
+    the two-tile kernel) against fp32 PyTorch, forward and backward (the backward consumes their lse), odd
     tile counts included; reruns are bit-identical."""
     from paper_2406_08756_b200._native import lib
     g = torch.Generator(device=cuda).manual_seed(S * D + H + tiles)

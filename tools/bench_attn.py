@@ -46,7 +46,7 @@ def main():
         tb = timeit(lambda: ops.attention_bwd(qkv, out, dout, lse, B, S, H, D))
         print(f"tcgen05 bwd, {wg} row warpgroups: {tb:7.3f} ms {2.5 * f_fwd / tb / 1e9:7.1f} TF/s", flush=True)
     lib().lynx_op_attention_bwd_warpgroups(0)
-    for tiles in (1, 2, 3):  # tcgen05 forward variant (3: 64-key blocks, P apart from S)
+    for tiles in (1, 2, 3, 4):  # tcgen05 forward variant (3: 64-key blocks, P apart from S; 4: CTA pair)
         lib().lynx_op_attention_fwd_tiles(tiles)
         tf = timeit(lambda: ops.attention_fwd(qkv, B, S, H, D))
         print(f"tcgen05 fwd, {tiles} query tile(s) per CTA: {tf:7.3f} ms {f_fwd / tf / 1e9:7.1f} TF/s", flush=True)
