@@ -115,7 +115,9 @@ int lynx_op_attention_bwd(const void* qkv, const void* out, const void* dout, co
 void lynx_op_attention_mode(int mode);
 /* Row warpgroups of the tcgen05 attention backward kernels: 2 or 4 (0: the default, 2). */
 void lynx_op_attention_bwd_warpgroups(int n);
-/* Query tiles per CTA of the tcgen05 attention forward: 1 or 2 (0: the default, 2). */
+/* tcgen05 attention forward variant (0: the default, 2): 1 = one query tile per CTA, 2 = two query tiles
+ * per CTA (persistent), 3 = 64-key blocks with P apart from S, 4 = CTA pair (cta_group::2; head_dim 128
+ * and an even tile count, else 2). Environment: LYNX_ATTN_FWD_TILES. */
 void lynx_op_attention_fwd_tiles(int n);
 /* 1 when attention of this shape runs on the tcgen05 kernels (head_dim 64/96/112/128, seq % 128 == 0). */
 int lynx_op_attention_tc_supported(int seq, int head_dim);
