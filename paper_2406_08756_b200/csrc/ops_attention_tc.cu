@@ -439,8 +439,9 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = align1k(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
   uint64_t *q_full = bar, *q_free = bar + 1, *k_full = bar + 2, *k_empty = bar + 4, *v_full = bar + 6,
-           *v_empty = bar + 8, *s_full = bar + 10, *p_full = bar + 12, *pv_done = bar + 14;  // s/p/pv: per tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+           *v_empty = bar + 8, *s_full = bar + 10, *p_full = bar + 12, *pv_done = bar + 14,
+           *p_full_b = bar + 16;  // s / p / pv: per tile; p_full: P columns 0-63, p_full_b: 64-127
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n_qt = S / 128, np = (n_qt + 1) / 2, n_items = np * H * B;
   const int HD = H * D;
@@ -455,6 +456,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(v_empty + i, 1);
       mbar_init(s_full + i, 1);
       mbar_init(p_full + i, 128);
+      mbar_init(p_full_b + i, 128);
       mbar_init(pv_done + i, 1);
     }
     fence_barrier_init();
@@ -517,15 +519,22 @@ __global__ void __launch_bounds__(384, 1)
           if (k == 0) ATRACE(t ? 7 : 0, j);
         };
         auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P packed bf16 over S_t in TMEM
+          // in two halves: keys 0-63 as soon as the softmax handed them over, while it computes 64-127
           const int st = (g + j) & 1;
-          mbar_wait(p_full + t, (t ? cp1 : cp0) & 1);
+          const uint32_t ph = (t ? cp1 : cp0) & 1;
           if (t) ++cp1; else ++cp0;
+          mbar_wait(p_full + t, ph);
           if (k == 0) ATRACE(t ? 6 : 1, j);
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
+          for (int kk = 0; kk < 4; ++kk)
             umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj(sV + st * L::kTile, kk, 16384), idO,
                         (j | kk) != 0);
+          mbar_wait(p_full_b + t, ph);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 4; kk < 8; ++kk)
+            umma_f16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, mnmaj(sV + st * L::kTile, kk, 16384), idO, 1u);
           umma_commit(pv_done + t);
         };
         auto wait_k = [&](int j) {
@@ -597,15 +606,6 @@ __global__ void __launch_bounds__(384, 1)
           corr = exp2f(m_run - m_new);
           m_run = m_new;
         }
-        float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          const float a = fmaf(x[i], scale_log2, -m_run);
-          x[i] = (kPoly > 0 && i % (kPoly > 0 ? kPoly : 1) == (kPoly > 0 ? kPoly : 1) - 1) ? ex2_poly(a) : ex2(a);
-          rv[i & 7] += x[i];
-        }
-        const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
-        l_run = l_run * corr + rs;
         if (j > 0 && need) {  // O_t rescale after PV_t(j-1) completes (PV_t(j) needs this tile's P)
           mbar_wait(pv_done + t, (c - 1) & 1);
           tc_fence_after();
@@ -618,16 +618,30 @@ __global__ void __launch_bounds__(384, 1)
           });
           tmem_st_wait();
         }
+        // P in two halves (keys 0-63, then 64-127), each handed to the MMA warp as soon as it is in TMEM;
+        // per-element math and the row-sum chains are those of the one-tile kernel (bit-identical)
+        float rv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          uint32_t packed[16];
+        for (int half = 0; half < 2; ++half) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(x[32 * cc + 2 * i], x[32 * cc + 2 * i + 1]);
-          tmem_st16(s_col + cc * 16, packed);
+          for (int i = 64 * half; i < 64 * half + 64; ++i) {
+            const float a = fmaf(x[i], scale_log2, -m_run);
+            x[i] = (kPoly > 0 && i % (kPoly > 0 ? kPoly : 1) == (kPoly > 0 ? kPoly : 1) - 1) ? ex2_poly(a) : ex2(a);
+            rv[i & 7] += x[i];
+          }
+#pragma unroll
+          for (int cc = 2 * half; cc < 2 * half + 2; ++cc) {
+            uint32_t packed[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(x[32 * cc + 2 * i], x[32 * cc + 2 * i + 1]);
+            tmem_st16(s_col + cc * 16, packed);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          mbar_arrive(half ? p_full_b + t : p_full + t);
         }
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(p_full + t);
+        const float rs = ((rv[0] + rv[1]) + (rv[2] + rv[3])) + ((rv[4] + rv[5]) + (rv[6] + rv[7]));
+        l_run = l_run * corr + rs;
         if (k == 0 && warp % 4 == 0 && lane == 0) ATRACE(t ? 5 : 3, j);
       }
       mbar_wait(pv_done + t, (c - 1) & 1);
