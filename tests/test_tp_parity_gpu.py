@@ -214,18 +214,22 @@ def test_fused_tp_reduction_is_bit_identical_and_matches_oracle(cuda, tp, pp, n_
         assert any(r["recompute_overlapped_ms"] > 0 for r in fused["reports"].values())
 
 
-@pytest.mark.parametrize("tp,baseline,vocab", [(1, "full", 50304), (2, "retain_all", 50432)])
-def test_7b_layer_shapes_match_oracle(cuda, tp, baseline, vocab):
-    """One GPT-7B layer at its real widths (hidden 4096, 32 heads of 128, sequence 2048, the GPT-2 vocabulary)
-    with hidden dropout 0.1, at TP1 (Megatron full recompute: every forward op regenerated before its
-    backward) and TP2 (the headline configuration's per-rank shapes: 16 heads, column / row-split GEMMs of
-    hp = 2048, vocab-parallel LM head, real loopback all-reduces) against the CPU fp32 oracle on the
-    unsharded weights — the tcgen05 GEMM / attention kernels at the shapes the bench runs, not the
-    tiny test model's."""
+@pytest.mark.parametrize("model,tp,baseline", [("7b", 1, "full"), ("7b", 2, "retain_all"), ("1.3b", 2, "full"),
+                                               ("13b", 4, "retain_all"), ("20b", 8, "retain_all")])
+def test_real_layer_shapes_match_oracle(cuda, model, tp, baseline):
+    """One layer of each BASELINE model at its real widths and its headline TP degree (sequence 2048, the
+    GPT-2 vocabulary padded to 128 * tp, vocab-parallel head at TP > 1, hidden dropout 0.1), every TP rank
+    in the loopback grid, against the CPU fp32 oracle on the unsharded weights: the tcgen05 GEMM and
+    attention kernels at the per-rank shapes the configurations run — GPT-7B (h 4096, 32 heads of 128;
+    TP1 under full recompute, TP2 = 16 heads per rank), GPT-1.3B (h 1792, head_dim 112, TP2 under full
+    recompute), GPT-13B (h 5120, TP4 = 10 heads per rank), GPT-20B (h 6144, head_dim 96, TP8 = 8 heads
+    per rank) — not the tiny test model's."""
     from paper_2406_08756_b200 import gpt_profile as gp
-    c = gp.GPTConfig(name=f"gpt-7b-layer-tp{tp}", n_layers=1, hidden=4096, heads=32, seq=2048, micro_batch=1,
-                     vocab=vocab, tp=tp, pp=1, n_microbatches=1, dropout=0.1)
-    assert c.vocab_parallel == (tp == 2)
+    base = gp.CONFIGS[model]
+    c = gp.GPTConfig(name=f"gpt-{model}-layer-tp{tp}", n_layers=1, hidden=base.hidden, heads=base.heads,
+                     seq=base.seq, micro_batch=1, vocab=gp.padded_vocab(tp), tp=tp, pp=1, n_microbatches=1,
+                     dropout=0.1)
+    assert c.vocab_parallel == (tp > 1)
     res = grid_run(c, baseline)
     worst = compare_with_oracle(c, res)
-    print(f"7B layer tp{tp} {baseline} V{vocab}: worst max-rel {worst[0]:.3e} cos {worst[1]:.6f} ({worst[2]})")
+    print(f"{model} layer tp{tp} {baseline} V{c.vocab}: worst max-rel {worst[0]:.3e} cos {worst[1]:.6f} ({worst[2]})")
