@@ -108,7 +108,7 @@ char* lynx_plan_opt_timeline(const char* profile_json, int stage, const int* lay
  *   nccl_id (hex, from lynx_rt_nccl_unique_id on rank 0)}, "train": {dropout,
  *   seed, lr, beta1, beta2, eps, weight_decay, init_std}, "exec": {trace,
  *   check_recompute, elide_recompute, dry_run, head_chunk, probe_fc1, probe_ops,
- *   reserve_pool, pool_internal_deps, standalone_stage, comm_standin_us, comm_standin_ctas,
+ *   reserve_pool, pool_internal_deps, standalone_stage, comm_standin_us, comm_standin_ctas, comm_standin_passes,
  *   standin_grad_wait_us, ledger_pass_start_us, window_join, elide_fill, op_timing,
  *   tp_fused}}; parallel.loopback = "<name>" instead of
  *   nccl_id runs every rank of the grid in this process on one GPU (one thread per rank).

@@ -173,6 +173,9 @@ int fill_noise_bf16(void* p, size_t bytes, uint64_t seed, cudaStream_t s);
 // Single-GPU stand-in for a collective (exec.comm_standin_us): `ctas` CTAs of 512 threads hold
 // the stream for `ns` nanoseconds of %globaltimer, sleeping between polls. Models the transfer
 // time of an NCCL all-reduce the plan's window capacity assumes; not its SM / HBM traffic.
-int comm_standin(unsigned long long ns, int ctas, cudaStream_t s);
+// With buf / passes > 0 the CTAs first stream `bytes` of buf in place (read + write, `passes` times): the
+// local HBM traffic and SM occupancy of a real collective on that buffer.
+int comm_standin(unsigned long long ns, int ctas, cudaStream_t s, void* buf = nullptr, long long bytes = 0,
+                 int passes = 0);
 
 }  // namespace lynx

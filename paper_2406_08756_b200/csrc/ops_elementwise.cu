@@ -794,8 +794,50 @@ __global__ void __launch_bounds__(512) comm_standin_kernel(unsigned long long ns
   } while (t - t0 < ns);
 }
 
-int comm_standin(unsigned long long ns, int ctas, cudaStream_t s) {
-  comm_standin_kernel<<<ctas, 512, 0, s>>>(ns);
+// Traffic variant: the CTAs also stream the collective's buffer through HBM (`passes` in-place read +
+// write passes of 16-B vectors, the data unchanged) before sleeping out the rest of the time — the local
+// HBM reads / writes and SM occupancy an NCCL ring all-reduce of that buffer costs a rank, which the
+// sleeping stand-in leaves out.
+__global__ void __launch_bounds__(512) comm_standin_traffic_kernel(uint4* buf, long long n16, int passes,
+                                                                   unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  // 8 independent 16-B loads in flight per thread (16 CTAs x 512 threads: ~1 MB outstanding), enough to
+  // stream a TP all-reduce buffer within its modelled transfer time; .cs (evict-first): a collective's
+  // buffer streams through L2 without displacing the compute kernels' working sets
+  constexpr int kU = 8;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (int p = 0; p < passes; ++p)
+    for (long long i0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n16; i0 += kU * stride) {
+      uint4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const long long i = i0 + u * stride;
+        if (i < n16)
+          asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                       : "l"(buf + i));
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const long long i = i0 + u * stride;
+        if (i < n16)
+          asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(buf + i), "r"(v[u].x), "r"(v[u].y),
+                       "r"(v[u].z), "r"(v[u].w)
+                       : "memory");
+      }
+    }
+  do {
+    __nanosleep(500);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+int comm_standin(unsigned long long ns, int ctas, cudaStream_t s, void* buf, long long bytes, int passes) {
+  if (buf && bytes >= 16 && passes > 0)
+    comm_standin_traffic_kernel<<<ctas, 512, 0, s>>>(static_cast<uint4*>(buf), bytes / 16, passes, ns);
+  else
+    comm_standin_kernel<<<ctas, 512, 0, s>>>(ns);
   return check_launch("comm_standin");
 }
 

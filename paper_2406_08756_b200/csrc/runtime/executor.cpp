@@ -225,6 +225,7 @@ void Executor::parse_config(const std::string& text) {
   opt_.pool_internal_deps = ex.value("pool_internal_deps", false);
   opt_.comm_standin_us = ex.value("comm_standin_us", 0.0);
   opt_.comm_standin_ctas = ex.value("comm_standin_ctas", 16);
+  opt_.comm_standin_passes = ex.value("comm_standin_passes", 0);
   opt_.standin_grad_wait_us = ex.value("standin_grad_wait_us", std::vector<double>());
   opt_.ledger_pass_start_us = ex.value("ledger_pass_start_us", std::vector<std::string>());
   cfg_.head_chunk = static_cast<int>(std::min<long long>(ex.value("head_chunk", 4096), cfg_.tokens()));
@@ -1012,7 +1013,8 @@ host::Rat Executor::comm_element(int mb, bool bwd, int l, const host::Element& e
   } else if (!opt_.dry_run) {
     span_begin(tp_s_, 1, mb, e.op);
     if (opt_.comm_standin_us > 0)
-      ck_op(comm_standin(static_cast<unsigned long long>(opt_.comm_standin_us * 1e3), opt_.comm_standin_ctas, tp_s_),
+      ck_op(comm_standin(static_cast<unsigned long long>(opt_.comm_standin_us * 1e3), opt_.comm_standin_ctas, tp_s_,
+                         buf, T * h * 2, opt_.comm_standin_passes),
             "comm stand-in");
     else
       comms_->allreduce_sum_bf16(buf, static_cast<size_t>(T * h), tp_s_);
@@ -1220,7 +1222,8 @@ void Executor::head_forward(int mb) {
     if (comms_)
       comms_->allreduce_sum_bf16(head_dy_[mb], static_cast<size_t>(T * h), main_);
     else if (opt_.comm_standin_us > 0)
-      ck_op(comm_standin(static_cast<unsigned long long>(opt_.comm_standin_us * 1e3), opt_.comm_standin_ctas, main_),
+      ck_op(comm_standin(static_cast<unsigned long long>(opt_.comm_standin_us * 1e3), opt_.comm_standin_ctas, main_,
+                         head_dy_[mb], T * h * 2, opt_.comm_standin_passes),
             "head dX stand-in");
   }
 }

@@ -66,6 +66,8 @@ struct ExecOptions {
                                 // activations / gradients, sends are skipped (measured partitioning)
   double comm_standin_us = 0;   // > 0 (standalone only): each TP all-reduce is replaced by a stand-in
   int comm_standin_ctas = 16;   // kernel holding the TP stream this long, so one GPU runs one TP rank
+  int comm_standin_passes = 0;  // > 0: the stand-in also streams the all-reduce buffer through HBM this many
+                                // times (in-place read + write): the local traffic of a real collective
                                 // of a TP > 1 stage with the plan's comm windows (window overlap)
   std::vector<double> standin_grad_wait_us;  // standalone: per microbatch m, the pipeline stall before
                                              // B(m)'s gradient receive (from the simulator's trace),

@@ -47,6 +47,9 @@ def main():
                     help="comma list of heu, elided, full_recompute, selective")
     ap.add_argument("--op-timing", action="store_true", help="per-operator device times of the HEU run")
     ap.add_argument("--window-join", type=int, default=1, help="exec.window_join (1: reference semantics)")
+    ap.add_argument("--standin-passes", type=int, default=0,
+                    help="exec.comm_standin_passes: the stand-in all-reduce also streams its buffer through HBM "
+                         "this many times (the local traffic and SM occupancy of a ring all-reduce; 0: sleep only)")
     ap.add_argument("--out", default="gpurun_out/emulate_tp2pp4.json")
     a = ap.parse_args()
     torch.cuda.set_device(0)
@@ -67,8 +70,11 @@ def main():
                        f"{c.n_microbatches} microbatches; TP rank 0 of each stage alone on one B200",
            "comm_model": {"standin_us_per_allreduce": round(se.standin_us(c), 3),
                           "nvlink_bus_gbs": profiler.NVLINK_BUS_GBS, "bytes": 2 * c.tokens * c.hidden, "ctas": a.ctas,
-                          "note": "stand-in kernel holds the TP stream for the modelled transfer time; "
-                                  "real NCCL SM/HBM contention not modelled"},
+                          "standin_passes": a.standin_passes,
+                          "note": "stand-in kernel holds the TP stream for the modelled transfer time"
+                                  + ("; real NCCL SM/HBM contention not modelled" if not a.standin_passes else
+                                     f", streaming its buffer through HBM {a.standin_passes}x (in-place read + write) "
+                                     "on the stand-in CTAs: a ring all-reduce's local traffic")},
            "profiler_s": round(prof_s, 2), "ledger_budget_bytes": c.mem_budget_bytes,
            "profile_op_us": {k: float(v) for k, v in times.items()}, "window_join": bool(a.window_join),
            "budget": "reduced (--budget-gb)" if a.budget_gb else "device HBM minus unmodelled reserve",
@@ -76,7 +82,8 @@ def main():
     for s in (int(x) for x in a.stages.split(",")):
         row = se.emulate(c, text, [s], steps=a.steps, warmup=a.warmup, ctas=a.ctas,
                          variants=tuple(a.variants.split(",")), op_timing=a.op_timing,
-                         extra_opts={"window_join": bool(a.window_join)})[str(s)]
+                         extra_opts={"window_join": bool(a.window_join),
+                                     "comm_standin_passes": a.standin_passes})[str(s)]
         out["stages"][str(s)] = row
         print(json.dumps({"stage": s, "exposed_fraction_of_iteration": row.get("exposed_fraction_of_iteration"),
                           "crosscheck_ms": row.get("crosscheck_ms"),
