@@ -110,7 +110,7 @@ char* lynx_plan_opt_timeline(const char* profile_json, int stage, const int* lay
  *   check_recompute, elide_recompute, dry_run, head_chunk, probe_fc1, probe_ops,
  *   reserve_pool, pool_internal_deps, standalone_stage, comm_standin_us, comm_standin_ctas, comm_standin_passes,
  *   standin_grad_wait_us, ledger_pass_start_us, window_join, elide_fill, op_timing,
- *   tp_fused}}; parallel.loopback = "<name>" instead of
+ *   tp_fused, dw_concurrent}}; parallel.loopback = "<name>" instead of
  *   nccl_id runs every rank of the grid in this process on one GPU (one thread per rank).
  * Weights are initialised on the device from Philox streams keyed by seed. */
 typedef struct lynx_rt lynx_rt;

@@ -66,6 +66,7 @@ struct ExecOptions {
                                 // activations / gradients, sends are skipped (measured partitioning)
   double comm_standin_us = 0;   // > 0 (standalone only): each TP all-reduce is replaced by a stand-in
   int comm_standin_ctas = 16;   // kernel holding the TP stream this long, so one GPU runs one TP rank
+  bool dw_concurrent = true;    // attention backward: dW_proj on the aux stream beside dW_qkv (wave fill)
   int comm_standin_passes = 0;  // > 0: the stand-in also streams the all-reduce buffer through HBM this many
                                 // times (in-place read + write): the local traffic of a real collective
                                 // of a TP > 1 stage with the plan's comm windows (window overlap)
@@ -206,6 +207,7 @@ class Executor {
   std::map<int, std::vector<host::Recompute>> stall_;
 
   cudaStream_t main_ = nullptr, side_ = nullptr, tp_s_ = nullptr, pa_s_ = nullptr, pg_s_ = nullptr;
+  cudaStream_t aux_ = nullptr;  // intra-op concurrency of the main stream's work (attention backward dW GEMMs)
   std::unique_ptr<Comms> comms_;
   std::string loopback_;           // parallel.loopback: in-process grid name (all ranks on this GPU)
   cudaMemPool_t pool_ = nullptr;   // private stream-ordered pool of this executor (activations)
