@@ -19,13 +19,13 @@ def tiny(n_micro=2, dropout=0.0, budget=0):
     return gp.GPTConfig("gpt-tiny", 4, 512, 8, 256, 2, 50304, 1, 1, n_micro, dropout=dropout, mem_budget_bytes=budget)
 
 
-def run(c, baseline="heu", check=False, steps=1):
+def run(c, baseline="heu", check=False, steps=1, opts=None):
     from paper_2406_08756_b200 import executor as ex
     from paper_2406_08756_b200 import gpt_profile as gp
     text = gp.profile_text(c)
     plan = ex.plan_for(text, 0, baseline)
     e = ex.Executor(text, plan["timeline"], ex.make_config(c, plan["layers_per_stage"],
-                                                          exec_opts={"check_recompute": check}))
+                                                          exec_opts={"check_recompute": check, **(opts or {})}))
     tok, lab = ex.synthetic_batch(c)
     params = None
     shapes = ex.param_shapes(c, c.n_layers, True, True)
@@ -218,6 +218,18 @@ def test_heu_async_recompute_is_bit_identical_to_retain_all(cuda):
     assert l_heu == l_keep
     for k in g_keep:
         assert np.array_equal(g_keep[k], g_heu[k]), k
+
+
+def test_concurrent_weight_gradient_gemms_are_bit_identical(cuda):
+    """exec.dw_concurrent (attention backward: dW_proj on an auxiliary stream beside dW_qkv) changes only
+    where the two GEMMs run, not what they compute: loss and every gradient equal the serial order's, over
+    two steps and four microbatches (bf16 weight-gradient accumulation across microbatches, AdamW)."""
+    c = tiny(n_micro=4, dropout=0.1)
+    l_on, g_on, *_ = run(c, "retain_all", steps=2, opts={"dw_concurrent": True})
+    l_off, g_off, *_ = run(c, "retain_all", steps=2, opts={"dw_concurrent": False})
+    assert l_on == l_off
+    for k in g_on:
+        assert np.array_equal(g_on[k], g_off[k]), k
 
 
 def test_gradients_are_deterministic_under_token_collisions(cuda):
