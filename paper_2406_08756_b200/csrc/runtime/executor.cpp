@@ -1231,10 +1231,23 @@ void Executor::head_forward(int mb) {
     GemmDesc dw{sc_main_.logits, V, true, yc, h, true, gw, h, V, h, C, nullptr,
                 head_first_ ? EPI_STORE_F32 : EPI_ACC_F32};
     head_first_ = false;
-    ck_op(gemm_run(dw, main_), "lm_head dW");
     GemmDesc dx{sc_main_.logits, V, false, w, h, true, static_cast<__nv_bfloat16*>(head_dy_[mb]) + c0 * h, h, C, h, V,
                 nullptr, EPI_BF16};
-    ck_op(gemm_run(dx, main_), "lm_head dX");
+    // exec.dw_concurrent: dX (128 wide tiles at the 7B shape, 1.73 waves of CTA pairs) on the aux stream
+    // beside dW (3152 tiles), joined before the next chunk's logits overwrite the buffer both read
+    if (opt_.dw_concurrent) {
+      cudaEvent_t fork = ev();
+      ck(cudaEventRecord(fork, main_), "event");
+      ck(cudaStreamWaitEvent(aux_, fork, 0), "wait");
+      ck_op(gemm_run(dx, aux_), "lm_head dX");
+      ck_op(gemm_run(dw, main_), "lm_head dW");
+      cudaEvent_t joined = ev();
+      ck(cudaEventRecord(joined, aux_), "event");
+      ck(cudaStreamWaitEvent(main_, joined, 0), "wait");
+    } else {
+      ck_op(gemm_run(dw, main_), "lm_head dW");
+      ck_op(gemm_run(dx, main_), "lm_head dX");
+    }
   }
   if (vp) {  // the rows' gradient w.r.t. the final LayerNorm output: partial per vocabulary slice
     if (comms_)
