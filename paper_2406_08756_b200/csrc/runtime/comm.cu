@@ -127,6 +127,16 @@ class NcclComms final : public Comms {
       throw RtError(last_error(), kCudaError);
   }
   ~NcclComms() override {
+    if (base_ && tp_) {
+      // Peers read this rank's staging slots in place: free them only after every TP rank got here.
+      // Each executor synchronises its own streams before destroying its communicators, so once all
+      // ranks passed this collective no consumer kernel reads a slot any more.
+      void* one = nullptr;
+      if (cudaMalloc(&one, sizeof(float)) == cudaSuccess) {
+        if (ncclAllReduce(one, one, 1, ncclFloat, ncclSum, tp_, nullptr) == ncclSuccess) cudaStreamSynchronize(nullptr);
+        cudaFree(one);
+      }
+    }
     for (int r = 0; r < n_; ++r)
       if (r != me_) {
         if (peer_base_[r]) cudaIpcCloseMemHandle(peer_base_[r]);
