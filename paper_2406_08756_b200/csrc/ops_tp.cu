@@ -79,13 +79,22 @@ __global__ void tp_signal_kernel(TpFlags peers, int n, int me, unsigned long lon
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peers.f[r] + me), "l"(value) : "memory");
 }
 
+// A peer that never signals (a rank died, or took a different path) must not hang the GPU: after
+// kWaitTimeoutNs the kernel traps, the launch fails and the executor reports a CUDA error.
+constexpr unsigned long long kWaitTimeoutNs = 60ull * 1000 * 1000 * 1000;
+
 __global__ void tp_wait_kernel(const unsigned long long* flags, int n, unsigned long long value) {
   const int r = threadIdx.x;
   if (r >= n) return;
-  unsigned long long v = 0;
+  unsigned long long v = 0, t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   do {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + r) : "memory");
-    if (v < value) __nanosleep(200);
+    if (v < value) {
+      __nanosleep(200);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > kWaitTimeoutNs) __trap();
+    }
   } while (v < value);
 }
 
