@@ -45,6 +45,17 @@ extern "C" {
 const char* lynx_last_error(void);
 int lynx_abi_version(void);
 
+/* exec.tp_fused building blocks (the executor's row-parallel reductions; ops_tp.cu). Replace the TP
+ * all-reduce + bias_dropout_residual of Megatron's row-parallel layers (the reference's CTime windows,
+ * heusched.cpp:62-70). peer_flags / partials: n device pointers in rank order, this rank's own at `me`.
+ * signal_wait: every rank's flag array gets `value` in slot `me` (st.release.sys), then the stream waits
+ * until all n slots of `my_flags` reached `value` (ld.acquire.sys; traps after 60 s).
+ * reduce_residual: out = res + dropout(bias + bf16(sum of partials in rank order)). */
+int lynx_op_tp_signal_wait(void* const* peer_flags, const void* my_flags, int n, int me, unsigned long long value,
+                           void* stream);
+int lynx_op_tp_reduce_residual(const void* const* partials, int n, const void* bias, const void* res, void* out,
+                               long long rows, int width, float p, unsigned long long seed,
+                               unsigned long long stream_id, void* stream);
 /* C[M,N] = A[M,K] * B[N,K]^T on tcgen05 tensor cores (fp32 accumulation in TMEM).
  * a_mn_major=0: A stored [M][K] (row pitch lda); 1: A stored [K][M] (pitch lda).
  * b_mn_major=0: B stored [N][K] (row pitch ldb); 1: B stored [K][N] (pitch ldb).

@@ -24,6 +24,8 @@ _SIGNATURES: dict[str, tuple] = {
     "lynx_abi_version": (_i, []),
     "lynx_op_gemm": (_i, [_vp, _ll, _i, _vp, _ll, _i, _vp, _ll, _i, _i, _i, _vp, _i, _vp]),
     "lynx_op_gemm_gelu": (_i, [_vp, _ll, _i, _vp, _ll, _i, _vp, _vp, _ll, _i, _i, _i, _vp, _vp]),
+    "lynx_op_tp_signal_wait": (_i, [_vp, _vp, _i, _i, _ull, _vp]),
+    "lynx_op_tp_reduce_residual": (_i, [_vp, _i, _vp, _vp, _vp, _ll, _i, _f, _ull, _ull, _vp]),
     "lynx_op_gemm_residual": (_i, [_vp, _ll, _vp, _ll, _vp, _ll, _i, _i, _i, _vp, _vp, _f, _ull, _ull, _vp]),
     "lynx_op_gemm_gelu_bwd": (_i, [_vp, _ll, _vp, _ll, _i, _vp, _ll, _i, _i, _i, _vp, _vp]),
     "lynx_op_gemm_mode": (None, [_i]),

@@ -53,6 +53,26 @@ int lynx_op_gemm(const void* a, long long lda, int a_mn_major, const void* b, lo
   return gemm_run(g, STREAM(stream));
 }
 
+// exec.tp_fused building blocks (the executor's row-parallel reductions), for multi-process checks:
+// `partials` / `peer_flags` hold n device pointers in rank order (this rank's own at index me).
+int lynx_op_tp_signal_wait(void* const* peer_flags, const void* my_flags, int n, int me, unsigned long long value,
+                           void* stream) {
+  if (n < 1 || n > kMaxTpRanks || me < 0 || me >= n) return set_error("tp_signal_wait: ranks", kValidation);
+  TpFlags f{};
+  for (int r = 0; r < n; ++r) f.f[r] = static_cast<unsigned long long*>(peer_flags[r]);
+  return tp_signal_wait(f, static_cast<const unsigned long long*>(my_flags), n, me, value, STREAM(stream));
+}
+
+int lynx_op_tp_reduce_residual(const void* const* partials, int n, const void* bias, const void* res, void* out,
+                               long long rows, int width, float p, unsigned long long seed,
+                               unsigned long long stream_id, void* stream) {
+  if (n < 1 || n > kMaxTpRanks) return set_error("tp_reduce_residual: ranks", kValidation);
+  TpPartials parts{};
+  parts.n = n;
+  for (int r = 0; r < n; ++r) parts.p[r] = CBF(partials[r]);
+  return tp_reduce_residual(parts, CBF(bias), CBF(res), BF(out), rows, width, p, seed, stream_id, STREAM(stream));
+}
+
 int lynx_op_gemm_gelu(const void* a, long long lda, int a_mn_major, const void* b, long long ldb, int b_mn_major,
                       void* c, void* c_gelu, long long ldc, int m, int n, int k, const void* bias, void* stream) {
   GemmDesc g{a, lda, a_mn_major != 0, b, ldb, b_mn_major != 0, c, ldc, m, n, k, CBF(bias), EPI_BF16_GELU, c_gelu};
