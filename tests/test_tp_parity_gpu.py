@@ -214,11 +214,13 @@ def test_fused_tp_reduction_is_bit_identical_and_matches_oracle(cuda, tp, pp, n_
         assert any(r["recompute_overlapped_ms"] > 0 for r in fused["reports"].values())
 
 
-@pytest.mark.parametrize("model,tp,baseline,fused", [("7b", 1, "full", False), ("7b", 2, "retain_all", False),
-                                                     ("1.3b", 2, "full", False), ("13b", 4, "retain_all", False),
-                                                     ("20b", 8, "retain_all", False), ("7b", 2, "retain_all", True),
-                                                     ("20b", 8, "retain_all", True)])
-def test_real_layer_shapes_match_oracle(cuda, model, tp, baseline, fused):
+@pytest.mark.parametrize("model,tp,baseline,fused,pp", [("7b", 1, "full", False, 1), ("7b", 2, "retain_all", False, 1),
+                                                        ("1.3b", 2, "full", False, 1), ("13b", 4, "retain_all", False, 1),
+                                                        ("20b", 8, "retain_all", False, 1),
+                                                        ("7b", 2, "retain_all", True, 1),
+                                                        ("20b", 8, "retain_all", True, 1),
+                                                        ("7b", 2, "full", False, 2)])
+def test_real_layer_shapes_match_oracle(cuda, model, tp, baseline, fused, pp):
     """One layer of each BASELINE model at its real widths and its headline TP degree (sequence 2048, the
     GPT-2 vocabulary padded to 128 * tp, vocab-parallel head at TP > 1, hidden dropout 0.1), every TP rank
     in the loopback grid, against the CPU fp32 oracle on the unsharded weights: the tcgen05 GEMM and
@@ -226,11 +228,13 @@ def test_real_layer_shapes_match_oracle(cuda, model, tp, baseline, fused):
     TP1 under full recompute, TP2 = 16 heads per rank), GPT-1.3B (h 1792, head_dim 112, TP2 under full
     recompute), GPT-13B (h 5120, TP4 = 10 heads per rank), GPT-20B (h 6144, head_dim 96, TP8 = 8 heads
     per rank) — not the tiny test model's. With `fused`, the exec.tp_fused reductions (7B TP2, 20B TP8)
-    are also checked bit-identical to the collective path."""
+    are also checked bit-identical to the collective path; with pp = 2, two 7B layers on a TP2·PP2 grid
+    (one layer per stage, two microbatches through 1F1B, full recompute) — the headline's pipeline
+    hand-off at its real activation size."""
     from paper_2406_08756_b200 import gpt_profile as gp
     base = gp.CONFIGS[model]
-    c = gp.GPTConfig(name=f"gpt-{model}-layer-tp{tp}", n_layers=1, hidden=base.hidden, heads=base.heads,
-                     seq=base.seq, micro_batch=1, vocab=gp.padded_vocab(tp), tp=tp, pp=1, n_microbatches=1,
+    c = gp.GPTConfig(name=f"gpt-{model}-layer-tp{tp}pp{pp}", n_layers=pp, hidden=base.hidden, heads=base.heads,
+                     seq=base.seq, micro_batch=1, vocab=gp.padded_vocab(tp), tp=tp, pp=pp, n_microbatches=pp,
                      dropout=0.1)
     assert c.vocab_parallel == (tp > 1)
     res = grid_run(c, baseline)
@@ -241,5 +245,5 @@ def test_real_layer_shapes_match_oracle(cuda, model, tp, baseline, fused):
             for k in plain["grads"][key]:
                 assert np.array_equal(plain["grads"][key][k], res["grads"][key][k]), (key, k)
     worst = compare_with_oracle(c, res)
-    print(f"{model} layer tp{tp} {baseline}{' fused' if fused else ''} V{c.vocab}: worst max-rel {worst[0]:.3e} "
+    print(f"{model} layer tp{tp} pp{pp} {baseline}{' fused' if fused else ''} V{c.vocab}: worst max-rel {worst[0]:.3e} "
           f"cos {worst[1]:.6f} ({worst[2]})")
