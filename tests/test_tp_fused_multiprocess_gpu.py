@@ -52,7 +52,7 @@ def rank_main(r, slots, flags, bias, res, outs, errq):
                                              ctypes.c_float(0.1), 42, 7 + k, st):
                 raise RuntimeError(L.lynx_last_error().decode())
         s.synchronize()
-        del slots, flags, outs
+        del slots, flags, outs, bias, res  # release the shared storages before the producer collects them
         torch.cuda.synchronize()
         errq.put(None)
     except Exception as e:  # noqa: BLE001
@@ -75,6 +75,7 @@ def test_fused_reduction_across_processes_matches_one_process(cuda):
     errs = [errq.get(timeout=600) for _ in procs]
     for p in procs:
         p.join(timeout=120)
+    torch.cuda.synchronize()
     torch.cuda.ipc_collect()
     assert errs == [None] * N, errs
     assert [int(f[:N].max()) for f in flags] == [CALLS] * N
